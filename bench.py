@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Benchmark: VGICP correspondences linearized per second (BASELINE.json metric) on the
+global-mapping workload (config 5: 1000 submaps, 50 nearest-neighbour binary factors each,
+~20M correspondences per linearization, 1.0 m maps), synthetic data.
+
+One step = one linearization of every factor of the graph: compose T_ij from the pose table
+(K-compose), fused transform/lookup/fused-covariance/accumulate (K4), fixed-order finalize
+into the per-factor H_ii/H_ij/H_jj/b_i/b_j/cost records (K5).  Under torchrun the factors are
+LPT-sharded by point count across ranks (strong scaling of the fixed graph); each step
+broadcasts the pose table from the solver rank and gathers the per-factor blocks to it
+over NCCL.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_CORR = 84  # SURVEY.md §8d algorithmic bytes per correspondence
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+METRIC = "VGICP correspondences linearized/sec"
+UNIT = "corr/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--submaps", type=int, default=1000)
+    ap.add_argument("--neighbors", type=int, default=50)
+    ap.add_argument("--cpu-targets", type=int, default=16,
+                    help="target maps in the bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    return ap.parse_args()
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        cmd = ["nvidia-smi", "-i", str(self.index),
+               "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+               "--format=csv,noheader,nounits"]
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(cmd, capture_output=True, text=True, timeout=5).stdout
+                sm, smax, act = [x.strip() for x in out.strip().split(",")]
+                self.samples.append((float(sm), float(smax), int(act, 16)))
+            except Exception:
+                pass
+            self._stop.wait(0.05)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        reasons = set()
+        for _, _, act in self.samples:
+            for bit, name in self.REASONS.items():
+                if act & bit and name != "gpu_idle":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference(wl, args, steps, warmup):
+    from oracle import cpu_baseline
+
+    sample = cpu_baseline.build_sample(wl, args.cpu_targets)
+    rate, sec, procs = cpu_baseline.time_sample(sample, steps, warmup)
+    desc = (f"{len(sample['pairs'])} factors (every factor whose target is one of submaps "
+            f"0..{args.cpu_targets - 1}), {sample['points']} correspondences per pass, "
+            f"oracle linearization, {procs}-process fork pool, {steps} passes")
+    return rate, sec, procs, desc
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup(args)
+    if rank != 0:
+        return 0
+    from paper_2202_00242_b200 import workloads
+
+    wl = workloads.global_mapping(args.submaps, args.neighbors, device_objects=False)
+    steps = max(1, args.steps)
+    rate, sec, procs, desc = cpu_reference(wl, args, steps, max(1, min(args.warmup, 3)))
+    line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "global-mapping (BASELINE config 5): bounded CPU sample",
+                       "submaps": args.submaps, "neighbors": args.neighbors},
+            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": procs, "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2202_00242_b200 import _lib, workloads
+
+    _lib.set_device(local)
+    ctx = _lib.context(local)
+    # a real (non-legacy) stream shared by torch events, NCCL and the library's launches
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+
+    t0 = time.perf_counter()
+    wl = workloads.global_mapping(args.submaps, args.neighbors)
+    weights = np.array([len(wl.source_index[i]) for i in wl.pairs[:, 0]])
+    shards = workloads.lpt_shards(weights, world) if world > 1 else [np.arange(len(wl.pairs))]
+    mine = shards[rank]
+    batch = wl.batch(mine, ctx=ctx)
+    ctx.set_stream(stream.cuda_stream)
+    setup_s = time.perf_counter() - t0
+    F_r = len(mine)
+    F_max = max(len(s) for s in shards)
+    total_points = wl.num_points
+    my_points = int(weights[mine].sum())
+    V = wl.pose_table.shape[0]
+    REC = _lib.RECORD_SIZE[_lib.MODE_LINEARIZE]
+
+    poses_dev = torch.from_numpy(wl.pose_table).to("cuda")
+    out_dev = torch.zeros((F_max, REC), dtype=torch.float64, device="cuda")
+    gather = ([torch.empty_like(out_dev) for _ in range(world)] if (world > 1 and rank == 0)
+              else None)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+
+    def step(e=None):
+        if world > 1:
+            dist.broadcast(poses_dev, 0)
+        if e:
+            e[0].record()
+        batch.compose_device(poses_dev.data_ptr(), V)
+        if e:
+            e[1].record()
+        batch.accumulate_device(_lib.MODE_LINEARIZE)
+        if e:
+            e[2].record()
+        batch.finalize_device(_lib.MODE_LINEARIZE, out_dev.data_ptr())
+        if world > 1:
+            dist.gather(out_dev, gather, dst=0)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.zero_()  # evict L2 between timed steps (outside the timed events)
+            starts[k].record()
+            step(ev[k])
+            ends[k].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    k4_ms = [e[1].elapsed_time(e[2]) for e in ev]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = total_points * args.steps / (total_ms / 1e3)
+
+    # ---- e2e: through the public batch API with host buffers (H2D poses, D2H records) ----
+    poses_host = torch.from_numpy(wl.pose_table.copy()).pin_memory()
+    out_host = torch.empty((F_max, REC), dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    if world == 1:
+        out_np = out_host.numpy()
+        poses_np = poses_host.numpy()
+        for k in range(args.e2e_steps + 2):
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            batch.linearize_poses(poses_np, _lib.MODE_LINEARIZE, out=out_np)
+            if k >= 2:
+                e2e_ms.append((time.perf_counter() - a) * 1e3)
+        h2d = poses_host.numel() * 8
+        d2h = F_r * REC * 8
+    else:
+        for k in range(args.e2e_steps + 2):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a = time.perf_counter()
+            if rank == 0:
+                poses_dev.copy_(poses_host, non_blocking=True)
+            step()
+            if rank == 0:
+                out_host.copy_(gather[0] if gather else out_dev, non_blocking=False)
+                for g in gather[1:]:
+                    out_host.copy_(g, non_blocking=False)
+            torch.cuda.synchronize()
+            dt = torch.tensor([(time.perf_counter() - a) * 1e3], dtype=torch.float64,
+                              device="cuda")
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            if k >= 2:
+                e2e_ms.append(float(dt.item()))
+        h2d = poses_host.numel() * 8
+        d2h = world * F_max * REC * 8
+    e2e_value = total_points / (statistics.median(e2e_ms) / 1e3)
+
+    # ---- roofline of the dominant kernel (K4) ----
+    peak, peak_kind = hbm_peak()
+    k4_avg_s = statistics.mean(k4_ms) / 1e3
+    achieved = BYTES_PER_CORR * my_points / k4_avg_s / 1e9
+
+    line = None
+    if rank == 0:
+        clocks = clk.summary()
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rate, sec, procs, desc = cpu_reference(wl, args, steps=3, warmup=1)
+            cpu = {"value": rate, "unit": UNIT, "cores": procs, "kind": "port", "sample": desc}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32+f64", "data": "synthetic",
+            "config": {"workload": "global-mapping (BASELINE config 5)",
+                       "submaps": args.submaps, "neighbors": args.neighbors,
+                       "factors": int(len(wl.pairs)), "corr_per_step": total_points,
+                       "voxel_resolution_m": wl.resolution, "scan_points": 16384,
+                       "source_points": "U[200,600]", "parallelism": f"factor-shard x{world}",
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "setup_s": round(setup_s, 2)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": statistics.median(e2e_ms)},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_linearize<0> (K4)",
+                         "kernel_ms": statistics.mean(k4_ms),
+                         "bytes_per_corr": BYTES_PER_CORR, "peak_kind": peak_kind},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,171 @@
+/*
+ * vgicp.h — C-ABI of the B200-native VGICP matching-cost path (libvgicp.so).
+ *
+ * This is the drop-in boundary for the hot path of arXiv 2202.00242 as restated by the
+ * reference package `limapper` (pure Python/NumPy).  Every entry point below replaces one
+ * reference function; the citation is `file:line` under /root/reference/pkg/src/limapper/.
+ * The Python mirror of the reference API (paper_2202_00242_b200/registration.py,
+ * preprocess.py, factor_graph.py) binds these with ctypes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no torch/CUDA types in signatures (streams are void*).
+ *   - Host arrays are C-contiguous float64 / int64, caller-owned and only borrowed for the
+ *     duration of the call.  Device objects (ctx, cloud, map, batch) are owned by handles.
+ *   - A rigid transform "T" is 12 doubles: R row-major (9) then t (3); p' = R p + t.
+ *   - A pose-table entry is 8 doubles: quaternion (x, y, z, w) then translation (3), then
+ *     one pad — the layout of limapper.geometry.Se3Pose (geometry.py:47-60,208-237).
+ *   - Every function returns a status code (VG_OK == 0).  vg_last_error() returns a
+ *     thread-local message for the last failure.  Nothing throws or longjmps across the ABI.
+ *   - Results are deterministic: fixed-order reductions, no floating-point atomics.
+ */
+#ifndef VGICP_H_
+#define VGICP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VGICP_ABI_VERSION 1
+
+/* status codes; the Python wrapper maps each to the reference exception type */
+#define VG_OK 0
+#define VG_ERR_INVALID 1    /* ValueError (registration.py:80-81, preprocess.py:149-150) */
+#define VG_ERR_CUDA 2       /* RuntimeError: a CUDA call failed */
+#define VG_ERR_DEGENERATE 3 /* DegenerateConstraint (errors.py:24-25, registration.py:213-215) */
+#define VG_ERR_TOO_SPARSE 4 /* FrameTooSparse (errors.py:8-9, preprocess.py:129-130) */
+#define VG_ERR_NOMEM 5      /* MemoryError: device allocation failed */
+
+/* batch evaluation modes and per-factor output record sizes (doubles) */
+#define VG_MODE_LINEARIZE 0 /* blocks: H_ii(21) H_ij(36) H_jj(21) b_i(6) b_j(6) cost inliers */
+#define VG_MODE_COST 1      /* cost inliers */
+#define VG_MODE_COMPACT 2   /* H'(21) b'(6) cost inliers: pre-adjoint record */
+#define VG_REC_LINEARIZE 92
+#define VG_REC_COST 2
+#define VG_REC_COMPACT 29
+
+/* factor flags */
+#define VG_FACTOR_UNARY 1 /* target pose fixed (factor_graph.py:219-245) */
+
+typedef struct vg_ctx vg_ctx;
+typedef struct vg_cloud vg_cloud;
+typedef struct vg_map vg_map;
+typedef struct vg_batch vg_batch;
+
+typedef struct vg_factor_spec {
+  const vg_cloud* source; /* MatchingCostFactor.source (factor_graph.py:219-229) */
+  const vg_map* target;   /* MatchingCostFactor.target_map */
+  int32_t flags;          /* VG_FACTOR_UNARY or 0 */
+  int32_t min_inliers;    /* MatchingCostFactor.min_inliers (default 10, registration.py:26) */
+  int32_t var_source;     /* pose-table index of the source variable (pose-table mode) */
+  int32_t var_target;     /* pose-table index of the target variable / fixed pose */
+} vg_factor_spec;
+
+/* ---- library / context ---------------------------------------------------------------- */
+int vg_abi_version(void);
+const char* vg_last_error(void);
+int vg_ctx_create(int device, vg_ctx** out);
+int vg_ctx_destroy(vg_ctx* ctx);
+/* route all work of ctx onto an existing cudaStream_t (NULL = the context's own stream) */
+int vg_ctx_set_stream(vg_ctx* ctx, void* stream);
+int vg_ctx_synchronize(vg_ctx* ctx);
+/* number of kernels this library has launched on ctx so far (bench evidence) */
+int vg_ctx_launch_count(const vg_ctx* ctx, int64_t* count);
+
+/* ---- voxel keys ------------------------------------------------------------------------ */
+/* replaces pack_voxel_keys (preprocess.py:21-22,68-70): floor(p/res)+2^20 packed 21 bits/axis */
+int vg_pack_voxel_keys(vg_ctx* ctx, const double* xyz, int64_t n, double resolution,
+                       int64_t* keys_out);
+
+/* ---- clouds (Frame: preprocess.py:46-60) ----------------------------------------------- */
+/* xyz: n x 3; cov: n x 3 x 3 or NULL.  Points exactly representable in fp32 take the fast
+ * 36 B/point fp32 SoA path; any other input keeps an fp64 copy so voxel keys stay exact. */
+int vg_cloud_create(vg_ctx* ctx, const double* xyz, const double* cov, int64_t n,
+                    vg_cloud** out);
+int vg_cloud_info(const vg_cloud* cloud, int64_t* n, int32_t* has_cov, int32_t* exact_fp32);
+int vg_cloud_destroy(vg_cloud* cloud);
+
+/* ---- Gaussian voxel maps (GaussianVoxelMap: registration.py:29-71) --------------------- */
+/* replaces build_voxelmap (registration.py:74-98); exported arrays are bit-identical */
+int vg_map_build(vg_ctx* ctx, const vg_cloud* cloud, double resolution, vg_map** out);
+/* adopt reference arrays (GaussianVoxelMap.__init__, registration.py:36-42); row = index */
+int vg_map_from_arrays(vg_ctx* ctx, double resolution, const int64_t* keys,
+                       const double* means, const double* covs, const int64_t* counts,
+                       int64_t m, vg_map** out);
+int vg_map_info(const vg_map* map, int64_t* m, double* resolution, int64_t* table_capacity);
+/* any output pointer may be NULL */
+int vg_map_export(vg_ctx* ctx, const vg_map* map, int64_t* keys, double* means, double* covs,
+                  int64_t* counts);
+int vg_map_destroy(vg_map* map);
+
+/* ---- correspondence lookup ------------------------------------------------------------- */
+/* replaces GaussianVoxelMap.lookup (registration.py:47-55): row per point or -1 */
+int vg_map_lookup(vg_ctx* ctx, const vg_map* map, const double* xyz, int64_t n,
+                  int64_t* rows_out, int64_t* hits_out);
+/* transform + lookup of a device cloud: overlap_rate (registration.py:168-173) and the
+ * hit count of _try_binary_factor (odometry.py:335-346); rows_out may be NULL */
+int vg_cloud_lookup(vg_ctx* ctx, const vg_cloud* cloud, const vg_map* map, const double T[12],
+                    int64_t* rows_out, int64_t* hits_out);
+
+/* ---- per-point terms ------------------------------------------------------------------- */
+/* replaces match_terms (registration.py:146-157).  Per source point (n rows, miss rows are
+ * zero): rows (n), moved (n x 3), d (n x 3), weight (n x 3 x 3), wd (n x 3).  The caller
+ * compacts by rows >= 0 to obtain MatchTerms.  cost/inliers are the fixed-order sums. */
+int vg_match_terms(vg_ctx* ctx, const vg_cloud* cloud, const vg_map* map, const double T[12],
+                   int64_t* rows, double* moved, double* d, double* weight, double* wd,
+                   double* cost, int64_t* inliers);
+
+/* ---- batched linearization (the hot path) ---------------------------------------------- */
+/* A batch is the set of MatchingCostFactors of one graph (factor_graph.py:209-308); it is
+ * flattened once into (factor, chunk) work items resident in HBM. */
+int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t num_factors,
+                    vg_batch** out);
+int vg_batch_info(const vg_batch* batch, int64_t* num_factors, int64_t* num_items,
+                  int64_t* num_points);
+int vg_batch_destroy(vg_batch* batch);
+
+/* explicit transforms: T_ij = T_j^-1 T_i per factor (registration.py:264), F x 12 host
+ * doubles.  out: F x record(mode) host doubles.  One call = match_terms +
+ * linearize_from_terms (registration.py:146-157,207-248) for every factor. */
+int vg_batch_linearize(vg_batch* batch, const double* T_host, int mode, double* out_host);
+
+/* pose-table mode: poses V x 8 (quat xyzw, t, pad).  T_ij is composed on the device from
+ * var_source / var_target exactly as pose_compose(pose_inverse(t_j), t_i). */
+int vg_batch_linearize_poses(vg_batch* batch, const double* poses_host, int64_t num_poses,
+                             int mode, double* out_host);
+
+/* device-resident variant: all pointers are device pointers on ctx's device; no host sync.
+ * poses_dev may be NULL to reuse the poses of the previous call. */
+int vg_batch_linearize_poses_device(vg_batch* batch, const double* poses_dev,
+                                    int64_t num_poses, int mode, double* out_dev);
+/* the three stages of vg_batch_linearize_poses_device, exposed separately so a caller can
+ * time each kernel with events on the same stream: K-compose (T_ij from the pose table),
+ * K4 (fused per-point accumulate into per-item partials), K5 (fixed-order finalize). */
+int vg_batch_compose_device(vg_batch* batch, const double* poses_dev, int64_t num_poses);
+int vg_batch_accumulate_device(vg_batch* batch, int mode);
+int vg_batch_finalize_device(vg_batch* batch, int mode, double* out_dev);
+/* capture compose + accumulate + finalize into a CUDA graph and replay it */
+int vg_batch_graph_capture(vg_batch* batch, const double* poses_dev, int64_t num_poses,
+                           int mode, double* out_dev);
+int vg_batch_graph_launch(vg_batch* batch);
+
+/* ---- preprocessing (preprocess.py:122-164) --------------------------------------------- */
+/* replaces knn_search (preprocess.py:122-139): exact k nearest (self included), ordered by
+ * (squared distance, index).  Returns VG_ERR_TOO_SPARSE when n < k. */
+int vg_knn(vg_ctx* ctx, const vg_cloud* cloud, int32_t k, int64_t* neighbors_out);
+/* replaces estimate_covariances (preprocess.py:142-164): plane-regularised covariances */
+int vg_covariances(vg_ctx* ctx, const vg_cloud* cloud, const int64_t* neighbors, int32_t k,
+                   double plane_eps, double* covs_out, uint8_t* degenerate_out);
+/* fused kNN + covariance on a device cloud; results stay on the device and are attached
+ * to the cloud (so vg_map_build / linearization use them without a host round trip);
+ * neighbors_out / covs_out / degenerate_out may be NULL. */
+int vg_cloud_estimate_covariances(vg_ctx* ctx, vg_cloud* cloud, int32_t k, double plane_eps,
+                                  int64_t* neighbors_out, double* covs_out,
+                                  uint8_t* degenerate_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VGICP_H_ */

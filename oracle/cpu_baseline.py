@@ -1,0 +1,110 @@
+"""CPU baseline of the reference path (test/bench infrastructure; never a product path).
+
+Times the oracle (a restatement of limapper's NumPy VGICP linearization, the reference's
+own CPU implementation of this path) on a bounded sample of the global-mapping workload,
+on all host cores: factors are split across a fork()ed process pool (the reference is
+single-threaded NumPy; processes are how it uses more cores).
+
+Sample: every factor whose target is one of the first ``n_targets`` submaps.  Its inputs are
+recomputed on the CPU with the oracle (kNN + covariances of the target scans, covariances
+of the source subsamples against their full scans, voxel maps at the workload resolution).
+"""
+
+from __future__ import annotations
+
+import multiprocessing as mp
+import os
+import time
+
+import numpy as np
+from scipy.spatial import cKDTree
+
+from . import vgicp_oracle as O
+
+_SAMPLE = None
+
+
+def knn_query(full: np.ndarray, queries_idx: np.ndarray, k: int) -> np.ndarray:
+    """kNN (self included) of a subset of a scan's points among the whole scan, ordered by
+    (d2, index) like knn_search (preprocess.py:122-139)."""
+    q = full[queries_idx]
+    _, cand = cKDTree(full).query(q, k=k)
+    cand = np.asarray(cand, np.int64).reshape(len(q), k)
+    diff = full[cand] - q[:, None, :]
+    sq = diff * diff
+    d2 = (sq[..., 0] + sq[..., 2]) + sq[..., 1]
+    order = np.lexsort((cand, d2), axis=1)
+    return np.take_along_axis(cand, order, axis=1)
+
+
+def build_sample(wl, n_targets: int = 16, knn: int = 10):
+    targets = np.arange(min(n_targets, wl.n_submaps))
+    fids = np.flatnonzero(np.isin(wl.pairs[:, 1], targets))
+    maps = {}
+    for j in targets:
+        s = wl.scans[j]
+        covs, _ = O.estimate_covariances(s, O.knn_search(s, knn))
+        maps[int(j)] = O.build_voxelmap(s, covs, wl.resolution)
+    sources = {}
+    for i in np.unique(wl.pairs[fids, 0]):
+        s, sel = wl.scans[i], wl.source_index[i]
+        covs, _ = O.estimate_covariances(s, knn_query(s, sel, knn))
+        sources[int(i)] = (s[sel], covs)
+    R, t = O.relative_transforms(wl.pose_table, wl.pairs[fids, 0], wl.pairs[fids, 1])
+    return {"fids": fids, "pairs": wl.pairs[fids], "maps": maps, "sources": sources, "R": R,
+            "t": t, "points": int(sum(len(sources[int(i)][0]) for i in wl.pairs[fids, 0]))}
+
+
+def _work(chunk):
+    s = _SAMPLE
+    n = 0
+    for f in chunk:
+        i, j = s["pairs"][f]
+        pts, covs = s["sources"][int(i)]
+        try:
+            O.linearize(pts, covs, s["maps"][int(j)], s["R"][f], s["t"][f])
+        except ValueError:  # degenerate factor: still evaluated
+            pass
+        n += len(pts)
+    return n
+
+
+class Runner:
+    """Keeps a fork()ed pool alive across timed steps."""
+
+    def __init__(self, sample, processes: int | None = None):
+        global _SAMPLE
+        _SAMPLE = sample
+        self.sample = sample
+        self.processes = processes or os.cpu_count() or 1
+        F = len(sample["pairs"])
+        n_chunks = min(F, self.processes * 4)
+        self.chunks = [c for c in np.array_split(np.arange(F), n_chunks) if len(c)]
+        ctx = mp.get_context("fork")
+        self.pool = ctx.Pool(self.processes) if self.processes > 1 else None
+
+    def step(self) -> int:
+        if self.pool is None:
+            return sum(_work(c) for c in self.chunks)
+        return sum(self.pool.map(_work, self.chunks))
+
+    def close(self):
+        if self.pool is not None:
+            self.pool.close()
+            self.pool.join()
+
+
+def time_sample(sample, steps: int, warmup: int = 1, processes: int | None = None):
+    """Returns (corr_per_s, seconds_per_step, processes)."""
+    r = Runner(sample, processes)
+    try:
+        for _ in range(warmup):
+            r.step()
+        t0 = time.perf_counter()
+        n = 0
+        for _ in range(steps):
+            n += r.step()
+        dt = time.perf_counter() - t0
+    finally:
+        r.close()
+    return n / dt, dt / max(steps, 1), r.processes

@@ -1,0 +1,338 @@
+"""ctypes binding of libvgicp.so (include/vgicp.h).
+
+The shared library is the only compute path: importing a product module never falls back
+to NumPy.  If the library is missing or no B200 is visible, the first call raises
+:class:`VgicpUnavailable` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+import weakref
+from ctypes import POINTER, c_double, c_int, c_int32, c_int64, c_uint8, c_void_p, c_char_p
+from pathlib import Path
+
+import numpy as np
+
+from . import errors
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvgicp.so"
+
+VG_OK = 0
+VG_ERR_INVALID = 1
+VG_ERR_CUDA = 2
+VG_ERR_DEGENERATE = 3
+VG_ERR_TOO_SPARSE = 4
+VG_ERR_NOMEM = 5
+
+MODE_LINEARIZE = 0
+MODE_COST = 1
+MODE_COMPACT = 2
+RECORD_SIZE = {MODE_LINEARIZE: 92, MODE_COST: 2, MODE_COMPACT: 29}
+FACTOR_UNARY = 1
+
+
+class VgicpUnavailable(RuntimeError):
+    """libvgicp.so is not built or cannot run here (it needs an sm_100 GPU)."""
+
+
+class vg_factor_spec(ctypes.Structure):
+    _fields_ = [("source", c_void_p), ("target", c_void_p), ("flags", c_int32),
+                ("min_inliers", c_int32), ("var_source", c_int32), ("var_target", c_int32)]
+
+
+_P_D = POINTER(c_double)
+_P_I64 = POINTER(c_int64)
+_P_U8 = POINTER(c_uint8)
+_PP = POINTER(c_void_p)
+
+_SIGNATURES = {
+    "vg_abi_version": ([], c_int),
+    "vg_last_error": ([], c_char_p),
+    "vg_ctx_create": ([c_int, _PP], c_int),
+    "vg_ctx_destroy": ([c_void_p], c_int),
+    "vg_ctx_set_stream": ([c_void_p, c_void_p], c_int),
+    "vg_ctx_synchronize": ([c_void_p], c_int),
+    "vg_ctx_launch_count": ([c_void_p, _P_I64], c_int),
+    "vg_pack_voxel_keys": ([c_void_p, _P_D, c_int64, c_double, _P_I64], c_int),
+    "vg_cloud_create": ([c_void_p, _P_D, _P_D, c_int64, _PP], c_int),
+    "vg_cloud_info": ([c_void_p, _P_I64, POINTER(c_int32), POINTER(c_int32)], c_int),
+    "vg_cloud_destroy": ([c_void_p], c_int),
+    "vg_map_build": ([c_void_p, c_void_p, c_double, _PP], c_int),
+    "vg_map_from_arrays": ([c_void_p, c_double, _P_I64, _P_D, _P_D, _P_I64, c_int64, _PP], c_int),
+    "vg_map_info": ([c_void_p, _P_I64, _P_D, _P_I64], c_int),
+    "vg_map_export": ([c_void_p, c_void_p, _P_I64, _P_D, _P_D, _P_I64], c_int),
+    "vg_map_destroy": ([c_void_p], c_int),
+    "vg_map_lookup": ([c_void_p, c_void_p, _P_D, c_int64, _P_I64, _P_I64], c_int),
+    "vg_cloud_lookup": ([c_void_p, c_void_p, c_void_p, _P_D, _P_I64, _P_I64], c_int),
+    "vg_match_terms": ([c_void_p, c_void_p, c_void_p, _P_D, _P_I64, _P_D, _P_D, _P_D, _P_D,
+                        _P_D, _P_I64], c_int),
+    "vg_batch_create": ([c_void_p, POINTER(vg_factor_spec), c_int64, _PP], c_int),
+    "vg_batch_info": ([c_void_p, _P_I64, _P_I64, _P_I64], c_int),
+    "vg_batch_destroy": ([c_void_p], c_int),
+    "vg_batch_linearize": ([c_void_p, _P_D, c_int, _P_D], c_int),
+    "vg_batch_linearize_poses": ([c_void_p, _P_D, c_int64, c_int, _P_D], c_int),
+    "vg_batch_linearize_poses_device": ([c_void_p, c_void_p, c_int64, c_int, c_void_p], c_int),
+    "vg_batch_compose_device": ([c_void_p, c_void_p, c_int64], c_int),
+    "vg_batch_accumulate_device": ([c_void_p, c_int], c_int),
+    "vg_batch_finalize_device": ([c_void_p, c_int, c_void_p], c_int),
+    "vg_batch_graph_capture": ([c_void_p, c_void_p, c_int64, c_int, c_void_p], c_int),
+    "vg_batch_graph_launch": ([c_void_p], c_int),
+    "vg_knn": ([c_void_p, c_void_p, c_int32, _P_I64], c_int),
+    "vg_covariances": ([c_void_p, c_void_p, _P_I64, c_int32, c_double, _P_D, _P_U8], c_int),
+    "vg_cloud_estimate_covariances": ([c_void_p, c_void_p, c_int32, c_double, _P_I64, _P_D,
+                                       _P_U8], c_int),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: str | os.PathLike | None = None):
+    """Load libvgicp.so and declare every entry point (no GPU needed for this step)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise VgicpUnavailable(
+                f"{p} is missing: build it with `make` or `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (the CUDA library is the only compute path)")
+        lib = ctypes.CDLL(str(p))
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        if lib.vg_abi_version() != 1:
+            raise VgicpUnavailable("libvgicp ABI version mismatch")
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a C-ABI status code to the reference's exception types."""
+    if rc == VG_OK:
+        return
+    msg = (_lib.vg_last_error() or b"").decode(errors="replace") if _lib else ""
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == VG_ERR_DEGENERATE:
+        raise errors.DegenerateConstraint(msg)
+    if rc == VG_ERR_TOO_SPARSE:
+        raise errors.FrameTooSparse(msg)
+    if rc == VG_ERR_INVALID:
+        raise ValueError(msg)
+    if rc == VG_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise VgicpUnavailable(msg)
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(_P_D) if a is not None else None
+
+
+def iptr(a: np.ndarray):
+    return a.ctypes.data_as(_P_I64) if a is not None else None
+
+
+def f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Context:
+    """One CUDA device context of the library (one per process and device)."""
+
+    def __init__(self, device: int = 0):
+        lib = load_library()
+        h = c_void_p()
+        check(lib.vg_ctx_create(int(device), ctypes.byref(h)), "vg_ctx_create")
+        self.lib = lib
+        self.device = int(device)
+        self.handle = h
+        self._fin = weakref.finalize(self, lib.vg_ctx_destroy, h)
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        check(self.lib.vg_ctx_set_stream(self.handle, c_void_p(stream_ptr or 0)))
+
+    def synchronize(self) -> None:
+        check(self.lib.vg_ctx_synchronize(self.handle))
+
+    def launch_count(self) -> int:
+        n = c_int64()
+        check(self.lib.vg_ctx_launch_count(self.handle, ctypes.byref(n)))
+        return int(n.value)
+
+
+_contexts: dict[int, Context] = {}
+_default_device = int(os.environ.get("VGICP_DEVICE", "0"))
+
+
+def set_device(device: int) -> None:
+    """Select the CUDA device used by subsequent calls (e.g. LOCAL_RANK under torchrun)."""
+    global _default_device
+    _default_device = int(device)
+
+
+def context(device: int | None = None) -> Context:
+    dev = _default_device if device is None else int(device)
+    ctx = _contexts.get(dev)
+    if ctx is None:
+        ctx = Context(dev)
+        _contexts[dev] = ctx
+    return ctx
+
+
+class DeviceCloud:
+    """Device copy of a Frame's points (+ covariances): 36 B/point fp32 SoA in HBM."""
+
+    def __init__(self, points, covs=None, ctx: Context | None = None):
+        ctx = ctx or context()
+        pts = f64(points).reshape(-1, 3)
+        cov = None if covs is None else f64(covs).reshape(-1, 9)
+        if cov is not None and cov.shape[0] != pts.shape[0]:
+            raise ValueError("covariances and points differ in length")
+        h = c_void_p()
+        check(ctx.lib.vg_cloud_create(ctx.handle, dptr(pts), dptr(cov), pts.shape[0],
+                                      ctypes.byref(h)), "vg_cloud_create")
+        self.ctx = ctx
+        self.handle = h
+        self.n = pts.shape[0]
+        self.has_cov = cov is not None
+        self._fin = weakref.finalize(self, ctx.lib.vg_cloud_destroy, h)
+
+    def estimate_covariances(self, k: int, plane_eps: float, want_neighbors=True):
+        """Fused device kNN + covariance; results stay attached to this cloud."""
+        lib = self.ctx.lib
+        nbrs = np.empty((self.n, k), dtype=np.int64) if want_neighbors else None
+        covs = np.empty((self.n, 3, 3))
+        degen = np.empty(self.n, dtype=np.uint8)
+        check(lib.vg_cloud_estimate_covariances(self.ctx.handle, self.handle, int(k),
+                                                float(plane_eps), iptr(nbrs), dptr(covs),
+                                                degen.ctypes.data_as(_P_U8)))
+        self.has_cov = True
+        return nbrs, covs, degen.astype(bool)
+
+
+class DeviceMap:
+    """Device Gaussian voxel map: 64 B hash slots + the reference fp64 arrays."""
+
+    def __init__(self, handle, ctx: Context):
+        self.ctx = ctx
+        self.handle = handle
+        m = c_int64()
+        res = c_double()
+        cap = c_int64()
+        check(ctx.lib.vg_map_info(handle, ctypes.byref(m), ctypes.byref(res), ctypes.byref(cap)))
+        self.m = int(m.value)
+        self.resolution = float(res.value)
+        self.capacity = int(cap.value)
+        self._fin = weakref.finalize(self, ctx.lib.vg_map_destroy, handle)
+
+    @classmethod
+    def build(cls, cloud: DeviceCloud, resolution: float) -> "DeviceMap":
+        h = c_void_p()
+        check(cloud.ctx.lib.vg_map_build(cloud.ctx.handle, cloud.handle, float(resolution),
+                                         ctypes.byref(h)), "vg_map_build")
+        return cls(h, cloud.ctx)
+
+    @classmethod
+    def from_arrays(cls, resolution, keys, means, covs, counts, ctx: Context | None = None):
+        ctx = ctx or context()
+        keys = np.ascontiguousarray(keys, dtype=np.int64)
+        m = keys.shape[0]
+        means = f64(means).reshape(m, 3)
+        covs = f64(covs).reshape(m, 9)
+        counts = None if counts is None else np.ascontiguousarray(counts, dtype=np.int64)
+        h = c_void_p()
+        check(ctx.lib.vg_map_from_arrays(ctx.handle, float(resolution), iptr(keys), dptr(means),
+                                         dptr(covs), iptr(counts), m, ctypes.byref(h)),
+              "vg_map_from_arrays")
+        return cls(h, ctx)
+
+    def export(self):
+        m = self.m
+        keys = np.empty(m, dtype=np.int64)
+        means = np.empty((m, 3))
+        covs = np.empty((m, 3, 3))
+        counts = np.empty(m, dtype=np.int64)
+        check(self.ctx.lib.vg_map_export(self.ctx.handle, self.handle, iptr(keys), dptr(means),
+                                         dptr(covs), iptr(counts)))
+        return keys, means, covs, counts
+
+
+class DeviceBatch:
+    """A flattened set of matching-cost factors resident in HBM (vg_batch)."""
+
+    def __init__(self, clouds, maps, unary, min_inliers, var_source=None, var_target=None,
+                 ctx: Context | None = None):
+        ctx = ctx or context()
+        F = len(clouds)
+        specs = (vg_factor_spec * max(F, 1))()
+        for f in range(F):
+            s = specs[f]
+            s.source = clouds[f].handle.value
+            s.target = maps[f].handle.value
+            s.flags = FACTOR_UNARY if unary[f] else 0
+            s.min_inliers = int(min_inliers[f])
+            s.var_source = int(var_source[f]) if var_source is not None else 0
+            s.var_target = int(var_target[f]) if var_target is not None else 0
+        h = c_void_p()
+        check(ctx.lib.vg_batch_create(ctx.handle, specs, F, ctypes.byref(h)), "vg_batch_create")
+        self.ctx = ctx
+        self.handle = h
+        self.num_factors = F
+        # keep the device objects alive as long as the batch references them
+        self._keep = (list(clouds), list(maps))
+        nf, ni, npnt = c_int64(), c_int64(), c_int64()
+        check(ctx.lib.vg_batch_info(h, ctypes.byref(nf), ctypes.byref(ni), ctypes.byref(npnt)))
+        self.num_items = int(ni.value)
+        self.num_points = int(npnt.value)
+        self._fin = weakref.finalize(self, ctx.lib.vg_batch_destroy, h)
+
+    def linearize(self, T: np.ndarray, mode: int = MODE_LINEARIZE) -> np.ndarray:
+        T = f64(T).reshape(self.num_factors, 12)
+        out = np.empty((self.num_factors, RECORD_SIZE[mode]))
+        check(self.ctx.lib.vg_batch_linearize(self.handle, dptr(T), int(mode), dptr(out)),
+              "vg_batch_linearize")
+        return out
+
+    def linearize_poses(self, poses: np.ndarray, mode: int = MODE_LINEARIZE,
+                        out: np.ndarray | None = None) -> np.ndarray:
+        poses = f64(poses).reshape(-1, 8)
+        if out is None:
+            out = np.empty((self.num_factors, RECORD_SIZE[mode]))
+        check(self.ctx.lib.vg_batch_linearize_poses(self.handle, dptr(poses), poses.shape[0],
+                                                    int(mode), dptr(out)),
+              "vg_batch_linearize_poses")
+        return out
+
+    def linearize_poses_device(self, poses_dev_ptr: int | None, num_poses: int, mode: int,
+                               out_dev_ptr: int) -> None:
+        check(self.ctx.lib.vg_batch_linearize_poses_device(
+            self.handle, c_void_p(poses_dev_ptr or 0), int(num_poses), int(mode),
+            c_void_p(out_dev_ptr)), "vg_batch_linearize_poses_device")
+
+    def compose_device(self, poses_dev_ptr: int, num_poses: int) -> None:
+        check(self.ctx.lib.vg_batch_compose_device(self.handle, c_void_p(poses_dev_ptr),
+                                                   int(num_poses)))
+
+    def accumulate_device(self, mode: int) -> None:
+        check(self.ctx.lib.vg_batch_accumulate_device(self.handle, int(mode)))
+
+    def finalize_device(self, mode: int, out_dev_ptr: int) -> None:
+        check(self.ctx.lib.vg_batch_finalize_device(self.handle, int(mode),
+                                                    c_void_p(out_dev_ptr)))
+
+    def capture_graph(self, poses_dev_ptr: int, num_poses: int, mode: int, out_dev_ptr: int):
+        check(self.ctx.lib.vg_batch_graph_capture(self.handle, c_void_p(poses_dev_ptr),
+                                                  int(num_poses), int(mode),
+                                                  c_void_p(out_dev_ptr)))
+
+    def launch_graph(self) -> None:
+        check(self.ctx.lib.vg_batch_graph_launch(self.handle))

@@ -1,0 +1,662 @@
+// capi.cu — the extern "C" boundary (include/vgicp.h): handle lifetime, host<->device
+// staging, batch flattening, and status-code error reporting.  No exception crosses the ABI.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "vgicp.h"
+
+using namespace vg;
+
+static thread_local std::string g_err;
+
+void vg_set_error(const std::string& msg) { g_err = msg; }
+
+int vg_cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? VG_ERR_NOMEM : VG_ERR_CUDA;
+}
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define VG_CHECK(x)              \
+  do {                           \
+    int _rc = (x);               \
+    if (_rc != VG_OK) return _rc; \
+  } while (0)
+
+template <class T>
+static int dalloc(vg_ctx* ctx, T** p, size_t count) {
+  *p = nullptr;
+  if (count == 0) return VG_OK;
+  VG_CUDA(cudaMallocAsync((void**)p, sizeof(T) * count, ctx->stream));
+  return VG_OK;
+}
+template <class T>
+static void dfree(vg_ctx* ctx, T*& p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+  p = nullptr;
+}
+
+int vg_scratch(vg_ctx* ctx, size_t bytes, void** out) {
+  if (bytes > ctx->scratch_bytes) {
+    if (ctx->scratch) cudaFreeAsync(ctx->scratch, ctx->stream);
+    size_t nb = std::max<size_t>(bytes, 4096);
+    VG_CUDA(cudaMallocAsync(&ctx->scratch, nb, ctx->stream));
+    ctx->scratch_bytes = nb;
+  }
+  *out = ctx->scratch;
+  return VG_OK;
+}
+
+static int h2d(vg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (!bytes) return VG_OK;
+  VG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return VG_OK;
+}
+static int d2h_sync(vg_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  if (bytes) VG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return VG_OK;
+}
+
+extern "C" {
+
+int vg_abi_version(void) { return VGICP_ABI_VERSION; }
+
+const char* vg_last_error(void) { return g_err.c_str(); }
+
+int vg_ctx_create(int device, vg_ctx** out) {
+  if (!out) return fail(VG_ERR_INVALID, "out is null");
+  *out = nullptr;
+  int ndev = 0;
+  VG_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(VG_ERR_INVALID, "no such CUDA device");
+  VG_CUDA(cudaSetDevice(device));
+  int major = 0;
+  VG_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major != 10) return fail(VG_ERR_CUDA, "libvgicp is built for sm_100a (B200) only");
+  vg_ctx* c = new vg_ctx();
+  c->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return vg_cuda_fail(e, "cudaStreamCreateWithFlags");
+  }
+  c->stream = c->own_stream;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  *out = c;
+  return VG_OK;
+}
+
+int vg_ctx_destroy(vg_ctx* ctx) {
+  if (!ctx) return VG_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->scratch) cudaFreeAsync(ctx->scratch, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return VG_OK;
+}
+
+int vg_ctx_set_stream(vg_ctx* ctx, void* stream) {
+  if (!ctx) return fail(VG_ERR_INVALID, "ctx is null");
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own_stream;
+  return VG_OK;
+}
+
+int vg_ctx_synchronize(vg_ctx* ctx) {
+  if (!ctx) return fail(VG_ERR_INVALID, "ctx is null");
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return VG_OK;
+}
+
+int vg_ctx_launch_count(const vg_ctx* ctx, int64_t* count) {
+  if (!ctx || !count) return fail(VG_ERR_INVALID, "null argument");
+  *count = ctx->launches;
+  return VG_OK;
+}
+
+// ---- keys -------------------------------------------------------------------------------
+int vg_pack_voxel_keys(vg_ctx* ctx, const double* xyz, int64_t n, double res, int64_t* keys_out) {
+  if (!ctx || (n && (!xyz || !keys_out))) return fail(VG_ERR_INVALID, "null argument");
+  if (!(res > 0.0)) return fail(VG_ERR_INVALID, "resolution must be positive");
+  if (n == 0) return VG_OK;
+  double* dx = nullptr;
+  long long* dk = nullptr;
+  VG_CHECK(dalloc(ctx, &dx, 3 * n));
+  VG_CHECK(dalloc(ctx, &dk, n));
+  VG_CHECK(h2d(ctx, dx, xyz, sizeof(double) * 3 * n));
+  VG_CHECK(launch_pack_keys(ctx, dx, n, res, dk));
+  int rc = d2h_sync(ctx, keys_out, dk, sizeof(long long) * n);
+  dfree(ctx, dx);
+  dfree(ctx, dk);
+  return rc;
+}
+
+// ---- clouds -----------------------------------------------------------------------------
+int vg_cloud_create(vg_ctx* ctx, const double* xyz, const double* cov, int64_t n,
+                    vg_cloud** out) {
+  if (!ctx || !out || n < 0 || (n && !xyz)) return fail(VG_ERR_INVALID, "invalid cloud arguments");
+  VG_CUDA(cudaSetDevice(ctx->device));
+  vg_cloud* c = new vg_cloud();
+  c->ctx = ctx;
+  c->n = n;
+  c->has_cov = cov != nullptr;
+  bool exact = true;
+  for (int64_t i = 0; i < 3 * n && exact; ++i) exact = ((double)(float)xyz[i] == xyz[i]);
+  c->exact32 = exact;
+  int rc = VG_OK;
+  if (n) {
+    if ((rc = dalloc(ctx, &c->xyz64, 3 * n)) || (rc = dalloc(ctx, &c->a, n)) ||
+        (cov && ((rc = dalloc(ctx, &c->cov64, 9 * n)) || (rc = dalloc(ctx, &c->c0, n)) ||
+                 (rc = dalloc(ctx, &c->c1, n)) || (rc = dalloc(ctx, &c->c2, n)))) ||
+        (rc = h2d(ctx, c->xyz64, xyz, sizeof(double) * 3 * n)) ||
+        (cov && (rc = h2d(ctx, c->cov64, cov, sizeof(double) * 9 * n))) ||
+        (rc = launch_cloud_pack(ctx, c))) {
+      vg_cloud_destroy(c);
+      return rc;
+    }
+  }
+  *out = c;
+  return VG_OK;
+}
+
+int vg_cloud_info(const vg_cloud* c, int64_t* n, int32_t* has_cov, int32_t* exact32) {
+  if (!c) return fail(VG_ERR_INVALID, "cloud is null");
+  if (n) *n = c->n;
+  if (has_cov) *has_cov = c->has_cov;
+  if (exact32) *exact32 = c->exact32;
+  return VG_OK;
+}
+
+int vg_cloud_destroy(vg_cloud* c) {
+  if (!c) return VG_OK;
+  vg_ctx* ctx = c->ctx;
+  dfree(ctx, c->a);
+  dfree(ctx, c->c0);
+  dfree(ctx, c->c1);
+  dfree(ctx, c->c2);
+  dfree(ctx, c->xyz64);
+  dfree(ctx, c->cov64);
+  delete c;
+  return VG_OK;
+}
+
+// ---- maps -------------------------------------------------------------------------------
+int vg_map_build(vg_ctx* ctx, const vg_cloud* cloud, double res, vg_map** out) {
+  if (!ctx || !cloud || !out) return fail(VG_ERR_INVALID, "null argument");
+  if (!(res > 0.0)) return fail(VG_ERR_INVALID, "resolution must be positive");
+  if (cloud->n > 0 && !cloud->has_cov)  // registration.py:80-81
+    return fail(VG_ERR_INVALID, "frame needs covariances before voxelization");
+  if (cloud->n >= (1LL << 31)) return fail(VG_ERR_INVALID, "cloud too large for one map");
+  vg_map* m = new vg_map();
+  m->ctx = ctx;
+  int rc = launch_map_build(ctx, cloud, res, m);
+  if (rc) {
+    vg_map_destroy(m);
+    return rc;
+  }
+  *out = m;
+  return VG_OK;
+}
+
+int vg_map_from_arrays(vg_ctx* ctx, double res, const int64_t* keys, const double* means,
+                       const double* covs, const int64_t* counts, int64_t m, vg_map** out) {
+  if (!ctx || !out || m < 0 || (m && (!keys || !means || !covs)))
+    return fail(VG_ERR_INVALID, "invalid map arrays");
+  if (!(res > 0.0)) return fail(VG_ERR_INVALID, "resolution must be positive");
+  for (int64_t i = 1; i < m; ++i)
+    if (keys[i] <= keys[i - 1])
+      return fail(VG_ERR_INVALID, "GaussianVoxelMap keys must be strictly increasing");
+  vg_map* mp = new vg_map();
+  mp->ctx = ctx;
+  mp->m = m;
+  mp->res = res;
+  int rc = VG_OK;
+  if (m) {
+    std::vector<long long> cnt(m, 1);
+    if (counts) std::copy(counts, counts + m, cnt.begin());
+    if ((rc = dalloc(ctx, &mp->keys, m)) || (rc = dalloc(ctx, &mp->means, 3 * m)) ||
+        (rc = dalloc(ctx, &mp->covs, 9 * m)) || (rc = dalloc(ctx, &mp->counts, m)) ||
+        (rc = h2d(ctx, mp->keys, keys, sizeof(long long) * m)) ||
+        (rc = h2d(ctx, mp->means, means, sizeof(double) * 3 * m)) ||
+        (rc = h2d(ctx, mp->covs, covs, sizeof(double) * 9 * m)) ||
+        (rc = h2d(ctx, mp->counts, cnt.data(), sizeof(long long) * m)) ||
+        (rc = cudaStreamSynchronize(ctx->stream) ? VG_ERR_CUDA : VG_OK)) {
+      vg_map_destroy(mp);
+      return rc;
+    }
+  }
+  if ((rc = launch_map_finish(ctx, mp))) {
+    vg_map_destroy(mp);
+    return rc;
+  }
+  *out = mp;
+  return VG_OK;
+}
+
+int vg_map_info(const vg_map* m, int64_t* size, double* res, int64_t* cap) {
+  if (!m) return fail(VG_ERR_INVALID, "map is null");
+  if (size) *size = m->m;
+  if (res) *res = m->res;
+  if (cap) *cap = m->capacity;
+  return VG_OK;
+}
+
+int vg_map_export(vg_ctx* ctx, const vg_map* m, int64_t* keys, double* means, double* covs,
+                  int64_t* counts) {
+  if (!ctx || !m) return fail(VG_ERR_INVALID, "null argument");
+  const long long n = m->m;
+  if (n == 0) return VG_OK;
+  if (keys) VG_CUDA(cudaMemcpyAsync(keys, m->keys, sizeof(long long) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (means) VG_CUDA(cudaMemcpyAsync(means, m->means, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (covs) VG_CUDA(cudaMemcpyAsync(covs, m->covs, sizeof(double) * 9 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (counts) VG_CUDA(cudaMemcpyAsync(counts, m->counts, sizeof(long long) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return VG_OK;
+}
+
+int vg_map_destroy(vg_map* m) {
+  if (!m) return VG_OK;
+  vg_ctx* ctx = m->ctx;
+  dfree(ctx, m->table);
+  dfree(ctx, m->vox);
+  dfree(ctx, m->keys);
+  dfree(ctx, m->means);
+  dfree(ctx, m->covs);
+  dfree(ctx, m->counts);
+  delete m;
+  return VG_OK;
+}
+
+// ---- lookup / terms ---------------------------------------------------------------------
+static const double kIdentityT[12] = {1, 0, 0, 0, 1, 0, 0, 0, 1, 0, 0, 0};
+
+int vg_cloud_lookup(vg_ctx* ctx, const vg_cloud* cloud, const vg_map* map, const double T[12],
+                    int64_t* rows_out, int64_t* hits_out) {
+  if (!ctx || !cloud || !map || !T) return fail(VG_ERR_INVALID, "null argument");
+  const long long n = cloud->n;
+  void* scr = nullptr;
+  VG_CHECK(vg_scratch(ctx, 128, &scr));
+  double* dT = (double*)scr;
+  unsigned long long* dh = (unsigned long long*)((char*)scr + 96);
+  VG_CHECK(h2d(ctx, dT, T, 96));
+  VG_CUDA(cudaMemsetAsync(dh, 0, 8, ctx->stream));
+  long long* drows = nullptr;
+  if (rows_out) VG_CHECK(dalloc(ctx, &drows, n));
+  VG_CHECK(launch_lookup(ctx, cloud->view(), map->view(), dT, drows, dh));
+  unsigned long long hits = 0;
+  if (rows_out && n) VG_CUDA(cudaMemcpyAsync(rows_out, drows, sizeof(long long) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CHECK(d2h_sync(ctx, &hits, dh, 8));
+  dfree(ctx, drows);
+  if (hits_out) *hits_out = (int64_t)hits;
+  return VG_OK;
+}
+
+int vg_map_lookup(vg_ctx* ctx, const vg_map* map, const double* xyz, int64_t n, int64_t* rows_out,
+                  int64_t* hits_out) {
+  if (!ctx || !map || (n && !xyz)) return fail(VG_ERR_INVALID, "null argument");
+  if (n == 0) {
+    if (hits_out) *hits_out = 0;
+    return VG_OK;
+  }
+  vg_cloud* c = nullptr;
+  VG_CHECK(vg_cloud_create(ctx, xyz, nullptr, n, &c));
+  int rc = vg_cloud_lookup(ctx, c, map, kIdentityT, rows_out, hits_out);
+  vg_cloud_destroy(c);
+  return rc;
+}
+
+int vg_match_terms(vg_ctx* ctx, const vg_cloud* cloud, const vg_map* map, const double T[12],
+                   int64_t* rows, double* moved, double* d, double* weight, double* wd,
+                   double* cost, int64_t* inliers) {
+  if (!ctx || !cloud || !map || !T || !rows || !moved || !d || !weight || !wd)
+    return fail(VG_ERR_INVALID, "null argument");
+  if (!cloud->has_cov) return fail(VG_ERR_INVALID, "source frame has no covariances");
+  const long long n = cloud->n;
+  if (n == 0) {
+    if (cost) *cost = 0.0;
+    if (inliers) *inliers = 0;
+    return VG_OK;
+  }
+  const int nblocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  double *dT = nullptr, *dmoved = nullptr, *dd = nullptr, *dw = nullptr, *dwd = nullptr,
+         *pc = nullptr;
+  long long *drows = nullptr, *pi = nullptr;
+  VG_CHECK(dalloc(ctx, &dT, 12));
+  VG_CHECK(dalloc(ctx, &drows, n));
+  VG_CHECK(dalloc(ctx, &dmoved, 3 * n));
+  VG_CHECK(dalloc(ctx, &dd, 3 * n));
+  VG_CHECK(dalloc(ctx, &dw, 9 * n));
+  VG_CHECK(dalloc(ctx, &dwd, 3 * n));
+  VG_CHECK(dalloc(ctx, &pc, nblocks));
+  VG_CHECK(dalloc(ctx, &pi, nblocks));
+  VG_CHECK(h2d(ctx, dT, T, 96));
+  VG_CHECK(launch_terms(ctx, cloud->view(), map->view(), dT, drows, dmoved, dd, dw, dwd, pc, pi,
+                        nblocks));
+  std::vector<double> hc(nblocks);
+  std::vector<long long> hi(nblocks);
+  VG_CUDA(cudaMemcpyAsync(rows, drows, 8 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaMemcpyAsync(moved, dmoved, 24 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaMemcpyAsync(d, dd, 24 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaMemcpyAsync(weight, dw, 72 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaMemcpyAsync(wd, dwd, 24 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaMemcpyAsync(hc.data(), pc, 8 * nblocks, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CHECK(d2h_sync(ctx, hi.data(), pi, 8 * nblocks));
+  double cs = 0.0;
+  long long is = 0;
+  for (int b = 0; b < nblocks; ++b) cs += hc[b], is += hi[b];
+  if (cost) *cost = cs;
+  if (inliers) *inliers = is;
+  dfree(ctx, dT);
+  dfree(ctx, drows);
+  dfree(ctx, dmoved);
+  dfree(ctx, dd);
+  dfree(ctx, dw);
+  dfree(ctx, dwd);
+  dfree(ctx, pc);
+  dfree(ctx, pi);
+  return VG_OK;
+}
+
+// ---- batches ----------------------------------------------------------------------------
+int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batch** out) {
+  if (!ctx || !out || F < 0 || (F && !specs)) return fail(VG_ERR_INVALID, "invalid batch arguments");
+  if (F >= (1LL << 31)) return fail(VG_ERR_INVALID, "too many factors");
+  std::vector<const vg_cloud*> clouds;
+  std::vector<const vg_map*> maps;
+  std::vector<FactorDev> fac(F);
+  // dedupe clouds and maps (sort by handle address)
+  std::vector<std::pair<const void*, int64_t>> ck(F), mk(F);
+  for (int64_t f = 0; f < F; ++f) {
+    if (!specs[f].source || !specs[f].target) return fail(VG_ERR_INVALID, "factor without cloud/map");
+    if (!specs[f].source->has_cov && specs[f].source->n > 0)
+      return fail(VG_ERR_INVALID, "source frame has no covariances");
+    ck[f] = {specs[f].source, f};
+    mk[f] = {specs[f].target, f};
+  }
+  std::vector<int> cidx(F), midx(F);
+  auto dedupe = [&](std::vector<std::pair<const void*, int64_t>>& v, std::vector<int>& idx,
+                    auto& uniq) {
+    std::sort(v.begin(), v.end());
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (i == 0 || v[i].first != v[i - 1].first)
+        uniq.push_back((typename std::remove_reference<decltype(uniq)>::type::value_type)v[i].first);
+      idx[v[i].second] = (int)uniq.size() - 1;
+    }
+  };
+  dedupe(ck, cidx, clouds);
+  dedupe(mk, midx, maps);
+  long long max_var = -1;
+  for (int64_t f = 0; f < F; ++f) {
+    FactorDev& d = fac[f];
+    memset(&d, 0, sizeof(d));
+    d.T[0] = d.T[4] = d.T[8] = 1.0;
+    d.cloud = cidx[f];
+    d.map = midx[f];
+    d.flags = specs[f].flags;
+    d.min_inliers = specs[f].min_inliers;
+    d.var_source = specs[f].var_source;
+    d.var_target = specs[f].var_target;
+    max_var = std::max<long long>(max_var, std::max(d.var_source, d.var_target));
+  }
+  // work items: factors ordered by target map (L1/L2 reuse of the map's slots), chunks of
+  // <= kMaxChunk points, one warp per item
+  std::vector<int64_t> order(F);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int64_t a, int64_t b) { return fac[a].map < fac[b].map; });
+  std::vector<ItemDev> items;
+  long long npts = 0;
+  for (int64_t f : order) {
+    const long long n = specs[f].source->n;
+    npts += n;
+    fac[f].item_begin = (int)items.size();
+    long long nchunks = std::max<long long>(1, (n + kMaxChunk - 1) / kMaxChunk);
+    for (long long c = 0; c < nchunks; ++c) {
+      ItemDev it;
+      it.factor = (int)f;
+      it.begin = (int)(c * n / nchunks);
+      it.end = (int)((c + 1) * n / nchunks);
+      it.pad = 0;
+      items.push_back(it);
+    }
+    fac[f].item_count = (int)nchunks;
+  }
+  vg_batch* b = new vg_batch();
+  b->ctx = ctx;
+  b->F = F;
+  b->num_items = (long long)items.size();
+  b->num_points = npts;
+  b->num_clouds = (int)clouds.size();
+  b->num_maps = (int)maps.size();
+  b->max_var = (int)max_var;
+  b->host_factors = fac;
+  std::vector<CloudView> cv(clouds.size());
+  std::vector<MapView> mv(maps.size());
+  for (size_t i = 0; i < clouds.size(); ++i) cv[i] = clouds[i]->view();
+  for (size_t i = 0; i < maps.size(); ++i) mv[i] = maps[i]->view();
+  int rc = VG_OK;
+  if ((rc = dalloc(ctx, &b->factors, F)) || (rc = dalloc(ctx, &b->items, items.size())) ||
+      (rc = dalloc(ctx, &b->clouds, cv.size())) || (rc = dalloc(ctx, &b->maps, mv.size())) ||
+      (rc = dalloc(ctx, &b->partials, items.size() * kPartialStride)) ||
+      (rc = dalloc(ctx, &b->out, (size_t)F * VG_REC_LINEARIZE)) ||
+      (rc = h2d(ctx, b->factors, fac.data(), sizeof(FactorDev) * F)) ||
+      (rc = h2d(ctx, b->items, items.data(), sizeof(ItemDev) * items.size())) ||
+      (rc = h2d(ctx, b->clouds, cv.data(), sizeof(CloudView) * cv.size())) ||
+      (rc = h2d(ctx, b->maps, mv.data(), sizeof(MapView) * mv.size()))) {
+    vg_batch_destroy(b);
+    return rc;
+  }
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  *out = b;
+  return VG_OK;
+}
+
+int vg_batch_info(const vg_batch* b, int64_t* F, int64_t* items, int64_t* points) {
+  if (!b) return fail(VG_ERR_INVALID, "batch is null");
+  if (F) *F = b->F;
+  if (items) *items = b->num_items;
+  if (points) *points = b->num_points;
+  return VG_OK;
+}
+
+int vg_batch_destroy(vg_batch* b) {
+  if (!b) return VG_OK;
+  vg_ctx* ctx = b->ctx;
+  if (b->graph) cudaGraphExecDestroy(b->graph);
+  dfree(ctx, b->factors);
+  dfree(ctx, b->items);
+  dfree(ctx, b->clouds);
+  dfree(ctx, b->maps);
+  dfree(ctx, b->partials);
+  dfree(ctx, b->out);
+  dfree(ctx, b->poses);
+  cudaStreamSynchronize(ctx->stream);
+  delete b;
+  return VG_OK;
+}
+
+static size_t rec_of(int mode) {
+  return mode == VG_MODE_COST ? VG_REC_COST : mode == VG_MODE_COMPACT ? VG_REC_COMPACT : VG_REC_LINEARIZE;
+}
+
+static int run_device(vg_batch* b, int mode, double* out_dev) {
+  VG_CHECK(launch_linearize(b->ctx, b, mode == VG_MODE_COST ? 1 : 0));
+  VG_CHECK(launch_finalize(b->ctx, b, mode, out_dev));
+  return VG_OK;
+}
+
+int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_host) {
+  if (!b || (b->F && (!T_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
+  if (mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad mode");
+  if (b->F == 0) return VG_OK;
+  vg_ctx* ctx = b->ctx;
+  // scatter T_ij into the 128 B factor records (dst pitch 128, src pitch 96)
+  VG_CUDA(cudaMemcpy2DAsync(b->factors, sizeof(FactorDev), T_host, 12 * sizeof(double),
+                            12 * sizeof(double), (size_t)b->F, cudaMemcpyHostToDevice, ctx->stream));
+  VG_CHECK(run_device(b, mode, b->out));
+  return d2h_sync(ctx, out_host, b->out, sizeof(double) * rec_of(mode) * b->F);
+}
+
+static int ensure_poses(vg_batch* b, int64_t V) {
+  if (V > b->pose_cap) {
+    dfree(b->ctx, b->poses);
+    VG_CHECK(dalloc(b->ctx, &b->poses, 8 * (size_t)V));
+    b->pose_cap = V;
+  }
+  return VG_OK;
+}
+
+int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, int mode,
+                             double* out_host) {
+  if (!b || (b->F && (!poses_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
+  if (mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad mode");
+  if (b->F == 0) return VG_OK;
+  if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  VG_CHECK(ensure_poses(b, V));
+  VG_CHECK(h2d(b->ctx, b->poses, poses_host, sizeof(double) * 8 * V));
+  VG_CHECK(launch_compose(b->ctx, b, b->poses));
+  VG_CHECK(run_device(b, mode, b->out));
+  return d2h_sync(b->ctx, out_host, b->out, sizeof(double) * rec_of(mode) * b->F);
+}
+
+int vg_batch_linearize_poses_device(vg_batch* b, const double* poses_dev, int64_t V, int mode,
+                                    double* out_dev) {
+  if (!b || !out_dev) return fail(VG_ERR_INVALID, "null argument");
+  if (mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad mode");
+  if (b->F == 0) return VG_OK;
+  if (poses_dev) {
+    if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+    VG_CHECK(launch_compose(b->ctx, b, poses_dev));
+  }
+  return run_device(b, mode, out_dev);
+}
+
+int vg_batch_compose_device(vg_batch* b, const double* poses_dev, int64_t V) {
+  if (!b || !poses_dev) return fail(VG_ERR_INVALID, "null argument");
+  if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  return launch_compose(b->ctx, b, poses_dev);
+}
+
+int vg_batch_accumulate_device(vg_batch* b, int mode) {
+  if (!b || mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad arguments");
+  return launch_linearize(b->ctx, b, mode == VG_MODE_COST ? 1 : 0);
+}
+
+int vg_batch_finalize_device(vg_batch* b, int mode, double* out_dev) {
+  if (!b || !out_dev || mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad arguments");
+  return launch_finalize(b->ctx, b, mode, out_dev);
+}
+
+int vg_batch_graph_capture(vg_batch* b, const double* poses_dev, int64_t V, int mode,
+                           double* out_dev) {
+  if (!b || !out_dev) return fail(VG_ERR_INVALID, "null argument");
+  vg_ctx* ctx = b->ctx;
+  if (b->graph) {
+    cudaGraphExecDestroy(b->graph);
+    b->graph = nullptr;
+  }
+  cudaGraph_t g;
+  VG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = vg_batch_linearize_poses_device(b, poses_dev, V, mode, out_dev);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (rc) return rc;
+  if (e != cudaSuccess) return vg_cuda_fail(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&b->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return vg_cuda_fail(e, "cudaGraphInstantiate");
+  return VG_OK;
+}
+
+int vg_batch_graph_launch(vg_batch* b) {
+  if (!b || !b->graph) return fail(VG_ERR_INVALID, "no captured graph");
+  VG_CUDA(cudaGraphLaunch(b->graph, b->ctx->stream));
+  b->ctx->launches += 3;
+  return VG_OK;
+}
+
+// ---- preprocessing ----------------------------------------------------------------------
+int vg_knn(vg_ctx* ctx, const vg_cloud* cloud, int32_t k, int64_t* nbrs_out) {
+  if (!ctx || !cloud || !nbrs_out || k <= 0) return fail(VG_ERR_INVALID, "invalid kNN arguments");
+  if (cloud->n < k)  // preprocess.py:129-130
+    return fail(VG_ERR_TOO_SPARSE, "frame has " + std::to_string(cloud->n) +
+                                       " points, need at least " + std::to_string(k));
+  if (cloud->n >= (1LL << 31)) return fail(VG_ERR_INVALID, "cloud too large");
+  long long* dn = nullptr;
+  VG_CHECK(dalloc(ctx, &dn, (size_t)cloud->n * k));
+  VG_CHECK(launch_knn(ctx, cloud, k, dn));
+  int rc = d2h_sync(ctx, nbrs_out, dn, sizeof(long long) * cloud->n * k);
+  dfree(ctx, dn);
+  return rc;
+}
+
+int vg_covariances(vg_ctx* ctx, const vg_cloud* cloud, const int64_t* nbrs, int32_t k, double eps,
+                   double* covs_out, uint8_t* degen_out) {
+  if (!ctx || !cloud || (cloud->n && (!nbrs || !covs_out)) || k <= 0)
+    return fail(VG_ERR_INVALID, "invalid covariance arguments");
+  const long long n = cloud->n;
+  if (n == 0) return VG_OK;
+  for (long long i = 0; i < n * k; ++i)
+    if (nbrs[i] < 0 || nbrs[i] >= n) return fail(VG_ERR_INVALID, "neighbor index out of range");
+  long long* dn = nullptr;
+  double* dc = nullptr;
+  unsigned char* dg = nullptr;
+  VG_CHECK(dalloc(ctx, &dn, (size_t)n * k));
+  VG_CHECK(dalloc(ctx, &dc, 9 * (size_t)n));
+  VG_CHECK(dalloc(ctx, &dg, (size_t)n));
+  VG_CHECK(h2d(ctx, dn, nbrs, sizeof(long long) * n * k));
+  VG_CHECK(launch_cov(ctx, cloud, dn, k, eps, dc, dg));
+  if (degen_out) VG_CUDA(cudaMemcpyAsync(degen_out, dg, n, cudaMemcpyDeviceToHost, ctx->stream));
+  int rc = d2h_sync(ctx, covs_out, dc, sizeof(double) * 9 * n);
+  dfree(ctx, dn);
+  dfree(ctx, dc);
+  dfree(ctx, dg);
+  return rc;
+}
+
+int vg_cloud_estimate_covariances(vg_ctx* ctx, vg_cloud* cloud, int32_t k, double eps,
+                                  int64_t* nbrs_out, double* covs_out, uint8_t* degen_out) {
+  if (!ctx || !cloud || k <= 0) return fail(VG_ERR_INVALID, "invalid arguments");
+  const long long n = cloud->n;
+  if (n < k)
+    return fail(VG_ERR_TOO_SPARSE, "frame has " + std::to_string(n) + " points, need at least " +
+                                       std::to_string(k));
+  long long* dn = nullptr;
+  unsigned char* dg = nullptr;
+  VG_CHECK(dalloc(ctx, &dn, (size_t)n * k));
+  VG_CHECK(dalloc(ctx, &dg, (size_t)n));
+  if (!cloud->cov64) {
+    VG_CHECK(dalloc(ctx, &cloud->cov64, 9 * (size_t)n));
+    VG_CHECK(dalloc(ctx, &cloud->c0, (size_t)n));
+    VG_CHECK(dalloc(ctx, &cloud->c1, (size_t)n));
+    VG_CHECK(dalloc(ctx, &cloud->c2, (size_t)n));
+  }
+  VG_CHECK(launch_knn(ctx, cloud, k, dn));
+  VG_CHECK(launch_cov(ctx, cloud, dn, k, eps, cloud->cov64, dg));
+  cloud->has_cov = true;
+  VG_CHECK(launch_cloud_pack(ctx, cloud));
+  if (nbrs_out) VG_CUDA(cudaMemcpyAsync(nbrs_out, dn, 8 * n * k, cudaMemcpyDeviceToHost, ctx->stream));
+  if (covs_out) VG_CUDA(cudaMemcpyAsync(covs_out, cloud->cov64, 72 * n, cudaMemcpyDeviceToHost, ctx->stream));
+  if (degen_out) VG_CUDA(cudaMemcpyAsync(degen_out, dg, n, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  dfree(ctx, dn);
+  dfree(ctx, dg);
+  return VG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+// internal.h — host-side objects behind the opaque C-ABI handles and the kernel launchers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "vgicp.h"
+
+struct vg_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;  // where all work is enqueued
+  long long launches = 0;         // kernels launched (bench evidence)
+  // scratch (grown on demand, stream-ordered reuse)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+};
+
+struct vg_cloud {
+  vg_ctx* ctx = nullptr;
+  long long n = 0;
+  bool has_cov = false;
+  bool exact32 = true;
+  float4* a = nullptr;       // x, y, z fp32
+  double2* c0 = nullptr;     // covariance SoA (fp64)
+  double2* c1 = nullptr;
+  double2* c2 = nullptr;
+  double* xyz64 = nullptr;  // always kept: fp64 points (map build, kNN)
+  double* cov64 = nullptr;  // n*9 fp64 covariances (bit-exact map build), or null
+  vg::CloudView view() const {
+    vg::CloudView v;
+    v.a = a;
+    v.c0 = has_cov ? c0 : nullptr;
+    v.c1 = has_cov ? c1 : nullptr;
+    v.c2 = has_cov ? c2 : nullptr;
+    v.xyz64 = exact32 ? nullptr : xyz64;
+    v.n = n;
+    return v;
+  }
+};
+
+struct vg_map {
+  vg_ctx* ctx = nullptr;
+  long long m = 0;
+  double res = 1.0;
+  unsigned capacity = 0;
+  int log2cap = 0;
+  vg::Slot* table = nullptr;
+  vg::VoxelRec* vox = nullptr;  // m records, row-indexed
+  // reference arrays (device, fp64/int64): keys sorted ascending, means m*3, covs m*9
+  long long* keys = nullptr;
+  double* means = nullptr;
+  double* covs = nullptr;
+  long long* counts = nullptr;
+  vg::MapView view() const {
+    vg::MapView v;
+    v.table = table;
+    v.vox = vox;
+    v.res = res;
+    v.inv_res = 1.0 / res;
+    v.mask = capacity - 1;
+    v.shift = 64 - log2cap;
+    v.m = (int)m;
+    v.pad = 0;
+    return v;
+  }
+};
+
+struct vg_batch {
+  vg_ctx* ctx = nullptr;
+  long long F = 0;
+  long long num_items = 0;
+  long long num_points = 0;
+  int num_clouds = 0;
+  int num_maps = 0;
+  int max_var = -1;
+  vg::FactorDev* factors = nullptr;   // F
+  vg::ItemDev* items = nullptr;       // num_items (ordered by target map, then factor)
+  vg::CloudView* clouds = nullptr;    // num_clouds
+  vg::MapView* maps = nullptr;        // num_maps
+  double* partials = nullptr;         // num_items * kPartialStride
+  double* poses = nullptr;            // pose table (device), capacity pose_cap
+  long long pose_cap = 0;
+  double* out = nullptr;              // device output (F * 92)
+  double* T_host_stage = nullptr;     // unused placeholder
+  cudaGraphExec_t graph = nullptr;
+  std::vector<vg::FactorDev> host_factors;
+};
+
+// error plumbing (capi.cu)
+void vg_set_error(const std::string& msg);
+int vg_cuda_fail(cudaError_t e, const char* what);
+#define VG_CUDA(call)                                        \
+  do {                                                       \
+    cudaError_t _e = (call);                                 \
+    if (_e != cudaSuccess) return vg_cuda_fail(_e, #call);   \
+  } while (0)
+
+// scratch helpers
+int vg_scratch(vg_ctx* ctx, size_t bytes, void** out);
+
+// ---- launchers (each returns VG_OK or an error code; all stream-ordered on ctx) ----
+int launch_pack_keys(vg_ctx* ctx, const double* xyz_dev, long long n, double res,
+                     long long* keys_dev);
+int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cloud);  // fp64 xyz/cov -> fp32 SoA
+int launch_map_build(vg_ctx* ctx, const vg_cloud* cloud, double res, vg_map* map);
+int launch_map_finish(vg_ctx* ctx, vg_map* map);  // fp64 arrays -> slots + hash
+int launch_lookup(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
+                  const double* T_dev, long long* rows_dev, unsigned long long* hits_dev);
+int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
+                 const double* T_dev, long long* rows, double* moved, double* d, double* w,
+                 double* wd, double* partial_cost, long long* partial_inl, int nblocks);
+int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
+int launch_linearize(vg_ctx* ctx, vg_batch* b, int mode);
+int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
+int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);
+int launch_cov(vg_ctx* ctx, const vg_cloud* cloud, const long long* nbrs_dev, int k,
+               double eps, double* covs_dev, unsigned char* degen_dev);

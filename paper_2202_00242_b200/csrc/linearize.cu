@@ -1,0 +1,607 @@
+// linearize.cu — K3 lookup, K3t per-point terms, K4 fused VGICP linearize / cost, K5 finalize,
+// and the on-device pose composition T_ij = T_j^-1 T_i.
+//
+// Reference: registration.py:146-157 (match_terms), :207-248 (linearize_from_terms),
+// :251-269 (linearize_matching_cost), factor_graph.py:253-308 (MatchingCostFactor).
+//
+// Per correspondence the kernel reads the source Gaussian (fp32 xyz + fp64 covariance, SoA,
+// coalesced), one 16 B hash slot and one 64 B voxel record, and does all math in registers:
+//   x = R p + t (fp64) -> key (fp64 floor, bit-exact) -> probe -> d = mu' - x (cell-local,
+//   fp32) -> W = (C' + R C R^T)^-1 (fp64 fused covariance + adjugate, rounded to fp32 after
+//   inversion) -> accumulate the 6x6 target-frame block about the source origin (29 values,
+//   H_ii, H_ij, H_jj, b_i, b_j are exact fp64 adjoint transforms of it, so
+//   nothing else is accumulated per point).
+// Lane sums are fp32 over <= 16 points; the warp reduction and everything after is fp64 and
+// fixed-order, so results are deterministic run to run.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace vg {
+
+struct PointTerms {
+  float d[3];
+  float W[6];   // 00 01 02 11 12 22
+  float wd[3];
+  float xp[3];  // x - t == R p : lever arm about the source origin
+  float cost;
+};
+
+__device__ __forceinline__ void load_T(const double* __restrict__ T, double (&R)[9],
+                                       double (&t)[3]) {
+#pragma unroll
+  for (int i = 0; i < 9; ++i) R[i] = __ldg(T + i);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) t[i] = __ldg(T + 9 + i);
+}
+
+__device__ __forceinline__ void transform(const double (&R)[9], const double (&t)[3],
+                                          double px, double py, double pz, double& x,
+                                          double& y, double& z) {
+  // points @ R^T + t (registration.py:148)
+  x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
+  y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
+  z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
+}
+
+__device__ __forceinline__ void load_point(const CloudView& cv, long long i, double& px,
+                                           double& py, double& pz, float4& pa) {
+  pa = __ldg(cv.a + i);
+  if (cv.xyz64) {
+    px = __ldg(cv.xyz64 + 3 * i);
+    py = __ldg(cv.xyz64 + 3 * i + 1);
+    pz = __ldg(cv.xyz64 + 3 * i + 2);
+  } else {
+    px = pa.x;
+    py = pa.y;
+    pz = pa.z;
+  }
+}
+
+// centre of the cell with packed key `key` (decoded exactly as occupied_indices,
+// registration.py:65-71); identical for the query and the voxel whenever the keys match.
+__device__ __forceinline__ void cell_centre(long long key, double res, double& cx, double& cy,
+                                            double& cz) {
+  long long ix = (key >> 42) - kKeyOffset;
+  long long iy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
+  long long iz = (key & ((1LL << 21) - 1)) - kKeyOffset;
+  cx = ((double)ix + 0.5) * res;
+  cy = ((double)iy + 0.5) * res;
+  cz = ((double)iz + 0.5) * res;
+}
+
+// fused covariance (fp64), inverse (fp64), residual (cell-local fp32), cost for one
+// correspondence (registration.py:150-156).  W is rounded to fp32 only after inversion, so
+// its error is not amplified by the condition number of C' + R C R^T.
+__device__ __forceinline__ void point_terms(const double (&R)[9], const CloudView& cv,
+                                            long long i, const VoxelRec* __restrict__ vr,
+                                            double x, double y, double z, const double (&t)[3],
+                                            double res, long long key, PointTerms& o) {
+  const float4 vm = __ldg(&vr->mean);
+  const double2 v0 = __ldg(&vr->c0), v1 = __ldg(&vr->c1), v2 = __ldg(&vr->c2);
+  const double2 s0 = __ldg(cv.c0 + i), s1 = __ldg(cv.c1 + i), s2 = __ldg(cv.c2 + i);
+  double cx, cy, cz;
+  cell_centre(key, res, cx, cy, cz);
+  // d = mu' - moved, formed in cell-local coordinates (registration.py:152)
+  o.d[0] = vm.x - (float)(x - cx);
+  o.d[1] = vm.y - (float)(y - cy);
+  o.d[2] = vm.z - (float)(z - cz);
+  o.xp[0] = (float)(x - t[0]);
+  o.xp[1] = (float)(y - t[1]);
+  o.xp[2] = (float)(z - t[2]);
+  // source covariance C: c00 c01 c02 c11 c12 c22
+  const double C00 = s0.x, C01 = s0.y, C02 = s1.x, C11 = s1.y, C12 = s2.x, C22 = s2.y;
+  double A[9];  // A = R C
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const double r0 = R[3 * r], r1 = R[3 * r + 1], r2 = R[3 * r + 2];
+    A[3 * r + 0] = fma(r0, C00, fma(r1, C01, r2 * C02));
+    A[3 * r + 1] = fma(r0, C01, fma(r1, C11, r2 * C12));
+    A[3 * r + 2] = fma(r0, C02, fma(r1, C12, r2 * C22));
+  }
+  // F = C' + A R^T  (registration.py:153)
+  auto arT = [&](int r, int c) {
+    return fma(A[3 * r], R[3 * c], fma(A[3 * r + 1], R[3 * c + 1], A[3 * r + 2] * R[3 * c + 2]));
+  };
+  const double a = v0.x + arT(0, 0);
+  const double b = v0.y + arT(0, 1);
+  const double c = v1.x + arT(0, 2);
+  const double dd = v1.y + arT(1, 1);
+  const double e = v2.x + arT(1, 2);
+  const double f = v2.y + arT(2, 2);
+  // W = F^-1 by the adjugate (registration.py:113-130)
+  const double i00 = fma(dd, f, -e * e);
+  const double i01 = fma(c, e, -b * f);
+  const double i02 = fma(b, e, -c * dd);
+  const double i11 = fma(a, f, -c * c);
+  const double i12 = fma(b, c, -a * e);
+  const double i22 = fma(a, dd, -b * b);
+  const double det = fma(a, i00, fma(b, i01, c * i02));
+  const double inv = 1.0 / det;
+  o.W[0] = (float)(i00 * inv);
+  o.W[1] = (float)(i01 * inv);
+  o.W[2] = (float)(i02 * inv);
+  o.W[3] = (float)(i11 * inv);
+  o.W[4] = (float)(i12 * inv);
+  o.W[5] = (float)(i22 * inv);
+  o.wd[0] = fmaf(o.W[0], o.d[0], fmaf(o.W[1], o.d[1], o.W[2] * o.d[2]));
+  o.wd[1] = fmaf(o.W[1], o.d[0], fmaf(o.W[3], o.d[1], o.W[4] * o.d[2]));
+  o.wd[2] = fmaf(o.W[2], o.d[0], fmaf(o.W[4], o.d[1], o.W[5] * o.d[2]));
+  o.cost = fmaf(o.d[0], o.wd[0], fmaf(o.d[1], o.wd[1], o.d[2] * o.wd[2]));
+}
+
+// ---- warp reductions ---------------------------------------------------------------------
+
+// 32 values reduced across 32 lanes in 31 shuffle steps; lane L returns the sum of value L.
+__device__ __forceinline__ double warp_transpose_reduce32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = up ? v[i] : v[i + s];
+      const double keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+// ---- K4: fused linearize / cost over (factor, chunk) work items --------------------------
+// MODE 0: full (29-value partial per item); MODE 1: cost + inliers only.
+template <int MODE>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_linearize(const ItemDev* __restrict__ items, int n_items,
+                const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
+                const MapView* __restrict__ maps, double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (w >= n_items) return;
+  const ItemDev it = items[w];
+  const FactorDev* f = factors + it.factor;
+  double R[9], t[3];
+  load_T(f->T, R, t);
+  const CloudView cv = clouds[__ldg(&f->cloud)];
+  const MapView mv = maps[__ldg(&f->map)];
+
+  // lane accumulators: P(6) N(9) S(6) br(3) bt(3) cost(1)
+  float acc[28];
+#pragma unroll
+  for (int i = 0; i < 28; ++i) acc[i] = 0.f;
+  int inl = 0;
+
+  for (int i = it.begin + lane; i < it.end; i += 32) {
+    double px, py, pz;
+    float4 pa;
+    load_point(cv, i, px, py, pz, pa);
+    double x, y, z;
+    transform(R, t, px, py, pz, x, y, z);
+    const long long key = pack_key(floor_div(x, mv.res, mv.inv_res),
+                                   floor_div(y, mv.res, mv.inv_res),
+                                   floor_div(z, mv.res, mv.inv_res));
+    const int row = probe(mv, key);
+    if (row < 0) continue;  // misses contribute nothing (registration.py:150-156)
+    ++inl;
+    PointTerms o;
+    point_terms(R, cv, i, mv.vox + row, x, y, z, t, mv.res, key, o);
+    if (MODE == 1) {
+      acc[27] += o.cost;
+      continue;
+    }
+    const float vx = o.xp[0], vy = o.xp[1], vz = o.xp[2];
+    const float W00 = o.W[0], W01 = o.W[1], W02 = o.W[2], W11 = o.W[3], W12 = o.W[4],
+                W22 = o.W[5];
+    // N = hat(x') W   (rot-trans block of J'^T W J', J' = [-hat(x') | I])
+    const float N00 = fmaf(-vz, W01, vy * W02), N01 = fmaf(-vz, W11, vy * W12),
+                N02 = fmaf(-vz, W12, vy * W22);
+    const float N10 = fmaf(vz, W00, -vx * W02), N11 = fmaf(vz, W01, -vx * W12),
+                N12 = fmaf(vz, W02, -vx * W22);
+    const float N20 = fmaf(-vy, W00, vx * W01), N21 = fmaf(-vy, W01, vx * W11),
+                N22 = fmaf(-vy, W02, vx * W12);
+    // P = N hat(x')^T (rot-rot block), upper triangle
+    const float P00 = fmaf(-vz, N01, vy * N02);
+    const float P01 = fmaf(vz, N00, -vx * N02);
+    const float P02 = fmaf(-vy, N00, vx * N01);
+    const float P11 = fmaf(vz, N10, -vx * N12);
+    const float P12 = fmaf(-vy, N10, vx * N11);
+    const float P22 = fmaf(-vy, N20, vx * N21);
+    acc[0] += P00; acc[1] += P01; acc[2] += P02; acc[3] += P11; acc[4] += P12; acc[5] += P22;
+    acc[6] += N00; acc[7] += N01; acc[8] += N02;
+    acc[9] += N10; acc[10] += N11; acc[11] += N12;
+    acc[12] += N20; acc[13] += N21; acc[14] += N22;
+    acc[15] += W00; acc[16] += W01; acc[17] += W02; acc[18] += W11; acc[19] += W12; acc[20] += W22;
+    // b' = [x' x Wd ; Wd]
+    acc[21] += fmaf(vy, o.wd[2], -vz * o.wd[1]);
+    acc[22] += fmaf(vz, o.wd[0], -vx * o.wd[2]);
+    acc[23] += fmaf(vx, o.wd[1], -vy * o.wd[0]);
+    acc[24] += o.wd[0]; acc[25] += o.wd[1]; acc[26] += o.wd[2];
+    acc[27] += o.cost;
+  }
+
+  if (MODE == 1) {
+    double c = (double)acc[27];
+    long long n = inl;
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, s);
+      n += __shfl_xor_sync(0xffffffffu, n, s);
+    }
+    if (lane == 0) {
+      partials[2 * (size_t)w] = c;
+      partials[2 * (size_t)w + 1] = (double)n;
+    }
+    return;
+  }
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 28; ++i) v[i] = (double)acc[i];
+  v[28] = (double)inl;
+  v[29] = 0.0; v[30] = 0.0; v[31] = 0.0;
+  const double r = warp_transpose_reduce32(v, lane);
+  partials[(size_t)w * kPartialStride + lane] = r;
+}
+
+// ---- K5: per-factor fixed-order sum of item partials + fp64 adjoint expansion ------------
+__device__ __forceinline__ void mat3_mul(const double* A, const double* B, double* C) {
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      C[3 * r + c] = A[3 * r] * B[c] + A[3 * r + 1] * B[3 + c] + A[3 * r + 2] * B[6 + c];
+}
+__device__ __forceinline__ void mat3_tmul(const double* A, const double* B, double* C) {
+  // C = A^T B
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      C[3 * r + c] = A[r] * B[c] + A[3 + r] * B[3 + c] + A[6 + r] * B[6 + c];
+}
+
+// write the upper triangle of a 6x6 assembled from 3x3 blocks [[A, B], [B^T, D]]
+__device__ __forceinline__ void store_sym6(double* out, const double* A, const double* B,
+                                           const double* D, double scale) {
+  int k = 0;
+  for (int r = 0; r < 6; ++r)
+    for (int c = r; c < 6; ++c) {
+      double v;
+      if (r < 3 && c < 3) v = A[3 * r + c];
+      else if (r < 3) v = B[3 * r + (c - 3)];
+      else v = D[3 * (r - 3) + (c - 3)];
+      out[k++] = scale * v;
+    }
+}
+
+__global__ void k_finalize(const FactorDev* __restrict__ factors, int F,
+                           const double* __restrict__ partials, int mode,
+                           double* __restrict__ out) {
+  const int fi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (fi >= F) return;
+  const FactorDev& f = factors[fi];
+  if (mode == 1) {
+    double c = 0.0, n = 0.0;
+    for (int it = 0; it < f.item_count; ++it) {
+      c += partials[2 * (size_t)(f.item_begin + it)];
+      n += partials[2 * (size_t)(f.item_begin + it) + 1];
+    }
+    out[2 * (size_t)fi] = c;
+    out[2 * (size_t)fi + 1] = n;
+    return;
+  }
+  double s[29];
+#pragma unroll
+  for (int k = 0; k < 29; ++k) s[k] = 0.0;
+  for (int it = 0; it < f.item_count; ++it) {
+    const double* p = partials + (size_t)(f.item_begin + it) * kPartialStride;
+#pragma unroll
+    for (int k = 0; k < 29; ++k) s[k] += p[k];
+  }
+  if (mode == 2) {
+    double* o = out + (size_t)fi * 29;
+#pragma unroll
+    for (int k = 0; k < 29; ++k) o[k] = s[k];
+    return;
+  }
+  double* o = out + (size_t)fi * 92;
+  const double cost = s[27], inliers = s[28];
+  if (inliers < (double)f.min_inliers) {  // DegenerateConstraint -> zero blocks
+    for (int k = 0; k < 90; ++k) o[k] = 0.0;
+    o[90] = cost;
+    o[91] = inliers;
+    return;
+  }
+  // H' = [[P, N], [N^T, S]], b' = [br; bt]
+  const double P[9] = {s[0], s[1], s[2], s[1], s[3], s[4], s[2], s[4], s[5]};
+  const double N[9] = {s[6], s[7], s[8], s[9], s[10], s[11], s[12], s[13], s[14]};
+  const double S[9] = {s[15], s[16], s[17], s[16], s[18], s[19], s[17], s[19], s[20]};
+  const double br[3] = {s[21], s[22], s[23]};
+  const double bt[3] = {s[24], s[25], s[26]};
+  const double* R = f.T;
+  const double t0 = f.T[9], t1 = f.T[10], t2 = f.T[11];
+  const double Ch[9] = {0.0, -t2, t1, t2, 0.0, -t0, -t1, t0, 0.0};  // hat(t)
+  double Nt[9];
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) Nt[3 * r + c] = N[3 * c + r];
+  double tmp[9], tmp2[9];
+  // ---- source block: H_ii = Rd^T H' Rd, b_i = -Rd^T b'  (Rd = diag(R, R))
+  double RtP[9], RtN[9], RtS[9], Hii_a[9], Hii_b[9], Hii_d[9];
+  mat3_tmul(R, P, RtP);
+  mat3_tmul(R, N, RtN);
+  mat3_tmul(R, S, RtS);
+  mat3_mul(RtP, R, Hii_a);
+  mat3_mul(RtN, R, Hii_b);
+  mat3_mul(RtS, R, Hii_d);
+  store_sym6(o, Hii_a, Hii_b, Hii_d, 2.0);
+  double* bi = o + 78;
+  for (int r = 0; r < 3; ++r) {
+    bi[r] = -2.0 * (R[r] * br[0] + R[3 + r] * br[1] + R[6 + r] * br[2]);
+    bi[3 + r] = -2.0 * (R[r] * bt[0] + R[3 + r] * bt[1] + R[6 + r] * bt[2]);
+  }
+  o[90] = cost;
+  o[91] = inliers;
+  if (f.flags & 1) {  // unary: target fixed (registration.py:233-235)
+    for (int k = 21; k < 78; ++k) o[k] = 0.0;
+    for (int k = 84; k < 90; ++k) o[k] = 0.0;
+    return;
+  }
+  // ---- target block: H_jj = E^T H' E, E = [[I, 0], [-C, I]], C = hat(t)
+  double NC[9], CNt[9], CS[9], SC[9], CSC[9];
+  mat3_mul(N, Ch, NC);
+  mat3_mul(Ch, Nt, CNt);
+  mat3_mul(Ch, S, CS);
+  mat3_mul(S, Ch, SC);
+  mat3_mul(CS, Ch, CSC);
+  double Ja[9], Jb[9];
+  for (int k = 0; k < 9; ++k) {
+    Ja[k] = P[k] + CNt[k] - NC[k] - CSC[k];
+    Jb[k] = N[k] + CS[k];
+  }
+  store_sym6(o + 57, Ja, Jb, S, 2.0);
+  double* bj = o + 84;
+  bj[0] = 2.0 * (br[0] + Ch[0] * bt[0] + Ch[1] * bt[1] + Ch[2] * bt[2]);
+  bj[1] = 2.0 * (br[1] + Ch[3] * bt[0] + Ch[4] * bt[1] + Ch[5] * bt[2]);
+  bj[2] = 2.0 * (br[2] + Ch[6] * bt[0] + Ch[7] * bt[1] + Ch[8] * bt[2]);
+  bj[3] = 2.0 * bt[0];
+  bj[4] = 2.0 * bt[1];
+  bj[5] = 2.0 * bt[2];
+  // ---- cross block: H_ij = -Rd^T H' E = -[[R^T(P - N C), R^T N], [R^T(N^T - S C), R^T S]]
+  double* hij = o + 21;
+  for (int k = 0; k < 9; ++k) tmp[k] = P[k] - NC[k];
+  mat3_tmul(R, tmp, tmp2);  // R^T (P - N C)
+  double lowL[9];
+  for (int k = 0; k < 9; ++k) tmp[k] = Nt[k] - SC[k];
+  mat3_tmul(R, tmp, lowL);  // R^T (N^T - S C)
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) {
+      double v;
+      if (r < 3 && c < 3) v = tmp2[3 * r + c];
+      else if (r < 3) v = RtN[3 * r + (c - 3)];
+      else if (c < 3) v = lowL[3 * (r - 3) + c];
+      else v = RtS[3 * (r - 3) + (c - 3)];
+      hij[6 * r + c] = -2.0 * v;
+    }
+}
+
+// ---- pose composition on the device (geometry.py:47-144,231-237) ------------------------
+// Mirrors Rotation's quaternion arithmetic operation for operation without FMA contraction,
+// so T_ij matches pose_compose(pose_inverse(t_j), t_i) to the last bit except for numpy's
+// 4-term dot order in the renormalisation.
+struct Quat {
+  double x, y, z, w;
+};
+__device__ __forceinline__ Quat q_normalize(Quat q) {
+  const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(q.x, q.x), __dmul_rn(q.y, q.y)),
+                                                  __dmul_rn(q.z, q.z)),
+                                         __dmul_rn(q.w, q.w)));
+  return Quat{__ddiv_rn(q.x, n), __ddiv_rn(q.y, n), __ddiv_rn(q.z, n), __ddiv_rn(q.w, n)};
+}
+#define M_(a, b) __dmul_rn(a, b)
+#define A_(a, b) __dadd_rn(a, b)
+#define S_(a, b) __dsub_rn(a, b)
+__device__ __forceinline__ Quat q_mul(Quat a, Quat b) {
+  Quat r;
+  r.x = S_(A_(A_(M_(a.w, b.x), M_(b.w, a.x)), M_(a.y, b.z)), M_(a.z, b.y));
+  r.y = S_(A_(A_(M_(a.w, b.y), M_(b.w, a.y)), M_(a.z, b.x)), M_(a.x, b.z));
+  r.z = S_(A_(A_(M_(a.w, b.z), M_(b.w, a.z)), M_(a.x, b.y)), M_(a.y, b.x));
+  r.w = S_(S_(S_(M_(a.w, b.w), M_(a.x, b.x)), M_(a.y, b.y)), M_(a.z, b.z));
+  return r;
+}
+__device__ __forceinline__ void q_apply(Quat q, const double v[3], double out[3]) {
+  const double ux = q.x, uy = q.y, uz = q.z, w = q.w;
+  const double tx = M_(2.0, S_(M_(uy, v[2]), M_(uz, v[1])));
+  const double ty = M_(2.0, S_(M_(uz, v[0]), M_(ux, v[2])));
+  const double tz = M_(2.0, S_(M_(ux, v[1]), M_(uy, v[0])));
+  out[0] = S_(A_(A_(v[0], M_(w, tx)), M_(uy, tz)), M_(uz, ty));
+  out[1] = S_(A_(A_(v[1], M_(w, ty)), M_(uz, tx)), M_(ux, tz));
+  out[2] = S_(A_(A_(v[2], M_(w, tz)), M_(ux, ty)), M_(uy, tx));
+}
+__device__ __forceinline__ void q_matrix(Quat q, double* R) {
+  const double xx = M_(q.x, q.x), yy = M_(q.y, q.y), zz = M_(q.z, q.z);
+  const double xy = M_(q.x, q.y), xz = M_(q.x, q.z), yz = M_(q.y, q.z);
+  const double wx = M_(q.w, q.x), wy = M_(q.w, q.y), wz = M_(q.w, q.z);
+  R[0] = S_(1.0, M_(2.0, A_(yy, zz)));
+  R[1] = M_(2.0, S_(xy, wz));
+  R[2] = M_(2.0, A_(xz, wy));
+  R[3] = M_(2.0, A_(xy, wz));
+  R[4] = S_(1.0, M_(2.0, A_(xx, zz)));
+  R[5] = M_(2.0, S_(yz, wx));
+  R[6] = M_(2.0, S_(xz, wy));
+  R[7] = M_(2.0, A_(yz, wx));
+  R[8] = S_(1.0, M_(2.0, A_(xx, yy)));
+}
+#undef M_
+#undef A_
+#undef S_
+
+__global__ void k_compose(FactorDev* __restrict__ factors, int F, const double* __restrict__ poses) {
+  const int fi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (fi >= F) return;
+  FactorDev& f = factors[fi];
+  const double* pi = poses + 8 * (size_t)f.var_source;
+  const double* pj = poses + 8 * (size_t)f.var_target;
+  // pose_inverse(t_j): rotation inverse (renormalised by the constructor), t = -R^-1 t_j
+  Quat qj = q_normalize(Quat{-pj[0], -pj[1], -pj[2], pj[3]});
+  double tj[3] = {pj[4], pj[5], pj[6]}, tinv[3];
+  q_apply(qj, tj, tinv);
+  tinv[0] = -tinv[0];
+  tinv[1] = -tinv[1];
+  tinv[2] = -tinv[2];
+  // pose_compose(inv_j, t_i)
+  Quat qi{pi[0], pi[1], pi[2], pi[3]};
+  Quat q = q_normalize(q_mul(qj, qi));
+  double ti[3] = {pi[4], pi[5], pi[6]}, tt[3];
+  q_apply(qj, ti, tt);
+  q_matrix(q, f.T);
+  f.T[9] = __dadd_rn(tt[0], tinv[0]);
+  f.T[10] = __dadd_rn(tt[1], tinv[1]);
+  f.T[11] = __dadd_rn(tt[2], tinv[2]);
+}
+
+// ---- K3: transform + lookup (GaussianVoxelMap.lookup / overlap_rate) ----------------------
+__global__ void k_lookup(CloudView cv, MapView mv, const double* __restrict__ Tp,
+                         long long* __restrict__ rows, unsigned long long* __restrict__ hits) {
+  double R[9], t[3];
+  load_T(Tp, R, t);
+  unsigned long long local = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cv.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double px, py, pz;
+    float4 pa;
+    load_point(cv, i, px, py, pz, pa);
+    double x, y, z;
+    transform(R, t, px, py, pz, x, y, z);
+    const long long key = pack_key(floor_div(x, mv.res, mv.inv_res),
+                                   floor_div(y, mv.res, mv.inv_res),
+                                   floor_div(z, mv.res, mv.inv_res));
+    const long long row = probe(mv, key);
+    if (rows) rows[i] = row;
+    local += (row >= 0);
+  }
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) local += __shfl_xor_sync(0xffffffffu, local, s);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(hits, local);  // integer: deterministic
+}
+
+// ---- K3t: per-point match terms (match_terms materialised for API parity) -----------------
+__global__ void k_terms(CloudView cv, MapView mv, const double* __restrict__ Tp,
+                        long long* __restrict__ rows, double* __restrict__ moved,
+                        double* __restrict__ dout, double* __restrict__ wout,
+                        double* __restrict__ wdout, double* __restrict__ pcost,
+                        long long* __restrict__ pinl) {
+  double R[9], t[3];
+  load_T(Tp, R, t);
+  double csum = 0.0;
+  long long isum = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cv.n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double px, py, pz;
+    float4 pa;
+    load_point(cv, i, px, py, pz, pa);
+    double x, y, z;
+    transform(R, t, px, py, pz, x, y, z);
+    moved[3 * i] = x;
+    moved[3 * i + 1] = y;
+    moved[3 * i + 2] = z;
+    const long long key = pack_key(floor_div(x, mv.res, mv.inv_res),
+                                   floor_div(y, mv.res, mv.inv_res),
+                                   floor_div(z, mv.res, mv.inv_res));
+    const int row = probe(mv, key);
+    if (row < 0) {
+      rows[i] = -1;
+      for (int k = 0; k < 3; ++k) dout[3 * i + k] = 0.0, wdout[3 * i + k] = 0.0;
+      for (int k = 0; k < 9; ++k) wout[9 * i + k] = 0.0;
+      continue;
+    }
+    rows[i] = row;
+    PointTerms o;
+    point_terms(R, cv, i, mv.vox + row, x, y, z, t, mv.res, key, o);
+    const int sym[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
+    for (int k = 0; k < 3; ++k) dout[3 * i + k] = o.d[k], wdout[3 * i + k] = o.wd[k];
+    for (int k = 0; k < 9; ++k) wout[9 * i + k] = o.W[sym[k]];
+    csum += (double)o.cost;
+    ++isum;
+  }
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    csum += __shfl_xor_sync(0xffffffffu, csum, s);
+    isum += __shfl_xor_sync(0xffffffffu, isum, s);
+  }
+  __shared__ double sc[32];
+  __shared__ long long si[32];
+  const int wid = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) sc[wid] = csum, si[wid] = isum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double c = 0.0;
+    long long n = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) c += sc[k], n += si[k];
+    pcost[blockIdx.x] = c;
+    pinl[blockIdx.x] = n;
+  }
+}
+
+}  // namespace vg
+
+using namespace vg;
+
+static int grid_for(long long n, int threads, int cap) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+int launch_lookup(vg_ctx* ctx, const CloudView& cv, const MapView& mv, const double* T_dev,
+                  long long* rows_dev, unsigned long long* hits_dev) {
+  if (cv.n == 0) return 0;
+  k_lookup<<<grid_for(cv.n, 256, 148 * 16), 256, 0, ctx->stream>>>(cv, mv, T_dev, rows_dev,
+                                                                   hits_dev);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_terms(vg_ctx* ctx, const CloudView& cv, const MapView& mv, const double* T_dev,
+                 long long* rows, double* moved, double* d, double* w, double* wd,
+                 double* partial_cost, long long* partial_inl, int nblocks) {
+  if (cv.n == 0) return 0;
+  k_terms<<<nblocks, 256, 0, ctx->stream>>>(cv, mv, T_dev, rows, moved, d, w, wd, partial_cost,
+                                            partial_inl);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev) {
+  if (b->F == 0) return 0;
+  k_compose<<<grid_for(b->F, 128, 1 << 30), 128, 0, ctx->stream>>>(b->factors, (int)b->F,
+                                                                   poses_dev);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_linearize(vg_ctx* ctx, vg_batch* b, int mode) {
+  if (b->num_items == 0) return 0;
+  const int threads = kWarpsPerBlock * 32;
+  const int blocks = (int)((b->num_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  if (mode == 1)
+    k_linearize<1><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,
+                                                        b->clouds, b->maps, b->partials);
+  else
+    k_linearize<0><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,
+                                                        b->clouds, b->maps, b->partials);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev) {
+  if (b->F == 0) return 0;
+  k_finalize<<<grid_for(b->F, 128, 1 << 30), 128, 0, ctx->stream>>>(b->factors, (int)b->F,
+                                                                    b->partials, mode, out_dev);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}

@@ -1,0 +1,220 @@
+// map_build.cu — K1 voxel keys, cloud packing, K2 Gaussian voxel-map build + hash insert.
+//
+// build_voxelmap (registration.py:74-98) on the device, bit-identical to the reference:
+//   keys (preprocess.py:68-70) -> stable radix sort of (key, index) (== np.unique order and
+//   np.add.at's index order inside every cell) -> run-length encode -> one thread per cell
+//   sums its members sequentially in index order with correctly rounded fp64 adds (no FMA),
+//   exactly the rounding sequence of np.add.at + true division.
+// The fp64 arrays are kept on the device for export; the hot path reads the 64 B slots.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace vg {
+
+__global__ void k_pack_keys(const double* __restrict__ xyz, long long n, double res,
+                            long long* __restrict__ keys, int* __restrict__ idx) {
+  const double inv = 1.0 / res;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    keys[i] = pack_key(floor_div(xyz[3 * i], res, inv), floor_div(xyz[3 * i + 1], res, inv),
+                       floor_div(xyz[3 * i + 2], res, inv));
+    if (idx) idx[i] = (int)i;
+  }
+}
+
+// fp64 AoS (n x 3 points, n x 9 covariances) -> fp32 xyz + fp64 covariance SoA
+__global__ void k_cloud_pack(const double* __restrict__ xyz, const double* __restrict__ cov,
+                             long long n, float4* __restrict__ a, double2* __restrict__ c0,
+                             double2* __restrict__ c1, double2* __restrict__ c2) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    a[i] = make_float4((float)xyz[3 * i], (float)xyz[3 * i + 1], (float)xyz[3 * i + 2], 0.f);
+    if (cov) {
+      const double* C = cov + 9 * i;
+      c0[i] = make_double2(C[0], C[1]);
+      c1[i] = make_double2(C[2], C[4]);
+      c2[i] = make_double2(C[5], C[8]);
+    }
+  }
+}
+
+// one thread per cell: mean then scatter, both sequential in index order (np.add.at)
+__global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restrict__ counts,
+                             const int* __restrict__ perm, const double* __restrict__ xyz,
+                             const double* __restrict__ cov, int m, double* __restrict__ means,
+                             double* __restrict__ covs, long long* __restrict__ cnt_out) {
+  const int cidx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cidx >= m) return;
+  const int off = offsets[cidx], cnt = counts[cidx];
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+  for (int j = off; j < off + cnt; ++j) {
+    const int i = perm[j];
+    sx = add_rn(sx, xyz[3 * i]);
+    sy = add_rn(sy, xyz[3 * i + 1]);
+    sz = add_rn(sz, xyz[3 * i + 2]);
+  }
+  const double dc = (double)cnt;
+  const double mx = __ddiv_rn(sx, dc), my = __ddiv_rn(sy, dc), mz = __ddiv_rn(sz, dc);
+  double acc[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+  for (int j = off; j < off + cnt; ++j) {
+    const int i = perm[j];
+    const double c3[3] = {sub_rn(xyz[3 * i], mx), sub_rn(xyz[3 * i + 1], my),
+                          sub_rn(xyz[3 * i + 2], mz)};
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        acc[3 * r + c] = add_rn(acc[3 * r + c], add_rn(cov[9 * (size_t)i + 3 * r + c],
+                                                       mul_rn(c3[r], c3[c])));
+  }
+  means[3 * cidx] = mx;
+  means[3 * cidx + 1] = my;
+  means[3 * cidx + 2] = mz;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) covs[9 * (size_t)cidx + k] = __ddiv_rn(acc[k], dc);
+  cnt_out[cidx] = cnt;
+}
+
+// one thread per cell: write the 64 B voxel record (cell-local fp32 mean, fp64 covariance)
+// and claim a hash position by CAS on the slot's row field.
+__global__ void k_hash_insert(const long long* __restrict__ keys, const double* __restrict__ means,
+                              const double* __restrict__ covs, int m, double res,
+                              Slot* __restrict__ table, VoxelRec* __restrict__ vox,
+                              unsigned mask, int shift) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  const long long key = keys[r];
+  const long long ix = (key >> 42) - kKeyOffset;
+  const long long iy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
+  const long long iz = (key & ((1LL << 21) - 1)) - kKeyOffset;
+  const double cx = ((double)ix + 0.5) * res, cy = ((double)iy + 0.5) * res,
+               cz = ((double)iz + 0.5) * res;
+  const double* C = covs + 9 * (size_t)r;
+  VoxelRec v;
+  v.mean = make_float4((float)(means[3 * r] - cx), (float)(means[3 * r + 1] - cy),
+                       (float)(means[3 * r + 2] - cz), 0.f);
+  v.c0 = make_double2(C[0], C[1]);
+  v.c1 = make_double2(C[2], C[4]);
+  v.c2 = make_double2(C[5], C[8]);
+  vox[r] = v;
+  unsigned h = slot_of(key, shift);
+  for (;;) {
+    if (atomicCAS(&table[h].row, -1, r) == -1) break;
+    h = (h + 1) & mask;
+  }
+  table[h].key = key;
+}
+
+}  // namespace vg
+
+using namespace vg;
+
+static int grid1(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > 148 * 64) g = 148 * 64;
+  return (int)g;
+}
+
+int launch_pack_keys(vg_ctx* ctx, const double* xyz_dev, long long n, double res,
+                     long long* keys_dev) {
+  if (n == 0) return 0;
+  k_pack_keys<<<grid1(n, 256), 256, 0, ctx->stream>>>(xyz_dev, n, res, keys_dev, nullptr);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cl) {
+  if (cl->n == 0) return 0;
+  k_cloud_pack<<<grid1(cl->n, 256), 256, 0, ctx->stream>>>(cl->xyz64, cl->cov64, cl->n, cl->a,
+                                                           cl->c0, cl->c1, cl->c2);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+static int capacity_for(long long m, int* log2cap) {
+  int l = 1;
+  while ((1LL << l) < 2 * m) ++l;
+  *log2cap = l;
+  return 1 << l;
+}
+
+int launch_map_finish(vg_ctx* ctx, vg_map* map) {
+  int l2 = 1;
+  map->capacity = (unsigned)capacity_for(map->m, &l2);
+  map->log2cap = l2;
+  VG_CUDA(cudaMallocAsync((void**)&map->table, sizeof(Slot) * (size_t)map->capacity, ctx->stream));
+  VG_CUDA(cudaMemsetAsync(map->table, 0xff, sizeof(Slot) * (size_t)map->capacity, ctx->stream));
+  if (map->m == 0) return 0;
+  VG_CUDA(cudaMallocAsync((void**)&map->vox, sizeof(VoxelRec) * (size_t)map->m, ctx->stream));
+  k_hash_insert<<<(int)((map->m + 127) / 128), 128, 0, ctx->stream>>>(
+      map->keys, map->means, map->covs, (int)map->m, map->res, map->table, map->vox,
+      map->capacity - 1, 64 - l2);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_map_build(vg_ctx* ctx, const vg_cloud* cl, double res, vg_map* map) {
+  const long long n = cl->n;
+  map->res = res;
+  map->m = 0;
+  if (n == 0) return launch_map_finish(ctx, map);
+  cudaStream_t st = ctx->stream;
+  long long *keys = nullptr, *keys_sorted = nullptr, *ukeys = nullptr;
+  int *idx = nullptr, *perm = nullptr, *counts = nullptr, *offsets = nullptr, *num_runs = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0, t1 = 0, t2 = 0, t3 = 0;
+  VG_CUDA(cudaMallocAsync((void**)&keys, sizeof(long long) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&keys_sorted, sizeof(long long) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&ukeys, sizeof(long long) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&idx, sizeof(int) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&perm, sizeof(int) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&counts, sizeof(int) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&offsets, sizeof(int) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&num_runs, sizeof(int), st));
+  k_pack_keys<<<grid1(n, 256), 256, 0, st>>>(cl->xyz64, n, res, keys, idx);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st);
+  cub::DeviceRunLengthEncode::Encode(nullptr, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t3, counts, offsets, (int)n, st);
+  tmp_bytes = t1 > t2 ? t1 : t2;
+  tmp_bytes = tmp_bytes > t3 ? tmp_bytes : t3;
+  VG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  VG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st));
+  VG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st));
+  int m = 0;
+  VG_CUDA(cudaMemcpyAsync(&m, num_runs, sizeof(int), cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaStreamSynchronize(st));
+  VG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t3, counts, offsets, m, st));
+  ctx->launches += 6;  // cub: sort (>=2 passes) + rle + scan, counted conservatively
+  map->m = m;
+  VG_CUDA(cudaMallocAsync((void**)&map->keys, sizeof(long long) * m, st));
+  VG_CUDA(cudaMallocAsync((void**)&map->means, sizeof(double) * 3 * m, st));
+  VG_CUDA(cudaMallocAsync((void**)&map->covs, sizeof(double) * 9 * m, st));
+  VG_CUDA(cudaMallocAsync((void**)&map->counts, sizeof(long long) * m, st));
+  VG_CUDA(cudaMemcpyAsync(map->keys, ukeys, sizeof(long long) * m, cudaMemcpyDeviceToDevice, st));
+  k_cell_stats<<<(m + 127) / 128, 128, 0, st>>>(offsets, counts, perm, cl->xyz64, cl->cov64, m,
+                                                map->means, map->covs, map->counts);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  cudaFreeAsync(keys, st);
+  cudaFreeAsync(keys_sorted, st);
+  cudaFreeAsync(ukeys, st);
+  cudaFreeAsync(idx, st);
+  cudaFreeAsync(perm, st);
+  cudaFreeAsync(counts, st);
+  cudaFreeAsync(offsets, st);
+  cudaFreeAsync(num_runs, st);
+  cudaFreeAsync(tmp, st);
+  return launch_map_finish(ctx, map);
+}

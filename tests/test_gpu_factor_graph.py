@@ -1,0 +1,115 @@
+"""End-to-end through the drop-in boundary: MatchingCostFactor inside a factor graph's LM
+(the reference's test_factor_graph.py:120-139 and :174-191 scenarios), plus the batching
+shim's single-launch behaviour."""
+
+import numpy as np
+import pytest
+
+from oracle import vgicp_oracle as O
+from paper_2202_00242_b200 import geometry as G
+from paper_2202_00242_b200 import registration as RG
+from paper_2202_00242_b200.factor_graph import (
+    _BATCHER,
+    FactorGraph,
+    MatchingCostFactor,
+    PriorFactor,
+    submap_key,
+)
+from paper_2202_00242_b200.preprocess import make_frame
+
+pytestmark = pytest.mark.gpu
+
+
+def box_points(rng, n_per_wall=150, size=(6.0, 5.0, 3.0), center=(0.17, 0.13, 0.11)):
+    sx, sy, sz = size
+    pts = []
+    for _ in range(n_per_wall):
+        u, v = rng.uniform(0, 1, 2)
+        pts += [[u * sx - sx / 2, v * sy - sy / 2, -sz / 2], [u * sx - sx / 2, v * sy - sy / 2, sz / 2],
+                [u * sx - sx / 2, -sy / 2, v * sz - sz / 2], [u * sx - sx / 2, sy / 2, v * sz - sz / 2],
+                [-sx / 2, u * sy - sy / 2, v * sz - sz / 2], [sx / 2, u * sy - sy / 2, v * sz - sz / 2]]
+    return np.asarray(pts) + np.asarray(center)
+
+
+def plane_cloud(rng):
+    pts = box_points(rng)
+    covs, _ = O.estimate_covariances(pts, O.knn_search(pts, 10))
+    return pts, covs
+
+
+def two_pose_graph(seed=3):
+    rng = np.random.default_rng(seed)
+    pts, covs = plane_cloud(rng)
+    vmap = RG.build_voxelmap(make_frame(pts, covs), 0.5)
+    true_rel = G.Se3Pose(G.so3_exp([0.02, -0.03, 0.3]), np.array([0.4, -0.2, 0.1]))
+    moved = make_frame(G.pose_apply(G.pose_inverse(true_rel), pts), covs)
+    g = FactorGraph()
+    g.add_variable(submap_key(0), G.Se3Pose.identity())
+    perturb = np.concatenate([rng.normal(size=3) * (5 * np.pi / 180 / np.sqrt(3)),
+                              rng.normal(size=3) * (0.1 / np.sqrt(3))])
+    g.add_variable(submap_key(1), G.pose_retract(true_rel, perturb))
+    g.add_factor(PriorFactor(submap_key(0), G.Se3Pose.identity(), np.full(6, 1e6)))
+    g.add_factor(MatchingCostFactor(submap_key(1), moved, vmap, key_target=submap_key(0)))
+    return g, true_rel
+
+
+def test_two_pose_registration_recovers_truth():
+    g, true_rel = two_pose_graph()
+    res = g.optimize_lm()
+    err = G.pose_local(res.estimates[submap_key(1)], true_rel)
+    assert np.linalg.norm(err[3:]) < 1e-3
+    assert np.linalg.norm(err[:3]) < 1e-3
+
+
+def test_lm_is_deterministic():
+    a = two_pose_graph().optimize_lm()
+    b = two_pose_graph().optimize_lm()
+    assert a.iterations == b.iterations and a.final_cost == b.final_cost
+    for k in a.estimates:
+        assert np.array_equal(a.estimates[k].translation, b.estimates[k].translation)
+
+
+def test_shim_batches_all_factors_in_one_launch():
+    rng = np.random.default_rng(11)
+    pts, covs = plane_cloud(rng)
+    vmap = RG.build_voxelmap(make_frame(pts, covs), 0.5)
+    g = FactorGraph()
+    g.add_variable(submap_key(0), G.Se3Pose.identity())
+    g.add_factor(PriorFactor(submap_key(0), G.Se3Pose.identity(), np.full(6, 1e6)))
+    factors = []
+    for i in range(1, 9):
+        rel = G.Se3Pose(G.so3_exp(rng.uniform(-0.05, 0.05, 3)), rng.uniform(-0.1, 0.1, 3))
+        g.add_variable(submap_key(i), rel)
+        f = MatchingCostFactor(submap_key(i), make_frame(G.pose_apply(G.pose_inverse(rel), pts),
+                                                         covs), vmap, key_target=submap_key(0))
+        g.add_factor(f)
+        factors.append(f)
+    before = _BATCHER.evaluations
+    costs = [f.cost(g.values) for f in factors]
+    assert _BATCHER.evaluations == before + 1  # one batched evaluation served all 8
+    # and each equals the stand-alone oracle cost
+    for f, c in zip(factors, costs):
+        tij = G.pose_compose(G.pose_inverse(g.values[f.keys[1]]), g.values[f.keys[0]])
+        ref_map = (0.5, vmap.keys, vmap.means, vmap.covs, vmap.counts)
+        rc, _ = O.matching_cost(f.source.points, covs, ref_map, tij.rotation.matrix(),
+                                tij.translation)
+        assert abs(c - rc) <= max(1e-4 * abs(rc), 1e-6)
+    before = _BATCHER.evaluations
+    lins = [f.linearize(g.values) for f in factors]
+    assert _BATCHER.evaluations == before + 1
+    assert all(lin.h[(0, 0)].shape == (6, 6) for lin in lins)
+
+
+def test_unary_factor_in_graph():
+    rng = np.random.default_rng(13)
+    pts, covs = plane_cloud(rng)
+    vmap = RG.build_voxelmap(make_frame(pts, covs), 0.5)
+    true = G.Se3Pose(G.so3_exp([0.0, 0.0, 0.1]), np.array([0.2, 0.1, 0.0]))
+    g = FactorGraph()
+    g.add_variable(submap_key(0), G.pose_retract(true, [0.01, -0.01, 0.02, 0.03, -0.02, 0.01]))
+    g.add_factor(MatchingCostFactor(submap_key(0), make_frame(G.pose_apply(G.pose_inverse(true),
+                                                                           pts), covs),
+                                    vmap, fixed_target_pose=G.Se3Pose.identity()))
+    res = g.optimize_lm()
+    err = G.pose_local(res.estimates[submap_key(0)], true)
+    assert np.linalg.norm(err) < 1e-3

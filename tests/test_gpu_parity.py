@@ -1,0 +1,308 @@
+"""GPU parity: libvgicp (through the drop-in API / C-ABI) vs the pinned CPU oracle and the
+reference's golden fixtures.  Bar: bit-exact keys, rows, inliers, voxel-map arrays; H/b/cost
+within 1e-4 relative, 1e-6 absolute, per element."""
+
+import numpy as np
+import pytest
+
+from oracle import vgicp_oracle as O
+from paper_2202_00242_b200 import _lib, synthetic
+from paper_2202_00242_b200 import geometry as G
+from paper_2202_00242_b200 import registration as RG
+from paper_2202_00242_b200.errors import DegenerateConstraint
+from paper_2202_00242_b200.factor_graph import MatchingCostFactor, submap_key
+from paper_2202_00242_b200.preprocess import make_frame
+
+pytestmark = pytest.mark.gpu
+
+REL, ABS = 1e-4, 1e-6  # north_star parity tolerance for fp32 H/b/error vs fp64
+NAMES = ("h_ii", "b_i", "h_ij", "h_jj", "b_j")
+
+
+def assert_tol(got, ref, what=""):
+    got, ref = np.asarray(got, float), np.asarray(ref, float)
+    assert got.shape == ref.shape, what
+    bad = np.abs(got - ref) > np.maximum(REL * np.abs(ref), ABS)
+    assert not bad.any(), f"{what}: worst ratio " \
+        f"{np.max(np.abs(got - ref) / np.maximum(REL * np.abs(ref), ABS)):.3g}"
+
+
+def assert_lin(lin, ref, unary):
+    assert lin.inlier_count == ref["inliers"]
+    assert_tol(lin.cost, ref["cost"], "cost")
+    assert_tol(lin.h_ii, ref["h_ii"], "h_ii")
+    assert_tol(lin.b_i, ref["b_i"], "b_i")
+    if unary:
+        assert lin.h_ij is None and lin.h_jj is None and lin.b_j is None
+    else:
+        for k in ("h_ij", "h_jj", "b_j"):
+            assert_tol(getattr(lin, k), ref[k], k)
+
+
+def pose_from_Rt(R, t):
+    return G.Se3Pose(G.Rotation(_quat_from_matrix(R)), t)
+
+
+def _quat_from_matrix(m):
+    tr = m[0, 0] + m[1, 1] + m[2, 2]
+    s = np.sqrt(tr + 1.0) * 2.0
+    return np.array([(m[2, 1] - m[1, 2]) / s, (m[0, 2] - m[2, 0]) / s, (m[1, 0] - m[0, 1]) / s,
+                     0.25 * s])
+
+
+class _TPose:
+    """A transform handed over exactly (R, t) — bypasses quaternion round trips."""
+
+    class _Rot:
+        def __init__(self, R):
+            self._R = R
+
+        def matrix(self):
+            return self._R
+
+    def __init__(self, R, t):
+        self.rotation = self._Rot(np.asarray(R, float))
+        self.translation = np.asarray(t, float)
+
+
+def golden_map(g, res=0.5):
+    tag = str(res).replace(".", "p")
+    return (res, g[f"map{tag}_keys"], g[f"map{tag}_means"], g[f"map{tag}_covs"],
+            g[f"map{tag}_counts"])
+
+
+# ---- keys / maps ----------------------------------------------------------------------------
+
+def test_pack_voxel_keys_bit_exact(golden):
+    from paper_2202_00242_b200.preprocess import pack_voxel_keys
+
+    g = golden("keys")
+    for res in (0.25, 0.4, 0.5, 1.0, 2.0):
+        assert np.array_equal(pack_voxel_keys(g["points"], res), g[f"keys_{res}"]), res
+
+
+@pytest.mark.parametrize("res", [0.5, 1.0])
+def test_build_voxelmap_bit_exact(golden, res):
+    g = golden("registration")
+    frame = make_frame(g["tgt_points"], g["tgt_covs"])
+    vm = RG.build_voxelmap(frame, res)
+    tag = str(res).replace(".", "p")
+    assert len(vm) == len(g[f"map{tag}_keys"])
+    assert np.array_equal(vm.keys, g[f"map{tag}_keys"])
+    assert np.array_equal(vm.counts, g[f"map{tag}_counts"])
+    assert np.array_equal(vm.means, g[f"map{tag}_means"])
+    assert np.array_equal(vm.covs, g[f"map{tag}_covs"])
+
+
+def test_build_voxelmap_requires_covs_and_handles_empty():
+    with pytest.raises(ValueError):
+        RG.build_voxelmap(make_frame(np.zeros((3, 3))), 1.0)
+    assert len(RG.build_voxelmap(make_frame(np.zeros((0, 3)), np.zeros((0, 3, 3))), 1.0)) == 0
+
+
+# ---- lookup / match / linearize at the golden cases -----------------------------------------
+
+@pytest.mark.parametrize("adopt", [False, True])
+@pytest.mark.parametrize("case", range(6))
+def test_golden_cases(golden, case, adopt):
+    """adopt=True: map handed over as reference arrays (vg_map_from_arrays);
+    adopt=False: map built on the GPU (vg_map_build)."""
+    g = golden("registration")
+    src = make_frame(g["src_points"], g["src_covs"])
+    if adopt:
+        _, k, mu, c, n = golden_map(g)
+        vm = RG.GaussianVoxelMap(0.5, k, mu, c, n)
+    else:
+        vm = RG.build_voxelmap(make_frame(g["tgt_points"], g["tgt_covs"]), 0.5)
+    R, t = g[f"case{case}_R"], g[f"case{case}_t"]
+    tij = _TPose(R, t)
+    unary = bool(g[f"case{case}_unary"])
+    terms = RG.match_terms(src, vm, tij)
+    assert np.array_equal(terms.rows, g[f"case{case}_rows"])
+    assert terms.inliers == int(g[f"case{case}_inliers"])
+    assert_tol(terms.cost, g[f"case{case}_cost"], "cost")
+    assert RG.overlap_rate(src, vm, tij) == float(g[f"case{case}_overlap"])
+    c, n = RG.matching_cost(src, vm, tij)
+    assert n == int(g[f"case{case}_inliers"])
+    assert_tol(c, g[f"case{case}_cost"], "matching_cost")
+    lin = RG.linearize_from_terms(src, terms, tij, target_fixed=unary)
+    ref = {k: (g[f"case{case}_{k}"] if f"case{case}_{k}" in g.files else None)
+           for k in NAMES + ("cost", "inliers")}
+    ref["inliers"] = int(ref["inliers"])
+    assert_lin(lin, ref, unary)
+
+
+def test_match_terms_per_point(golden):
+    g = golden("registration")
+    src = make_frame(g["src_points"], g["src_covs"])
+    vm_t = golden_map(g)
+    vm = RG.GaussianVoxelMap(0.5, *vm_t[1:])
+    R, t = g["case1_R"], g["case1_t"]
+    ours = RG.match_terms(src, vm, _TPose(R, t))
+    ref = O.match_terms(g["src_points"], g["src_covs"], vm_t, R, t)
+    assert np.array_equal(ours.hit, ref["hit"])
+    np.testing.assert_allclose(ours.moved, ref["moved"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(ours.d, ref["d"], rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(ours.weight, ref["weight"], rtol=1e-5, atol=1e-4)
+    np.testing.assert_allclose(ours.wd, ref["wd"], rtol=1e-4, atol=1e-4)
+
+
+def test_lookup_and_cell(golden):
+    g = golden("registration")
+    vm_t = golden_map(g)
+    vm = RG.GaussianVoxelMap(0.5, *vm_t[1:])
+    pts = np.random.default_rng(3).uniform(-4, 4, (5000, 3))
+    assert np.array_equal(vm.lookup(pts), O.lookup(vm_t, pts))
+    idx = vm.occupied_indices()[7]
+    mean, cov, cnt = vm.cell(idx)
+    assert np.array_equal(mean, vm_t[2][7]) and cnt == vm_t[4][7]
+    with pytest.raises(KeyError):
+        vm.cell([10000, 0, 0])
+
+
+def test_non_fp32_points_keep_exact_keys():
+    """Points that are not fp32-representable take the fp64 path: rows stay bit-exact."""
+    rng = np.random.default_rng(12)
+    tgt = rng.uniform(-3, 3, (3000, 3))  # fp64, not fp32-exact
+    covs = np.tile(np.eye(3) * 0.01, (3000, 1, 1))
+    vm = RG.build_voxelmap(make_frame(tgt, covs), 0.5)
+    ref_map = O.build_voxelmap(tgt, covs, 0.5)
+    assert np.array_equal(vm.keys, ref_map[1]) and np.array_equal(vm.means, ref_map[2])
+    src = tgt[:1500] + rng.normal(scale=0.02, size=(1500, 3))
+    R = G.so3_exp([0.01, -0.02, 0.03]).matrix()
+    t = np.array([0.05, -0.02, 0.01])
+    terms = RG.match_terms(make_frame(src, covs[:1500]), vm, _TPose(R, t))
+    ref = O.match_terms(src, covs[:1500], ref_map, R, t)
+    assert np.array_equal(terms.rows, ref["rows"])
+
+
+# ---- config 1 at full size ------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def config1():
+    source, target, t_i, t_j = synthetic.config1_scans()
+    cs, _ = O.estimate_covariances(source, O.knn_search(source, 10))
+    ct, _ = O.estimate_covariances(target, O.knn_search(target, 10))
+    return source, cs, target, ct, t_i, t_j
+
+
+def test_config1_single_factor(config1, golden):
+    source, cs, target, ct, t_i, t_j = config1
+    vm = RG.build_voxelmap(make_frame(target, ct), 0.5)
+    ref_map = O.build_voxelmap(target, ct, 0.5)
+    assert np.array_equal(vm.keys, ref_map[1])
+    assert np.array_equal(vm.means, ref_map[2]) and np.array_equal(vm.covs, ref_map[3])
+    src = make_frame(source, cs)
+    lin = RG.linearize_matching_cost(src, vm, t_i, t_j)
+    tij = G.pose_compose(G.pose_inverse(t_j), t_i)
+    R, t = tij.rotation.matrix(), tij.translation
+    ref = O.linearize(source, cs, ref_map, R, t)
+    assert_lin(lin, ref, False)
+    # correspondence rows bit-exact; count points within 1e-12*res of a voxel face (expect 0)
+    moved = source @ R.T + t
+    frac = moved / 0.5 - np.floor(moved / 0.5)
+    near_face = np.sum((frac < 1e-12) | (frac > 1 - 1e-12))
+    assert near_face == 0
+    terms = RG.match_terms(src, vm, tij)
+    assert np.array_equal(terms.rows, O.lookup(ref_map, moved))
+    assert lin.inlier_count == int(golden("config1")["inliers"])
+
+
+def test_config1_converged_pose(config1):
+    """b -> 0 with heavy cancellation at the true pose; the 1e-6 absolute floor carries it."""
+    source, cs, target, ct, _, _ = config1
+    vm = RG.build_voxelmap(make_frame(target, ct), 0.5)
+    ref_map = O.build_voxelmap(target, ct, 0.5)
+    p_i = synthetic.yaw_pose(0.05, [0.3, 0.1, 0.0])
+    lin = RG.linearize_matching_cost(make_frame(source, cs), vm, p_i, G.Se3Pose.identity())
+    tij = G.pose_compose(G.pose_inverse(G.Se3Pose.identity()), p_i)
+    ref = O.linearize(source, cs, ref_map, tij.rotation.matrix(), tij.translation)
+    assert_lin(lin, ref, False)
+
+
+# ---- batched path (pose table, many factors) ------------------------------------------------
+
+@pytest.fixture(scope="module")
+def small_graph():
+    """12 submaps in the room, 600-point sources vs 1.0 m maps, nearest-5 factors."""
+    rng = np.random.default_rng(21)
+    poses = synthetic.random_submap_poses(rng, 12)
+    dirs = synthetic.ray_table(128, 32)
+    scans, covs, maps, srcs = [], [], [], []
+    for i, p in enumerate(poses):
+        s = synthetic.scan(p, dirs, np.random.default_rng(100 + i))
+        c, _ = O.estimate_covariances(s, O.knn_search(s, 10))
+        scans.append(s)
+        covs.append(c)
+        maps.append(O.build_voxelmap(s, c, 1.0))
+        sel = np.sort(rng.choice(len(s), 600, replace=False))
+        srcs.append((s[sel], c[sel]))
+    pairs = synthetic.nearest_pairs(poses, 5)
+    est = [G.pose_retract(p, synthetic.perturbation(rng, 0.05, 1.0)) for p in poses]
+    return poses, est, scans, covs, maps, srcs, pairs
+
+
+def test_batch_pose_table_vs_oracle(small_graph):
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
+    F = len(pairs)
+    unary = [(f % 7) == 3 for f in range(F)]
+    table = np.array([G.pose_row(p) for p in est])
+    batch = _lib.DeviceBatch([clouds[i] for i, _ in pairs], [dmaps[j] for _, j in pairs], unary,
+                             [10] * F, pairs[:, 0], pairs[:, 1])
+    out = batch.linearize_poses(table, _lib.MODE_LINEARIZE)
+    cost_out = batch.linearize_poses(table, _lib.MODE_COST)
+    R, t = O.relative_transforms(table, pairs[:, 0], pairs[:, 1])
+    checked = 0
+    for f, (i, j) in enumerate(pairs):
+        try:
+            ref = O.linearize(srcs[i][0], srcs[i][1], maps[j], R[f], t[f], target_fixed=unary[f])
+        except ValueError:  # degenerate: zero blocks, inliers below the gate
+            assert np.all(out[f][:90] == 0) and out[f][91] < 10
+            continue
+        assert_lin(RG.unpack_record(out[f], unary[f]), ref, unary[f])
+        assert cost_out[f][1] == ref["inliers"]
+        assert_tol(cost_out[f][0], ref["cost"], "cost mode")
+        checked += 1
+    assert checked >= F // 2
+
+
+def test_batch_explicit_transforms_and_determinism(small_graph):
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
+    F = len(pairs)
+    batch = _lib.DeviceBatch([clouds[i] for i, _ in pairs], [dmaps[j] for _, j in pairs],
+                             [False] * F, [10] * F)
+    table = np.array([G.pose_row(p) for p in est])
+    R, t = O.relative_transforms(table, pairs[:, 0], pairs[:, 1])
+    T = np.concatenate([R.reshape(F, 9), t], axis=1)
+    a = batch.linearize(T)
+    b = batch.linearize(T)
+    assert np.array_equal(a, b)  # bitwise deterministic
+    pt = _lib.DeviceBatch([clouds[i] for i, _ in pairs], [dmaps[j] for _, j in pairs],
+                          [False] * F, [10] * F, pairs[:, 0], pairs[:, 1]).linearize_poses(table)
+    for f in range(F):
+        if a[f][91] >= 10:
+            assert_tol(pt[f], a[f], "pose-table vs explicit")
+
+
+# ---- drop-in factor semantics ---------------------------------------------------------------
+
+def test_factor_degenerate_and_empty():
+    a = make_frame([[0, 0, 0]], np.eye(3)[None] * 0.01)
+    b = make_frame([[50, 0, 0]], np.eye(3)[None] * 0.01)
+    vm = RG.build_voxelmap(b, 0.5)
+    assert RG.matching_cost(a, vm, G.Se3Pose.identity()) == (0.0, 0)
+    with pytest.raises(DegenerateConstraint):
+        RG.linearize_matching_cost(a, vm, G.Se3Pose.identity(), G.Se3Pose.identity())
+    f = MatchingCostFactor(submap_key(0), a, vm, key_target=submap_key(1))
+    vals = {submap_key(0): G.Se3Pose.identity(), submap_key(1): G.Se3Pose.identity()}
+    assert f.cost(vals) == 0.0
+    lin = f.linearize(vals)
+    assert lin.cost == 0.0 and all(np.all(h == 0) for h in lin.h.values())
+    empty = make_frame(np.zeros((0, 3)), np.zeros((0, 3, 3)))
+    assert RG.overlap_rate(empty, vm, G.Se3Pose.identity()) == 0.0
+    with pytest.raises(DegenerateConstraint):
+        RG.linearize_matching_cost(empty, vm, G.Se3Pose.identity(), G.Se3Pose.identity())

@@ -1,0 +1,90 @@
+"""CPU checks of the host-side logic and of the kernel's arithmetic design.
+
+kernel_model restates K4/K5 in NumPy: in fp64 the compact 29-value accumulation + adjoint
+expansion must reproduce the oracle's explicit-Jacobian blocks to ~1e-12 (the algebra is
+exact); with the kernel's precision choices (fp64 covariances and inverse, fp32 per-point
+Jacobian terms and lane sums) it must stay within the 1e-4 rel / 1e-6 abs parity bar.
+"""
+
+import numpy as np
+import pytest
+
+import kernel_model as KM
+from oracle import vgicp_oracle as O
+from paper_2202_00242_b200 import geometry as G
+from paper_2202_00242_b200.registration import unpack_record, unpack_sym6
+
+NAMES = ("h_ii", "b_i", "h_ij", "h_jj", "b_j")
+
+
+def _map(g, res=0.5):
+    tag = str(res).replace(".", "p")
+    return (res, g[f"map{tag}_keys"], g[f"map{tag}_means"], g[f"map{tag}_covs"],
+            g[f"map{tag}_counts"])
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_adjoint_expansion_exact_in_fp64(golden, case):
+    g = golden("registration")
+    vm = _map(g)
+    R, t, unary = g[f"case{case}_R"], g[f"case{case}_t"], bool(g[f"case{case}_unary"])
+    ref = O.linearize(g["src_points"], g["src_covs"], vm, R, t, target_fixed=unary)
+    got = KM.expand(KM.compact(g["src_points"], g["src_covs"], vm, R, t), R, t, unary)
+    for k in NAMES:
+        if ref[k] is not None:
+            np.testing.assert_allclose(got[k], ref[k], rtol=1e-9, atol=1e-7)
+    assert got["inliers"] == ref["inliers"]
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_kernel_precision_budget(golden, case):
+    """fp32 per-point Jacobian terms + fp32 lane sums stay inside the parity tolerance."""
+    g = golden("registration")
+    vm = _map(g)
+    R, t, unary = g[f"case{case}_R"], g[f"case{case}_t"], bool(g[f"case{case}_unary"])
+    ref = O.linearize(g["src_points"], g["src_covs"], vm, R, t, target_fixed=unary)
+    got = KM.expand(KM.compact(g["src_points"], g["src_covs"], vm, R, t, dtype=np.float32),
+                    R, t, unary)
+    for k in NAMES:
+        if ref[k] is not None:
+            assert KM.within_tolerance(got[k], ref[k]) < 0.5, k
+    assert KM.within_tolerance(got["cost"], ref["cost"]) < 0.5
+
+
+def test_record_unpack_layout():
+    rec = np.arange(92, dtype=float)
+    lin = unpack_record(rec, unary=False)
+    assert lin.h_ii[0, 0] == 0 and lin.h_ii[0, 5] == 5 and lin.h_ii[5, 0] == 5
+    assert lin.h_ii[5, 5] == 20 and lin.h_ij[0, 0] == 21 and lin.h_ij[5, 5] == 56
+    assert lin.h_jj[0, 0] == 57 and lin.b_i[0] == 78 and lin.b_j[5] == 89
+    assert lin.cost == 90 and lin.inlier_count == 91
+    u = unpack_record(rec, unary=True)
+    assert u.h_ij is None and u.b_j is None
+
+
+def test_sym6_roundtrip():
+    a = np.random.default_rng(0).normal(size=(6, 6))
+    a = a + a.T
+    iu = np.triu_indices(6)
+    assert np.array_equal(unpack_sym6(a[iu]), a)
+
+
+def test_pose_table_composition_matches_host_geometry():
+    rng = np.random.default_rng(5)
+    poses = [G.Se3Pose(G.so3_exp(rng.uniform(-2, 2, 3)), rng.uniform(-20, 20, 3))
+             for _ in range(8)]
+    table = np.array([G.pose_row(p) for p in poses])
+    vs, vt = np.array([0, 3, 5, 7]), np.array([1, 2, 6, 0])
+    R, t = O.relative_transforms(table, vs, vt)
+    for f in range(4):
+        tij = G.pose_compose(G.pose_inverse(poses[vt[f]]), poses[vs[f]])
+        np.testing.assert_allclose(R[f], tij.rotation.matrix(), atol=1e-15, rtol=0)
+        np.testing.assert_allclose(t[f], tij.translation, atol=1e-13, rtol=0)
+
+
+def test_geometry_mirror_matches_reference_ops():
+    rng = np.random.default_rng(9)
+    for _ in range(20):
+        xi = rng.uniform(-1, 1, 6)
+        p = G.pose_retract(G.Se3Pose.identity(), xi)
+        np.testing.assert_allclose(G.pose_local(p, G.Se3Pose.identity()), xi, atol=1e-12)
