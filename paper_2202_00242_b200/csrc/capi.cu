@@ -274,7 +274,6 @@ int vg_map_destroy(vg_map* m) {
   if (!m) return VG_OK;
   vg_ctx* ctx = m->ctx;
   dfree(ctx, m->table);
-  dfree(ctx, m->vox);
   dfree(ctx, m->keys);
   dfree(ctx, m->means);
   dfree(ctx, m->covs);

@@ -3,8 +3,8 @@
 // HBM layouts:
 //   cloud  : SoA, 64 B/point: a[i] = (x, y, z) fp32, covariance as three fp64 double2 arrays
 //            + optional fp64 xyz (n x 3) when the points are not exactly fp32 (keys stay exact)
-//   map    : open-addressing hash table of 16 B slots (key -> row, load factor <= 0.5) and a
-//            row-indexed array of 64 B voxel records (cell-local fp32 mean + fp64 covariance).
+//   map    : open-addressing hash table (load factor <= 0.5) of 96 B slots carrying the
+//            voxel's key, reference row and fp64 Gaussian.
 //   work   : (factor, chunk) items, one warp per item; fp64 partials, fixed-order reduce.
 #pragma once
 #include <cstdint>
@@ -13,30 +13,25 @@
 namespace vg {
 
 constexpr int kKeyOffset = 1 << 20;   // preprocess.py:21-22
-constexpr int kWarpsPerBlock = 8;
+constexpr int kWarpsPerBlock = 4;
 constexpr int kPartialStride = 32;    // doubles per work-item partial (29 used)
 constexpr int kMaxChunk = 512;        // points per work item => <= 16 points per lane
 
-// 16-byte hash slot: packed key -> reference row.  row < 0 marks an empty slot (any int64
-// can be a key, so emptiness is not encoded in the key).
-struct __align__(16) Slot {
-  long long key;  // packed voxel key (registration.py:36-42 `keys`)
-  int row;        // rank of the key in ascending order == reference row index
-  int pad;
+// 96-byte inline hash slot: packed key, reference row and the voxel Gaussian in fp64.
+// row < 0 marks an empty slot (any int64 can be a key).  A hit reads exactly the slot's
+// three 32 B sectors with no dependent second gather.  Mean and covariance stay fp64: the
+// fused covariance C' + R C R^T has condition ~1e3 for plane-like cells and the parity bar
+// is per element (1e-4 rel) on H/b entries that cancel by up to ~1e5 — fp32 storage or fp32
+// per-point math exceeds it (tests/kernel_model.py, tests/test_host_logic.py quantify it).
+struct __align__(32) Slot {
+  long long key;    // packed voxel key (registration.py:36-42 `keys`)
+  int row;          // rank of the key in ascending order == reference row index
+  int pad0;
+  double mean[3];   // voxel mean (registration.py:90-92)
+  double cov[6];    // voxel covariance c00 c01 c02 c11 c12 c22 (registration.py:93-97)
+  double pad1;
 };
-static_assert(sizeof(Slot) == 16, "slot must be 16 B");
-
-// 64-byte voxel record, gathered by row.  Covariances stay fp64: a cell's fused covariance
-// C' + R C R^T has condition ~1e3 for plane-like neighbourhoods, and fp32 storage alone
-// perturbs W = F^-1 by ~3e-5 relative — enough to break the per-element 1e-4 parity bar on
-// cancelling H entries (tests/kernel_model.py quantifies it).
-struct __align__(64) VoxelRec {
-  float4 mean;    // voxel mean relative to the cell centre (x, y, z), pad
-  double2 c0;     // c00 c01
-  double2 c1;     // c02 c11
-  double2 c2;     // c12 c22
-};
-static_assert(sizeof(VoxelRec) == 64, "voxel record must be 64 B");
+static_assert(sizeof(Slot) == 96, "slot must be 96 B");
 
 struct CloudView {
   const float4* a;      // n: x, y, z (fp32), pad
@@ -49,7 +44,6 @@ struct CloudView {
 
 struct MapView {
   const Slot* table;
-  const VoxelRec* vox;
   double res;
   double inv_res;
   unsigned mask;        // capacity - 1
@@ -104,8 +98,8 @@ __device__ __forceinline__ unsigned slot_of(long long key, int shift) {
   return (unsigned)(((unsigned long long)key * 0x9E3779B97F4A7C15ull) >> shift);
 }
 
-// Probe for `key`; returns the reference row or -1 (one 16 B load per probe).  Average probe length <= 1.5 on hits
-// (load factor <= 0.5).
+// Probe for `key`; returns the slot index or -1 (one 16 B header load per probe; average
+// probe length <= 1.5 on hits at load factor <= 0.5).
 __device__ __forceinline__ int probe(const MapView& mv, long long key) {
   if (mv.m == 0) return -1;
   unsigned h = slot_of(key, mv.shift);
@@ -113,7 +107,7 @@ __device__ __forceinline__ int probe(const MapView& mv, long long key) {
     const int4 s = __ldg(reinterpret_cast<const int4*>(mv.table + h));
     const long long k = ((long long)(unsigned)s.y << 32) | (unsigned)s.x;
     if (s.z < 0) return -1;
-    if (k == key) return s.z;
+    if (k == key) return (int)h;
     h = (h + 1) & mv.mask;
   }
 }

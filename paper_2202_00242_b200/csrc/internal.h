@@ -51,7 +51,6 @@ struct vg_map {
   unsigned capacity = 0;
   int log2cap = 0;
   vg::Slot* table = nullptr;
-  vg::VoxelRec* vox = nullptr;  // m records, row-indexed
   // reference arrays (device, fp64/int64): keys sorted ascending, means m*3, covs m*9
   long long* keys = nullptr;
   double* means = nullptr;
@@ -60,7 +59,6 @@ struct vg_map {
   vg::MapView view() const {
     vg::MapView v;
     v.table = table;
-    v.vox = vox;
     v.res = res;
     v.inv_res = 1.0 / res;
     v.mask = capacity - 1;

@@ -5,14 +5,13 @@
 // :251-269 (linearize_matching_cost), factor_graph.py:253-308 (MatchingCostFactor).
 //
 // Per correspondence the kernel reads the source Gaussian (fp32 xyz + fp64 covariance, SoA,
-// coalesced), one 16 B hash slot and one 64 B voxel record, and does all math in registers:
-//   x = R p + t (fp64) -> key (fp64 floor, bit-exact) -> probe -> d = mu' - x (cell-local,
-//   fp32) -> W = (C' + R C R^T)^-1 (fp64 fused covariance + adjugate, rounded to fp32 after
-//   inversion) -> accumulate the 6x6 target-frame block about the source origin (29 values,
+// coalesced) and one 96 B hash slot carrying the voxel Gaussian, and does all math in
+// registers, in fp64:
+//   x = R p + t -> key (bit-exact floor) -> probe -> d = mu' - x -> W = (C' + R C R^T)^-1
+//   (adjugate) -> accumulate the 6x6 target-frame block about the source origin (29 values,
 //   H_ii, H_ij, H_jj, b_i, b_j are exact fp64 adjoint transforms of it, so
 //   nothing else is accumulated per point).
-// Lane sums are fp32 over <= 16 points; the warp reduction and everything after is fp64 and
-// fixed-order, so results are deterministic run to run.
+// The warp reduction and the per-factor sum are fixed-order, so results are deterministic.
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -21,11 +20,11 @@
 namespace vg {
 
 struct PointTerms {
-  float d[3];
-  float W[6];   // 00 01 02 11 12 22
-  float wd[3];
-  float xp[3];  // x - t == R p : lever arm about the source origin
-  float cost;
+  double d[3];
+  double W[6];   // 00 01 02 11 12 22
+  double wd[3];
+  double xp[3];  // x - t == R p : lever arm about the source origin
+  double cost;
 };
 
 __device__ __forceinline__ void load_T(const double* __restrict__ T, double (&R)[9],
@@ -59,37 +58,25 @@ __device__ __forceinline__ void load_point(const CloudView& cv, long long i, dou
   }
 }
 
-// centre of the cell with packed key `key` (decoded exactly as occupied_indices,
-// registration.py:65-71); identical for the query and the voxel whenever the keys match.
-__device__ __forceinline__ void cell_centre(long long key, double res, double& cx, double& cy,
-                                            double& cz) {
-  long long ix = (key >> 42) - kKeyOffset;
-  long long iy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
-  long long iz = (key & ((1LL << 21) - 1)) - kKeyOffset;
-  cx = ((double)ix + 0.5) * res;
-  cy = ((double)iy + 0.5) * res;
-  cz = ((double)iz + 0.5) * res;
-}
-
-// fused covariance (fp64), inverse (fp64), residual (cell-local fp32), cost for one
-// correspondence (registration.py:150-156).  W is rounded to fp32 only after inversion, so
-// its error is not amplified by the condition number of C' + R C R^T.
+// fused covariance, inverse, residual and Mahalanobis cost of one correspondence
+// (registration.py:150-156), all fp64.
 __device__ __forceinline__ void point_terms(const double (&R)[9], const CloudView& cv,
-                                            long long i, const VoxelRec* __restrict__ vr,
+                                            long long i, const Slot* __restrict__ sl,
                                             double x, double y, double z, const double (&t)[3],
-                                            double res, long long key, PointTerms& o) {
-  const float4 vm = __ldg(&vr->mean);
-  const double2 v0 = __ldg(&vr->c0), v1 = __ldg(&vr->c1), v2 = __ldg(&vr->c2);
+                                            PointTerms& o) {
+  const double2 m01 = __ldg(reinterpret_cast<const double2*>(&sl->mean[0]));
+  const double2 m2c0 = __ldg(reinterpret_cast<const double2*>(&sl->mean[2]));
+  const double2 c12 = __ldg(reinterpret_cast<const double2*>(&sl->cov[1]));
+  const double2 c34 = __ldg(reinterpret_cast<const double2*>(&sl->cov[3]));
+  const double v5 = __ldg(&sl->cov[5]);
   const double2 s0 = __ldg(cv.c0 + i), s1 = __ldg(cv.c1 + i), s2 = __ldg(cv.c2 + i);
-  double cx, cy, cz;
-  cell_centre(key, res, cx, cy, cz);
-  // d = mu' - moved, formed in cell-local coordinates (registration.py:152)
-  o.d[0] = vm.x - (float)(x - cx);
-  o.d[1] = vm.y - (float)(y - cy);
-  o.d[2] = vm.z - (float)(z - cz);
-  o.xp[0] = (float)(x - t[0]);
-  o.xp[1] = (float)(y - t[1]);
-  o.xp[2] = (float)(z - t[2]);
+  // d = mu' - moved (registration.py:152)
+  o.d[0] = m01.x - x;
+  o.d[1] = m01.y - y;
+  o.d[2] = m2c0.x - z;
+  o.xp[0] = x - t[0];
+  o.xp[1] = y - t[1];
+  o.xp[2] = z - t[2];
   // source covariance C: c00 c01 c02 c11 c12 c22
   const double C00 = s0.x, C01 = s0.y, C02 = s1.x, C11 = s1.y, C12 = s2.x, C22 = s2.y;
   double A[9];  // A = R C
@@ -104,12 +91,12 @@ __device__ __forceinline__ void point_terms(const double (&R)[9], const CloudVie
   auto arT = [&](int r, int c) {
     return fma(A[3 * r], R[3 * c], fma(A[3 * r + 1], R[3 * c + 1], A[3 * r + 2] * R[3 * c + 2]));
   };
-  const double a = v0.x + arT(0, 0);
-  const double b = v0.y + arT(0, 1);
-  const double c = v1.x + arT(0, 2);
-  const double dd = v1.y + arT(1, 1);
-  const double e = v2.x + arT(1, 2);
-  const double f = v2.y + arT(2, 2);
+  const double a = m2c0.y + arT(0, 0);
+  const double b = c12.x + arT(0, 1);
+  const double c = c12.y + arT(0, 2);
+  const double dd = c34.x + arT(1, 1);
+  const double e = c34.y + arT(1, 2);
+  const double f = v5 + arT(2, 2);
   // W = F^-1 by the adjugate (registration.py:113-130)
   const double i00 = fma(dd, f, -e * e);
   const double i01 = fma(c, e, -b * f);
@@ -119,16 +106,16 @@ __device__ __forceinline__ void point_terms(const double (&R)[9], const CloudVie
   const double i22 = fma(a, dd, -b * b);
   const double det = fma(a, i00, fma(b, i01, c * i02));
   const double inv = 1.0 / det;
-  o.W[0] = (float)(i00 * inv);
-  o.W[1] = (float)(i01 * inv);
-  o.W[2] = (float)(i02 * inv);
-  o.W[3] = (float)(i11 * inv);
-  o.W[4] = (float)(i12 * inv);
-  o.W[5] = (float)(i22 * inv);
-  o.wd[0] = fmaf(o.W[0], o.d[0], fmaf(o.W[1], o.d[1], o.W[2] * o.d[2]));
-  o.wd[1] = fmaf(o.W[1], o.d[0], fmaf(o.W[3], o.d[1], o.W[4] * o.d[2]));
-  o.wd[2] = fmaf(o.W[2], o.d[0], fmaf(o.W[4], o.d[1], o.W[5] * o.d[2]));
-  o.cost = fmaf(o.d[0], o.wd[0], fmaf(o.d[1], o.wd[1], o.d[2] * o.wd[2]));
+  o.W[0] = i00 * inv;
+  o.W[1] = i01 * inv;
+  o.W[2] = i02 * inv;
+  o.W[3] = i11 * inv;
+  o.W[4] = i12 * inv;
+  o.W[5] = i22 * inv;
+  o.wd[0] = fma(o.W[0], o.d[0], fma(o.W[1], o.d[1], o.W[2] * o.d[2]));
+  o.wd[1] = fma(o.W[1], o.d[0], fma(o.W[3], o.d[1], o.W[4] * o.d[2]));
+  o.wd[2] = fma(o.W[2], o.d[0], fma(o.W[4], o.d[1], o.W[5] * o.d[2]));
+  o.cost = fma(o.d[0], o.wd[0], fma(o.d[1], o.wd[1], o.d[2] * o.wd[2]));
 }
 
 // ---- warp reductions ---------------------------------------------------------------------
@@ -151,7 +138,7 @@ __device__ __forceinline__ double warp_transpose_reduce32(double (&v)[32], int l
 // ---- K4: fused linearize / cost over (factor, chunk) work items --------------------------
 // MODE 0: full (29-value partial per item); MODE 1: cost + inliers only.
 template <int MODE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     k_linearize(const ItemDev* __restrict__ items, int n_items,
                 const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
                 const MapView* __restrict__ maps, double* __restrict__ partials) {
@@ -166,9 +153,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const MapView mv = maps[__ldg(&f->map)];
 
   // lane accumulators: P(6) N(9) S(6) br(3) bt(3) cost(1)
-  float acc[28];
+  double acc[28];
 #pragma unroll
-  for (int i = 0; i < 28; ++i) acc[i] = 0.f;
+  for (int i = 0; i < 28; ++i) acc[i] = 0.0;
   int inl = 0;
 
   for (int i = it.begin + lane; i < it.end; i += 32) {
@@ -180,47 +167,46 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     const long long key = pack_key(floor_div(x, mv.res, mv.inv_res),
                                    floor_div(y, mv.res, mv.inv_res),
                                    floor_div(z, mv.res, mv.inv_res));
-    const int row = probe(mv, key);
-    if (row < 0) continue;  // misses contribute nothing (registration.py:150-156)
+    const int slot = probe(mv, key);
+    if (slot < 0) continue;  // misses contribute nothing (registration.py:150-156)
     ++inl;
     PointTerms o;
-    point_terms(R, cv, i, mv.vox + row, x, y, z, t, mv.res, key, o);
+    point_terms(R, cv, i, mv.table + slot, x, y, z, t, o);
     if (MODE == 1) {
       acc[27] += o.cost;
       continue;
     }
-    const float vx = o.xp[0], vy = o.xp[1], vz = o.xp[2];
-    const float W00 = o.W[0], W01 = o.W[1], W02 = o.W[2], W11 = o.W[3], W12 = o.W[4],
-                W22 = o.W[5];
+    const double vx = o.xp[0], vy = o.xp[1], vz = o.xp[2];
+    const double W00 = o.W[0], W01 = o.W[1], W02 = o.W[2], W11 = o.W[3], W12 = o.W[4],
+                 W22 = o.W[5];
     // N = hat(x') W   (rot-trans block of J'^T W J', J' = [-hat(x') | I])
-    const float N00 = fmaf(-vz, W01, vy * W02), N01 = fmaf(-vz, W11, vy * W12),
-                N02 = fmaf(-vz, W12, vy * W22);
-    const float N10 = fmaf(vz, W00, -vx * W02), N11 = fmaf(vz, W01, -vx * W12),
-                N12 = fmaf(vz, W02, -vx * W22);
-    const float N20 = fmaf(-vy, W00, vx * W01), N21 = fmaf(-vy, W01, vx * W11),
-                N22 = fmaf(-vy, W02, vx * W12);
+    const double N00 = fma(-vz, W01, vy * W02), N01 = fma(-vz, W11, vy * W12),
+                 N02 = fma(-vz, W12, vy * W22);
+    const double N10 = fma(vz, W00, -vx * W02), N11 = fma(vz, W01, -vx * W12),
+                 N12 = fma(vz, W02, -vx * W22);
+    const double N20 = fma(-vy, W00, vx * W01), N21 = fma(-vy, W01, vx * W11),
+                 N22 = fma(-vy, W02, vx * W12);
     // P = N hat(x')^T (rot-rot block), upper triangle
-    const float P00 = fmaf(-vz, N01, vy * N02);
-    const float P01 = fmaf(vz, N00, -vx * N02);
-    const float P02 = fmaf(-vy, N00, vx * N01);
-    const float P11 = fmaf(vz, N10, -vx * N12);
-    const float P12 = fmaf(-vy, N10, vx * N11);
-    const float P22 = fmaf(-vy, N20, vx * N21);
-    acc[0] += P00; acc[1] += P01; acc[2] += P02; acc[3] += P11; acc[4] += P12; acc[5] += P22;
+    acc[0] += fma(-vz, N01, vy * N02);
+    acc[1] += fma(vz, N00, -vx * N02);
+    acc[2] += fma(-vy, N00, vx * N01);
+    acc[3] += fma(vz, N10, -vx * N12);
+    acc[4] += fma(-vy, N10, vx * N11);
+    acc[5] += fma(-vy, N20, vx * N21);
     acc[6] += N00; acc[7] += N01; acc[8] += N02;
     acc[9] += N10; acc[10] += N11; acc[11] += N12;
     acc[12] += N20; acc[13] += N21; acc[14] += N22;
     acc[15] += W00; acc[16] += W01; acc[17] += W02; acc[18] += W11; acc[19] += W12; acc[20] += W22;
     // b' = [x' x Wd ; Wd]
-    acc[21] += fmaf(vy, o.wd[2], -vz * o.wd[1]);
-    acc[22] += fmaf(vz, o.wd[0], -vx * o.wd[2]);
-    acc[23] += fmaf(vx, o.wd[1], -vy * o.wd[0]);
+    acc[21] += fma(vy, o.wd[2], -vz * o.wd[1]);
+    acc[22] += fma(vz, o.wd[0], -vx * o.wd[2]);
+    acc[23] += fma(vx, o.wd[1], -vy * o.wd[0]);
     acc[24] += o.wd[0]; acc[25] += o.wd[1]; acc[26] += o.wd[2];
     acc[27] += o.cost;
   }
 
   if (MODE == 1) {
-    double c = (double)acc[27];
+    double c = acc[27];
     long long n = inl;
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) {
@@ -235,7 +221,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
   double v[32];
 #pragma unroll
-  for (int i = 0; i < 28; ++i) v[i] = (double)acc[i];
+  for (int i = 0; i < 28; ++i) v[i] = acc[i];
   v[28] = (double)inl;
   v[29] = 0.0; v[30] = 0.0; v[31] = 0.0;
   const double r = warp_transpose_reduce32(v, lane);
@@ -474,7 +460,8 @@ __global__ void k_lookup(CloudView cv, MapView mv, const double* __restrict__ Tp
     const long long key = pack_key(floor_div(x, mv.res, mv.inv_res),
                                    floor_div(y, mv.res, mv.inv_res),
                                    floor_div(z, mv.res, mv.inv_res));
-    const long long row = probe(mv, key);
+    const int slot = probe(mv, key);
+    const long long row = slot < 0 ? -1 : (long long)__ldg(&mv.table[slot].row);
     if (rows) rows[i] = row;
     local += (row >= 0);
   }
@@ -506,20 +493,20 @@ __global__ void k_terms(CloudView cv, MapView mv, const double* __restrict__ Tp,
     const long long key = pack_key(floor_div(x, mv.res, mv.inv_res),
                                    floor_div(y, mv.res, mv.inv_res),
                                    floor_div(z, mv.res, mv.inv_res));
-    const int row = probe(mv, key);
-    if (row < 0) {
+    const int slot = probe(mv, key);
+    if (slot < 0) {
       rows[i] = -1;
       for (int k = 0; k < 3; ++k) dout[3 * i + k] = 0.0, wdout[3 * i + k] = 0.0;
       for (int k = 0; k < 9; ++k) wout[9 * i + k] = 0.0;
       continue;
     }
-    rows[i] = row;
+    rows[i] = __ldg(&mv.table[slot].row);
     PointTerms o;
-    point_terms(R, cv, i, mv.vox + row, x, y, z, t, mv.res, key, o);
+    point_terms(R, cv, i, mv.table + slot, x, y, z, t, o);
     const int sym[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
     for (int k = 0; k < 3; ++k) dout[3 * i + k] = o.d[k], wdout[3 * i + k] = o.wd[k];
     for (int k = 0; k < 9; ++k) wout[9 * i + k] = o.W[sym[k]];
-    csum += (double)o.cost;
+    csum += o.cost;
     ++isum;
   }
 #pragma unroll

@@ -81,34 +81,33 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
   cnt_out[cidx] = cnt;
 }
 
-// one thread per cell: write the 64 B voxel record (cell-local fp32 mean, fp64 covariance)
-// and claim a hash position by CAS on the slot's row field.
+// one thread per cell: claim a hash slot by CAS on its row field, then fill the 96 B slot
+// with the key and the voxel Gaussian (fp64).
 __global__ void k_hash_insert(const long long* __restrict__ keys, const double* __restrict__ means,
-                              const double* __restrict__ covs, int m, double res,
-                              Slot* __restrict__ table, VoxelRec* __restrict__ vox,
+                              const double* __restrict__ covs, int m, Slot* __restrict__ table,
                               unsigned mask, int shift) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   const long long key = keys[r];
-  const long long ix = (key >> 42) - kKeyOffset;
-  const long long iy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
-  const long long iz = (key & ((1LL << 21) - 1)) - kKeyOffset;
-  const double cx = ((double)ix + 0.5) * res, cy = ((double)iy + 0.5) * res,
-               cz = ((double)iz + 0.5) * res;
-  const double* C = covs + 9 * (size_t)r;
-  VoxelRec v;
-  v.mean = make_float4((float)(means[3 * r] - cx), (float)(means[3 * r + 1] - cy),
-                       (float)(means[3 * r + 2] - cz), 0.f);
-  v.c0 = make_double2(C[0], C[1]);
-  v.c1 = make_double2(C[2], C[4]);
-  v.c2 = make_double2(C[5], C[8]);
-  vox[r] = v;
   unsigned h = slot_of(key, shift);
   for (;;) {
     if (atomicCAS(&table[h].row, -1, r) == -1) break;
     h = (h + 1) & mask;
   }
-  table[h].key = key;
+  Slot& s = table[h];
+  s.key = key;
+  s.pad0 = 0;
+  s.mean[0] = means[3 * r];
+  s.mean[1] = means[3 * r + 1];
+  s.mean[2] = means[3 * r + 2];
+  const double* C = covs + 9 * (size_t)r;
+  s.cov[0] = C[0];
+  s.cov[1] = C[1];
+  s.cov[2] = C[2];
+  s.cov[3] = C[4];
+  s.cov[4] = C[5];
+  s.cov[5] = C[8];
+  s.pad1 = 0.0;
 }
 
 }  // namespace vg
@@ -154,10 +153,8 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
   VG_CUDA(cudaMallocAsync((void**)&map->table, sizeof(Slot) * (size_t)map->capacity, ctx->stream));
   VG_CUDA(cudaMemsetAsync(map->table, 0xff, sizeof(Slot) * (size_t)map->capacity, ctx->stream));
   if (map->m == 0) return 0;
-  VG_CUDA(cudaMallocAsync((void**)&map->vox, sizeof(VoxelRec) * (size_t)map->m, ctx->stream));
   k_hash_insert<<<(int)((map->m + 127) / 128), 128, 0, ctx->stream>>>(
-      map->keys, map->means, map->covs, (int)map->m, map->res, map->table, map->vox,
-      map->capacity - 1, 64 - l2);
+      map->keys, map->means, map->covs, (int)map->m, map->table, map->capacity - 1, 64 - l2);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;

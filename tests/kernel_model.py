@@ -15,8 +15,14 @@ def _hat(v):
     return O._hat(v)
 
 
-def compact(points, covs, vmap, R, t, dtype=np.float64, lane_chunk=16):
-    """Return the 29-value compact record [P6 N9 S6 br3 bt3 cost inliers] (fp64)."""
+def compact(points, covs, vmap, R, t, dtype=np.float64, cov_dtype=np.float64, lane_chunk=16):
+    """Return the 29-value compact record [P6 N9 S6 br3 bt3 cost inliers] (fp64).
+
+    dtype=np.float64 is the kernel as built (all per-point math fp64).  dtype=np.float32 /
+    cov_dtype=np.float32 model the rejected cheaper designs: fp32 per-point math (residual in
+    cell-local fp32 coordinates, fp32 fused covariance and inverse, fp32 lane sums over
+    `lane_chunk` points) and fp32-stored covariances.
+    """
     res, keys, means, vcovs = vmap[0], vmap[1], vmap[2], vmap[3]
     R = np.asarray(R, float)
     t = np.asarray(t, float)
@@ -25,13 +31,17 @@ def compact(points, covs, vmap, R, t, dtype=np.float64, lane_chunk=16):
     hit = rows >= 0
     sel = rows[hit]
     x = moved[hit]
-    cc = (O.unpack_voxel_keys(keys[sel]).astype(float) + 0.5) * res
-    d = (means[sel] - cc).astype(dtype) - (x - cc).astype(dtype)
+    C = np.asarray(covs, float)[hit].astype(cov_dtype).astype(np.float64)
+    Cv = vcovs[sel].astype(cov_dtype).astype(np.float64)
+    if dtype == np.float64:
+        d = means[sel] - x
+        W = O._inverse3(Cv + R @ C @ R.T)
+    else:
+        cc = (O.unpack_voxel_keys(keys[sel]).astype(float) + 0.5) * res
+        d = (means[sel] - cc).astype(dtype) - (x - cc).astype(dtype)
+        Rf = R.astype(dtype)
+        W = O._inverse3(Cv.astype(dtype) + Rf @ C.astype(dtype) @ Rf.T)
     xp = (x - t).astype(dtype)
-    # fused covariance and its inverse in fp64 from fp64 covariances; W rounded afterwards
-    C = np.asarray(covs, float)[hit]
-    F = vcovs[sel] + R @ C @ R.T
-    W = O._inverse3(F).astype(dtype)
     wd = np.einsum("nij,nj->ni", W, d)
     cost = np.einsum("ni,ni->n", d, wd)
     H = _hat(xp)

@@ -62,8 +62,8 @@ def test_two_pose_registration_recovers_truth():
 
 
 def test_lm_is_deterministic():
-    a = two_pose_graph().optimize_lm()
-    b = two_pose_graph().optimize_lm()
+    a = two_pose_graph()[0].optimize_lm()
+    b = two_pose_graph()[0].optimize_lm()
     assert a.iterations == b.iterations and a.final_cost == b.final_cost
     for k in a.estimates:
         assert np.array_equal(a.estimates[k].translation, b.estimates[k].translation)

@@ -36,19 +36,23 @@ def test_adjoint_expansion_exact_in_fp64(golden, case):
     assert got["inliers"] == ref["inliers"]
 
 
-@pytest.mark.parametrize("case", range(6))
-def test_kernel_precision_budget(golden, case):
-    """fp32 per-point Jacobian terms + fp32 lane sums stay inside the parity tolerance."""
+def test_fp32_designs_would_break_parity(golden):
+    """Why the kernel is fp64 per correspondence: the cheaper designs (fp32 per-point math,
+    fp32-stored covariances) exceed the per-element 1e-4 bar on cancelling H/b entries."""
     g = golden("registration")
     vm = _map(g)
-    R, t, unary = g[f"case{case}_R"], g[f"case{case}_t"], bool(g[f"case{case}_unary"])
-    ref = O.linearize(g["src_points"], g["src_covs"], vm, R, t, target_fixed=unary)
-    got = KM.expand(KM.compact(g["src_points"], g["src_covs"], vm, R, t, dtype=np.float32),
-                    R, t, unary)
-    for k in NAMES:
-        if ref[k] is not None:
-            assert KM.within_tolerance(got[k], ref[k]) < 0.5, k
-    assert KM.within_tolerance(got["cost"], ref["cost"]) < 0.5
+    worst = {"fp32 math": 0.0, "fp32 storage": 0.0}
+    for case in range(6):
+        R, t, unary = g[f"case{case}_R"], g[f"case{case}_t"], bool(g[f"case{case}_unary"])
+        ref = O.linearize(g["src_points"], g["src_covs"], vm, R, t, target_fixed=unary)
+        for name, kw in (("fp32 math", {"dtype": np.float32}),
+                         ("fp32 storage", {"cov_dtype": np.float32})):
+            got = KM.expand(KM.compact(g["src_points"], g["src_covs"], vm, R, t, **kw), R, t,
+                            unary)
+            for k in NAMES:
+                if ref[k] is not None:
+                    worst[name] = max(worst[name], KM.within_tolerance(got[k], ref[k]))
+    assert worst["fp32 math"] > 1.0 and worst["fp32 storage"] > 1.0
 
 
 def test_record_unpack_layout():
