@@ -49,7 +49,7 @@ struct MapView {
   unsigned mask;        // capacity - 1
   int shift;            // 64 - log2(capacity)
   int m;                // occupied cells
-  int pad;
+  int pow2;             // res is a power of two: x * (1/res) == x / res exactly
 };
 
 // Per-factor record resident in HBM (128 B).  T = T_ij (R row-major, t), fp64.
@@ -78,9 +78,10 @@ struct __align__(16) ItemDev {
 // (preprocess.py:68-70).  x * (1/res) is used unless the quotient is within 1e-12 of an
 // integer, where the correctly rounded quotient decides — so the floor is bit-identical to
 // numpy's floor(p / res) for every input.
-__device__ __forceinline__ double floor_div(double x, double res, double inv_res) {
+__device__ __forceinline__ double floor_div(double x, double res, double inv_res, int pow2) {
   double q = x * inv_res;
   double f = floor(q);
+  if (pow2) return f;
   double frac = q - f;
   double tol = 1e-12 * fabs(q);
   if (frac <= tol || 1.0 - frac <= tol) f = floor(__ddiv_rn(x, res));

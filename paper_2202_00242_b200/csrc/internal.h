@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -64,7 +65,8 @@ struct vg_map {
     v.mask = capacity - 1;
     v.shift = 64 - log2cap;
     v.m = (int)m;
-    v.pad = 0;
+    int e2 = 0;
+    v.pow2 = (std::frexp(res, &e2) == 0.5) ? 1 : 0;
     return v;
   }
 };

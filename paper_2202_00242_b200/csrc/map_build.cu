@@ -18,10 +18,13 @@ namespace vg {
 __global__ void k_pack_keys(const double* __restrict__ xyz, long long n, double res,
                             long long* __restrict__ keys, int* __restrict__ idx) {
   const double inv = 1.0 / res;
+  int e2 = 0;
+  const int pow2 = (frexp(res, &e2) == 0.5) ? 1 : 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
-    keys[i] = pack_key(floor_div(xyz[3 * i], res, inv), floor_div(xyz[3 * i + 1], res, inv),
-                       floor_div(xyz[3 * i + 2], res, inv));
+    keys[i] = pack_key(floor_div(xyz[3 * i], res, inv, pow2),
+                       floor_div(xyz[3 * i + 1], res, inv, pow2),
+                       floor_div(xyz[3 * i + 2], res, inv, pow2));
     if (idx) idx[i] = (int)i;
   }
 }
