@@ -42,6 +42,7 @@ extern "C" {
 #define VG_MODE_LINEARIZE 0 /* blocks: H_ii(21) H_ij(36) H_jj(21) b_i(6) b_j(6) cost inliers */
 #define VG_MODE_COST 1      /* cost inliers */
 #define VG_MODE_COMPACT 2   /* H'(21) b'(6) cost inliers: pre-adjoint record */
+#define VG_MODE_INLIERS 3   /* 0 inliers: correspondence counts only (overlap gating) */
 #define VG_REC_LINEARIZE 92
 #define VG_REC_COST 2
 #define VG_REC_COMPACT 29

@@ -30,7 +30,8 @@ VG_ERR_NOMEM = 5
 MODE_LINEARIZE = 0
 MODE_COST = 1
 MODE_COMPACT = 2
-RECORD_SIZE = {MODE_LINEARIZE: 92, MODE_COST: 2, MODE_COMPACT: 29}
+MODE_INLIERS = 3
+RECORD_SIZE = {MODE_LINEARIZE: 92, MODE_COST: 2, MODE_COMPACT: 29, MODE_INLIERS: 2}
 FACTOR_UNARY = 1
 
 

@@ -1,0 +1,332 @@
+// accumulate.cu — K4a (correspondence lookup + per-item hit compaction) and K4b (fp64 fused
+// covariance / inverse / Jacobian accumulation over compacted hits).
+//
+// Reference: match_terms (registration.py:146-157) + linearize_from_terms (:207-248) for
+// every factor of a graph (factor_graph.py:522-536).
+//
+// K4a — one warp per (factor, <=512-point chunk) item, light on registers so many warps hide
+//   the two dependent memory latencies of a lookup (source point, then the probed 32 B key
+//   group).  x = R p + t (fp64) -> key (bit-exact floor) -> linear probe 4 slots per sector.
+//   Hits are written as (point, slot) pairs into the item's region of a batch-wide hit list
+//   with a warp ballot, preserving point order.  Misses contribute nothing (:150-156).
+// K4b — one warp per item over its compacted hits, so every lane of the expensive fp64 path
+//   does useful work.  Each round of 32 hits gathers the source point (16 B), source
+//   covariance (48 B) and voxel record (80 B) with cp.async into a 3-stage shared-memory
+//   pipeline, so the gathers of rounds r+1, r+2 are in flight while round r computes.
+//   The per-item 29-value partial (target-frame 6x6 about the source origin)
+//   is reduced across the warp in a fixed order.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace vg {
+
+// ---- K4a ------------------------------------------------------------------------------------
+constexpr int kLookupWarps = 8;
+constexpr int kLookupUnroll = 2;
+
+__global__ void __launch_bounds__(kLookupWarps * 32)
+    k_lookup_items(const ItemDev* __restrict__ items, int n_items,
+                   const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
+                   const MapView* __restrict__ maps, int2* __restrict__ hits,
+                   int* __restrict__ counts, double* __restrict__ partials2) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
+  if (w >= n_items) return;
+  const ItemDev it = items[w];
+  const FactorDev* f = factors + it.factor;
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(f->T + k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = __ldg(f->T + 9 + k);
+  const CloudView cv = clouds[__ldg(&f->cloud)];
+  const MapView mv = maps[__ldg(&f->map)];
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int2* out = hits + it.hoff;
+  int cnt = 0;
+  for (int base = it.begin; base < it.end; base += 32 * kLookupUnroll) {
+    double px[kLookupUnroll], py[kLookupUnroll], pz[kLookupUnroll];
+#pragma unroll
+    for (int u = 0; u < kLookupUnroll; ++u) {
+      const int i = base + lane + 32 * u;
+      px[u] = py[u] = pz[u] = 0.0;
+      if (i < it.end) {
+        if (cv.xyz64) {
+          px[u] = __ldg(cv.xyz64 + 3 * (size_t)i);
+          py[u] = __ldg(cv.xyz64 + 3 * (size_t)i + 1);
+          pz[u] = __ldg(cv.xyz64 + 3 * (size_t)i + 2);
+        } else {
+          const float4 a = __ldg(cv.a + i);
+          px[u] = a.x;
+          py[u] = a.y;
+          pz[u] = a.z;
+        }
+      }
+    }
+    long long key[kLookupUnroll];
+    unsigned h[kLookupUnroll];
+    ProbeGroup pg[kLookupUnroll];
+#pragma unroll
+    for (int u = 0; u < kLookupUnroll; ++u) {
+      // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
+      const double x = fma(R[0], px[u], fma(R[1], py[u], R[2] * pz[u])) + t[0];
+      const double y = fma(R[3], px[u], fma(R[4], py[u], R[5] * pz[u])) + t[1];
+      const double z = fma(R[6], px[u], fma(R[7], py[u], R[8] * pz[u])) + t[2];
+      key[u] = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                        floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                        floor_div(z, mv.res, mv.inv_res, mv.pow2));
+      h[u] = slot_of(key[u], mv.shift);
+      if (base + lane + 32 * u < it.end && mv.m) pg[u] = probe_load(mv, h[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kLookupUnroll; ++u) {
+      const int i = base + lane + 32 * u;
+      int slot = -1;
+      if (i < it.end && mv.m) {
+        while (probe_scan(mv, pg[u], h[u], key[u], slot) < 0) {
+          h[u] = ((h[u] & ~3u) + 4u) & mv.mask;
+          pg[u] = probe_load(mv, h[u]);
+        }
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
+      if (slot >= 0) out[cnt + __popc(m & lt_mask)] = make_int2(i, slot);
+      cnt += __popc(m);
+    }
+  }
+  if (lane == 0) {
+    counts[w] = cnt;
+    if (partials2) {  // inliers-only mode: the item's record is final
+      partials2[2 * (size_t)w] = 0.0;
+      partials2[2 * (size_t)w + 1] = (double)cnt;
+    }
+  }
+}
+
+// ---- K4b ------------------------------------------------------------------------------------
+constexpr int kAccWarps = 4;
+constexpr int kStages = 3;
+// stage layout (16 B units x 32 lanes): p0 p1 (point), c0 c1 c2 (source cov), r0..r4 (record)
+constexpr int kStageUnits = 10;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+struct AccSmem {
+  float4 stage[kStages][kStageUnits][32];
+};
+
+// gather one round (32 hits) into stage `round % kStages`; always commits a group so every
+// lane has the same number of outstanding groups
+__device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& mv, AccSmem& sm,
+                                            int round, int2 e, bool valid, int lane) {
+  if (valid) {
+    float4(*st)[32] = sm.stage[round % kStages];
+    if (cv.xyz64) {
+      const double* p = cv.xyz64 + 3 * (size_t)e.x;
+      double* d = reinterpret_cast<double*>(&st[0][lane]);
+      cp_async8(d, p);
+      cp_async8(d + 1, p + 1);
+      cp_async8(reinterpret_cast<double*>(&st[1][lane]), p + 2);
+    } else {
+      cp_async16(&st[0][lane], cv.a + e.x);
+    }
+    cp_async16(&st[2][lane], cv.c0 + e.x);
+    cp_async16(&st[3][lane], cv.c1 + e.x);
+    cp_async16(&st[4][lane], cv.c2 + e.x);
+    const char* rec = reinterpret_cast<const char*>(mv.recs + e.y);
+#pragma unroll
+    for (int u = 0; u < 5; ++u) cp_async16(&st[5 + u][lane], rec + 16 * u);
+  }
+  cp_async_commit();
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kAccWarps * 32, 3)
+    k_accumulate(const ItemDev* __restrict__ items, int n_items,
+                 const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
+                 const MapView* __restrict__ maps, const int2* __restrict__ hits,
+                 const int* __restrict__ counts, double* __restrict__ partials) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int w = blockIdx.x * kAccWarps + wib;
+  if (w >= n_items) return;
+  AccSmem& sm = reinterpret_cast<AccSmem*>(smem_raw)[wib];
+  const ItemDev it = items[w];
+  const FactorDev* f = factors + it.factor;
+  const int n = counts[w];
+  const int2* hl = hits + it.hoff;
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(f->T + k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = __ldg(f->T + 9 + k);
+  const CloudView cv = clouds[__ldg(&f->cloud)];
+  const MapView mv = maps[__ldg(&f->map)];
+
+  double acc[28];
+#pragma unroll
+  for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+  const int rounds = (n + 31) / 32;
+#pragma unroll
+  for (int r = 0; r < kStages - 1; ++r) {
+    const int k = r * 32 + lane;
+    issue_round(cv, mv, sm, r, k < n ? hl[k] : make_int2(0, 0), k < n, lane);
+  }
+  // hit entries are prefetched one round ahead of their gather
+  int kn = (kStages - 1) * 32 + lane;
+  int2 nxt = kn < n ? hl[kn] : make_int2(0, 0);
+  for (int r = 0; r < rounds; ++r) {
+    issue_round(cv, mv, sm, r + kStages - 1, nxt, kn < n, lane);
+    kn += 32;
+    if (kn < n) nxt = hl[kn];
+    cp_async_wait<kStages - 1>();
+    __syncwarp();
+    const int k = r * 32 + lane;
+    if (k < n) {
+      const float4(*st)[32] = sm.stage[r % kStages];
+      double px, py, pz;
+      if (cv.xyz64) {
+        const double* d = reinterpret_cast<const double*>(&st[0][lane]);
+        px = d[0];
+        py = d[1];
+        pz = reinterpret_cast<const double*>(&st[1][lane])[0];
+      } else {
+        const float4 a = st[0][lane];
+        px = a.x;
+        py = a.y;
+        pz = a.z;
+      }
+      const double2 s0 = *reinterpret_cast<const double2*>(&st[2][lane]);
+      const double2 s1 = *reinterpret_cast<const double2*>(&st[3][lane]);
+      const double2 s2 = *reinterpret_cast<const double2*>(&st[4][lane]);
+      const double2 m01 = *reinterpret_cast<const double2*>(&st[5][lane]);
+      const double2 m2c0 = *reinterpret_cast<const double2*>(&st[6][lane]);
+      const double2 c12 = *reinterpret_cast<const double2*>(&st[7][lane]);
+      const double2 c34 = *reinterpret_cast<const double2*>(&st[8][lane]);
+      const double v5 = reinterpret_cast<const double*>(&st[9][lane])[0];
+      // moved point (registration.py:148) and residual d = mu' - moved (:152)
+      const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
+      const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
+      const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
+      const double d0 = m01.x - x, d1 = m01.y - y, d2 = m2c0.x - z;
+      // F = C' + R C R^T (:153)
+      const double C00 = s0.x, C01 = s0.y, C02 = s1.x, C11 = s1.y, C12 = s2.x, C22 = s2.y;
+      double A[9];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const double r0 = R[3 * q], r1 = R[3 * q + 1], r2 = R[3 * q + 2];
+        A[3 * q + 0] = fma(r0, C00, fma(r1, C01, r2 * C02));
+        A[3 * q + 1] = fma(r0, C01, fma(r1, C11, r2 * C12));
+        A[3 * q + 2] = fma(r0, C02, fma(r1, C12, r2 * C22));
+      }
+      auto arT = [&](int a_, int c_) {
+        return fma(A[3 * a_], R[3 * c_], fma(A[3 * a_ + 1], R[3 * c_ + 1], A[3 * a_ + 2] * R[3 * c_ + 2]));
+      };
+      const double fa = m2c0.y + arT(0, 0), fb = c12.x + arT(0, 1), fc = c12.y + arT(0, 2);
+      const double fd = c34.x + arT(1, 1), fe = c34.y + arT(1, 2), ff = v5 + arT(2, 2);
+      // W = F^-1 (:113-130)
+      const double i00 = fma(fd, ff, -fe * fe), i01 = fma(fc, fe, -fb * ff),
+                   i02 = fma(fb, fe, -fc * fd), i11 = fma(fa, ff, -fc * fc),
+                   i12 = fma(fb, fc, -fa * fe), i22 = fma(fa, fd, -fb * fb);
+      const double inv = rcp64(fma(fa, i00, fma(fb, i01, fc * i02)));
+      const double W00 = i00 * inv, W01 = i01 * inv, W02 = i02 * inv, W11 = i11 * inv,
+                   W12 = i12 * inv, W22 = i22 * inv;
+      const double wd0 = fma(W00, d0, fma(W01, d1, W02 * d2));
+      const double wd1 = fma(W01, d0, fma(W11, d1, W12 * d2));
+      const double wd2 = fma(W02, d0, fma(W12, d1, W22 * d2));
+      acc[27] += fma(d0, wd0, fma(d1, wd1, d2 * wd2));  // cost (:156)
+      if (MODE == 0) {
+        const double vx = x - t[0], vy = y - t[1], vz = z - t[2];
+        // N = hat(x') W, P = N hat(x')^T, b' = [x' x Wd ; Wd]  (J' = [-hat(x') | I])
+        const double N00 = fma(-vz, W01, vy * W02), N01 = fma(-vz, W11, vy * W12),
+                     N02 = fma(-vz, W12, vy * W22);
+        const double N10 = fma(vz, W00, -vx * W02), N11 = fma(vz, W01, -vx * W12),
+                     N12 = fma(vz, W02, -vx * W22);
+        const double N20 = fma(-vy, W00, vx * W01), N21 = fma(-vy, W01, vx * W11),
+                     N22 = fma(-vy, W02, vx * W12);
+        acc[0] += fma(-vz, N01, vy * N02);
+        acc[1] += fma(vz, N00, -vx * N02);
+        acc[2] += fma(-vy, N00, vx * N01);
+        acc[3] += fma(vz, N10, -vx * N12);
+        acc[4] += fma(-vy, N10, vx * N11);
+        acc[5] += fma(-vy, N20, vx * N21);
+        acc[6] += N00; acc[7] += N01; acc[8] += N02;
+        acc[9] += N10; acc[10] += N11; acc[11] += N12;
+        acc[12] += N20; acc[13] += N21; acc[14] += N22;
+        acc[15] += W00; acc[16] += W01; acc[17] += W02;
+        acc[18] += W11; acc[19] += W12; acc[20] += W22;
+        acc[21] += fma(vy, wd2, -vz * wd1);
+        acc[22] += fma(vz, wd0, -vx * wd2);
+        acc[23] += fma(vx, wd1, -vy * wd0);
+        acc[24] += wd0; acc[25] += wd1; acc[26] += wd2;
+      }
+    }
+    __syncwarp();  // stage r % kStages is reused by round r + kStages
+  }
+  cp_async_wait<0>();
+
+  if (MODE == 1) {
+    double c = acc[27];
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+    if (lane == 0) {
+      partials[2 * (size_t)w] = c;
+      partials[2 * (size_t)w + 1] = (double)n;
+    }
+    return;
+  }
+  double v[32];
+#pragma unroll
+  for (int k = 0; k < 28; ++k) v[k] = acc[k];
+  v[28] = lane == 0 ? (double)n : 0.0;
+  v[29] = 0.0;
+  v[30] = 0.0;
+  v[31] = 0.0;
+  partials[(size_t)w * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
+}
+
+}  // namespace vg
+
+using namespace vg;
+
+int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
+  if (b->num_items == 0) return 0;
+  const int n = (int)b->num_items;
+  k_lookup_items<<<(n + kLookupWarps - 1) / kLookupWarps, kLookupWarps * 32, 0, ctx->stream>>>(
+      b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
+      kmode == 2 ? b->partials : nullptr);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  if (kmode == 2) return 0;
+  const size_t smem = sizeof(AccSmem) * kAccWarps;
+  static bool attr_set = false;
+  if (!attr_set) {
+    VG_CUDA(cudaFuncSetAttribute(k_accumulate<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    VG_CUDA(cudaFuncSetAttribute(k_accumulate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  const int blocks = (n + kAccWarps - 1) / kAccWarps;
+  if (kmode == 1)
+    k_accumulate<1><<<blocks, kAccWarps * 32, smem, ctx->stream>>>(
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, b->partials);
+  else
+    k_accumulate<0><<<blocks, kAccWarps * 32, smem, ctx->stream>>>(
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, b->partials);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}

@@ -273,7 +273,8 @@ int vg_map_export(vg_ctx* ctx, const vg_map* m, int64_t* keys, double* means, do
 int vg_map_destroy(vg_map* m) {
   if (!m) return VG_OK;
   vg_ctx* ctx = m->ctx;
-  dfree(ctx, m->table);
+  dfree(ctx, m->pkeys);
+  dfree(ctx, m->recs);
   dfree(ctx, m->keys);
   dfree(ctx, m->means);
   dfree(ctx, m->covs);
@@ -420,7 +421,7 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   std::stable_sort(order.begin(), order.end(),
                    [&](int64_t a, int64_t b) { return fac[a].map < fac[b].map; });
   std::vector<ItemDev> items;
-  long long npts = 0;
+  long long npts = 0, hoff = 0;
   for (int64_t f : order) {
     const long long n = specs[f].source->n;
     npts += n;
@@ -431,13 +432,16 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
       it.factor = (int)f;
       it.begin = (int)(c * n / nchunks);
       it.end = (int)((c + 1) * n / nchunks);
-      it.pad = 0;
+      it.hoff = (int)hoff;
+      hoff += ((it.end - it.begin) + 1) & ~1LL;  // keep regions 16 B aligned
       items.push_back(it);
     }
     fac[f].item_count = (int)nchunks;
   }
+  if (hoff >= (1LL << 31)) return fail(VG_ERR_INVALID, "batch too large (2^31 points)");
   vg_batch* b = new vg_batch();
   b->ctx = ctx;
+  b->hit_capacity = hoff;
   b->F = F;
   b->num_items = (long long)items.size();
   b->num_points = npts;
@@ -453,6 +457,8 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   if ((rc = dalloc(ctx, &b->factors, F)) || (rc = dalloc(ctx, &b->items, items.size())) ||
       (rc = dalloc(ctx, &b->clouds, cv.size())) || (rc = dalloc(ctx, &b->maps, mv.size())) ||
       (rc = dalloc(ctx, &b->partials, items.size() * kPartialStride)) ||
+      (rc = dalloc(ctx, &b->hits, (size_t)hoff + 2)) ||
+      (rc = dalloc(ctx, &b->hit_counts, items.size())) ||
       (rc = dalloc(ctx, &b->out, (size_t)F * VG_REC_LINEARIZE)) ||
       (rc = h2d(ctx, b->factors, fac.data(), sizeof(FactorDev) * F)) ||
       (rc = h2d(ctx, b->items, items.data(), sizeof(ItemDev) * items.size())) ||
@@ -483,6 +489,8 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->clouds);
   dfree(ctx, b->maps);
   dfree(ctx, b->partials);
+  dfree(ctx, b->hits);
+  dfree(ctx, b->hit_counts);
   dfree(ctx, b->out);
   dfree(ctx, b->poses);
   cudaStreamSynchronize(ctx->stream);
@@ -491,18 +499,23 @@ int vg_batch_destroy(vg_batch* b) {
 }
 
 static size_t rec_of(int mode) {
-  return mode == VG_MODE_COST ? VG_REC_COST : mode == VG_MODE_COMPACT ? VG_REC_COMPACT : VG_REC_LINEARIZE;
+  return (mode == VG_MODE_COST || mode == VG_MODE_INLIERS) ? VG_REC_COST
+         : mode == VG_MODE_COMPACT                          ? VG_REC_COMPACT
+                                                             : VG_REC_LINEARIZE;
+}
+static int kmode_of(int mode) {
+  return mode == VG_MODE_COST ? 1 : mode == VG_MODE_INLIERS ? 2 : 0;
 }
 
 static int run_device(vg_batch* b, int mode, double* out_dev) {
-  VG_CHECK(launch_linearize(b->ctx, b, mode == VG_MODE_COST ? 1 : 0));
+  VG_CHECK(launch_accumulate(b->ctx, b, kmode_of(mode)));
   VG_CHECK(launch_finalize(b->ctx, b, mode, out_dev));
   return VG_OK;
 }
 
 int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_host) {
   if (!b || (b->F && (!T_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
-  if (mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad mode");
+  if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
   if (b->F == 0) return VG_OK;
   vg_ctx* ctx = b->ctx;
   // scatter T_ij into the 128 B factor records (dst pitch 128, src pitch 96)
@@ -524,7 +537,7 @@ static int ensure_poses(vg_batch* b, int64_t V) {
 int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, int mode,
                              double* out_host) {
   if (!b || (b->F && (!poses_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
-  if (mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad mode");
+  if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
   if (b->F == 0) return VG_OK;
   if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
   VG_CHECK(ensure_poses(b, V));
@@ -537,7 +550,7 @@ int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, i
 int vg_batch_linearize_poses_device(vg_batch* b, const double* poses_dev, int64_t V, int mode,
                                     double* out_dev) {
   if (!b || !out_dev) return fail(VG_ERR_INVALID, "null argument");
-  if (mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad mode");
+  if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
   if (b->F == 0) return VG_OK;
   if (poses_dev) {
     if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
@@ -553,12 +566,12 @@ int vg_batch_compose_device(vg_batch* b, const double* poses_dev, int64_t V) {
 }
 
 int vg_batch_accumulate_device(vg_batch* b, int mode) {
-  if (!b || mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad arguments");
-  return launch_linearize(b->ctx, b, mode == VG_MODE_COST ? 1 : 0);
+  if (!b || mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad arguments");
+  return launch_accumulate(b->ctx, b, kmode_of(mode));
 }
 
 int vg_batch_finalize_device(vg_batch* b, int mode, double* out_dev) {
-  if (!b || !out_dev || mode < 0 || mode > 2) return fail(VG_ERR_INVALID, "bad arguments");
+  if (!b || !out_dev || mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad arguments");
   return launch_finalize(b->ctx, b, mode, out_dev);
 }
 

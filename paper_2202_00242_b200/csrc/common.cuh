@@ -3,10 +3,11 @@
 // HBM layouts:
 //   cloud  : SoA, 64 B/point: a[i] = (x, y, z) fp32, covariance as three fp64 double2 arrays
 //            + optional fp64 xyz (n x 3) when the points are not exactly fp32 (keys stay exact)
-//   map    : open-addressing hash table (load factor <= 0.5) of 96 B slots carrying the
-//            voxel's key, reference row and fp64 Gaussian.
+//   map    : open-addressing hash table (load factor <= 0.5): dense int64 key array probed
+//            4 slots per 32 B sector + parallel 96 B records (reference row, fp64 Gaussian).
 //   work   : (factor, chunk) items, one warp per item; fp64 partials, fixed-order reduce.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -17,21 +18,23 @@ constexpr int kWarpsPerBlock = 4;
 constexpr int kPartialStride = 32;    // doubles per work-item partial (29 used)
 constexpr int kMaxChunk = 512;        // points per work item => <= 16 points per lane
 
-// 96-byte inline hash slot: packed key, reference row and the voxel Gaussian in fp64.
-// row < 0 marks an empty slot (any int64 can be a key).  A hit reads exactly the slot's
-// three 32 B sectors with no dependent second gather.  Mean and covariance stay fp64: the
-// fused covariance C' + R C R^T has condition ~1e3 for plane-like cells and the parity bar
-// is per element (1e-4 rel) on H/b entries that cancel by up to ~1e5 — fp32 storage or fp32
-// per-point math exceeds it (tests/kernel_model.py, tests/test_host_logic.py quantify it).
-struct __align__(32) Slot {
-  long long key;    // packed voxel key (registration.py:36-42 `keys`)
+// Voxel map on the device = open-addressing hash table in two parallel arrays indexed by
+// slot: a dense int64 key array (probed 4 slots per 32 B sector) and 96 B records carrying the
+// reference row and the voxel Gaussian in fp64.  Empty slots hold `empty_key`, a value that is
+// not a key of this map.  Mean and covariance stay fp64: the fused covariance C' + R C R^T
+// has condition ~1e3 for plane-like cells and the parity bar is per element (1e-4 rel) on
+// H/b entries that cancel by up to ~1e5 — fp32 storage or fp32 per-point math exceeds it
+// (tests/kernel_model.py, tests/test_host_logic.py quantify it).
+struct __align__(32) VoxelRec {
+  double mean[3];   // voxel mean (registration.py:90-92)          offsets  0..24
+  double cov[6];    // covariance c00 c01 c02 c11 c12 c22 (:93-97)  offsets 24..72
   int row;          // rank of the key in ascending order == reference row index
   int pad0;
-  double mean[3];   // voxel mean (registration.py:90-92)
-  double cov[6];    // voxel covariance c00 c01 c02 c11 c12 c22 (registration.py:93-97)
-  double pad1;
+  double pad1[2];
 };
-static_assert(sizeof(Slot) == 96, "slot must be 96 B");
+static_assert(sizeof(VoxelRec) == 96, "voxel record must be 96 B");
+static_assert(offsetof(VoxelRec, mean) % 16 == 0 && offsetof(VoxelRec, cov) % 16 == 8,
+              "double2 loads at mean[0], mean[2], cov[1], cov[3] must be 16 B aligned");
 
 struct CloudView {
   const float4* a;      // n: x, y, z (fp32), pad
@@ -43,7 +46,9 @@ struct CloudView {
 };
 
 struct MapView {
-  const Slot* table;
+  const long long* keys;    // capacity (multiple of 4), 32 B aligned
+  const VoxelRec* recs;     // capacity, parallel to keys
+  long long empty_key;
   double res;
   double inv_res;
   unsigned mask;        // capacity - 1
@@ -68,9 +73,9 @@ static_assert(sizeof(FactorDev) == 128, "factor record must be 128 B");
 
 struct __align__(16) ItemDev {
   int factor;
-  int begin;
+  int begin;  // point range [begin, end) of the factor's source cloud
   int end;
-  int pad;
+  int hoff;   // offset of this item's region in the batch hit list (even, 16 B aligned)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -99,17 +104,40 @@ __device__ __forceinline__ unsigned slot_of(long long key, int shift) {
   return (unsigned)(((unsigned long long)key * 0x9E3779B97F4A7C15ull) >> shift);
 }
 
-// Probe for `key`; returns the slot index or -1 (one 16 B header load per probe; average
-// probe length <= 1.5 on hits at load factor <= 0.5).
+// Linear probing, resolved 4 slots (one 32 B sector) per memory access.  Returns the slot
+// index or -1.  Lookups of any key (including empty_key itself) terminate at an empty slot.
+struct ProbeGroup {
+  longlong2 k01, k23;
+};
+__device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned h) {
+  const longlong2* g = reinterpret_cast<const longlong2*>(mv.keys + (h & ~3u));
+  return ProbeGroup{__ldg(g), __ldg(g + 1)};
+}
+// scan the group loaded for position h; returns 1 found (slot set), 0 missing, -1 continue
+__device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& pg, unsigned h,
+                                          long long key, int& slot) {
+  const long long ks[4] = {pg.k01.x, pg.k01.y, pg.k23.x, pg.k23.y};
+  const unsigned j0 = h & 3u;
+#pragma unroll
+  for (unsigned j = 0; j < 4; ++j) {
+    if (j < j0) continue;
+    if (ks[j] == key) {
+      slot = (int)((h & ~3u) + j);
+      return 1;
+    }
+    if (ks[j] == mv.empty_key) return 0;
+  }
+  return -1;
+}
 __device__ __forceinline__ int probe(const MapView& mv, long long key) {
   if (mv.m == 0) return -1;
   unsigned h = slot_of(key, mv.shift);
   for (;;) {
-    const int4 s = __ldg(reinterpret_cast<const int4*>(mv.table + h));
-    const long long k = ((long long)(unsigned)s.y << 32) | (unsigned)s.x;
-    if (s.z < 0) return -1;
-    if (k == key) return (int)h;
-    h = (h + 1) & mv.mask;
+    const ProbeGroup pg = probe_load(mv, h);
+    int slot = -1;
+    const int r = probe_scan(mv, pg, h, key, slot);
+    if (r >= 0) return r ? slot : -1;
+    h = ((h & ~3u) + 4u) & mv.mask;
   }
 }
 
@@ -118,5 +146,30 @@ __device__ __forceinline__ int probe(const MapView& mv, long long key) {
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// 1/a: hardware approximation + two Newton steps (error squares each step), no slow path
+__device__ __forceinline__ double rcp64(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
+// 32 values reduced across 32 lanes in 31 shuffle steps; lane L returns the sum of value L.
+__device__ __forceinline__ double warp_transpose_reduce32(double (&v)[32], int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = up ? v[i] : v[i + s];
+      const double keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
 
 }  // namespace vg

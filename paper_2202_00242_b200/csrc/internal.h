@@ -51,7 +51,9 @@ struct vg_map {
   double res = 1.0;
   unsigned capacity = 0;
   int log2cap = 0;
-  vg::Slot* table = nullptr;
+  long long* pkeys = nullptr;     // probe array (capacity)
+  vg::VoxelRec* recs = nullptr;   // records parallel to pkeys
+  long long empty_key = 0;
   // reference arrays (device, fp64/int64): keys sorted ascending, means m*3, covs m*9
   long long* keys = nullptr;
   double* means = nullptr;
@@ -59,7 +61,9 @@ struct vg_map {
   long long* counts = nullptr;
   vg::MapView view() const {
     vg::MapView v;
-    v.table = table;
+    v.keys = pkeys;
+    v.recs = recs;
+    v.empty_key = empty_key;
     v.res = res;
     v.inv_res = 1.0 / res;
     v.mask = capacity - 1;
@@ -84,6 +88,9 @@ struct vg_batch {
   vg::CloudView* clouds = nullptr;    // num_clouds
   vg::MapView* maps = nullptr;        // num_maps
   double* partials = nullptr;         // num_items * kPartialStride
+  int2* hits = nullptr;               // compacted (point, slot) hits, per-item regions
+  int* hit_counts = nullptr;          // num_items
+  long long hit_capacity = 0;
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;
   double* out = nullptr;              // device output (F * 92)
@@ -117,6 +124,7 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                  double* wd, double* partial_cost, long long* partial_inl, int nblocks);
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
 int launch_linearize(vg_ctx* ctx, vg_batch* b, int mode);
+int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);
 int launch_cov(vg_ctx* ctx, const vg_cloud* cloud, const long long* nbrs_dev, int k,

@@ -58,20 +58,10 @@ __device__ __forceinline__ void load_point(const CloudView& cv, long long i, dou
   }
 }
 
-// 1/a: hardware approximation + two Newton steps (error squares each step), no slow path
-__device__ __forceinline__ double rcp64(double a) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
-  double e = fma(-a, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-a, r, 1.0);
-  return fma(r, e, r);
-}
-
 // fused covariance, inverse, residual and Mahalanobis cost of one correspondence
 // (registration.py:150-156), all fp64.
 __device__ __forceinline__ void point_terms(const double (&R)[9], const CloudView& cv,
-                                            long long i, const Slot* __restrict__ sl,
+                                            long long i, const VoxelRec* __restrict__ sl,
                                             double x, double y, double z, const double (&t)[3],
                                             PointTerms& o) {
   const double2 m01 = __ldg(reinterpret_cast<const double2*>(&sl->mean[0]));
@@ -130,21 +120,6 @@ __device__ __forceinline__ void point_terms(const double (&R)[9], const CloudVie
 
 // ---- warp reductions ---------------------------------------------------------------------
 
-// 32 values reduced across 32 lanes in 31 shuffle steps; lane L returns the sum of value L.
-__device__ __forceinline__ double warp_transpose_reduce32(double (&v)[32], int lane) {
-#pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) {
-    const bool up = (lane & s) != 0;
-#pragma unroll
-    for (int i = 0; i < s; ++i) {
-      const double send = up ? v[i] : v[i + s];
-      const double keep = up ? v[i + s] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-    }
-  }
-  return v[0];
-}
-
 // ---- K4: fused linearize / cost over (factor, chunk) work items --------------------------
 // One warp per item.  Phase A (per 32 points): load, transform, key, probe.  Hits are
 // compacted through a per-warp shared-memory ring so phase B — the fp64 fused-covariance /
@@ -160,8 +135,9 @@ template <int MODE>
 __device__ __forceinline__ void accumulate_hit(const double (&R)[9], const double (&t)[3],
                                                const CloudView& cv, const MapView& mv,
                                                const QEntry& e, double (&acc)[28]) {
+  if (MODE == 2) return;  // correspondence counting only
   PointTerms o;
-  point_terms(R, cv, e.i, mv.table + e.slot, e.x, e.y, e.z, t, o);
+  point_terms(R, cv, e.i, mv.recs + e.slot, e.x, e.y, e.z, t, o);
   if (MODE == 1) {
     acc[27] += o.cost;
     return;
@@ -226,7 +202,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
   double x = 0.0, y = 0.0, z = 0.0;
   long long key = 0;
   unsigned h = 0;
-  int4 s0 = make_int4(0, 0, -1, 0);
+  ProbeGroup pg{};
   auto issue = [&]() {
     if (!live) return;
     double px, py, pz;
@@ -238,7 +214,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
                    floor_div(z, mv.res, mv.inv_res, mv.pow2));
     if (mv.m == 0) return;
     h = slot_of(key, mv.shift);
-    s0 = __ldg(reinterpret_cast<const int4*>(mv.table + h));
+    pg = probe_load(mv, h);
   };
   issue();
   for (int base = it.begin; base < it.end; base += 32) {
@@ -252,15 +228,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     // resolve this batch's probes (misses contribute nothing, registration.py:150-156)
     int slot = -1;
     if (live && mv.m != 0) {
-      for (;;) {
-        const long long k = ((long long)(unsigned)s0.y << 32) | (unsigned)s0.x;
-        if (s0.z < 0) break;
-        if (k == key) {
-          slot = (int)h;
-          break;
-        }
-        h = (h + 1) & mv.mask;
-        s0 = __ldg(reinterpret_cast<const int4*>(mv.table + h));
+      while (probe_scan(mv, pg, h, key, slot) < 0) {
+        h = ((h & ~3u) + 4u) & mv.mask;
+        pg = probe_load(mv, h);
       }
     }
     const unsigned hits = __ballot_sync(0xffffffffu, slot >= 0);
@@ -290,7 +260,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
   }
   const int inl = (int)tail;  // every hit was queued exactly once
 
-  if (MODE == 1) {
+  if (MODE >= 1) {
     double c = acc[27];
 #pragma unroll
     for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
@@ -346,7 +316,7 @@ __global__ void k_finalize(const FactorDev* __restrict__ factors, int F,
   const int fi = blockIdx.x * blockDim.x + threadIdx.x;
   if (fi >= F) return;
   const FactorDev& f = factors[fi];
-  if (mode == 1) {
+  if (mode == 1 || mode == 3) {
     double c = 0.0, n = 0.0;
     for (int it = 0; it < f.item_count; ++it) {
       c += partials[2 * (size_t)(f.item_begin + it)];
@@ -542,7 +512,7 @@ __global__ void k_lookup(CloudView cv, MapView mv, const double* __restrict__ Tp
                                    floor_div(y, mv.res, mv.inv_res, mv.pow2),
                                    floor_div(z, mv.res, mv.inv_res, mv.pow2));
     const int slot = probe(mv, key);
-    const long long row = slot < 0 ? -1 : (long long)__ldg(&mv.table[slot].row);
+    const long long row = slot < 0 ? -1 : (long long)__ldg(&mv.recs[slot].row);
     if (rows) rows[i] = row;
     local += (row >= 0);
   }
@@ -581,9 +551,9 @@ __global__ void k_terms(CloudView cv, MapView mv, const double* __restrict__ Tp,
       for (int k = 0; k < 9; ++k) wout[9 * i + k] = 0.0;
       continue;
     }
-    rows[i] = __ldg(&mv.table[slot].row);
+    rows[i] = __ldg(&mv.recs[slot].row);
     PointTerms o;
-    point_terms(R, cv, i, mv.table + slot, x, y, z, t, o);
+    point_terms(R, cv, i, mv.recs + slot, x, y, z, t, o);
     const int sym[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
     for (int k = 0; k < 3; ++k) dout[3 * i + k] = o.d[k], wdout[3 * i + k] = o.wd[k];
     for (int k = 0; k < 9; ++k) wout[9 * i + k] = o.W[sym[k]];
@@ -656,6 +626,9 @@ int launch_linearize(vg_ctx* ctx, vg_batch* b, int mode) {
   const int blocks = (int)((b->num_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
   if (mode == 1)
     k_linearize<1><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,
+                                                        b->clouds, b->maps, b->partials);
+  else if (mode == 2)
+    k_linearize<2><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,
                                                         b->clouds, b->maps, b->partials);
   else
     k_linearize<0><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,

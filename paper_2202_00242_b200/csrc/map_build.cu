@@ -6,6 +6,8 @@
 //   sums its members sequentially in index order with correctly rounded fp64 adds (no FMA),
 //   exactly the rounding sequence of np.add.at + true division.
 // The fp64 arrays are kept on the device for export; the hot path reads the 64 B slots.
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
@@ -84,33 +86,43 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
   cnt_out[cidx] = cnt;
 }
 
-// one thread per cell: claim a hash slot by CAS on its row field, then fill the 96 B slot
-// with the key and the voxel Gaussian (fp64).
+// one thread per cell: claim a slot by CAS on the key array (linear probing), then write the
+// parallel 96 B record (reference row + fp64 Gaussian).
 __global__ void k_hash_insert(const long long* __restrict__ keys, const double* __restrict__ means,
-                              const double* __restrict__ covs, int m, Slot* __restrict__ table,
-                              unsigned mask, int shift) {
+                              const double* __restrict__ covs, int m, long long* __restrict__ pkeys,
+                              VoxelRec* __restrict__ recs, long long empty_key, unsigned mask,
+                              int shift) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   const long long key = keys[r];
   unsigned h = slot_of(key, shift);
   for (;;) {
-    if (atomicCAS(&table[h].row, -1, r) == -1) break;
+    const unsigned long long prev =
+        atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
+                  (unsigned long long)empty_key, (unsigned long long)key);
+    if (prev == (unsigned long long)empty_key) break;
     h = (h + 1) & mask;
   }
-  Slot& s = table[h];
-  s.key = key;
-  s.pad0 = 0;
-  s.mean[0] = means[3 * r];
-  s.mean[1] = means[3 * r + 1];
-  s.mean[2] = means[3 * r + 2];
+  VoxelRec v;
+  v.row = r;
+  v.pad0 = 0;
+  v.mean[0] = means[3 * r];
+  v.mean[1] = means[3 * r + 1];
+  v.mean[2] = means[3 * r + 2];
   const double* C = covs + 9 * (size_t)r;
-  s.cov[0] = C[0];
-  s.cov[1] = C[1];
-  s.cov[2] = C[2];
-  s.cov[3] = C[4];
-  s.cov[4] = C[5];
-  s.cov[5] = C[8];
-  s.pad1 = 0.0;
+  v.cov[0] = C[0];
+  v.cov[1] = C[1];
+  v.cov[2] = C[2];
+  v.cov[3] = C[4];
+  v.cov[4] = C[5];
+  v.cov[5] = C[8];
+  v.pad1[0] = v.pad1[1] = 0.0;
+  recs[h] = v;
+}
+
+__global__ void k_fill(long long* __restrict__ p, long long v, unsigned n) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = v;
 }
 
 }  // namespace vg
@@ -143,21 +155,38 @@ int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cl) {
 }
 
 static int capacity_for(long long m, int* log2cap) {
-  int l = 1;
+  int l = 2;  // at least one 4-slot probe group
   while ((1LL << l) < 2 * m) ++l;
   *log2cap = l;
   return 1 << l;
 }
 
 int launch_map_finish(vg_ctx* ctx, vg_map* map) {
-  int l2 = 1;
+  int l2 = 2;
   map->capacity = (unsigned)capacity_for(map->m, &l2);
   map->log2cap = l2;
-  VG_CUDA(cudaMallocAsync((void**)&map->table, sizeof(Slot) * (size_t)map->capacity, ctx->stream));
-  VG_CUDA(cudaMemsetAsync(map->table, 0xff, sizeof(Slot) * (size_t)map->capacity, ctx->stream));
+  // empty marker: a value that is not a key of this map (keys are sorted on the device; the
+  // smallest candidate absent from them is found on the host from the first few keys)
+  long long empty = (long long)0x8000000000000000ull;
+  if (map->m) {
+    const int probe_n = (int)std::min<long long>(map->m, 64);
+    long long head[64];
+    VG_CUDA(cudaMemcpyAsync(head, map->keys, sizeof(long long) * probe_n, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    VG_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < probe_n && head[i] == empty; ++i) ++empty;  // keys strictly increasing
+  }
+  map->empty_key = empty;
+  VG_CUDA(cudaMallocAsync((void**)&map->pkeys, sizeof(long long) * (size_t)map->capacity, ctx->stream));
+  VG_CUDA(cudaMallocAsync((void**)&map->recs, sizeof(VoxelRec) * (size_t)map->capacity, ctx->stream));
+  k_fill<<<(int)std::min<unsigned>((map->capacity + 255) / 256, 148 * 16), 256, 0, ctx->stream>>>(
+      map->pkeys, empty, map->capacity);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
   if (map->m == 0) return 0;
   k_hash_insert<<<(int)((map->m + 127) / 128), 128, 0, ctx->stream>>>(
-      map->keys, map->means, map->covs, (int)map->m, map->table, map->capacity - 1, 64 - l2);
+      map->keys, map->means, map->covs, (int)map->m, map->pkeys, map->recs, empty,
+      map->capacity - 1, 64 - l2);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
