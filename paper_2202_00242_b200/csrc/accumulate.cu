@@ -17,6 +17,8 @@
 //   is reduced across the warp in a fixed order.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -24,9 +26,9 @@ namespace vg {
 
 // ---- K4a ------------------------------------------------------------------------------------
 constexpr int kLookupWarps = 8;
-constexpr int kLookupUnroll = 2;
 
-__global__ void __launch_bounds__(kLookupWarps * 32)
+template <int kLookupUnroll, int kMinBlocks>
+__global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     k_lookup_items(const ItemDev* __restrict__ items, int n_items,
                    const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
                    const MapView* __restrict__ maps, int2* __restrict__ hits,
@@ -77,7 +79,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32)
       key[u] = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
                         floor_div(y, mv.res, mv.inv_res, mv.pow2),
                         floor_div(z, mv.res, mv.inv_res, mv.pow2));
-      h[u] = slot_of(key[u], mv.shift);
+      h[u] = bucket_of(key[u], mv);
       if (base + lane + 32 * u < it.end && mv.m) pg[u] = probe_load(mv, h[u]);
     }
 #pragma unroll
@@ -86,7 +88,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32)
       int slot = -1;
       if (i < it.end && mv.m) {
         while (probe_scan(mv, pg[u], h[u], key[u], slot) < 0) {
-          h[u] = ((h[u] & ~3u) + 4u) & mv.mask;
+          h[u] = next_bucket(h[u], mv);
           pg[u] = probe_load(mv, h[u]);
         }
       }
@@ -124,31 +126,49 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// per-warp stage: own point (2 x 16 B, fp32 or fp64 xyz), own source covariance (3 x 16 B),
+// and 32 voxel records gathered cooperatively (5 x 16 B each, padded to 7 units so the
+// per-lane 16 B reads of a record are bank-conflict free)
+constexpr int kRecUnits = 5;
+constexpr int kRecStride = 7;
+struct AccStage {
+  float4 pt[2][32];
+  float4 cov[3][32];
+  float4 rec[32][kRecStride];
+};
 struct AccSmem {
-  float4 stage[kStages][kStageUnits][32];
+  AccStage stage[kStages];
 };
 
-// gather one round (32 hits) into stage `round % kStages`; always commits a group so every
-// lane has the same number of outstanding groups
+// Gather one round (<= 32 hits) into stage `round % kStages`.  Point and covariance rows are
+// lane-own (hits are in point order, so these are nearly coalesced); the random 80 B voxel
+// records are gathered cooperatively: each cp.async instruction covers 32 consecutive 16 B
+// units of 6-7 records instead of one unit of 32 records, cutting L1 wavefronts ~4x.
+// Always commits one group so every lane has the same number of outstanding groups.
 __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& mv, AccSmem& sm,
-                                            int round, int2 e, bool valid, int lane) {
-  if (valid) {
-    float4(*st)[32] = sm.stage[round % kStages];
+                                            int round, int2 e, int nvalid, int lane) {
+  AccStage& st = sm.stage[round % kStages];
+  if (lane < nvalid) {
     if (cv.xyz64) {
       const double* p = cv.xyz64 + 3 * (size_t)e.x;
-      double* d = reinterpret_cast<double*>(&st[0][lane]);
+      double* d = reinterpret_cast<double*>(&st.pt[0][lane]);
       cp_async8(d, p);
       cp_async8(d + 1, p + 1);
-      cp_async8(reinterpret_cast<double*>(&st[1][lane]), p + 2);
+      cp_async8(reinterpret_cast<double*>(&st.pt[1][lane]), p + 2);
     } else {
-      cp_async16(&st[0][lane], cv.a + e.x);
+      cp_async16(&st.pt[0][lane], cv.a + e.x);
     }
-    cp_async16(&st[2][lane], cv.c0 + e.x);
-    cp_async16(&st[3][lane], cv.c1 + e.x);
-    cp_async16(&st[4][lane], cv.c2 + e.x);
-    const char* rec = reinterpret_cast<const char*>(mv.recs + e.y);
+    cp_async16(&st.cov[0][lane], cv.c0 + e.x);
+    cp_async16(&st.cov[1][lane], cv.c1 + e.x);
+    cp_async16(&st.cov[2][lane], cv.c2 + e.x);
+  }
 #pragma unroll
-    for (int u = 0; u < 5; ++u) cp_async16(&st[5 + u][lane], rec + 16 * u);
+  for (int c = 0; c < kRecUnits; ++c) {
+    const int u = c * 32 + lane;
+    const int q = u / kRecUnits, j = u - q * kRecUnits;
+    const int slot = __shfl_sync(0xffffffffu, e.y, q);
+    if (q < nvalid)
+      cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(mv.recs + slot) + 16 * j);
   }
   cp_async_commit();
 }
@@ -184,40 +204,40 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
 #pragma unroll
   for (int r = 0; r < kStages - 1; ++r) {
     const int k = r * 32 + lane;
-    issue_round(cv, mv, sm, r, k < n ? hl[k] : make_int2(0, 0), k < n, lane);
+    issue_round(cv, mv, sm, r, k < n ? hl[k] : make_int2(0, 0), n - r * 32, lane);
   }
   // hit entries are prefetched one round ahead of their gather
   int kn = (kStages - 1) * 32 + lane;
   int2 nxt = kn < n ? hl[kn] : make_int2(0, 0);
   for (int r = 0; r < rounds; ++r) {
-    issue_round(cv, mv, sm, r + kStages - 1, nxt, kn < n, lane);
+    issue_round(cv, mv, sm, r + kStages - 1, nxt, n - (r + kStages - 1) * 32, lane);
     kn += 32;
     if (kn < n) nxt = hl[kn];
     cp_async_wait<kStages - 1>();
     __syncwarp();
     const int k = r * 32 + lane;
     if (k < n) {
-      const float4(*st)[32] = sm.stage[r % kStages];
+      const AccStage& st = sm.stage[r % kStages];
       double px, py, pz;
       if (cv.xyz64) {
-        const double* d = reinterpret_cast<const double*>(&st[0][lane]);
+        const double* d = reinterpret_cast<const double*>(&st.pt[0][lane]);
         px = d[0];
         py = d[1];
-        pz = reinterpret_cast<const double*>(&st[1][lane])[0];
+        pz = reinterpret_cast<const double*>(&st.pt[1][lane])[0];
       } else {
-        const float4 a = st[0][lane];
+        const float4 a = st.pt[0][lane];
         px = a.x;
         py = a.y;
         pz = a.z;
       }
-      const double2 s0 = *reinterpret_cast<const double2*>(&st[2][lane]);
-      const double2 s1 = *reinterpret_cast<const double2*>(&st[3][lane]);
-      const double2 s2 = *reinterpret_cast<const double2*>(&st[4][lane]);
-      const double2 m01 = *reinterpret_cast<const double2*>(&st[5][lane]);
-      const double2 m2c0 = *reinterpret_cast<const double2*>(&st[6][lane]);
-      const double2 c12 = *reinterpret_cast<const double2*>(&st[7][lane]);
-      const double2 c34 = *reinterpret_cast<const double2*>(&st[8][lane]);
-      const double v5 = reinterpret_cast<const double*>(&st[9][lane])[0];
+      const double2 s0 = *reinterpret_cast<const double2*>(&st.cov[0][lane]);
+      const double2 s1 = *reinterpret_cast<const double2*>(&st.cov[1][lane]);
+      const double2 s2 = *reinterpret_cast<const double2*>(&st.cov[2][lane]);
+      const double2 m01 = *reinterpret_cast<const double2*>(&st.rec[lane][0]);
+      const double2 m2c0 = *reinterpret_cast<const double2*>(&st.rec[lane][1]);
+      const double2 c12 = *reinterpret_cast<const double2*>(&st.rec[lane][2]);
+      const double2 c34 = *reinterpret_cast<const double2*>(&st.rec[lane][3]);
+      const double v5 = reinterpret_cast<const double*>(&st.rec[lane][4])[0];
       // moved point (registration.py:148) and residual d = mu' - moved (:152)
       const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
       const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
@@ -306,9 +326,19 @@ using namespace vg;
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   if (b->num_items == 0) return 0;
   const int n = (int)b->num_items;
-  k_lookup_items<<<(n + kLookupWarps - 1) / kLookupWarps, kLookupWarps * 32, 0, ctx->stream>>>(
-      b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
-      kmode == 2 ? b->partials : nullptr);
+  static const int unroll = [] {
+    const char* e = getenv("VGICP_LOOKUP_UNROLL");
+    return e ? atoi(e) : 1;
+  }();
+  const int lb = (n + kLookupWarps - 1) / kLookupWarps;
+  if (unroll == 2)
+    k_lookup_items<2, 2><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
+        kmode == 2 ? b->partials : nullptr);
+  else
+    k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
+        kmode == 2 ? b->partials : nullptr);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   if (kmode == 2) return 0;

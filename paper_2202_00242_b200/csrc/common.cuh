@@ -3,8 +3,8 @@
 // HBM layouts:
 //   cloud  : SoA, 64 B/point: a[i] = (x, y, z) fp32, covariance as three fp64 double2 arrays
 //            + optional fp64 xyz (n x 3) when the points are not exactly fp32 (keys stay exact)
-//   map    : open-addressing hash table (load factor <= 0.5): dense int64 key array probed
-//            4 slots per 32 B sector + parallel 96 B records (reference row, fp64 Gaussian).
+//   map    : bucketized open-addressing hash table (load factor <= 0.25): dense int64 key
+//            array in 64 B buckets of 8 slots + parallel 96 B records (row, fp64 Gaussian).
 //   work   : (factor, chunk) items, one warp per item; fp64 partials, fixed-order reduce.
 #pragma once
 #include <cstddef>
@@ -19,7 +19,7 @@ constexpr int kPartialStride = 32;    // doubles per work-item partial (29 used)
 constexpr int kMaxChunk = 512;        // points per work item => <= 16 points per lane
 
 // Voxel map on the device = open-addressing hash table in two parallel arrays indexed by
-// slot: a dense int64 key array (probed 4 slots per 32 B sector) and 96 B records carrying the
+// slot: a dense int64 key array (probed one 64 B bucket at a time) and 96 B records carrying the
 // reference row and the voxel Gaussian in fp64.  Empty slots hold `empty_key`, a value that is
 // not a key of this map.  Mean and covariance stay fp64: the fused covariance C' + R C R^T
 // has condition ~1e3 for plane-like cells and the parity bar is per element (1e-4 rel) on
@@ -51,8 +51,8 @@ struct MapView {
   long long empty_key;
   double res;
   double inv_res;
-  unsigned mask;        // capacity - 1
-  int shift;            // 64 - log2(capacity)
+  unsigned mask;        // buckets - 1
+  int shift;            // 64 - log2(buckets)
   int m;                // occupied cells
   int pow2;             // res is a power of two: x * (1/res) == x / res exactly
 };
@@ -104,40 +104,58 @@ __device__ __forceinline__ unsigned slot_of(long long key, int shift) {
   return (unsigned)(((unsigned long long)key * 0x9E3779B97F4A7C15ull) >> shift);
 }
 
-// Linear probing, resolved 4 slots (one 32 B sector) per memory access.  Returns the slot
-// index or -1.  Lookups of any key (including empty_key itself) terminate at an empty slot.
+// Bucketized open addressing: a key hashes to a 64 B bucket of 8 slots (two 256-bit loads);
+// insertion fills the home bucket before spilling to the next one, so a lookup resolves in
+// its home bucket unless that bucket is full (load factor <= 0.25: ~0.1% of lookups).
+// Returns the slot index or -1.  Lookups of any key (including empty_key) terminate.
+constexpr int kBucket = 8;
 struct ProbeGroup {
-  longlong2 k01, k23;
+  long long k[kBucket];
 };
-__device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned h) {
-  const longlong2* g = reinterpret_cast<const longlong2*>(mv.keys + (h & ~3u));
-  return ProbeGroup{__ldg(g), __ldg(g + 1)};
+__device__ __forceinline__ void ld256(const void* p, long long& a, long long& b, long long& c,
+                                      long long& d) {
+  asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+               : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+               : "l"(p));
 }
-// scan the group loaded for position h; returns 1 found (slot set), 0 missing, -1 continue
-__device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& pg, unsigned h,
-                                          long long key, int& slot) {
-  const long long ks[4] = {pg.k01.x, pg.k01.y, pg.k23.x, pg.k23.y};
-  const unsigned j0 = h & 3u;
+__device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned bucket) {
+  ProbeGroup g;
+  const long long* p = mv.keys + (size_t)bucket * kBucket;
+  ld256(p, g.k[0], g.k[1], g.k[2], g.k[3]);
+  ld256(p + 4, g.k[4], g.k[5], g.k[6], g.k[7]);
+  return g;
+}
+// 1 found (slot set), 0 missing, -1 continue with the next bucket
+__device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& g,
+                                          unsigned bucket, long long key, int& slot) {
+  int found = -1;
+  bool empty = false;
 #pragma unroll
-  for (unsigned j = 0; j < 4; ++j) {
-    if (j < j0) continue;
-    if (ks[j] == key) {
-      slot = (int)((h & ~3u) + j);
-      return 1;
-    }
-    if (ks[j] == mv.empty_key) return 0;
+  for (int j = kBucket - 1; j >= 0; --j) {
+    if (g.k[j] == key) found = j;
+    empty |= (g.k[j] == mv.empty_key);
   }
-  return -1;
+  if (found >= 0) {
+    slot = (int)(bucket * kBucket + found);
+    return 1;
+  }
+  return empty ? 0 : -1;
+}
+__device__ __forceinline__ unsigned bucket_of(long long key, const MapView& mv) {
+  return slot_of(key, mv.shift);  // shift = 64 - log2(#buckets)
+}
+__device__ __forceinline__ unsigned next_bucket(unsigned b, const MapView& mv) {
+  return (b + 1) & mv.mask;  // mask = #buckets - 1
 }
 __device__ __forceinline__ int probe(const MapView& mv, long long key) {
   if (mv.m == 0) return -1;
-  unsigned h = slot_of(key, mv.shift);
+  unsigned b = bucket_of(key, mv);
   for (;;) {
-    const ProbeGroup pg = probe_load(mv, h);
+    const ProbeGroup g = probe_load(mv, b);
     int slot = -1;
-    const int r = probe_scan(mv, pg, h, key, slot);
+    const int r = probe_scan(mv, g, b, key, slot);
     if (r >= 0) return r ? slot : -1;
-    h = ((h & ~3u) + 4u) & mv.mask;
+    b = next_bucket(b, mv);
   }
 }
 

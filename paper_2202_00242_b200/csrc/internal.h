@@ -66,8 +66,8 @@ struct vg_map {
     v.empty_key = empty_key;
     v.res = res;
     v.inv_res = 1.0 / res;
-    v.mask = capacity - 1;
-    v.shift = 64 - log2cap;
+    v.mask = (capacity / vg::kBucket) - 1;
+    v.shift = 64 - (log2cap - 3);
     v.m = (int)m;
     int e2 = 0;
     v.pow2 = (std::frexp(res, &e2) == 0.5) ? 1 : 0;

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
                    floor_div(y, mv.res, mv.inv_res, mv.pow2),
                    floor_div(z, mv.res, mv.inv_res, mv.pow2));
     if (mv.m == 0) return;
-    h = slot_of(key, mv.shift);
+    h = bucket_of(key, mv);
     pg = probe_load(mv, h);
   };
   issue();
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     int slot = -1;
     if (live && mv.m != 0) {
       while (probe_scan(mv, pg, h, key, slot) < 0) {
-        h = ((h & ~3u) + 4u) & mv.mask;
+        h = next_bucket(h, mv);
         pg = probe_load(mv, h);
       }
     }

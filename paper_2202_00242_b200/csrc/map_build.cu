@@ -95,13 +95,16 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   const long long key = keys[r];
-  unsigned h = slot_of(key, shift);
-  for (;;) {
-    const unsigned long long prev =
-        atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
-                  (unsigned long long)empty_key, (unsigned long long)key);
-    if (prev == (unsigned long long)empty_key) break;
-    h = (h + 1) & mask;
+  unsigned b = slot_of(key, shift);  // home bucket
+  unsigned h = 0;
+  for (bool placed = false; !placed; b = (b + 1) & mask) {
+    for (int j = 0; j < kBucket && !placed; ++j) {
+      h = b * kBucket + j;
+      const unsigned long long prev =
+          atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
+                    (unsigned long long)empty_key, (unsigned long long)key);
+      placed = prev == (unsigned long long)empty_key;
+    }
   }
   VoxelRec v;
   v.row = r;
@@ -155,14 +158,14 @@ int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cl) {
 }
 
 static int capacity_for(long long m, int* log2cap) {
-  int l = 2;  // at least one 4-slot probe group
-  while ((1LL << l) < 2 * m) ++l;
+  int l = 3;  // at least one 8-slot bucket; load factor <= 0.25
+  while ((1LL << l) < 4 * m) ++l;
   *log2cap = l;
   return 1 << l;
 }
 
 int launch_map_finish(vg_ctx* ctx, vg_map* map) {
-  int l2 = 2;
+  int l2 = 3;
   map->capacity = (unsigned)capacity_for(map->m, &l2);
   map->log2cap = l2;
   // empty marker: a value that is not a key of this map (keys are sorted on the device; the
@@ -186,7 +189,7 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
   if (map->m == 0) return 0;
   k_hash_insert<<<(int)((map->m + 127) / 128), 128, 0, ctx->stream>>>(
       map->keys, map->means, map->covs, (int)map->m, map->pkeys, map->recs, empty,
-      map->capacity - 1, 64 - l2);
+      (map->capacity / kBucket) - 1, 64 - (l2 - 3));
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
