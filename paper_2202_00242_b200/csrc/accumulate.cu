@@ -27,7 +27,7 @@ namespace vg {
 // ---- K4a ------------------------------------------------------------------------------------
 constexpr int kLookupWarps = 8;
 
-template <int kLookupUnroll, int kMinBlocks>
+template <int kMinBlocks>
 __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     k_lookup_items(const ItemDev* __restrict__ items, int n_items,
                    const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
@@ -48,54 +48,47 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
   const unsigned lt_mask = (1u << lane) - 1u;
   int2* out = hits + it.hoff;
   int cnt = 0;
-  for (int base = it.begin; base < it.end; base += 32 * kLookupUnroll) {
-    double px[kLookupUnroll], py[kLookupUnroll], pz[kLookupUnroll];
-#pragma unroll
-    for (int u = 0; u < kLookupUnroll; ++u) {
-      const int i = base + lane + 32 * u;
-      px[u] = py[u] = pz[u] = 0.0;
-      if (i < it.end) {
-        if (cv.xyz64) {
-          px[u] = __ldg(cv.xyz64 + 3 * (size_t)i);
-          py[u] = __ldg(cv.xyz64 + 3 * (size_t)i + 1);
-          pz[u] = __ldg(cv.xyz64 + 3 * (size_t)i + 2);
-        } else {
-          const float4 a = __ldg(cv.a + i);
-          px[u] = a.x;
-          py[u] = a.y;
-          pz[u] = a.z;
-        }
+  // the next iteration's source point is loaded before this iteration's probe is resolved,
+  // so the two dependent latencies of consecutive iterations overlap
+  const int last = it.end - 1;
+  auto load_pt = [&](int i, double& px, double& py, double& pz) {
+    const int ic = min(i, last);
+    if (cv.xyz64) {
+      px = __ldg(cv.xyz64 + 3 * (size_t)ic);
+      py = __ldg(cv.xyz64 + 3 * (size_t)ic + 1);
+      pz = __ldg(cv.xyz64 + 3 * (size_t)ic + 2);
+    } else {
+      const float4 a = __ldg(cv.a + ic);
+      px = a.x;
+      py = a.y;
+      pz = a.z;
+    }
+  };
+  double nx, ny, nz;
+  load_pt(it.begin + lane, nx, ny, nz);
+  for (int base = it.begin; base < it.end; base += 32) {
+    const int i = base + lane;
+    const double px = nx, py = ny, pz = nz;
+    load_pt(i + 32, nx, ny, nz);
+    // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
+    const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
+    const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
+    const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
+    const long long key = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                                   floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                                   floor_div(z, mv.res, mv.inv_res, mv.pow2));
+    int slot = -1;
+    if (i < it.end && mv.m) {
+      unsigned bk = bucket_of(key, mv);
+      ProbeGroup pg = probe_load(mv, bk);
+      while (probe_scan(mv, pg, bk, key, slot) < 0) {
+        bk = next_bucket(bk, mv);
+        pg = probe_load(mv, bk);
       }
     }
-    long long key[kLookupUnroll];
-    unsigned h[kLookupUnroll];
-    ProbeGroup pg[kLookupUnroll];
-#pragma unroll
-    for (int u = 0; u < kLookupUnroll; ++u) {
-      // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
-      const double x = fma(R[0], px[u], fma(R[1], py[u], R[2] * pz[u])) + t[0];
-      const double y = fma(R[3], px[u], fma(R[4], py[u], R[5] * pz[u])) + t[1];
-      const double z = fma(R[6], px[u], fma(R[7], py[u], R[8] * pz[u])) + t[2];
-      key[u] = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                        floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                        floor_div(z, mv.res, mv.inv_res, mv.pow2));
-      h[u] = bucket_of(key[u], mv);
-      if (base + lane + 32 * u < it.end && mv.m) pg[u] = probe_load(mv, h[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < kLookupUnroll; ++u) {
-      const int i = base + lane + 32 * u;
-      int slot = -1;
-      if (i < it.end && mv.m) {
-        while (probe_scan(mv, pg[u], h[u], key[u], slot) < 0) {
-          h[u] = next_bucket(h[u], mv);
-          pg[u] = probe_load(mv, h[u]);
-        }
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
-      if (slot >= 0) out[cnt + __popc(m & lt_mask)] = make_int2(i, slot);
-      cnt += __popc(m);
-    }
+    const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
+    if (slot >= 0) out[cnt + __popc(m & lt_mask)] = make_int2(i, slot);
+    cnt += __popc(m);
   }
   if (lane == 0) {
     counts[w] = cnt;
@@ -206,13 +199,15 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
     const int k = r * 32 + lane;
     issue_round(cv, mv, sm, r, k < n ? hl[k] : make_int2(0, 0), n - r * 32, lane);
   }
-  // hit entries are prefetched one round ahead of their gather
+  // hit entries are prefetched one round ahead of their gather; the load is unconditional
+  // (index clamped) so its first use is the next iteration's gather, not a predicated move
   int kn = (kStages - 1) * 32 + lane;
-  int2 nxt = kn < n ? hl[kn] : make_int2(0, 0);
+  const int klast = n > 0 ? n - 1 : 0;
+  int2 nxt = __ldg(hl + min(kn, klast));
   for (int r = 0; r < rounds; ++r) {
     issue_round(cv, mv, sm, r + kStages - 1, nxt, n - (r + kStages - 1) * 32, lane);
     kn += 32;
-    if (kn < n) nxt = hl[kn];
+    nxt = __ldg(hl + min(kn, klast));
     cp_async_wait<kStages - 1>();
     __syncwarp();
     const int k = r * 32 + lane;
@@ -326,17 +321,17 @@ using namespace vg;
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   if (b->num_items == 0) return 0;
   const int n = (int)b->num_items;
-  static const int unroll = [] {
-    const char* e = getenv("VGICP_LOOKUP_UNROLL");
-    return e ? atoi(e) : 1;
+  static const int min_blocks = [] {
+    const char* e = getenv("VGICP_LOOKUP_BLOCKS");
+    return e ? atoi(e) : 3;
   }();
   const int lb = (n + kLookupWarps - 1) / kLookupWarps;
-  if (unroll == 2)
-    k_lookup_items<2, 2><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
+  if (min_blocks >= 4)
+    k_lookup_items<4><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
         b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
         kmode == 2 ? b->partials : nullptr);
   else
-    k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
+    k_lookup_items<3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
         b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
         kmode == 2 ? b->partials : nullptr);
   ctx->launches++;
