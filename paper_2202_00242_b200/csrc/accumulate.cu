@@ -101,7 +101,6 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
 
 // ---- K4b ------------------------------------------------------------------------------------
 constexpr int kAccWarps = 4;
-constexpr int kStages = 3;
 // stage layout (16 B units x 32 lanes): p0 p1 (point), c0 c1 c2 (source cov), r0..r4 (record)
 constexpr int kStageUnits = 10;
 
@@ -120,15 +119,16 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // per-warp stage: own point (2 x 16 B, fp32 or fp64 xyz), own source covariance (3 x 16 B),
-// and 32 voxel records gathered cooperatively (5 x 16 B each, padded to 7 units so the
-// per-lane 16 B reads of a record are bank-conflict free)
+// and 32 voxel records gathered cooperatively (5 x 16 B each; the 80 B lane stride is 20
+// banks, so 8 lanes of a 16 B shared-memory read hit 8 distinct 4-bank groups: conflict free)
 constexpr int kRecUnits = 5;
-constexpr int kRecStride = 7;
+constexpr int kRecStride = 5;
 struct AccStage {
   float4 pt[2][32];
   float4 cov[3][32];
   float4 rec[32][kRecStride];
 };
+template <int kStages>
 struct AccSmem {
   AccStage stage[kStages];
 };
@@ -138,8 +138,10 @@ struct AccSmem {
 // records are gathered cooperatively: each cp.async instruction covers 32 consecutive 16 B
 // units of 6-7 records instead of one unit of 32 records, cutting L1 wavefronts ~4x.
 // Always commits one group so every lane has the same number of outstanding groups.
-__device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& mv, AccSmem& sm,
-                                            int round, int2 e, int nvalid, int lane) {
+template <int kStages>
+__device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& mv,
+                                            AccSmem<kStages>& sm, int round, int2 e, int nvalid,
+                                            int lane) {
   AccStage& st = sm.stage[round % kStages];
   if (lane < nvalid) {
     if (cv.xyz64) {
@@ -166,8 +168,8 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
   cp_async_commit();
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kAccWarps * 32, 3)
+template <int MODE, int kStages, int kMinBlocks>
+__global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     k_accumulate(const ItemDev* __restrict__ items, int n_items,
                  const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
                  const MapView* __restrict__ maps, const int2* __restrict__ hits,
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, 3)
   const int wib = threadIdx.x >> 5;
   const int w = blockIdx.x * kAccWarps + wib;
   if (w >= n_items) return;
-  AccSmem& sm = reinterpret_cast<AccSmem*>(smem_raw)[wib];
+  AccSmem<kStages>& sm = reinterpret_cast<AccSmem<kStages>*>(smem_raw)[wib];
   const ItemDev it = items[w];
   const FactorDev* f = factors + it.factor;
   const int n = counts[w];
@@ -337,20 +339,32 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   if (kmode == 2) return 0;
-  const size_t smem = sizeof(AccSmem) * kAccWarps;
-  static bool attr_set = false;
-  if (!attr_set) {
-    VG_CUDA(cudaFuncSetAttribute(k_accumulate<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    VG_CUDA(cudaFuncSetAttribute(k_accumulate<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_set = true;
-  }
+  static const int variant = [] {
+    const char* e = getenv("VGICP_ACC_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
   const int blocks = (n + kAccWarps - 1) / kAccWarps;
-  if (kmode == 1)
-    k_accumulate<1><<<blocks, kAccWarps * 32, smem, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, b->partials);
-  else
-    k_accumulate<0><<<blocks, kAccWarps * 32, smem, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, b->partials);
+  auto go = [&](auto kern, size_t smem) -> int {
+    VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<blocks, kAccWarps * 32, smem, ctx->stream>>>(b->items, n, b->factors, b->clouds,
+                                                        b->maps, b->hits, b->hit_counts,
+                                                        b->partials);
+    return 0;
+  };
+  // variants (stages, min CTAs/SM): 0 = (3,3), 1 = (2,4), 2 = (2,3), 3 = (4,2)
+  int rc = 0;
+  if (kmode == 1) {
+    rc = go(k_accumulate<1, 3, 3>, sizeof(AccSmem<3>) * kAccWarps);
+  } else if (variant == 1) {
+    rc = go(k_accumulate<0, 2, 4>, sizeof(AccSmem<2>) * kAccWarps);
+  } else if (variant == 2) {
+    rc = go(k_accumulate<0, 2, 3>, sizeof(AccSmem<2>) * kAccWarps);
+  } else if (variant == 3) {
+    rc = go(k_accumulate<0, 4, 2>, sizeof(AccSmem<4>) * kAccWarps);
+  } else {
+    rc = go(k_accumulate<0, 3, 3>, sizeof(AccSmem<3>) * kAccWarps);
+  }
+  if (rc) return rc;
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
