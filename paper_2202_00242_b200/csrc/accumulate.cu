@@ -325,7 +325,7 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   const int n = (int)b->num_items;
   static const int min_blocks = [] {
     const char* e = getenv("VGICP_LOOKUP_BLOCKS");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 4;
   }();
   const int lb = (n + kLookupWarps - 1) / kLookupWarps;
   if (min_blocks >= 4)
@@ -341,7 +341,7 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   if (kmode == 2) return 0;
   static const int variant = [] {
     const char* e = getenv("VGICP_ACC_VARIANT");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 2;
   }();
   const int blocks = (n + kAccWarps - 1) / kAccWarps;
   auto go = [&](auto kern, size_t smem) -> int {
@@ -354,7 +354,7 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   // variants (stages, min CTAs/SM): 0 = (3,3), 1 = (2,4), 2 = (2,3), 3 = (4,2)
   int rc = 0;
   if (kmode == 1) {
-    rc = go(k_accumulate<1, 3, 3>, sizeof(AccSmem<3>) * kAccWarps);
+    rc = go(k_accumulate<1, 2, 3>, sizeof(AccSmem<2>) * kAccWarps);
   } else if (variant == 1) {
     rc = go(k_accumulate<0, 2, 4>, sizeof(AccSmem<2>) * kAccWarps);
   } else if (variant == 2) {
