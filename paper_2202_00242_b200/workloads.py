@@ -67,13 +67,6 @@ def global_mapping(n_submaps: int = 1000, neighbors: int = 50, resolution: float
 
 
 def lpt_shards(weights: np.ndarray, n_shards: int) -> list:
-    """Longest-processing-time partition of factors by point count; each shard is sorted
-    (keeps target-map grouping inside a shard)."""
-    order = np.argsort(-np.asarray(weights), kind="stable")
-    loads = np.zeros(n_shards)
-    members = [[] for _ in range(n_shards)]
-    for f in order:
-        r = int(np.argmin(loads))
-        members[r].append(int(f))
-        loads[r] += weights[f]
-    return [np.sort(np.array(m, dtype=np.int64)) for m in members]
+    from .sharding import lpt_shards as _lpt
+
+    return _lpt(weights, n_shards)
