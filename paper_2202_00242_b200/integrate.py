@@ -1,0 +1,89 @@
+"""Swap the reference package's VGICP path for this one, in place.
+
+    import limapper, paper_2202_00242_b200.integrate as vg
+    undo = vg.patch(limapper)      # limapper.* now run on the B200 through libvgicp
+    ...
+    undo()
+
+Every replaced name keeps the reference's signature, argument meaning and exceptions
+(registration.py:29-269, preprocess.py:68-164, factor_graph.py:209-308).  Modules that
+imported a name with ``from .registration import ...`` (factor_graph.py:49-55,
+odometry.py:21-46) get their module-level binding replaced too; the reference's
+FactorGraph, LM solver, IMU factors and odometry logic are untouched and call the drop-in
+through the unchanged per-factor Factor protocol.
+"""
+
+from __future__ import annotations
+
+import importlib
+import sys
+
+from . import factor_graph as _fg
+from . import preprocess as _pp
+from . import registration as _rg
+
+REPLACEMENTS = {
+    "registration": {
+        "GaussianVoxelMap": _rg.GaussianVoxelMap,
+        "build_voxelmap": _rg.build_voxelmap,
+        "d2d_error": _rg.d2d_error,
+        "match_terms": _rg.match_terms,
+        "matching_cost": _rg.matching_cost,
+        "overlap_rate": _rg.overlap_rate,
+        "linearize_from_terms": _rg.linearize_from_terms,
+        "linearize_matching_cost": _rg.linearize_matching_cost,
+        "MatchTerms": _rg.MatchTerms,
+        "MatchingCostLinearization": _rg.MatchingCostLinearization,
+    },
+    "preprocess": {
+        "pack_voxel_keys": _pp.pack_voxel_keys,
+        "knn_search": _pp.knn_search,
+        "estimate_covariances": _pp.estimate_covariances,
+    },
+    "factor_graph": {
+        "MatchingCostFactor": _fg.MatchingCostFactor,
+        "GaussianVoxelMap": _rg.GaussianVoxelMap,
+        "match_terms": _rg.match_terms,
+        "linearize_from_terms": _rg.linearize_from_terms,
+    },
+    "odometry": {
+        "MatchingCostFactor": _fg.MatchingCostFactor,
+        "GaussianVoxelMap": _rg.GaussianVoxelMap,
+        "build_voxelmap": _rg.build_voxelmap,
+        "overlap_rate": _rg.overlap_rate,
+        "knn_search": _pp.knn_search,
+        "estimate_covariances": _pp.estimate_covariances,
+    },
+}
+
+
+def _module(pkg, sub):
+    if isinstance(pkg, str):
+        name = f"{pkg}.{sub}"
+    else:
+        name = f"{pkg.__name__}.{sub}"
+    if name in sys.modules:
+        return sys.modules[name]
+    try:
+        return importlib.import_module(name)
+    except ImportError:
+        return None
+
+
+def patch(pkg="limapper"):
+    """Replace the reference's VGICP path inside package `pkg`; returns an undo callable."""
+    saved = []
+    for sub, names in REPLACEMENTS.items():
+        mod = _module(pkg, sub) if not hasattr(pkg, sub) else getattr(pkg, sub)
+        if mod is None:
+            continue
+        for name, obj in names.items():
+            if hasattr(mod, name):
+                saved.append((mod, name, getattr(mod, name)))
+                setattr(mod, name, obj)
+
+    def undo():
+        for mod, name, obj in reversed(saved):
+            setattr(mod, name, obj)
+
+    return undo

@@ -92,3 +92,26 @@ def test_geometry_mirror_matches_reference_ops():
         xi = rng.uniform(-1, 1, 6)
         p = G.pose_retract(G.Se3Pose.identity(), xi)
         np.testing.assert_allclose(G.pose_local(p, G.Se3Pose.identity()), xi, atol=1e-12)
+
+
+def test_integrate_patch_replaces_and_restores():
+    import types
+
+    from paper_2202_00242_b200 import factor_graph, integrate, registration
+
+    sentinel = object()
+    pkg = types.SimpleNamespace(
+        __name__="fakepkg",
+        registration=types.SimpleNamespace(build_voxelmap=sentinel, match_terms=sentinel,
+                                           unrelated=sentinel),
+        factor_graph=types.SimpleNamespace(MatchingCostFactor=sentinel),
+        preprocess=types.SimpleNamespace(knn_search=sentinel),
+        odometry=types.SimpleNamespace(overlap_rate=sentinel))
+    undo = integrate.patch(pkg)
+    assert pkg.registration.build_voxelmap is registration.build_voxelmap
+    assert pkg.factor_graph.MatchingCostFactor is factor_graph.MatchingCostFactor
+    assert pkg.odometry.overlap_rate is registration.overlap_rate
+    assert pkg.registration.unrelated is sentinel
+    undo()
+    assert pkg.registration.build_voxelmap is sentinel
+    assert pkg.preprocess.knn_search is sentinel
