@@ -5,8 +5,8 @@
 // every factor of a graph (factor_graph.py:522-536).
 //
 // K4a — one warp per (factor, <=512-point chunk) item, light on registers so many warps hide
-//   the two dependent memory latencies of a lookup (source point, then the probed 32 B key
-//   group).  x = R p + t (fp64) -> key (bit-exact floor) -> linear probe 4 slots per sector.
+//   the two dependent memory latencies of a lookup (source point, then the probed key
+//   bucket).  x = R p + t (fp64) -> key (bit-exact floor) -> one 32 B bucket of 8 local keys.
 //   Hits are written as (point, slot) pairs into the item's region of a batch-wide hit list
 //   with a warp ballot, preserving point order.  Misses contribute nothing (:150-156).
 // K4b — one warp per item over its compacted hits, so every lane of the expensive fp64 path
@@ -27,7 +27,8 @@ namespace vg {
 // ---- K4a ------------------------------------------------------------------------------------
 constexpr int kLookupWarps = 8;
 
-template <int kMinBlocks>
+// KM: 1 = every map of the batch uses 32-bit local keys, 0 = all int64, 2 = mixed (runtime)
+template <int KM, int kMinBlocks>
 __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     k_lookup_items(const ItemDev* __restrict__ items, int n_items,
                    const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
@@ -45,6 +46,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
   for (int k = 0; k < 3; ++k) t[k] = __ldg(f->T + 9 + k);
   const CloudView cv = clouds[__ldg(&f->cloud)];
   const MapView mv = maps[__ldg(&f->map)];
+  const int kmode = KM == 2 ? mv.kmode : KM;
   const unsigned lt_mask = (1u << lane) - 1u;
   int2* out = hits + it.hoff;
   int cnt = 0;
@@ -74,16 +76,16 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
     const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
     const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
-    const long long key = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                                   floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                                   floor_div(z, mv.res, mv.inv_res, mv.pow2));
+    const Query qy = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                                floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                                floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
     int slot = -1;
-    if (i < it.end && mv.m) {
-      unsigned bk = bucket_of(key, mv);
-      ProbeGroup pg = probe_load(mv, bk);
-      while (probe_scan(mv, pg, bk, key, slot) < 0) {
+    if (i < it.end && mv.m && qy.inside) {
+      unsigned bk = qy.bucket;
+      ProbeGroup pg = probe_load(mv, bk, kmode);
+      while (probe_scan(mv, pg, bk, qy, slot, kmode) < 0) {
         bk = next_bucket(bk, mv);
-        pg = probe_load(mv, bk);
+        pg = probe_load(mv, bk, kmode);
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
@@ -323,19 +325,17 @@ using namespace vg;
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   if (b->num_items == 0) return 0;
   const int n = (int)b->num_items;
-  static const int min_blocks = [] {
-    const char* e = getenv("VGICP_LOOKUP_BLOCKS");
-    return e ? atoi(e) : 4;
-  }();
   const int lb = (n + kLookupWarps - 1) / kLookupWarps;
-  if (min_blocks >= 4)
-    k_lookup_items<4><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
-        kmode == 2 ? b->partials : nullptr);
+  double* p2 = kmode == 2 ? b->partials : nullptr;
+  if (b->key_mode == 1)
+    k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2);
+  else if (b->key_mode == 0)
+    k_lookup_items<0, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2);
   else
-    k_lookup_items<3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts,
-        kmode == 2 ? b->partials : nullptr);
+    k_lookup_items<2, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   if (kmode == 2) return 0;

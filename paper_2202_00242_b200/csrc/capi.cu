@@ -274,6 +274,7 @@ int vg_map_destroy(vg_map* m) {
   if (!m) return VG_OK;
   vg_ctx* ctx = m->ctx;
   dfree(ctx, m->pkeys);
+  dfree(ctx, m->pkeys32);
   dfree(ctx, m->recs);
   dfree(ctx, m->keys);
   dfree(ctx, m->means);
@@ -452,7 +453,12 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   std::vector<CloudView> cv(clouds.size());
   std::vector<MapView> mv(maps.size());
   for (size_t i = 0; i < clouds.size(); ++i) cv[i] = clouds[i]->view();
-  for (size_t i = 0; i < maps.size(); ++i) mv[i] = maps[i]->view();
+  int n32 = 0;
+  for (size_t i = 0; i < maps.size(); ++i) {
+    mv[i] = maps[i]->view();
+    n32 += maps[i]->kmode;
+  }
+  b->key_mode = n32 == (int)maps.size() ? 1 : (n32 == 0 ? 0 : 2);
   int rc = VG_OK;
   if ((rc = dalloc(ctx, &b->factors, F)) || (rc = dalloc(ctx, &b->items, items.size())) ||
       (rc = dalloc(ctx, &b->clouds, cv.size())) || (rc = dalloc(ctx, &b->maps, mv.size())) ||

@@ -46,15 +46,19 @@ struct CloudView {
 };
 
 struct MapView {
-  const long long* keys;    // capacity (multiple of 4), 32 B aligned
-  const VoxelRec* recs;     // capacity, parallel to keys
-  long long empty_key;
+  const long long* keys;    // kmode 0: int64 packed keys, buckets of 8 (64 B)
+  const unsigned* keys32;   // kmode 1: 32-bit cell-local keys, buckets of 8 (32 B)
+  const VoxelRec* recs;     // capacity, parallel to the probe array
+  long long empty_key;      // kmode 0 empty marker (a value that is not a key of the map)
   double res;
   double inv_res;
   unsigned mask;        // buckets - 1
   int shift;            // 64 - log2(buckets)
   int m;                // occupied cells
   int pow2;             // res is a power of two: x * (1/res) == x / res exactly
+  int kmode;            // 1: every cell fits the 11/11/10-bit local frame below
+  int bx, by, bz;       // local frame origin (min cell index)
+  int ex, ey, ez;       // local frame extents (cells)
 };
 
 // Per-factor record resident in HBM (128 B).  T = T_ij (R row-major, t), fp64.
@@ -104,36 +108,89 @@ __device__ __forceinline__ unsigned slot_of(long long key, int shift) {
   return (unsigned)(((unsigned long long)key * 0x9E3779B97F4A7C15ull) >> shift);
 }
 
-// Bucketized open addressing: a key hashes to a 64 B bucket of 8 slots (two 256-bit loads);
-// insertion fills the home bucket before spilling to the next one, so a lookup resolves in
-// its home bucket unless that bucket is full (load factor <= 0.25: ~0.1% of lookups).
-// Returns the slot index or -1.  Lookups of any key (including empty_key) terminate.
+// Bucketized open addressing: a key hashes to a bucket of 8 slots; insertion fills the home
+// bucket before spilling to the next one, so a lookup resolves in its home bucket unless that
+// bucket is full (load factor <= 0.25: ~0.1% of lookups).  Two key encodings:
+//   kmode 1 — 32-bit cell-local keys (lx | ly << 11 | lz << 22 relative to the map's min
+//             cell); a bucket is 32 B = one 256-bit load.  Used whenever the map fits.
+//   kmode 0 — the reference's packed int64 keys; a bucket is 64 B = two 256-bit loads.
+// The local key is built from decode(pack(floor)) — the reference's own key round trip —
+// so aliasing of out-of-range indices behaves exactly as the reference's packed keys.
 constexpr int kBucket = 8;
-struct ProbeGroup {
-  long long k[kBucket];
+constexpr unsigned kEmpty32 = 0xffffffffu;
+
+struct Query {
+  long long key;   // packed reference key
+  unsigned k32;    // local key (kmode 1)
+  unsigned bucket;
+  bool inside;     // kmode 1: cell lies in the map's local frame (else certainly a miss)
 };
+struct ProbeGroup {
+  long long k[kBucket];  // kmode 0: 8 keys; kmode 1: k[0..3] hold 8 packed 32-bit keys
+};
+
 __device__ __forceinline__ void ld256(const void* p, long long& a, long long& b, long long& c,
                                       long long& d) {
   asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
                : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
                : "l"(p));
 }
-__device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned bucket) {
+
+// `kmode` is mv.kmode, passed separately so callers specialised on a key encoding fold it
+__device__ __forceinline__ Query make_query(const MapView& mv, double fx, double fy, double fz,
+                                            int kmode) {
+  Query q;
+  q.key = pack_key(fx, fy, fz);
+  if (kmode) {
+    const long long dx = (q.key >> 42) - kKeyOffset;
+    const long long dy = ((q.key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
+    const long long dz = (q.key & ((1LL << 21) - 1)) - kKeyOffset;
+    const unsigned long long lx = (unsigned long long)(dx - mv.bx);
+    const unsigned long long ly = (unsigned long long)(dy - mv.by);
+    const unsigned long long lz = (unsigned long long)(dz - mv.bz);
+    q.inside = lx < (unsigned long long)mv.ex && ly < (unsigned long long)mv.ey &&
+               lz < (unsigned long long)mv.ez;
+    q.k32 = (unsigned)lx | ((unsigned)ly << 11) | ((unsigned)lz << 22);
+    q.bucket = (q.k32 * 0x9E3779B9u) >> (mv.shift - 32);
+  } else {
+    q.inside = true;
+    q.k32 = 0;
+    q.bucket = slot_of(q.key, mv.shift);
+  }
+  return q;
+}
+
+__device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned bucket, int kmode) {
   ProbeGroup g;
-  const long long* p = mv.keys + (size_t)bucket * kBucket;
-  ld256(p, g.k[0], g.k[1], g.k[2], g.k[3]);
-  ld256(p + 4, g.k[4], g.k[5], g.k[6], g.k[7]);
+  if (kmode) {
+    ld256(mv.keys32 + (size_t)bucket * kBucket, g.k[0], g.k[1], g.k[2], g.k[3]);
+  } else {
+    const long long* p = mv.keys + (size_t)bucket * kBucket;
+    ld256(p, g.k[0], g.k[1], g.k[2], g.k[3]);
+    ld256(p + 4, g.k[4], g.k[5], g.k[6], g.k[7]);
+  }
   return g;
 }
+
 // 1 found (slot set), 0 missing, -1 continue with the next bucket
 __device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& g,
-                                          unsigned bucket, long long key, int& slot) {
+                                          unsigned bucket, const Query& q, int& slot,
+                                          int kmode) {
   int found = -1;
   bool empty = false;
+  if (kmode) {
 #pragma unroll
-  for (int j = kBucket - 1; j >= 0; --j) {
-    if (g.k[j] == key) found = j;
-    empty |= (g.k[j] == mv.empty_key);
+    for (int j = kBucket - 1; j >= 0; --j) {
+      const unsigned kj = (unsigned)((unsigned long long)g.k[j >> 1] >> (32 * (j & 1)));
+      if (kj == q.k32) found = j;
+      empty |= (kj == kEmpty32);
+    }
+  } else {
+#pragma unroll
+    for (int j = kBucket - 1; j >= 0; --j) {
+      if (g.k[j] == q.key) found = j;
+      empty |= (g.k[j] == mv.empty_key);
+    }
   }
   if (found >= 0) {
     slot = (int)(bucket * kBucket + found);
@@ -141,19 +198,19 @@ __device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& g
   }
   return empty ? 0 : -1;
 }
-__device__ __forceinline__ unsigned bucket_of(long long key, const MapView& mv) {
-  return slot_of(key, mv.shift);  // shift = 64 - log2(#buckets)
-}
+
 __device__ __forceinline__ unsigned next_bucket(unsigned b, const MapView& mv) {
   return (b + 1) & mv.mask;  // mask = #buckets - 1
 }
-__device__ __forceinline__ int probe(const MapView& mv, long long key) {
-  if (mv.m == 0) return -1;
-  unsigned b = bucket_of(key, mv);
+
+// full lookup: slot index or -1
+__device__ __forceinline__ int probe_query(const MapView& mv, const Query& q) {
+  if (mv.m == 0 || !q.inside) return -1;
+  unsigned b = q.bucket;
   for (;;) {
-    const ProbeGroup g = probe_load(mv, b);
+    const ProbeGroup g = probe_load(mv, b, mv.kmode);
     int slot = -1;
-    const int r = probe_scan(mv, g, b, key, slot);
+    const int r = probe_scan(mv, g, b, q, slot, mv.kmode);
     if (r >= 0) return r ? slot : -1;
     b = next_bucket(b, mv);
   }

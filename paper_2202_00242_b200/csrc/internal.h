@@ -51,9 +51,12 @@ struct vg_map {
   double res = 1.0;
   unsigned capacity = 0;
   int log2cap = 0;
-  long long* pkeys = nullptr;     // probe array (capacity)
-  vg::VoxelRec* recs = nullptr;   // records parallel to pkeys
+  long long* pkeys = nullptr;     // kmode 0 probe array (capacity)
+  unsigned* pkeys32 = nullptr;    // kmode 1 probe array (capacity)
+  vg::VoxelRec* recs = nullptr;   // records parallel to the probe array
   long long empty_key = 0;
+  int kmode = 0;
+  int bx = 0, by = 0, bz = 0, ex = 0, ey = 0, ez = 0;
   // reference arrays (device, fp64/int64): keys sorted ascending, means m*3, covs m*9
   long long* keys = nullptr;
   double* means = nullptr;
@@ -62,8 +65,16 @@ struct vg_map {
   vg::MapView view() const {
     vg::MapView v;
     v.keys = pkeys;
+    v.keys32 = pkeys32;
     v.recs = recs;
     v.empty_key = empty_key;
+    v.kmode = kmode;
+    v.bx = bx;
+    v.by = by;
+    v.bz = bz;
+    v.ex = ex;
+    v.ey = ey;
+    v.ez = ez;
     v.res = res;
     v.inv_res = 1.0 / res;
     v.mask = (capacity / vg::kBucket) - 1;
@@ -83,6 +94,7 @@ struct vg_batch {
   int num_clouds = 0;
   int num_maps = 0;
   int max_var = -1;
+  int key_mode = 2;                   // 1: all maps 32-bit local keys, 0: all int64, 2: mixed
   vg::FactorDev* factors = nullptr;   // F
   vg::ItemDev* items = nullptr;       // num_items (ordered by target map, then factor)
   vg::CloudView* clouds = nullptr;    // num_clouds
@@ -123,7 +135,6 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                  const double* T_dev, long long* rows, double* moved, double* d, double* w,
                  double* wd, double* partial_cost, long long* partial_inl, int nblocks);
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
-int launch_linearize(vg_ctx* ctx, vg_batch* b, int mode);
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);

@@ -120,165 +120,6 @@ __device__ __forceinline__ void point_terms(const double (&R)[9], const CloudVie
 
 // ---- warp reductions ---------------------------------------------------------------------
 
-// ---- K4: fused linearize / cost over (factor, chunk) work items --------------------------
-// One warp per item.  Phase A (per 32 points): load, transform, key, probe.  Hits are
-// compacted through a per-warp shared-memory ring so phase B — the fp64 fused-covariance /
-// inverse / Jacobian accumulation — always runs on full warps (misses no longer idle lanes
-// of the expensive path).  MODE 0: full 29-value partial per item; MODE 1: cost + inliers.
-struct QEntry {
-  double x, y, z;
-  int i, slot;
-};
-constexpr int kRing = 64;
-
-template <int MODE>
-__device__ __forceinline__ void accumulate_hit(const double (&R)[9], const double (&t)[3],
-                                               const CloudView& cv, const MapView& mv,
-                                               const QEntry& e, double (&acc)[28]) {
-  if (MODE == 2) return;  // correspondence counting only
-  PointTerms o;
-  point_terms(R, cv, e.i, mv.recs + e.slot, e.x, e.y, e.z, t, o);
-  if (MODE == 1) {
-    acc[27] += o.cost;
-    return;
-  }
-  const double vx = o.xp[0], vy = o.xp[1], vz = o.xp[2];
-  const double W00 = o.W[0], W01 = o.W[1], W02 = o.W[2], W11 = o.W[3], W12 = o.W[4],
-               W22 = o.W[5];
-  // N = hat(x') W   (rot-trans block of J'^T W J', J' = [-hat(x') | I])
-  const double N00 = fma(-vz, W01, vy * W02), N01 = fma(-vz, W11, vy * W12),
-               N02 = fma(-vz, W12, vy * W22);
-  const double N10 = fma(vz, W00, -vx * W02), N11 = fma(vz, W01, -vx * W12),
-               N12 = fma(vz, W02, -vx * W22);
-  const double N20 = fma(-vy, W00, vx * W01), N21 = fma(-vy, W01, vx * W11),
-               N22 = fma(-vy, W02, vx * W12);
-  // P = N hat(x')^T (rot-rot block), upper triangle
-  acc[0] += fma(-vz, N01, vy * N02);
-  acc[1] += fma(vz, N00, -vx * N02);
-  acc[2] += fma(-vy, N00, vx * N01);
-  acc[3] += fma(vz, N10, -vx * N12);
-  acc[4] += fma(-vy, N10, vx * N11);
-  acc[5] += fma(-vy, N20, vx * N21);
-  acc[6] += N00; acc[7] += N01; acc[8] += N02;
-  acc[9] += N10; acc[10] += N11; acc[11] += N12;
-  acc[12] += N20; acc[13] += N21; acc[14] += N22;
-  acc[15] += W00; acc[16] += W01; acc[17] += W02; acc[18] += W11; acc[19] += W12; acc[20] += W22;
-  // b' = [x' x Wd ; Wd]
-  acc[21] += fma(vy, o.wd[2], -vz * o.wd[1]);
-  acc[22] += fma(vz, o.wd[0], -vx * o.wd[2]);
-  acc[23] += fma(vx, o.wd[1], -vy * o.wd[0]);
-  acc[24] += o.wd[0]; acc[25] += o.wd[1]; acc[26] += o.wd[2];
-  acc[27] += o.cost;
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
-    k_linearize(const ItemDev* __restrict__ items, int n_items,
-                const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
-                const MapView* __restrict__ maps, double* __restrict__ partials) {
-  __shared__ QEntry ring[kWarpsPerBlock][kRing];
-  const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if (w >= n_items) return;
-  QEntry* q = ring[threadIdx.x >> 5];
-  const ItemDev it = items[w];
-  const FactorDev* f = factors + it.factor;
-  double R[9], t[3];
-  load_T(f->T, R, t);
-  const CloudView cv = clouds[__ldg(&f->cloud)];
-  const MapView mv = maps[__ldg(&f->map)];
-  const unsigned lt_mask = (1u << lane) - 1u;
-
-  // lane accumulators: P(6) N(9) S(6) br(3) bt(3) cost(1)
-  double acc[28];
-#pragma unroll
-  for (int k = 0; k < 28; ++k) acc[k] = 0.0;
-  unsigned head = 0, tail = 0;  // warp-uniform ring cursors
-
-  // Software pipeline: the first probe load of batch b+1 is issued before the fp64 compute
-  // round, so its L2/HBM latency overlaps the math of earlier hits.
-  int i = it.begin + lane;
-  bool live = i < it.end;
-  double x = 0.0, y = 0.0, z = 0.0;
-  long long key = 0;
-  unsigned h = 0;
-  ProbeGroup pg{};
-  auto issue = [&]() {
-    if (!live) return;
-    double px, py, pz;
-    float4 pa;
-    load_point(cv, i, px, py, pz, pa);
-    transform(R, t, px, py, pz, x, y, z);
-    key = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                   floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                   floor_div(z, mv.res, mv.inv_res, mv.pow2));
-    if (mv.m == 0) return;
-    h = bucket_of(key, mv);
-    pg = probe_load(mv, h);
-  };
-  issue();
-  for (int base = it.begin; base < it.end; base += 32) {
-    // phase B: one full-warp compute round if 32 hits are queued
-    if (tail - head >= 32) {
-      const QEntry e = q[(head + lane) & (kRing - 1)];
-      head += 32;
-      __syncwarp();
-      accumulate_hit<MODE>(R, t, cv, mv, e, acc);
-    }
-    // resolve this batch's probes (misses contribute nothing, registration.py:150-156)
-    int slot = -1;
-    if (live && mv.m != 0) {
-      while (probe_scan(mv, pg, h, key, slot) < 0) {
-        h = next_bucket(h, mv);
-        pg = probe_load(mv, h);
-      }
-    }
-    const unsigned hits = __ballot_sync(0xffffffffu, slot >= 0);
-    if (slot >= 0) {
-      QEntry& e = q[(tail + __popc(hits & lt_mask)) & (kRing - 1)];
-      e.x = x;
-      e.y = y;
-      e.z = z;
-      e.i = i;
-      e.slot = slot;
-    }
-    tail += __popc(hits);
-    __syncwarp();
-    // issue the next batch's loads and first probe
-    i += 32;
-    live = i < it.end;
-    issue();
-  }
-  while (tail - head >= 32) {
-    const QEntry e = q[(head + lane) & (kRing - 1)];
-    head += 32;
-    accumulate_hit<MODE>(R, t, cv, mv, e, acc);
-  }
-  if (tail > head && lane < (int)(tail - head)) {
-    const QEntry e = q[(head + lane) & (kRing - 1)];
-    accumulate_hit<MODE>(R, t, cv, mv, e, acc);
-  }
-  const int inl = (int)tail;  // every hit was queued exactly once
-
-  if (MODE >= 1) {
-    double c = acc[27];
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
-    if (lane == 0) {
-      partials[2 * (size_t)w] = c;
-      partials[2 * (size_t)w + 1] = (double)inl;
-    }
-    return;
-  }
-  double v[32];
-#pragma unroll
-  for (int k = 0; k < 28; ++k) v[k] = acc[k];
-  v[28] = lane == 0 ? (double)inl : 0.0;
-  v[29] = 0.0; v[30] = 0.0; v[31] = 0.0;
-  const double r = warp_transpose_reduce32(v, lane);
-  partials[(size_t)w * kPartialStride + lane] = r;
-}
-
 // ---- K5: per-factor fixed-order sum of item partials + fp64 adjoint expansion ------------
 __device__ __forceinline__ void mat3_mul(const double* A, const double* B, double* C) {
 #pragma unroll
@@ -508,10 +349,10 @@ __global__ void k_lookup(CloudView cv, MapView mv, const double* __restrict__ Tp
     load_point(cv, i, px, py, pz, pa);
     double x, y, z;
     transform(R, t, px, py, pz, x, y, z);
-    const long long key = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                                   floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                                   floor_div(z, mv.res, mv.inv_res, mv.pow2));
-    const int slot = probe(mv, key);
+    const Query q = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                               floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                               floor_div(z, mv.res, mv.inv_res, mv.pow2), mv.kmode);
+    const int slot = probe_query(mv, q);
     const long long row = slot < 0 ? -1 : (long long)__ldg(&mv.recs[slot].row);
     if (rows) rows[i] = row;
     local += (row >= 0);
@@ -541,10 +382,10 @@ __global__ void k_terms(CloudView cv, MapView mv, const double* __restrict__ Tp,
     moved[3 * i] = x;
     moved[3 * i + 1] = y;
     moved[3 * i + 2] = z;
-    const long long key = pack_key(floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                                   floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                                   floor_div(z, mv.res, mv.inv_res, mv.pow2));
-    const int slot = probe(mv, key);
+    const Query q = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                               floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                               floor_div(z, mv.res, mv.inv_res, mv.pow2), mv.kmode);
+    const int slot = probe_query(mv, q);
     if (slot < 0) {
       rows[i] = -1;
       for (int k = 0; k < 3; ++k) dout[3 * i + k] = 0.0, wdout[3 * i + k] = 0.0;
@@ -615,24 +456,6 @@ int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev) {
   if (b->F == 0) return 0;
   k_compose<<<grid_for(b->F, 128, 1 << 30), 128, 0, ctx->stream>>>(b->factors, (int)b->F,
                                                                    poses_dev);
-  ctx->launches++;
-  VG_CUDA(cudaGetLastError());
-  return 0;
-}
-
-int launch_linearize(vg_ctx* ctx, vg_batch* b, int mode) {
-  if (b->num_items == 0) return 0;
-  const int threads = kWarpsPerBlock * 32;
-  const int blocks = (int)((b->num_items + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  if (mode == 1)
-    k_linearize<1><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,
-                                                        b->clouds, b->maps, b->partials);
-  else if (mode == 2)
-    k_linearize<2><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,
-                                                        b->clouds, b->maps, b->partials);
-  else
-    k_linearize<0><<<blocks, threads, 0, ctx->stream>>>(b->items, (int)b->num_items, b->factors,
-                                                        b->clouds, b->maps, b->partials);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;

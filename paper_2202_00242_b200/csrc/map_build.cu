@@ -7,6 +7,8 @@
 //   exactly the rounding sequence of np.add.at + true division.
 // The fp64 arrays are kept on the device for export; the hot path reads the 64 B slots.
 #include <algorithm>
+#include <climits>
+#include <vector>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
@@ -86,24 +88,38 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
   cnt_out[cidx] = cnt;
 }
 
-// one thread per cell: claim a slot by CAS on the key array (linear probing), then write the
-// parallel 96 B record (reference row + fp64 Gaussian).
+// one thread per cell: claim a slot by CAS on the probe array (bucketized: the home bucket's
+// 8 slots first, then the next bucket), then write the parallel 96 B record (reference row +
+// fp64 Gaussian).  kmode 1 probes 32-bit cell-local keys, kmode 0 the packed int64 keys.
 __global__ void k_hash_insert(const long long* __restrict__ keys, const double* __restrict__ means,
-                              const double* __restrict__ covs, int m, long long* __restrict__ pkeys,
-                              VoxelRec* __restrict__ recs, long long empty_key, unsigned mask,
-                              int shift) {
+                              const double* __restrict__ covs, int m, MapView mv,
+                              long long* __restrict__ pkeys, unsigned* __restrict__ pkeys32,
+                              VoxelRec* __restrict__ recs) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   const long long key = keys[r];
-  unsigned b = slot_of(key, shift);  // home bucket
-  unsigned h = 0;
-  for (bool placed = false; !placed; b = (b + 1) & mask) {
+  unsigned b, h = 0;
+  unsigned k32 = 0;
+  if (mv.kmode) {
+    const long long dx = (key >> 42) - kKeyOffset;
+    const long long dy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
+    const long long dz = (key & ((1LL << 21) - 1)) - kKeyOffset;
+    k32 = (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
+    b = (k32 * 0x9E3779B9u) >> (mv.shift - 32);
+  } else {
+    b = slot_of(key, mv.shift);
+  }
+  for (bool placed = false; !placed; b = (b + 1) & mv.mask) {
     for (int j = 0; j < kBucket && !placed; ++j) {
       h = b * kBucket + j;
-      const unsigned long long prev =
-          atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
-                    (unsigned long long)empty_key, (unsigned long long)key);
-      placed = prev == (unsigned long long)empty_key;
+      if (mv.kmode) {
+        placed = atomicCAS(pkeys32 + h, kEmpty32, k32) == kEmpty32;
+      } else {
+        const unsigned long long prev =
+            atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
+                      (unsigned long long)mv.empty_key, (unsigned long long)key);
+        placed = prev == (unsigned long long)mv.empty_key;
+      }
     }
   }
   VoxelRec v;
@@ -121,6 +137,11 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
   v.cov[5] = C[8];
   v.pad1[0] = v.pad1[1] = 0.0;
   recs[h] = v;
+}
+
+__global__ void k_fill32(unsigned* __restrict__ p, unsigned v, unsigned n) {
+  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    p[i] = v;
 }
 
 __global__ void k_fill(long long* __restrict__ p, long long v, unsigned n) {
@@ -168,28 +189,55 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
   int l2 = 3;
   map->capacity = (unsigned)capacity_for(map->m, &l2);
   map->log2cap = l2;
-  // empty marker: a value that is not a key of this map (keys are sorted on the device; the
-  // smallest candidate absent from them is found on the host from the first few keys)
   long long empty = (long long)0x8000000000000000ull;
+  map->kmode = 0;
   if (map->m) {
-    const int probe_n = (int)std::min<long long>(map->m, 64);
-    long long head[64];
-    VG_CUDA(cudaMemcpyAsync(head, map->keys, sizeof(long long) * probe_n, cudaMemcpyDeviceToHost,
-                            ctx->stream));
+    // local key frame from the decoded keys (sorted ascending: any cell index extreme may sit
+    // anywhere in y/z, so all keys are scanned on the host)
+    std::vector<long long> hk((size_t)map->m);
+    VG_CUDA(cudaMemcpyAsync(hk.data(), map->keys, sizeof(long long) * map->m,
+                            cudaMemcpyDeviceToHost, ctx->stream));
     VG_CUDA(cudaStreamSynchronize(ctx->stream));
-    for (int i = 0; i < probe_n && head[i] == empty; ++i) ++empty;  // keys strictly increasing
+    long long lo[3] = {LLONG_MAX, LLONG_MAX, LLONG_MAX}, hi[3] = {LLONG_MIN, LLONG_MIN, LLONG_MIN};
+    for (long long k : hk) {
+      const long long d[3] = {(k >> 42) - kKeyOffset, ((k >> 21) & ((1LL << 21) - 1)) - kKeyOffset,
+                              (k & ((1LL << 21) - 1)) - kKeyOffset};
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = std::min(lo[a], d[a]);
+        hi[a] = std::max(hi[a], d[a]);
+      }
+    }
+    const bool fits = hi[0] - lo[0] < 2048 && hi[1] - lo[1] < 2048 && hi[2] - lo[2] < 1023 &&
+                      lo[0] > INT_MIN && lo[1] > INT_MIN && lo[2] > INT_MIN &&
+                      hi[0] < INT_MAX && hi[1] < INT_MAX && hi[2] < INT_MAX;
+    if (fits) {
+      map->kmode = 1;
+      map->bx = (int)lo[0];
+      map->by = (int)lo[1];
+      map->bz = (int)lo[2];
+      map->ex = (int)(hi[0] - lo[0] + 1);
+      map->ey = (int)(hi[1] - lo[1] + 1);
+      map->ez = (int)(hi[2] - lo[2] + 1);
+    }
+    // kmode 0 empty marker: the smallest value absent from the (strictly increasing) keys
+    for (size_t i = 0; i < hk.size() && hk[i] == empty; ++i) ++empty;
   }
   map->empty_key = empty;
-  VG_CUDA(cudaMallocAsync((void**)&map->pkeys, sizeof(long long) * (size_t)map->capacity, ctx->stream));
-  VG_CUDA(cudaMallocAsync((void**)&map->recs, sizeof(VoxelRec) * (size_t)map->capacity, ctx->stream));
-  k_fill<<<(int)std::min<unsigned>((map->capacity + 255) / 256, 148 * 16), 256, 0, ctx->stream>>>(
-      map->pkeys, empty, map->capacity);
+  const int gfill = (int)std::min<unsigned>((map->capacity + 255) / 256, 148 * 16);
+  if (map->kmode) {
+    VG_CUDA(cudaMallocAsync((void**)&map->pkeys32, sizeof(unsigned) * (size_t)map->capacity, ctx->stream));
+    k_fill32<<<gfill, 256, 0, ctx->stream>>>(map->pkeys32, kEmpty32, map->capacity);
+  } else {
+    VG_CUDA(cudaMallocAsync((void**)&map->pkeys, sizeof(long long) * (size_t)map->capacity, ctx->stream));
+    k_fill<<<gfill, 256, 0, ctx->stream>>>(map->pkeys, empty, map->capacity);
+  }
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
+  VG_CUDA(cudaMallocAsync((void**)&map->recs, sizeof(VoxelRec) * (size_t)map->capacity, ctx->stream));
   if (map->m == 0) return 0;
   k_hash_insert<<<(int)((map->m + 127) / 128), 128, 0, ctx->stream>>>(
-      map->keys, map->means, map->covs, (int)map->m, map->pkeys, map->recs, empty,
-      (map->capacity / kBucket) - 1, 64 - (l2 - 3));
+      map->keys, map->means, map->covs, (int)map->m, map->view(), map->pkeys, map->pkeys32,
+      map->recs);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
