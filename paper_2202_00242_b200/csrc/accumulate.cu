@@ -33,7 +33,8 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     k_lookup_items(const ItemDev* __restrict__ items, int n_items,
                    const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
                    const MapView* __restrict__ maps, int2* __restrict__ hits,
-                   int* __restrict__ counts, double* __restrict__ partials2) {
+                   int* __restrict__ counts, double* __restrict__ partials2,
+                   AccDesc* __restrict__ descs) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
   if (w >= n_items) return;
@@ -47,6 +48,24 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
   const CloudView cv = clouds[__ldg(&f->cloud)];
   const MapView mv = maps[__ldg(&f->map)];
   const int kmode = KM == 2 ? mv.kmode : KM;
+  if (descs) {
+    AccDesc& d = descs[w];
+    double tv = 0.0;  // static register indexing (no local-memory copy of R)
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (lane == k) tv = R[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (lane == 9 + k) tv = t[k];
+    if (lane < 12) d.T[lane] = tv;
+    else if (lane == 12) d.a = cv.a;
+    else if (lane == 13) d.xyz64 = cv.xyz64;
+    else if (lane == 14) d.c0 = cv.c0;
+    else if (lane == 15) d.c1 = cv.c1;
+    else if (lane == 16) d.c2 = cv.c2;
+    else if (lane == 17) d.recs = mv.recs;
+    else if (lane == 18) d.hoff = it.hoff;
+  }
   const unsigned lt_mask = (1u << lane) - 1u;
   int2* out = hits + it.hoff;
   int cnt = 0;
@@ -99,6 +118,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
       partials2[2 * (size_t)w + 1] = (double)cnt;
     }
   }
+  if (descs && lane == 0) descs[w].n = cnt;
 }
 
 // ---- K4b ------------------------------------------------------------------------------------
@@ -108,7 +128,7 @@ constexpr int kStageUnits = 10;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -172,27 +192,31 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
 
 template <int MODE, int kStages, int kMinBlocks>
 __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
-    k_accumulate(const ItemDev* __restrict__ items, int n_items,
-                 const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
-                 const MapView* __restrict__ maps, const int2* __restrict__ hits,
-                 const int* __restrict__ counts, double* __restrict__ partials) {
+    k_accumulate(const AccDesc* __restrict__ descs, int n_items, const int2* __restrict__ hits,
+                 double* __restrict__ partials) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int w = blockIdx.x * kAccWarps + wib;
   if (w >= n_items) return;
   AccSmem<kStages>& sm = reinterpret_cast<AccSmem<kStages>*>(smem_raw)[wib];
-  const ItemDev it = items[w];
-  const FactorDev* f = factors + it.factor;
-  const int n = counts[w];
-  const int2* hl = hits + it.hoff;
+  const AccDesc* dsc = descs + w;
+  const int n = __ldg(&dsc->n);
+  const int2* hl = hits + __ldg(&dsc->hoff);
   double R[9], t[3];
 #pragma unroll
-  for (int k = 0; k < 9; ++k) R[k] = __ldg(f->T + k);
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(dsc->T + k);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) t[k] = __ldg(f->T + 9 + k);
-  const CloudView cv = clouds[__ldg(&f->cloud)];
-  const MapView mv = maps[__ldg(&f->map)];
+  for (int k = 0; k < 3; ++k) t[k] = __ldg(dsc->T + 9 + k);
+  CloudView cv;
+  cv.a = (const float4*)__ldg((const unsigned long long*)&dsc->a);
+  cv.xyz64 = (const double*)__ldg((const unsigned long long*)&dsc->xyz64);
+  cv.c0 = (const double2*)__ldg((const unsigned long long*)&dsc->c0);
+  cv.c1 = (const double2*)__ldg((const unsigned long long*)&dsc->c1);
+  cv.c2 = (const double2*)__ldg((const unsigned long long*)&dsc->c2);
+  cv.n = 0;
+  MapView mv;
+  mv.recs = (const VoxelRec*)__ldg((const unsigned long long*)&dsc->recs);
 
   double acc[28];
 #pragma unroll
@@ -329,13 +353,13 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   double* p2 = kmode == 2 ? b->partials : nullptr;
   if (b->key_mode == 1)
     k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2);
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2, b->descs);
   else if (b->key_mode == 0)
     k_lookup_items<0, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2);
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2, b->descs);
   else
     k_lookup_items<2, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2);
+        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2, b->descs);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   if (kmode == 2) return 0;
@@ -346,9 +370,7 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   const int blocks = (n + kAccWarps - 1) / kAccWarps;
   auto go = [&](auto kern, size_t smem) -> int {
     VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<blocks, kAccWarps * 32, smem, ctx->stream>>>(b->items, n, b->factors, b->clouds,
-                                                        b->maps, b->hits, b->hit_counts,
-                                                        b->partials);
+    kern<<<blocks, kAccWarps * 32, smem, ctx->stream>>>(b->descs, n, b->hits, b->partials);
     return 0;
   };
   // variants (stages, min CTAs/SM): 0 = (3,3), 1 = (2,4), 2 = (2,3), 3 = (4,2)

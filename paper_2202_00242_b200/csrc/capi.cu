@@ -465,6 +465,7 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
       (rc = dalloc(ctx, &b->partials, items.size() * kPartialStride)) ||
       (rc = dalloc(ctx, &b->hits, (size_t)hoff + 2)) ||
       (rc = dalloc(ctx, &b->hit_counts, items.size())) ||
+      (rc = dalloc(ctx, &b->descs, items.size())) ||
       (rc = dalloc(ctx, &b->out, (size_t)F * VG_REC_LINEARIZE)) ||
       (rc = h2d(ctx, b->factors, fac.data(), sizeof(FactorDev) * F)) ||
       (rc = h2d(ctx, b->items, items.data(), sizeof(ItemDev) * items.size())) ||
@@ -497,6 +498,7 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->partials);
   dfree(ctx, b->hits);
   dfree(ctx, b->hit_counts);
+  dfree(ctx, b->descs);
   dfree(ctx, b->out);
   dfree(ctx, b->poses);
   cudaStreamSynchronize(ctx->stream);

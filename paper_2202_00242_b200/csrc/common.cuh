@@ -75,6 +75,21 @@ struct __align__(16) FactorDev {
 };
 static_assert(sizeof(FactorDev) == 128, "factor record must be 128 B");
 
+// Per-item descriptor written by K4a for K4b: everything K4b's prologue needs in one
+// broadcast load (instead of item -> factor -> cloud/map view dependency chains).
+struct __align__(16) AccDesc {
+  double T[12];            // T_ij of the item's factor
+  const float4* a;         // source points (fp32)
+  const double* xyz64;     // source points (fp64 path) or null
+  const double2* c0;       // source covariance SoA
+  const double2* c1;
+  const double2* c2;
+  const struct VoxelRec* recs;  // target map records
+  int hoff;                // hit-list offset
+  int n;                   // hits
+  int pad[2];
+};
+
 struct __align__(16) ItemDev {
   int factor;
   int begin;  // point range [begin, end) of the factor's source cloud

@@ -102,6 +102,7 @@ struct vg_batch {
   double* partials = nullptr;         // num_items * kPartialStride
   int2* hits = nullptr;               // compacted (point, slot) hits, per-item regions
   int* hit_counts = nullptr;          // num_items
+  vg::AccDesc* descs = nullptr;       // num_items (K4a -> K4b)
   long long hit_capacity = 0;
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;
