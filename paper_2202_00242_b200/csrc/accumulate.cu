@@ -7,7 +7,7 @@
 // K4a — one warp per (factor, <=512-point chunk) item, light on registers so many warps hide
 //   the two dependent memory latencies of a lookup (source point, then the probed key
 //   bucket).  x = R p + t (fp64) -> key (bit-exact floor) -> one 32 B bucket of 8 local keys.
-//   Hits are written as (point, slot) pairs into the item's region of a batch-wide hit list
+//   Hits are written as (point, row) pairs into the item's region of a batch-wide hit list
 //   with a warp ballot, preserving point order.  Misses contribute nothing (:150-156).
 // K4b — one warp per item over its compacted hits, so every lane of the expensive fp64 path
 //   does useful work.  Each round of 32 hits gathers the source point (16 B), source
@@ -17,7 +17,9 @@
 //   is reduced across the warp in a fixed order.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -34,7 +36,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
                    const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
                    const MapView* __restrict__ maps, int2* __restrict__ hits,
                    int* __restrict__ counts, double* __restrict__ partials2,
-                   AccDesc* __restrict__ descs) {
+                   AccDesc* __restrict__ descs, int prefetch_recs) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
   if (w >= n_items) return;
@@ -98,14 +100,19 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     const Query qy = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
                                 floor_div(y, mv.res, mv.inv_res, mv.pow2),
                                 floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
-    int slot = -1;
+    int slot = -1;  // becomes the reference row of the hit
     if (i < it.end && mv.m && qy.inside) {
       unsigned bk = qy.bucket;
       ProbeGroup pg = probe_load(mv, bk, kmode);
-      while (probe_scan(mv, pg, bk, qy, slot, kmode) < 0) {
+      int r;
+      while ((r = probe_scan(mv, pg, bk, qy, slot, kmode)) < 0) {
         bk = next_bucket(bk, mv);
         pg = probe_load(mv, bk, kmode);
       }
+      if (r == 1 && !kmode) slot = hit_row(mv, slot, 0);
+      // warm L2 with the record line K4b will gather for this hit
+      if (r == 1 && prefetch_recs)
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(mv.recs + slot));
     }
     const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
     if (slot >= 0) out[cnt + __popc(m & lt_mask)] = make_int2(i, slot);
@@ -128,7 +135,7 @@ constexpr int kStageUnits = 10;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -155,7 +162,8 @@ struct AccSmem {
   AccStage stage[kStages];
 };
 
-// Gather one round (<= 32 hits) into stage `round % kStages`.  Point and covariance rows are
+// Gather one round (32 hits; the last round of an item pads with replays of its last hit) into
+// stage `round % kStages`.  Point and covariance rows are
 // lane-own (hits are in point order, so these are nearly coalesced); the random 80 B voxel
 // records are gathered cooperatively: each cp.async instruction covers 32 consecutive 16 B
 // units of 6-7 records instead of one unit of 32 records, cutting L1 wavefronts ~4x.
@@ -183,17 +191,107 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
   for (int c = 0; c < kRecUnits; ++c) {
     const int u = c * 32 + lane;
     const int q = u / kRecUnits, j = u - q * kRecUnits;
-    const int slot = __shfl_sync(0xffffffffu, e.y, q);
+    const int row = __shfl_sync(0xffffffffu, e.y, q);
     if (q < nvalid)
-      cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(mv.recs + slot) + 16 * j);
+      cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(mv.recs + row) + 16 * j);
   }
   cp_async_commit();
 }
 
-template <int MODE, int kStages, int kMinBlocks>
+// per-hit fp64 math of K4b on one staged hit: moved point, residual, fused covariance and its
+// inverse, cost, and the target-frame Jacobian blocks about the source origin
+template <int MODE>
+__device__ __forceinline__ void hit_math(const AccStage& st, int lane, bool f64pts,
+                                         const double (&R)[9], const double (&t)[3],
+                                         double scale, double (&acc)[28]) {
+  double px, py, pz;
+  if (f64pts) {
+    const double* d = reinterpret_cast<const double*>(&st.pt[0][lane]);
+    px = d[0];
+    py = d[1];
+    pz = reinterpret_cast<const double*>(&st.pt[1][lane])[0];
+  } else {
+    const float4 a = st.pt[0][lane];
+    px = a.x;
+    py = a.y;
+    pz = a.z;
+  }
+  const double2 s0 = *reinterpret_cast<const double2*>(&st.cov[0][lane]);
+  const double2 s1 = *reinterpret_cast<const double2*>(&st.cov[1][lane]);
+  const double2 s2 = *reinterpret_cast<const double2*>(&st.cov[2][lane]);
+  const double2 m01 = *reinterpret_cast<const double2*>(&st.rec[lane][0]);
+  const double2 m2c0 = *reinterpret_cast<const double2*>(&st.rec[lane][1]);
+  const double2 c12 = *reinterpret_cast<const double2*>(&st.rec[lane][2]);
+  const double2 c34 = *reinterpret_cast<const double2*>(&st.rec[lane][3]);
+  const double v5 = reinterpret_cast<const double*>(&st.rec[lane][4])[0];
+  // moved point (registration.py:148) and residual d = mu' - moved (:152)
+  const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
+  const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
+  const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
+  const double d0 = m01.x - x, d1 = m01.y - y, d2 = m2c0.x - z;
+  // F = C' + R C R^T (:153)
+  const double C00 = s0.x, C01 = s0.y, C02 = s1.x, C11 = s1.y, C12 = s2.x, C22 = s2.y;
+  double A[9];
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const double r0 = R[3 * q], r1 = R[3 * q + 1], r2 = R[3 * q + 2];
+    A[3 * q + 0] = fma(r0, C00, fma(r1, C01, r2 * C02));
+    A[3 * q + 1] = fma(r0, C01, fma(r1, C11, r2 * C12));
+    A[3 * q + 2] = fma(r0, C02, fma(r1, C12, r2 * C22));
+  }
+  auto arT = [&](int a_, int c_) {
+    return fma(A[3 * a_], R[3 * c_], fma(A[3 * a_ + 1], R[3 * c_ + 1], A[3 * a_ + 2] * R[3 * c_ + 2]));
+  };
+  const double fa = m2c0.y + arT(0, 0), fb = c12.x + arT(0, 1), fc = c12.y + arT(0, 2);
+  const double fd = c34.x + arT(1, 1), fe = c34.y + arT(1, 2), ff = v5 + arT(2, 2);
+  // W = F^-1 (:113-130)
+  const double i00 = fma(fd, ff, -fe * fe), i01 = fma(fc, fe, -fb * ff),
+               i02 = fma(fb, fe, -fc * fd), i11 = fma(fa, ff, -fc * fc),
+               i12 = fma(fb, fc, -fa * fe), i22 = fma(fa, fd, -fb * fb);
+  // `scale` is 0 for padding lanes (which replay a valid hit): W, Wd and every accumulated
+  // term are linear in it, so padding contributes exact zeros without a branch
+  const double inv = rcp64(fma(fa, i00, fma(fb, i01, fc * i02))) * scale;
+  const double W00 = i00 * inv, W01 = i01 * inv, W02 = i02 * inv, W11 = i11 * inv,
+               W12 = i12 * inv, W22 = i22 * inv;
+  const double wd0 = fma(W00, d0, fma(W01, d1, W02 * d2));
+  const double wd1 = fma(W01, d0, fma(W11, d1, W12 * d2));
+  const double wd2 = fma(W02, d0, fma(W12, d1, W22 * d2));
+  acc[27] += fma(d0, wd0, fma(d1, wd1, d2 * wd2));  // cost (:156)
+  if (MODE == 0) {
+    const double vx = x - t[0], vy = y - t[1], vz = z - t[2];
+    // N = hat(x') W, P = N hat(x')^T, b' = [x' x Wd ; Wd]  (J' = [-hat(x') | I])
+    const double N00 = fma(-vz, W01, vy * W02), N01 = fma(-vz, W11, vy * W12),
+                 N02 = fma(-vz, W12, vy * W22);
+    const double N10 = fma(vz, W00, -vx * W02), N11 = fma(vz, W01, -vx * W12),
+                 N12 = fma(vz, W02, -vx * W22);
+    const double N20 = fma(-vy, W00, vx * W01), N21 = fma(-vy, W01, vx * W11),
+                 N22 = fma(-vy, W02, vx * W12);
+    acc[0] += fma(-vz, N01, vy * N02);
+    acc[1] += fma(vz, N00, -vx * N02);
+    acc[2] += fma(-vy, N00, vx * N01);
+    acc[3] += fma(vz, N10, -vx * N12);
+    acc[4] += fma(-vy, N10, vx * N11);
+    acc[5] += fma(-vy, N20, vx * N21);
+    acc[6] += N00; acc[7] += N01; acc[8] += N02;
+    acc[9] += N10; acc[10] += N11; acc[11] += N12;
+    acc[12] += N20; acc[13] += N21; acc[14] += N22;
+    acc[15] += W00; acc[16] += W01; acc[17] += W02;
+    acc[18] += W11; acc[19] += W12; acc[20] += W22;
+    acc[21] += fma(vy, wd2, -vz * wd1);
+    acc[22] += fma(vz, wd0, -vx * wd2);
+    acc[23] += fma(vx, wd1, -vy * wd0);
+    acc[24] += wd0; acc[25] += wd1; acc[26] += wd2;
+  }
+}
+
+// K4b.  ILP rounds of 32 hits are computed per iteration (ILP = 2 gives each lane two
+// independent fp64 dependency chains); kStages >= 2 * ILP staged rounds keep the gathers of
+// the next kStages - ILP rounds in flight during the math.
+template <int MODE, int kStages, int kMinBlocks, int ILP>
 __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     k_accumulate(const AccDesc* __restrict__ descs, int n_items, const int2* __restrict__ hits,
-                 double* __restrict__ partials) {
+                 double* __restrict__ partials, int dbg) {
+  static_assert(kStages >= 2 * ILP || (ILP == 1 && kStages >= 2), "stage reuse hazard");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -217,110 +315,53 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   cv.n = 0;
   MapView mv;
   mv.recs = (const VoxelRec*)__ldg((const unsigned long long*)&dsc->recs);
+  const bool f64pts = cv.xyz64 != nullptr;
 
   double acc[28];
 #pragma unroll
   for (int k = 0; k < 28; ++k) acc[k] = 0.0;
   const int rounds = (n + 31) / 32;
-#pragma unroll
-  for (int r = 0; r < kStages - 1; ++r) {
-    const int k = r * 32 + lane;
-    issue_round(cv, mv, sm, r, k < n ? hl[k] : make_int2(0, 0), n - r * 32, lane);
-  }
-  // hit entries are prefetched one round ahead of their gather; the load is unconditional
-  // (index clamped) so its first use is the next iteration's gather, not a predicated move
-  int kn = (kStages - 1) * 32 + lane;
+  constexpr int kAhead = kStages - ILP;  // rounds in flight beyond the ones being computed
   const int klast = n > 0 ? n - 1 : 0;
-  int2 nxt = __ldg(hl + min(kn, klast));
-  for (int r = 0; r < rounds; ++r) {
-    issue_round(cv, mv, sm, r + kStages - 1, nxt, n - (r + kStages - 1) * 32, lane);
-    kn += 32;
-    nxt = __ldg(hl + min(kn, klast));
-    cp_async_wait<kStages - 1>();
-    __syncwarp();
-    const int k = r * 32 + lane;
-    if (k < n) {
-      const AccStage& st = sm.stage[r % kStages];
-      double px, py, pz;
-      if (cv.xyz64) {
-        const double* d = reinterpret_cast<const double*>(&st.pt[0][lane]);
-        px = d[0];
-        py = d[1];
-        pz = reinterpret_cast<const double*>(&st.pt[1][lane])[0];
-      } else {
-        const float4 a = st.pt[0][lane];
-        px = a.x;
-        py = a.y;
-        pz = a.z;
-      }
-      const double2 s0 = *reinterpret_cast<const double2*>(&st.cov[0][lane]);
-      const double2 s1 = *reinterpret_cast<const double2*>(&st.cov[1][lane]);
-      const double2 s2 = *reinterpret_cast<const double2*>(&st.cov[2][lane]);
-      const double2 m01 = *reinterpret_cast<const double2*>(&st.rec[lane][0]);
-      const double2 m2c0 = *reinterpret_cast<const double2*>(&st.rec[lane][1]);
-      const double2 c12 = *reinterpret_cast<const double2*>(&st.rec[lane][2]);
-      const double2 c34 = *reinterpret_cast<const double2*>(&st.rec[lane][3]);
-      const double v5 = reinterpret_cast<const double*>(&st.rec[lane][4])[0];
-      // moved point (registration.py:148) and residual d = mu' - moved (:152)
-      const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
-      const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
-      const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
-      const double d0 = m01.x - x, d1 = m01.y - y, d2 = m2c0.x - z;
-      // F = C' + R C R^T (:153)
-      const double C00 = s0.x, C01 = s0.y, C02 = s1.x, C11 = s1.y, C12 = s2.x, C22 = s2.y;
-      double A[9];
+  // ILP > 1: every staged round is a full round of valid hits (rounds past the end replay hit
+  // n-1 and are masked by scale = 0), so the branch-free math never reads uninitialised data
+  if (n > 0) {
 #pragma unroll
-      for (int q = 0; q < 3; ++q) {
-        const double r0 = R[3 * q], r1 = R[3 * q + 1], r2 = R[3 * q + 2];
-        A[3 * q + 0] = fma(r0, C00, fma(r1, C01, r2 * C02));
-        A[3 * q + 1] = fma(r0, C01, fma(r1, C11, r2 * C12));
-        A[3 * q + 2] = fma(r0, C02, fma(r1, C12, r2 * C22));
-      }
-      auto arT = [&](int a_, int c_) {
-        return fma(A[3 * a_], R[3 * c_], fma(A[3 * a_ + 1], R[3 * c_ + 1], A[3 * a_ + 2] * R[3 * c_ + 2]));
-      };
-      const double fa = m2c0.y + arT(0, 0), fb = c12.x + arT(0, 1), fc = c12.y + arT(0, 2);
-      const double fd = c34.x + arT(1, 1), fe = c34.y + arT(1, 2), ff = v5 + arT(2, 2);
-      // W = F^-1 (:113-130)
-      const double i00 = fma(fd, ff, -fe * fe), i01 = fma(fc, fe, -fb * ff),
-                   i02 = fma(fb, fe, -fc * fd), i11 = fma(fa, ff, -fc * fc),
-                   i12 = fma(fb, fc, -fa * fe), i22 = fma(fa, fd, -fb * fb);
-      const double inv = rcp64(fma(fa, i00, fma(fb, i01, fc * i02)));
-      const double W00 = i00 * inv, W01 = i01 * inv, W02 = i02 * inv, W11 = i11 * inv,
-                   W12 = i12 * inv, W22 = i22 * inv;
-      const double wd0 = fma(W00, d0, fma(W01, d1, W02 * d2));
-      const double wd1 = fma(W01, d0, fma(W11, d1, W12 * d2));
-      const double wd2 = fma(W02, d0, fma(W12, d1, W22 * d2));
-      acc[27] += fma(d0, wd0, fma(d1, wd1, d2 * wd2));  // cost (:156)
-      if (MODE == 0) {
-        const double vx = x - t[0], vy = y - t[1], vz = z - t[2];
-        // N = hat(x') W, P = N hat(x')^T, b' = [x' x Wd ; Wd]  (J' = [-hat(x') | I])
-        const double N00 = fma(-vz, W01, vy * W02), N01 = fma(-vz, W11, vy * W12),
-                     N02 = fma(-vz, W12, vy * W22);
-        const double N10 = fma(vz, W00, -vx * W02), N11 = fma(vz, W01, -vx * W12),
-                     N12 = fma(vz, W02, -vx * W22);
-        const double N20 = fma(-vy, W00, vx * W01), N21 = fma(-vy, W01, vx * W11),
-                     N22 = fma(-vy, W02, vx * W12);
-        acc[0] += fma(-vz, N01, vy * N02);
-        acc[1] += fma(vz, N00, -vx * N02);
-        acc[2] += fma(-vy, N00, vx * N01);
-        acc[3] += fma(vz, N10, -vx * N12);
-        acc[4] += fma(-vy, N10, vx * N11);
-        acc[5] += fma(-vy, N20, vx * N21);
-        acc[6] += N00; acc[7] += N01; acc[8] += N02;
-        acc[9] += N10; acc[10] += N11; acc[11] += N12;
-        acc[12] += N20; acc[13] += N21; acc[14] += N22;
-        acc[15] += W00; acc[16] += W01; acc[17] += W02;
-        acc[18] += W11; acc[19] += W12; acc[20] += W22;
-        acc[21] += fma(vy, wd2, -vz * wd1);
-        acc[22] += fma(vz, wd0, -vx * wd2);
-        acc[23] += fma(vx, wd1, -vy * wd0);
-        acc[24] += wd0; acc[25] += wd1; acc[26] += wd2;
+  for (int r = 0; r < kAhead; ++r) {
+    const int k = r * 32 + lane;
+    issue_round(cv, mv, sm, r, hl[min(k, klast)], dbg == 1 ? 0 : (ILP > 1 ? 32 : n - r * 32),
+                lane);
+  }
+  // hit entries are prefetched one iteration ahead of their gather; the loads are
+  // unconditional (index clamped) so their first use is the next iteration's gather
+  int2 nxt[ILP];
+#pragma unroll
+  for (int u = 0; u < ILP; ++u) nxt[u] = __ldg(hl + min((kAhead + u) * 32 + lane, klast));
+  for (int r = 0; r < rounds; r += ILP) {
+#pragma unroll
+    for (int u = 0; u < ILP; ++u) {
+      const int ri = r + kAhead + u;
+      issue_round(cv, mv, sm, ri, nxt[u], dbg == 1 ? 0 : (ILP > 1 ? 32 : n - ri * 32), lane);
+    }
+#pragma unroll
+    for (int u = 0; u < ILP; ++u)
+      nxt[u] = __ldg(hl + min((r + ILP + kAhead + u) * 32 + lane, klast));
+    cp_async_wait<kAhead>();
+    __syncwarp();
+    if (dbg != 2) {
+      if (ILP == 1) {  // branch over padding lanes
+        if (r * 32 + lane < n) hit_math<MODE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
+      } else {  // branch-free so the ILP rounds interleave; padding lanes replay valid data
+#pragma unroll
+        for (int u = 0; u < ILP; ++u)
+          hit_math<MODE>(sm.stage[(r + u) % kStages], lane, f64pts, R, t,
+                         (r + u) * 32 + lane < n ? 1.0 : 0.0, acc);
       }
     }
-    __syncwarp();  // stage r % kStages is reused by round r + kStages
+    __syncwarp();  // the stages of rounds r..r+ILP-1 are reused by later rounds
   }
   cp_async_wait<0>();
+  }
 
   if (MODE == 1) {
     double c = acc[27];
@@ -346,48 +387,93 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 
 using namespace vg;
 
+static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
+                               cudaStream_t st, int prefetch) {
+  const int lb = (cnt + kLookupWarps - 1) / kLookupWarps;
+  double* p2 = kmode == 2 ? b->partials + 2 * (size_t)off : nullptr;
+  const ItemDev* it = b->items + off;
+  int* hc = b->hit_counts + off;
+  AccDesc* dd = b->descs + off;
+  if (b->key_mode == 1)
+    k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                           b->maps, b->hits, hc, p2, dd,
+                                                           prefetch);
+  else if (b->key_mode == 0)
+    k_lookup_items<0, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                           b->maps, b->hits, hc, p2, dd,
+                                                           prefetch);
+  else
+    k_lookup_items<2, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                           b->maps, b->hits, hc, p2, dd,
+                                                           prefetch);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <class K>
+static int launch_acc_kernel(vg_ctx* ctx, K kern, size_t smem, const AccDesc* d, int cnt,
+                             const int2* hits, double* partials, cudaStream_t st) {
+  static const int dbg = [] {
+    const char* e = getenv("VGICP_K4B_DEBUG");  // profiling only: 1 no gathers, 2 no math
+    return e ? atoi(e) : 0;
+  }();
+  VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(cnt + kAccWarps - 1) / kAccWarps, kAccWarps * 32, smem, st>>>(d, cnt, hits, partials,
+                                                                        dbg);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
+                            cudaStream_t st, bool shared_sm) {
+  static const int variant = [] {
+    const char* e = getenv("VGICP_ACC_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  const AccDesc* d = b->descs + off;
+  if (kmode == 1)
+    return launch_acc_kernel(ctx, k_accumulate<1, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
+                             cnt, b->hits, b->partials + 2 * (size_t)off, st);
+  double* p = b->partials + (size_t)off * kPartialStride;
+  (void)shared_sm;
+  // variants (stages, min CTAs/SM, ILP): 0 = (2,3,1), 1 = (4,2,2), 2 = (3,3,1), 3 = (4,3,2)
+  switch (variant) {
+    case 1:
+      return launch_acc_kernel(ctx, k_accumulate<0, 4, 2, 2>, sizeof(AccSmem<4>) * kAccWarps, d,
+                               cnt, b->hits, p, st);
+    case 2:
+      return launch_acc_kernel(ctx, k_accumulate<0, 3, 3, 1>, sizeof(AccSmem<3>) * kAccWarps, d,
+                               cnt, b->hits, p, st);
+    case 3:
+      return launch_acc_kernel(ctx, k_accumulate<0, 4, 3, 2>, sizeof(AccSmem<4>) * kAccWarps, d,
+                               cnt, b->hits, p, st);
+    default:
+      return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
+                               cnt, b->hits, p, st);
+  }
+}
+
+// K4a + K4b.  Experiment knobs (measured slower on config 5, kept off): VGICP_CHUNKS > 1
+// alternates K4a/K4b over item chunks; VGICP_PREFETCH=1 makes K4a prefetch record lines to L2.
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   if (b->num_items == 0) return 0;
   const int n = (int)b->num_items;
-  const int lb = (n + kLookupWarps - 1) / kLookupWarps;
-  double* p2 = kmode == 2 ? b->partials : nullptr;
-  if (b->key_mode == 1)
-    k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2, b->descs);
-  else if (b->key_mode == 0)
-    k_lookup_items<0, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2, b->descs);
-  else
-    k_lookup_items<2, 3><<<lb, kLookupWarps * 32, 0, ctx->stream>>>(
-        b->items, n, b->factors, b->clouds, b->maps, b->hits, b->hit_counts, p2, b->descs);
-  ctx->launches++;
-  VG_CUDA(cudaGetLastError());
-  if (kmode == 2) return 0;
-  static const int variant = [] {
-    const char* e = getenv("VGICP_ACC_VARIANT");
-    return e ? atoi(e) : 2;
+  static const int chunks_env = [] {
+    const char* e = getenv("VGICP_CHUNKS");
+    return e ? atoi(e) : 1;
   }();
-  const int blocks = (n + kAccWarps - 1) / kAccWarps;
-  auto go = [&](auto kern, size_t smem) -> int {
-    VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<blocks, kAccWarps * 32, smem, ctx->stream>>>(b->descs, n, b->hits, b->partials);
-    return 0;
-  };
-  // variants (stages, min CTAs/SM): 0 = (3,3), 1 = (2,4), 2 = (2,3), 3 = (4,2)
-  int rc = 0;
-  if (kmode == 1) {
-    rc = go(k_accumulate<1, 2, 3>, sizeof(AccSmem<2>) * kAccWarps);
-  } else if (variant == 1) {
-    rc = go(k_accumulate<0, 2, 4>, sizeof(AccSmem<2>) * kAccWarps);
-  } else if (variant == 2) {
-    rc = go(k_accumulate<0, 2, 3>, sizeof(AccSmem<2>) * kAccWarps);
-  } else if (variant == 3) {
-    rc = go(k_accumulate<0, 4, 2>, sizeof(AccSmem<4>) * kAccWarps);
-  } else {
-    rc = go(k_accumulate<0, 3, 3>, sizeof(AccSmem<3>) * kAccWarps);
+  static const int prefetch_env = [] {
+    const char* e = getenv("VGICP_PREFETCH");
+    return e ? atoi(e) : 0;
+  }();
+  const int chunks = (kmode == 2 || n < 4096) ? 1 : std::max(1, std::min(chunks_env, 256));
+  const int prefetch = kmode != 2 && prefetch_env;
+  for (int c = 0; c < chunks; ++c) {
+    const int lo = (int)((long long)n * c / chunks), hi = (int)((long long)n * (c + 1) / chunks);
+    VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream, prefetch));
+    if (kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream, false));
   }
-  if (rc) return rc;
-  ctx->launches++;
-  VG_CUDA(cudaGetLastError());
   return 0;
 }

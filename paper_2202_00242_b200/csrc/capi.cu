@@ -2,6 +2,7 @@
 // staging, batch flattening, and status-code error reporting.  No exception crosses the ABI.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -26,11 +27,6 @@ static int fail(int code, const std::string& msg) {
   return code;
 }
 
-#define VG_CHECK(x)              \
-  do {                           \
-    int _rc = (x);               \
-    if (_rc != VG_OK) return _rc; \
-  } while (0)
 
 template <class T>
 static int dalloc(vg_ctx* ctx, T** p, size_t count) {
@@ -106,6 +102,11 @@ int vg_ctx_destroy(vg_ctx* ctx) {
   if (ctx->scratch) cudaFreeAsync(ctx->scratch, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->side_stream) {
+    cudaStreamSynchronize(ctx->side_stream);
+    cudaStreamDestroy(ctx->side_stream);
+    for (auto& e : ctx->events) cudaEventDestroy(e);
+  }
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return VG_OK;
@@ -274,7 +275,8 @@ int vg_map_destroy(vg_map* m) {
   if (!m) return VG_OK;
   vg_ctx* ctx = m->ctx;
   dfree(ctx, m->pkeys);
-  dfree(ctx, m->pkeys32);
+  dfree(ctx, m->prows);
+  dfree(ctx, m->pkv32);
   dfree(ctx, m->recs);
   dfree(ctx, m->keys);
   dfree(ctx, m->means);
@@ -419,8 +421,16 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   // <= kMaxChunk points, one warp per item
   std::vector<int64_t> order(F);
   std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int64_t a, int64_t b) { return fac[a].map < fac[b].map; });
+  static const int order_mode = [] {
+    const char* e = getenv("VGICP_ITEM_ORDER");  // 0 target-major (default), 1 source-major, 2 input
+    return e ? atoi(e) : 0;
+  }();
+  if (order_mode == 0)
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return fac[a].map < fac[b].map; });
+  else if (order_mode == 1)
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return fac[a].cloud < fac[b].cloud; });
   std::vector<ItemDev> items;
   long long npts = 0, hoff = 0;
   for (int64_t f : order) {

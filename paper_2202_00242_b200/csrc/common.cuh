@@ -3,8 +3,9 @@
 // HBM layouts:
 //   cloud  : SoA, 64 B/point: a[i] = (x, y, z) fp32, covariance as three fp64 double2 arrays
 //            + optional fp64 xyz (n x 3) when the points are not exactly fp32 (keys stay exact)
-//   map    : bucketized open-addressing hash table (load factor <= 0.25): dense int64 key
-//            array in 64 B buckets of 8 slots + parallel 96 B records (row, fp64 Gaussian).
+//   map    : bucketized open-addressing hash (key -> row): 32 B buckets of 4 (key32, row)
+//            pairs (load <= 0.125), or int64 keys in 64 B buckets of 8 (+ row array) when
+//            the map does not fit the 32-bit local frame; row-indexed 128 B fp64 records.
 //   work   : (factor, chunk) items, one warp per item; fp64 partials, fixed-order reduce.
 #pragma once
 #include <cstddef>
@@ -18,21 +19,18 @@ constexpr int kWarpsPerBlock = 4;
 constexpr int kPartialStride = 32;    // doubles per work-item partial (29 used)
 constexpr int kMaxChunk = 512;        // points per work item => <= 16 points per lane
 
-// Voxel map on the device = open-addressing hash table in two parallel arrays indexed by
-// slot: a dense int64 key array (probed one 64 B bucket at a time) and 96 B records carrying the
-// reference row and the voxel Gaussian in fp64.  Empty slots hold `empty_key`, a value that is
-// not a key of this map.  Mean and covariance stay fp64: the fused covariance C' + R C R^T
-// has condition ~1e3 for plane-like cells and the parity bar is per element (1e-4 rel) on
-// H/b entries that cancel by up to ~1e5 — fp32 storage or fp32 per-point math exceeds it
-// (tests/kernel_model.py, tests/test_host_logic.py quantify it).
-struct __align__(32) VoxelRec {
-  double mean[3];   // voxel mean (registration.py:90-92)          offsets  0..24
-  double cov[6];    // covariance c00 c01 c02 c11 c12 c22 (:93-97)  offsets 24..72
-  int row;          // rank of the key in ascending order == reference row index
-  int pad0;
-  double pad1[2];
+// Voxel map on the device = open-addressing hash table (key -> reference row) + dense,
+// row-indexed, line-aligned voxel records.  Each record is one 128 B cache line, so a
+// cooperative gather touches one line per record.  Mean and covariance stay fp64: the fused
+// covariance C' + R C R^T has condition ~1e3 for plane-like cells and the parity bar is per
+// element (1e-4 rel) on H/b entries that cancel by up to ~1e5 — fp32 storage or fp32
+// per-point math exceeds it (tests/kernel_model.py, tests/test_host_logic.py quantify it).
+struct __align__(128) VoxelRec {
+  double mean[3];   // voxel mean (registration.py:90-92)                 bytes  0..24
+  double cov[6];    // covariance c00 c01 c02 c11 c12 c22 (:93-97)        bytes 24..72
+  double pad[7];
 };
-static_assert(sizeof(VoxelRec) == 96, "voxel record must be 96 B");
+static_assert(sizeof(VoxelRec) == 128, "voxel record must be one 128 B line");
 static_assert(offsetof(VoxelRec, mean) % 16 == 0 && offsetof(VoxelRec, cov) % 16 == 8,
               "double2 loads at mean[0], mean[2], cov[1], cov[3] must be 16 B aligned");
 
@@ -47,13 +45,14 @@ struct CloudView {
 
 struct MapView {
   const long long* keys;    // kmode 0: int64 packed keys, buckets of 8 (64 B)
-  const unsigned* keys32;   // kmode 1: 32-bit cell-local keys, buckets of 8 (32 B)
-  const VoxelRec* recs;     // capacity, parallel to the probe array
+  const int* rows;          // kmode 0: reference row per slot (parallel to keys)
+  const uint2* kv32;        // kmode 1: (32-bit cell-local key, row) pairs, buckets of 4 (32 B)
+  const VoxelRec* recs;     // m records, row-indexed
   long long empty_key;      // kmode 0 empty marker (a value that is not a key of the map)
   double res;
   double inv_res;
   unsigned mask;        // buckets - 1
-  int shift;            // 64 - log2(buckets)
+  int shift;            // kmode 0: 64 - log2(buckets); kmode 1: 32 - log2(buckets)
   int m;                // occupied cells
   int pow2;             // res is a power of two: x * (1/res) == x / res exactly
   int kmode;            // 1: every cell fits the 11/11/10-bit local frame below
@@ -123,15 +122,19 @@ __device__ __forceinline__ unsigned slot_of(long long key, int shift) {
   return (unsigned)(((unsigned long long)key * 0x9E3779B97F4A7C15ull) >> shift);
 }
 
-// Bucketized open addressing: a key hashes to a bucket of 8 slots; insertion fills the home
-// bucket before spilling to the next one, so a lookup resolves in its home bucket unless that
-// bucket is full (load factor <= 0.25: ~0.1% of lookups).  Two key encodings:
+// Bucketized open addressing: a key hashes to a bucket; insertion fills the home bucket
+// before spilling to the next one, so a lookup resolves in its home bucket unless that
+// bucket is full.  Two key encodings:
 //   kmode 1 — 32-bit cell-local keys (lx | ly << 11 | lz << 22 relative to the map's min
-//             cell); a bucket is 32 B = one 256-bit load.  Used whenever the map fits.
-//   kmode 0 — the reference's packed int64 keys; a bucket is 64 B = two 256-bit loads.
+//             cell), stored with the row as (key32, row) pairs: a bucket of 4 pairs is 32 B =
+//             one 256-bit load that yields the row directly.  Load <= 0.125 (~0.2% spill).
+//             Used whenever the map fits the local frame.
+//   kmode 0 — the reference's packed int64 keys in 64 B buckets of 8 (two 256-bit loads,
+//             load <= 0.25) and a parallel row array.
 // The local key is built from decode(pack(floor)) — the reference's own key round trip —
 // so aliasing of out-of-range indices behaves exactly as the reference's packed keys.
-constexpr int kBucket = 8;
+constexpr int kBucket64 = 8;
+constexpr int kBucket32 = 4;
 constexpr unsigned kEmpty32 = 0xffffffffu;
 
 struct Query {
@@ -141,7 +144,7 @@ struct Query {
   bool inside;     // kmode 1: cell lies in the map's local frame (else certainly a miss)
 };
 struct ProbeGroup {
-  long long k[kBucket];  // kmode 0: 8 keys; kmode 1: k[0..3] hold 8 packed 32-bit keys
+  long long k[kBucket64];  // kmode 0: 8 keys; kmode 1: k[0..3] = (key32 | row << 32)
 };
 
 __device__ __forceinline__ void ld256(const void* p, long long& a, long long& b, long long& c,
@@ -166,7 +169,7 @@ __device__ __forceinline__ Query make_query(const MapView& mv, double fx, double
     q.inside = lx < (unsigned long long)mv.ex && ly < (unsigned long long)mv.ey &&
                lz < (unsigned long long)mv.ez;
     q.k32 = (unsigned)lx | ((unsigned)ly << 11) | ((unsigned)lz << 22);
-    q.bucket = (q.k32 * 0x9E3779B9u) >> (mv.shift - 32);
+    q.bucket = (q.k32 * 0x9E3779B9u) >> mv.shift;
   } else {
     q.inside = true;
     q.k32 = 0;
@@ -178,38 +181,42 @@ __device__ __forceinline__ Query make_query(const MapView& mv, double fx, double
 __device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned bucket, int kmode) {
   ProbeGroup g;
   if (kmode) {
-    ld256(mv.keys32 + (size_t)bucket * kBucket, g.k[0], g.k[1], g.k[2], g.k[3]);
+    ld256(mv.kv32 + (size_t)bucket * kBucket32, g.k[0], g.k[1], g.k[2], g.k[3]);
   } else {
-    const long long* p = mv.keys + (size_t)bucket * kBucket;
+    const long long* p = mv.keys + (size_t)bucket * kBucket64;
     ld256(p, g.k[0], g.k[1], g.k[2], g.k[3]);
     ld256(p + 4, g.k[4], g.k[5], g.k[6], g.k[7]);
   }
   return g;
 }
 
-// 1 found (slot set), 0 missing, -1 continue with the next bucket
+// 1 found (`hit` = row for kmode 1, slot for kmode 0), 0 missing, -1 next bucket
 __device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& g,
-                                          unsigned bucket, const Query& q, int& slot,
+                                          unsigned bucket, const Query& q, int& hit,
                                           int kmode) {
   int found = -1;
   bool empty = false;
   if (kmode) {
 #pragma unroll
-    for (int j = kBucket - 1; j >= 0; --j) {
-      const unsigned kj = (unsigned)((unsigned long long)g.k[j >> 1] >> (32 * (j & 1)));
-      if (kj == q.k32) found = j;
+    for (int j = kBucket32 - 1; j >= 0; --j) {
+      const unsigned kj = (unsigned)((unsigned long long)g.k[j] & 0xffffffffull);
+      if (kj == q.k32) found = (int)((unsigned long long)g.k[j] >> 32);
       empty |= (kj == kEmpty32);
+    }
+    if (found >= 0) {
+      hit = found;
+      return 1;
     }
   } else {
 #pragma unroll
-    for (int j = kBucket - 1; j >= 0; --j) {
+    for (int j = kBucket64 - 1; j >= 0; --j) {
       if (g.k[j] == q.key) found = j;
       empty |= (g.k[j] == mv.empty_key);
     }
-  }
-  if (found >= 0) {
-    slot = (int)(bucket * kBucket + found);
-    return 1;
+    if (found >= 0) {
+      hit = (int)(bucket * kBucket64 + found);
+      return 1;
+    }
   }
   return empty ? 0 : -1;
 }
@@ -218,15 +225,20 @@ __device__ __forceinline__ unsigned next_bucket(unsigned b, const MapView& mv) {
   return (b + 1) & mv.mask;  // mask = #buckets - 1
 }
 
-// full lookup: slot index or -1
+// probe result -> reference row
+__device__ __forceinline__ int hit_row(const MapView& mv, int hit, int kmode) {
+  return kmode ? hit : __ldg(mv.rows + hit);
+}
+
+// full lookup: reference row or -1
 __device__ __forceinline__ int probe_query(const MapView& mv, const Query& q) {
   if (mv.m == 0 || !q.inside) return -1;
   unsigned b = q.bucket;
   for (;;) {
     const ProbeGroup g = probe_load(mv, b, mv.kmode);
-    int slot = -1;
-    const int r = probe_scan(mv, g, b, q, slot, mv.kmode);
-    if (r >= 0) return r ? slot : -1;
+    int hit = -1;
+    const int r = probe_scan(mv, g, b, q, hit, mv.kmode);
+    if (r >= 0) return r ? hit_row(mv, hit, mv.kmode) : -1;
     b = next_bucket(b, mv);
   }
 }

@@ -14,6 +14,8 @@ struct vg_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // where all work is enqueued
+  cudaStream_t side_stream = nullptr;  // K4a/K4b overlap (fork/join with events)
+  cudaEvent_t events[65] = {};
   long long launches = 0;         // kernels launched (bench evidence)
   // scratch (grown on demand, stream-ordered reuse)
   void* scratch = nullptr;
@@ -51,9 +53,10 @@ struct vg_map {
   double res = 1.0;
   unsigned capacity = 0;
   int log2cap = 0;
-  long long* pkeys = nullptr;     // kmode 0 probe array (capacity)
-  unsigned* pkeys32 = nullptr;    // kmode 1 probe array (capacity)
-  vg::VoxelRec* recs = nullptr;   // records parallel to the probe array
+  long long* pkeys = nullptr;     // kmode 0 probe keys (capacity)
+  int* prows = nullptr;           // kmode 0 row per slot (capacity)
+  uint2* pkv32 = nullptr;         // kmode 1 (key32, row) slots (capacity)
+  vg::VoxelRec* recs = nullptr;   // m records, row-indexed
   long long empty_key = 0;
   int kmode = 0;
   int bx = 0, by = 0, bz = 0, ex = 0, ey = 0, ez = 0;
@@ -65,7 +68,8 @@ struct vg_map {
   vg::MapView view() const {
     vg::MapView v;
     v.keys = pkeys;
-    v.keys32 = pkeys32;
+    v.rows = prows;
+    v.kv32 = pkv32;
     v.recs = recs;
     v.empty_key = empty_key;
     v.kmode = kmode;
@@ -77,8 +81,13 @@ struct vg_map {
     v.ez = ez;
     v.res = res;
     v.inv_res = 1.0 / res;
-    v.mask = (capacity / vg::kBucket) - 1;
-    v.shift = 64 - (log2cap - 3);
+    if (kmode) {
+      v.mask = (capacity / vg::kBucket32) - 1;
+      v.shift = 32 - (log2cap - 2);
+    } else {
+      v.mask = (capacity / vg::kBucket64) - 1;
+      v.shift = 64 - (log2cap - 3);
+    }
     v.m = (int)m;
     int e2 = 0;
     v.pow2 = (std::frexp(res, &e2) == 0.5) ? 1 : 0;
@@ -119,6 +128,12 @@ int vg_cuda_fail(cudaError_t e, const char* what);
   do {                                                       \
     cudaError_t _e = (call);                                 \
     if (_e != cudaSuccess) return vg_cuda_fail(_e, #call);   \
+  } while (0)
+
+#define VG_CHECK(x)               \
+  do {                            \
+    int _rc = (x);                \
+    if (_rc != VG_OK) return _rc; \
   } while (0)
 
 // scratch helpers

@@ -352,8 +352,7 @@ __global__ void k_lookup(CloudView cv, MapView mv, const double* __restrict__ Tp
     const Query q = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
                                floor_div(y, mv.res, mv.inv_res, mv.pow2),
                                floor_div(z, mv.res, mv.inv_res, mv.pow2), mv.kmode);
-    const int slot = probe_query(mv, q);
-    const long long row = slot < 0 ? -1 : (long long)__ldg(&mv.recs[slot].row);
+    const long long row = probe_query(mv, q);
     if (rows) rows[i] = row;
     local += (row >= 0);
   }
@@ -385,16 +384,16 @@ __global__ void k_terms(CloudView cv, MapView mv, const double* __restrict__ Tp,
     const Query q = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
                                floor_div(y, mv.res, mv.inv_res, mv.pow2),
                                floor_div(z, mv.res, mv.inv_res, mv.pow2), mv.kmode);
-    const int slot = probe_query(mv, q);
-    if (slot < 0) {
+    const int row = probe_query(mv, q);
+    if (row < 0) {
       rows[i] = -1;
       for (int k = 0; k < 3; ++k) dout[3 * i + k] = 0.0, wdout[3 * i + k] = 0.0;
       for (int k = 0; k < 9; ++k) wout[9 * i + k] = 0.0;
       continue;
     }
-    rows[i] = __ldg(&mv.recs[slot].row);
+    rows[i] = row;
     PointTerms o;
-    point_terms(R, cv, i, mv.recs + slot, x, y, z, t, o);
+    point_terms(R, cv, i, mv.recs + row, x, y, z, t, o);
     const int sym[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
     for (int k = 0; k < 3; ++k) dout[3 * i + k] = o.d[k], wdout[3 * i + k] = o.wd[k];
     for (int k = 0; k < 9; ++k) wout[9 * i + k] = o.W[sym[k]];

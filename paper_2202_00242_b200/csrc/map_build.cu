@@ -88,43 +88,16 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
   cnt_out[cidx] = cnt;
 }
 
-// one thread per cell: claim a slot by CAS on the probe array (bucketized: the home bucket's
-// 8 slots first, then the next bucket), then write the parallel 96 B record (reference row +
-// fp64 Gaussian).  kmode 1 probes 32-bit cell-local keys, kmode 0 the packed int64 keys.
+// one thread per cell: write the dense 128 B record (fp64 Gaussian) and insert key -> row
+// into the bucketized hash (home bucket first, then the next bucket; CAS on the key field).
 __global__ void k_hash_insert(const long long* __restrict__ keys, const double* __restrict__ means,
                               const double* __restrict__ covs, int m, MapView mv,
-                              long long* __restrict__ pkeys, unsigned* __restrict__ pkeys32,
-                              VoxelRec* __restrict__ recs) {
+                              long long* __restrict__ pkeys, int* __restrict__ prows,
+                              uint2* __restrict__ pkv32, VoxelRec* __restrict__ recs) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   const long long key = keys[r];
-  unsigned b, h = 0;
-  unsigned k32 = 0;
-  if (mv.kmode) {
-    const long long dx = (key >> 42) - kKeyOffset;
-    const long long dy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
-    const long long dz = (key & ((1LL << 21) - 1)) - kKeyOffset;
-    k32 = (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
-    b = (k32 * 0x9E3779B9u) >> (mv.shift - 32);
-  } else {
-    b = slot_of(key, mv.shift);
-  }
-  for (bool placed = false; !placed; b = (b + 1) & mv.mask) {
-    for (int j = 0; j < kBucket && !placed; ++j) {
-      h = b * kBucket + j;
-      if (mv.kmode) {
-        placed = atomicCAS(pkeys32 + h, kEmpty32, k32) == kEmpty32;
-      } else {
-        const unsigned long long prev =
-            atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
-                      (unsigned long long)mv.empty_key, (unsigned long long)key);
-        placed = prev == (unsigned long long)mv.empty_key;
-      }
-    }
-  }
   VoxelRec v;
-  v.row = r;
-  v.pad0 = 0;
   v.mean[0] = means[3 * r];
   v.mean[1] = means[3 * r + 1];
   v.mean[2] = means[3 * r + 2];
@@ -135,13 +108,38 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
   v.cov[3] = C[4];
   v.cov[4] = C[5];
   v.cov[5] = C[8];
-  v.pad1[0] = v.pad1[1] = 0.0;
-  recs[h] = v;
-}
-
-__global__ void k_fill32(unsigned* __restrict__ p, unsigned v, unsigned n) {
-  for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    p[i] = v;
+#pragma unroll
+  for (int k = 0; k < 7; ++k) v.pad[k] = 0.0;
+  recs[r] = v;
+  if (mv.kmode) {
+    const long long dx = (key >> 42) - kKeyOffset;
+    const long long dy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
+    const long long dz = (key & ((1LL << 21) - 1)) - kKeyOffset;
+    const unsigned k32 =
+        (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
+    for (unsigned b = (k32 * 0x9E3779B9u) >> mv.shift;; b = (b + 1) & mv.mask) {
+      for (int j = 0; j < kBucket32; ++j) {
+        uint2* sl = pkv32 + (size_t)b * kBucket32 + j;
+        if (atomicCAS(&sl->x, kEmpty32, k32) == kEmpty32) {
+          sl->y = (unsigned)r;
+          return;
+        }
+      }
+    }
+  } else {
+    for (unsigned b = slot_of(key, mv.shift);; b = (b + 1) & mv.mask) {
+      for (int j = 0; j < kBucket64; ++j) {
+        const size_t h = (size_t)b * kBucket64 + j;
+        const unsigned long long prev =
+            atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
+                      (unsigned long long)mv.empty_key, (unsigned long long)key);
+        if (prev == (unsigned long long)mv.empty_key) {
+          prows[h] = r;
+          return;
+        }
+      }
+    }
+  }
 }
 
 __global__ void k_fill(long long* __restrict__ p, long long v, unsigned n) {
@@ -178,22 +176,11 @@ int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cl) {
   return 0;
 }
 
-static int capacity_for(long long m, int* log2cap) {
-  int l = 3;  // at least one 8-slot bucket; load factor <= 0.25
-  while ((1LL << l) < 4 * m) ++l;
-  *log2cap = l;
-  return 1 << l;
-}
-
 int launch_map_finish(vg_ctx* ctx, vg_map* map) {
-  int l2 = 3;
-  map->capacity = (unsigned)capacity_for(map->m, &l2);
-  map->log2cap = l2;
   long long empty = (long long)0x8000000000000000ull;
   map->kmode = 0;
   if (map->m) {
-    // local key frame from the decoded keys (sorted ascending: any cell index extreme may sit
-    // anywhere in y/z, so all keys are scanned on the host)
+    // local key frame from the decoded keys (all keys scanned on the host)
     std::vector<long long> hk((size_t)map->m);
     VG_CUDA(cudaMemcpyAsync(hk.data(), map->keys, sizeof(long long) * map->m,
                             cudaMemcpyDeviceToHost, ctx->stream));
@@ -209,7 +196,8 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
     }
     const bool fits = hi[0] - lo[0] < 2048 && hi[1] - lo[1] < 2048 && hi[2] - lo[2] < 1023 &&
                       lo[0] > INT_MIN && lo[1] > INT_MIN && lo[2] > INT_MIN &&
-                      hi[0] < INT_MAX && hi[1] < INT_MAX && hi[2] < INT_MAX;
+                      hi[0] < INT_MAX && hi[1] < INT_MAX && hi[2] < INT_MAX &&
+                      map->m < (1LL << 31);
     if (fits) {
       map->kmode = 1;
       map->bx = (int)lo[0];
@@ -223,21 +211,27 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
     for (size_t i = 0; i < hk.size() && hk[i] == empty; ++i) ++empty;
   }
   map->empty_key = empty;
+  // capacity: kmode 1 pow2 >= 8m slots in 4-slot buckets, kmode 0 pow2 >= 4m in 8-slot ones
+  int l2 = map->kmode ? 2 : 3;
+  while ((1LL << l2) < (map->kmode ? 8 : 4) * map->m) ++l2;
+  map->capacity = 1u << l2;
+  map->log2cap = l2;
   const int gfill = (int)std::min<unsigned>((map->capacity + 255) / 256, 148 * 16);
   if (map->kmode) {
-    VG_CUDA(cudaMallocAsync((void**)&map->pkeys32, sizeof(unsigned) * (size_t)map->capacity, ctx->stream));
-    k_fill32<<<gfill, 256, 0, ctx->stream>>>(map->pkeys32, kEmpty32, map->capacity);
+    VG_CUDA(cudaMallocAsync((void**)&map->pkv32, sizeof(uint2) * (size_t)map->capacity, ctx->stream));
+    VG_CUDA(cudaMemsetAsync(map->pkv32, 0xff, sizeof(uint2) * (size_t)map->capacity, ctx->stream));
   } else {
     VG_CUDA(cudaMallocAsync((void**)&map->pkeys, sizeof(long long) * (size_t)map->capacity, ctx->stream));
+    VG_CUDA(cudaMallocAsync((void**)&map->prows, sizeof(int) * (size_t)map->capacity, ctx->stream));
     k_fill<<<gfill, 256, 0, ctx->stream>>>(map->pkeys, empty, map->capacity);
+    ctx->launches++;
+    VG_CUDA(cudaGetLastError());
   }
-  ctx->launches++;
-  VG_CUDA(cudaGetLastError());
-  VG_CUDA(cudaMallocAsync((void**)&map->recs, sizeof(VoxelRec) * (size_t)map->capacity, ctx->stream));
   if (map->m == 0) return 0;
+  VG_CUDA(cudaMallocAsync((void**)&map->recs, sizeof(VoxelRec) * (size_t)map->m, ctx->stream));
   k_hash_insert<<<(int)((map->m + 127) / 128), 128, 0, ctx->stream>>>(
-      map->keys, map->means, map->covs, (int)map->m, map->view(), map->pkeys, map->pkeys32,
-      map->recs);
+      map->keys, map->means, map->covs, (int)map->m, map->view(), map->pkeys, map->prows,
+      map->pkv32, map->recs);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
