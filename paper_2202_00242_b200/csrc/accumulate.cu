@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
         bk = next_bucket(bk, mv);
         pg = probe_load(mv, bk, kmode);
       }
-      if (r == 1 && !kmode) slot = hit_row(mv, slot, 0);
+      if (r == 1) slot = rec_index(mv, slot, kmode);
       // warm L2 with the record line K4b will gather for this hit
       if (r == 1 && prefetch_recs)
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(mv.recs + slot));
@@ -383,6 +383,342 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   partials[(size_t)w * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
 }
 
+
+// ---- K4ws: warp-specialised persistent fused lookup + accumulate ---------------------------
+// One CTA per SM, 16 warps = 8 producer/consumer pairs.  A producer warp claims items
+// (dynamic, in target-major order), resolves the correspondences of the item's points
+// (4 lookups in flight per lane), compacts the hits in shared memory and streams them as
+// rounds of <= 32 hits into its consumer's 4-slot ring: each slot receives the round's
+// source points / covariances and voxel records by cp.async (records gathered
+// cooperatively), plus the item's T_ij and round flags; completion is signalled through an
+// mbarrier (cp.async.mbarrier.arrive), so the consumer never waits on global memory.  The
+// consumer warp runs the fp64 math of a full round at a time (the math saturates the fp64
+// pipe with 4-8 warps/SM, tools/microbench/mathbench.cu) and reduces each item's 29-value
+// partial in a fixed order.  Registers: 512 threads x 128.
+constexpr int kPairs = 8;
+constexpr int kRing = 4;
+constexpr int kLookupU = 4;
+
+enum : int { kFlagFirst = 1, kFlagLast = 2, kFlagEnd = 4, kFlagF64 = 8 };
+
+struct __align__(16) SlotMeta {
+  double T[12];
+  int item;
+  int nvalid;
+  int flags;
+  int total;
+};
+
+struct __align__(16) PairSmem {
+  AccStage slot[kRing];
+  SlotMeta meta[kRing];
+  unsigned long long full[kRing];
+  unsigned long long empty[kRing];
+  ItemHdr hdr;
+  int2 hits[kMaxChunk];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// LOOKUP = 1: producers resolve correspondences themselves (fully fused);
+// LOOKUP = 0: producers stream the compacted hit lists K4a wrote (descs/hits).
+template <int MODE, int KM, int LOOKUP>
+__global__ void __launch_bounds__(2 * kPairs * 32, 1)
+    k_fused_ws(const ItemHdr* __restrict__ hdrs, const AccDesc* __restrict__ descs,
+               const int2* __restrict__ hit_list, int n_items, int* __restrict__ work_counter,
+               double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PairSmem* pairs = reinterpret_cast<PairSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x < kPairs * kRing) {
+    PairSmem& ps = pairs[threadIdx.x / kRing];
+    mbar_init(&ps.full[threadIdx.x % kRing], 33);  // 32 cp.async arrivals + 1 metadata arrive
+    mbar_init(&ps.empty[threadIdx.x % kRing], 1);
+  }
+  __syncthreads();
+
+  if (warp < kPairs) {
+    // ================================ producer ================================
+    PairSmem& ps = pairs[warp];
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned k = 0;  // ring cursor
+    int item = 0;
+    if (lane == 0) item = atomicAdd(work_counter, 1);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    // header of the next item is loaded into registers while the current one is processed
+    // LOOKUP: 256 B ItemHdr (16 lanes x 16 B); else 160 B AccDesc (10 lanes x 16 B)
+    constexpr int kHdrLanes = LOOKUP ? 16 : (int)(sizeof(AccDesc) / 16);
+    auto hdr_src = [&](int it) -> const int4* {
+      return LOOKUP ? reinterpret_cast<const int4*>(hdrs + it)
+                    : reinterpret_cast<const int4*>(descs + it);
+    };
+    int4 hreg = make_int4(0, 0, 0, 0);
+    if (item < n_items && lane < kHdrLanes) hreg = __ldg(hdr_src(item) + lane);
+    for (;;) {
+      if (item >= n_items) {  // tell the consumer to stop
+        const unsigned slot = k % kRing;
+        mbar_wait(&ps.empty[slot], ((k / kRing) & 1) ^ 1);
+        if (lane == 0) ps.meta[slot].flags = kFlagEnd;
+        __syncwarp();
+        mbar_arrive_cp_async(&ps.full[slot]);
+        if (lane == 0) mbar_arrive(&ps.full[slot]);
+        break;
+      }
+      if (lane < kHdrLanes) reinterpret_cast<int4*>(&ps.hdr)[lane] = hreg;
+      int next = 0;
+      if (lane == 0) next = atomicAdd(work_counter, 1);
+      next = __shfl_sync(0xffffffffu, next, 0);
+      __syncwarp();
+      if (next < n_items && lane < kHdrLanes) hreg = __ldg(hdr_src(next) + lane);
+      if (!LOOKUP) {
+        // ---- stream K4a's hit list: the descriptor holds T, the gather pointers, n, hoff
+        const AccDesc& dd = *reinterpret_cast<const AccDesc*>(&ps.hdr);
+        const int nh = dd.n;
+        const int2* hl = hit_list + dd.hoff;
+        const int rounds = nh > 0 ? (nh + 31) / 32 : 1;
+        const int klast = nh > 0 ? nh - 1 : 0;
+        CloudView cv;
+        cv.a = dd.a;
+        cv.xyz64 = dd.xyz64;
+        cv.c0 = dd.c0;
+        cv.c1 = dd.c1;
+        cv.c2 = dd.c2;
+        cv.n = 0;
+        const VoxelRec* recs = dd.recs;
+        int2 e = __ldg(hl + min(lane, klast));
+        for (int r = 0; r < rounds; ++r, ++k) {
+          const int2 en = __ldg(hl + min((r + 1) * 32 + lane, klast));  // next round's entry
+          const unsigned slot = k % kRing;
+          mbar_wait(&ps.empty[slot], ((k / kRing) & 1) ^ 1);
+          SlotMeta& md = ps.meta[slot];
+          if (lane < 12) md.T[lane] = dd.T[lane];
+          if (lane == 12) md.item = item;
+          if (lane == 13) md.nvalid = max(0, min(32, nh - r * 32));
+          if (lane == 14)
+            md.flags = (r == 0 ? kFlagFirst : 0) | (r == rounds - 1 ? kFlagLast : 0) |
+                       (cv.xyz64 ? kFlagF64 : 0);
+          if (lane == 15) md.total = nh;
+          AccStage& st = ps.slot[slot];
+          const int nvalid = max(0, min(32, nh - r * 32));
+          if (lane < nvalid) {
+            if (cv.xyz64) {
+              const double* q = cv.xyz64 + 3 * (size_t)e.x;
+              double* d8 = reinterpret_cast<double*>(&st.pt[0][lane]);
+              cp_async8(d8, q);
+              cp_async8(d8 + 1, q + 1);
+              cp_async8(reinterpret_cast<double*>(&st.pt[1][lane]), q + 2);
+            } else {
+              cp_async16(&st.pt[0][lane], cv.a + e.x);
+            }
+            cp_async16(&st.cov[0][lane], cv.c0 + e.x);
+            cp_async16(&st.cov[1][lane], cv.c1 + e.x);
+            cp_async16(&st.cov[2][lane], cv.c2 + e.x);
+          }
+#pragma unroll
+          for (int c = 0; c < kRecUnits; ++c) {
+            const int u = c * 32 + lane;
+            const int q = u / kRecUnits, j = u - q * kRecUnits;
+            const int row = __shfl_sync(0xffffffffu, e.y, q);
+            if (q < nvalid)
+              cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(recs + row) + 16 * j);
+          }
+          __syncwarp();
+          mbar_arrive_cp_async(&ps.full[slot]);
+          if (lane == 0) mbar_arrive(&ps.full[slot]);
+          e = en;
+        }
+        item = next;
+        continue;
+      }
+      const ItemHdr& h = ps.hdr;
+      double R[9], t[3];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) R[q] = h.T[q];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) t[q] = h.T[9 + q];
+      const MapView& mv = h.mv;
+      const float4* pa = h.a;
+      const double* p64 = h.xyz64;
+      const int begin = h.begin, end = h.end;
+      const int kmode = KM == 2 ? mv.kmode : KM;
+      // ---- lookups: kLookupU points per lane in flight
+      int nh = 0;
+      for (int base = begin; base < end; base += 32 * kLookupU) {
+        Query qy[kLookupU];
+        ProbeGroup pg[kLookupU];
+        bool live[kLookupU];
+#pragma unroll
+        for (int u = 0; u < kLookupU; ++u) {
+          const int i = base + 32 * u + lane;
+          live[u] = i < end;
+          const int ic = min(i, end - 1);
+          double px, py, pz;
+          if (p64) {
+            px = p64[3 * (size_t)ic];
+            py = p64[3 * (size_t)ic + 1];
+            pz = p64[3 * (size_t)ic + 2];
+          } else {
+            const float4 a = __ldg(pa + ic);
+            px = a.x;
+            py = a.y;
+            pz = a.z;
+          }
+          // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
+          const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
+          const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
+          const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
+          qy[u] = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                             floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                             floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
+          live[u] = live[u] && mv.m && qy[u].inside;
+          if (live[u]) pg[u] = probe_load(mv, qy[u].bucket, kmode);
+        }
+#pragma unroll
+        for (int u = 0; u < kLookupU; ++u) {
+          int row = -1;
+          if (live[u]) {
+            unsigned bk = qy[u].bucket;
+            int r;
+            while ((r = probe_scan(mv, pg[u], bk, qy[u], row, kmode)) < 0) {
+              bk = next_bucket(bk, mv);
+              pg[u] = probe_load(mv, bk, kmode);
+            }
+            if (r == 1) row = rec_index(mv, row, kmode);
+            if (r != 1) row = -1;
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, row >= 0);
+          if (row >= 0) ps.hits[nh + __popc(m & lt_mask)] = make_int2(base + 32 * u + lane, row);
+          nh += __popc(m);
+        }
+      }
+      __syncwarp();
+      // ---- stream the hits to the consumer, one round (<= 32 hits) per ring slot
+      const int rounds = nh > 0 ? (nh + 31) / 32 : 1;
+      CloudView cv;
+      cv.a = pa;
+      cv.xyz64 = p64;
+      cv.c0 = h.c0;
+      cv.c1 = h.c1;
+      cv.c2 = h.c2;
+      cv.n = 0;
+      for (int r = 0; r < rounds; ++r, ++k) {
+        const unsigned slot = k % kRing;
+        mbar_wait(&ps.empty[slot], ((k / kRing) & 1) ^ 1);
+        SlotMeta& md = ps.meta[slot];
+        if (lane < 12) md.T[lane] = h.T[lane];
+        if (lane == 12) md.item = item;
+        if (lane == 13) md.nvalid = min(32, nh - r * 32);
+        if (lane == 14)
+          md.flags = (r == 0 ? kFlagFirst : 0) | (r == rounds - 1 ? kFlagLast : 0) |
+                     (p64 ? kFlagF64 : 0);
+        if (lane == 15) md.total = nh;
+        const int kh = r * 32 + lane;
+        const int2 e = ps.hits[min(kh, max(nh - 1, 0))];
+        // gather into the slot (the AccStage layout K4b uses)
+        AccStage& st = ps.slot[slot];
+        const int nvalid = max(0, min(32, nh - r * 32));
+        if (lane < nvalid) {
+          if (p64) {
+            const double* q = p64 + 3 * (size_t)e.x;
+            double* dd = reinterpret_cast<double*>(&st.pt[0][lane]);
+            cp_async8(dd, q);
+            cp_async8(dd + 1, q + 1);
+            cp_async8(reinterpret_cast<double*>(&st.pt[1][lane]), q + 2);
+          } else {
+            cp_async16(&st.pt[0][lane], pa + e.x);
+          }
+          cp_async16(&st.cov[0][lane], cv.c0 + e.x);
+          cp_async16(&st.cov[1][lane], cv.c1 + e.x);
+          cp_async16(&st.cov[2][lane], cv.c2 + e.x);
+        }
+#pragma unroll
+        for (int c = 0; c < kRecUnits; ++c) {
+          const int u = c * 32 + lane;
+          const int q = u / kRecUnits, j = u - q * kRecUnits;
+          const int row = __shfl_sync(0xffffffffu, e.y, q);
+          if (q < nvalid)
+            cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(mv.recs + row) + 16 * j);
+        }
+        __syncwarp();  // metadata stores of all lanes before lane 0's release-arrive
+        mbar_arrive_cp_async(&ps.full[slot]);
+        if (lane == 0) mbar_arrive(&ps.full[slot]);
+      }
+      item = next;
+    }
+  } else {
+    // ================================ consumer ================================
+    PairSmem& ps = pairs[warp - kPairs];
+    double acc[28];
+#pragma unroll
+    for (int q = 0; q < 28; ++q) acc[q] = 0.0;
+    for (unsigned k = 0;; ++k) {
+      const unsigned slot = k % kRing;
+      mbar_wait(&ps.full[slot], (k / kRing) & 1);
+      const SlotMeta& md = ps.meta[slot];
+      const int flags = md.flags;
+      if (flags & kFlagEnd) break;
+      const int nvalid = md.nvalid, item = md.item, total = md.total;
+      double R[9], t[3];
+#pragma unroll
+      for (int q = 0; q < 9; ++q) R[q] = md.T[q];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) t[q] = md.T[9 + q];
+      if (flags & kFlagFirst) {
+#pragma unroll
+        for (int q = 0; q < 28; ++q) acc[q] = 0.0;
+      }
+      if (lane < nvalid)
+        hit_math<MODE>(ps.slot[slot], lane, (flags & kFlagF64) != 0, R, t, 1.0, acc);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ps.empty[slot]);  // slot data fully consumed
+      if (flags & kFlagLast) {
+        if (MODE == 1) {
+          double c = acc[27];
+#pragma unroll
+          for (int q = 16; q >= 1; q >>= 1) c += __shfl_xor_sync(0xffffffffu, c, q);
+          if (lane == 0) {
+            partials[2 * (size_t)item] = c;
+            partials[2 * (size_t)item + 1] = (double)total;
+          }
+        } else {
+          double v[32];
+#pragma unroll
+          for (int q = 0; q < 28; ++q) v[q] = acc[q];
+          v[28] = lane == 0 ? (double)total : 0.0;
+          v[29] = 0.0;
+          v[30] = 0.0;
+          v[31] = 0.0;
+          partials[(size_t)item * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace vg
 
 using namespace vg;
@@ -457,9 +793,53 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
 
 // K4a + K4b.  Experiment knobs (measured slower on config 5, kept off): VGICP_CHUNKS > 1
 // alternates K4a/K4b over item chunks; VGICP_PREFETCH=1 makes K4a prefetch record lines to L2.
+static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
+                               cudaStream_t st, int prefetch);
+
+static int launch_fused_ws(vg_ctx* ctx, vg_batch* b, int kmode) {
+  const int n = (int)b->num_items;
+  static int sms = 0;
+  if (!sms) VG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const size_t smem = sizeof(PairSmem) * kPairs;
+  VG_CUDA(cudaMemsetAsync(b->work_counter, 0, sizeof(int), ctx->stream));
+  const int grid = std::min(sms, (n + 7) / 8);
+  auto go = [&](auto kern) -> int {
+    VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, 2 * kPairs * 32, smem, ctx->stream>>>(b->hdrs, b->descs, b->hits, n,
+                                                       b->work_counter, b->partials);
+    return 0;
+  };
+  static const int ws_mode = [] {
+    const char* e = getenv("VGICP_FUSED_WS");  // 1: K4a + streaming WS kernel, 2: fully fused
+    return e ? atoi(e) : 1;
+  }();
+  int rc;
+  if (ws_mode == 2) {
+    if (b->key_mode == 1)
+      rc = kmode == 1 ? go(k_fused_ws<1, 1, 1>) : go(k_fused_ws<0, 1, 1>);
+    else
+      rc = kmode == 1 ? go(k_fused_ws<1, 2, 1>) : go(k_fused_ws<0, 2, 1>);
+  } else {
+    VG_CHECK(launch_lookup_range(ctx, b, kmode, 0, n, ctx->stream, 0));
+    VG_CUDA(cudaMemsetAsync(b->work_counter, 0, sizeof(int), ctx->stream));
+    rc = kmode == 1 ? go(k_fused_ws<1, 1, 0>) : go(k_fused_ws<0, 1, 0>);
+  }
+  if (rc) return rc;
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   if (b->num_items == 0) return 0;
   const int n = (int)b->num_items;
+  static const int use_ws = [] {
+    // 0 (default): K4a + K4b; 1: K4a + streaming warp-specialised kernel; 2: fully fused
+    // warp-specialised kernel (both measured slower on config 5, kept for experiments)
+    const char* e = getenv("VGICP_FUSED_WS");
+    return e ? atoi(e) : 0;
+  }();
+  if (use_ws && kmode != 2) return launch_fused_ws(ctx, b, kmode);
   static const int chunks_env = [] {
     const char* e = getenv("VGICP_CHUNKS");
     return e ? atoi(e) : 1;

@@ -276,7 +276,7 @@ int vg_map_destroy(vg_map* m) {
   vg_ctx* ctx = m->ctx;
   dfree(ctx, m->pkeys);
   dfree(ctx, m->prows);
-  dfree(ctx, m->pkv32);
+  dfree(ctx, m->pkeys32);
   dfree(ctx, m->recs);
   dfree(ctx, m->keys);
   dfree(ctx, m->means);
@@ -469,6 +469,24 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     n32 += maps[i]->kmode;
   }
   b->key_mode = n32 == (int)maps.size() ? 1 : (n32 == 0 ? 0 : 2);
+  std::vector<ItemHdr> hdrs(items.size());
+  for (size_t i = 0; i < items.size(); ++i) {
+    ItemHdr& h = hdrs[i];
+    memset(&h, 0, sizeof(h));
+    const FactorDev& fd = fac[items[i].factor];
+    for (int q = 0; q < 12; ++q) h.T[q] = fd.T[q];
+    const CloudView& c = cv[fd.cloud];
+    h.a = c.a;
+    h.xyz64 = c.xyz64;
+    h.c0 = c.c0;
+    h.c1 = c.c1;
+    h.c2 = c.c2;
+    h.mv = mv[fd.map];
+    h.factor = items[i].factor;
+    h.begin = items[i].begin;
+    h.end = items[i].end;
+    h.hoff = items[i].hoff;
+  }
   int rc = VG_OK;
   if ((rc = dalloc(ctx, &b->factors, F)) || (rc = dalloc(ctx, &b->items, items.size())) ||
       (rc = dalloc(ctx, &b->clouds, cv.size())) || (rc = dalloc(ctx, &b->maps, mv.size())) ||
@@ -476,11 +494,14 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
       (rc = dalloc(ctx, &b->hits, (size_t)hoff + 2)) ||
       (rc = dalloc(ctx, &b->hit_counts, items.size())) ||
       (rc = dalloc(ctx, &b->descs, items.size())) ||
+      (rc = dalloc(ctx, &b->hdrs, items.size())) ||
+      (rc = dalloc(ctx, &b->work_counter, 1)) ||
       (rc = dalloc(ctx, &b->out, (size_t)F * VG_REC_LINEARIZE)) ||
       (rc = h2d(ctx, b->factors, fac.data(), sizeof(FactorDev) * F)) ||
       (rc = h2d(ctx, b->items, items.data(), sizeof(ItemDev) * items.size())) ||
       (rc = h2d(ctx, b->clouds, cv.data(), sizeof(CloudView) * cv.size())) ||
-      (rc = h2d(ctx, b->maps, mv.data(), sizeof(MapView) * mv.size()))) {
+      (rc = h2d(ctx, b->maps, mv.data(), sizeof(MapView) * mv.size())) ||
+      (rc = h2d(ctx, b->hdrs, hdrs.data(), sizeof(ItemHdr) * hdrs.size()))) {
     vg_batch_destroy(b);
     return rc;
   }
@@ -509,6 +530,8 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->hits);
   dfree(ctx, b->hit_counts);
   dfree(ctx, b->descs);
+  dfree(ctx, b->hdrs);
+  dfree(ctx, b->work_counter);
   dfree(ctx, b->out);
   dfree(ctx, b->poses);
   cudaStreamSynchronize(ctx->stream);
@@ -539,6 +562,7 @@ int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_
   // scatter T_ij into the 128 B factor records (dst pitch 128, src pitch 96)
   VG_CUDA(cudaMemcpy2DAsync(b->factors, sizeof(FactorDev), T_host, 12 * sizeof(double),
                             12 * sizeof(double), (size_t)b->F, cudaMemcpyHostToDevice, ctx->stream));
+  VG_CHECK(launch_spread_T(ctx, b));
   VG_CHECK(run_device(b, mode, b->out));
   return d2h_sync(ctx, out_host, b->out, sizeof(double) * rec_of(mode) * b->F);
 }

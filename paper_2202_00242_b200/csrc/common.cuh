@@ -3,9 +3,10 @@
 // HBM layouts:
 //   cloud  : SoA, 64 B/point: a[i] = (x, y, z) fp32, covariance as three fp64 double2 arrays
 //            + optional fp64 xyz (n x 3) when the points are not exactly fp32 (keys stay exact)
-//   map    : bucketized open-addressing hash (key -> row): 32 B buckets of 4 (key32, row)
-//            pairs (load <= 0.125), or int64 keys in 64 B buckets of 8 (+ row array) when
-//            the map does not fit the 32-bit local frame; row-indexed 128 B fp64 records.
+//   map    : bucketized open-addressing hash: 32-bit cell-local keys in 32 B buckets of 8
+//            (load <= 0.25, ~16 B/cell: the probe arrays of all maps stay L2-resident) with
+//            128 B fp64 records parallel to the slots; maps that do not fit the local frame
+//            use int64 keys (64 B buckets) + a row array and row-indexed records.
 //   work   : (factor, chunk) items, one warp per item; fp64 partials, fixed-order reduce.
 #pragma once
 #include <cstddef>
@@ -28,7 +29,8 @@ constexpr int kMaxChunk = 512;        // points per work item => <= 16 points pe
 struct __align__(128) VoxelRec {
   double mean[3];   // voxel mean (registration.py:90-92)                 bytes  0..24
   double cov[6];    // covariance c00 c01 c02 c11 c12 c22 (:93-97)        bytes 24..72
-  double pad[7];
+  long long row;    // reference row (kmode 1 records sit at hash slots)  bytes 72..80
+  double pad[6];
 };
 static_assert(sizeof(VoxelRec) == 128, "voxel record must be one 128 B line");
 static_assert(offsetof(VoxelRec, mean) % 16 == 0 && offsetof(VoxelRec, cov) % 16 == 8,
@@ -46,8 +48,8 @@ struct CloudView {
 struct MapView {
   const long long* keys;    // kmode 0: int64 packed keys, buckets of 8 (64 B)
   const int* rows;          // kmode 0: reference row per slot (parallel to keys)
-  const uint2* kv32;        // kmode 1: (32-bit cell-local key, row) pairs, buckets of 4 (32 B)
-  const VoxelRec* recs;     // m records, row-indexed
+  const unsigned* keys32;   // kmode 1: 32-bit cell-local keys, buckets of 8 (32 B)
+  const VoxelRec* recs;     // kmode 1: parallel to keys32 (slot-indexed); kmode 0: row-indexed
   long long empty_key;      // kmode 0 empty marker (a value that is not a key of the map)
   double res;
   double inv_res;
@@ -59,6 +61,23 @@ struct MapView {
   int bx, by, bz;       // local frame origin (min cell index)
   int ex, ey, ez;       // local frame extents (cells)
 };
+
+// Per-item header for the fused kernel (256 B, one coalesced load by 16 lanes): T_ij (written
+// by K-compose every step) + the static views of the item's source cloud and target map.
+struct __align__(16) ItemHdr {
+  double T[12];
+  const float4* a;
+  const double* xyz64;
+  const double2* c0;
+  const double2* c1;
+  const double2* c2;
+  MapView mv;
+  int factor;
+  int begin;
+  int end;
+  int hoff;
+};
+static_assert(sizeof(ItemHdr) == 256, "item header must be 256 B");
 
 // Per-factor record resident in HBM (128 B).  T = T_ij (R row-major, t), fp64.
 struct __align__(16) FactorDev {
@@ -126,15 +145,14 @@ __device__ __forceinline__ unsigned slot_of(long long key, int shift) {
 // before spilling to the next one, so a lookup resolves in its home bucket unless that
 // bucket is full.  Two key encodings:
 //   kmode 1 — 32-bit cell-local keys (lx | ly << 11 | lz << 22 relative to the map's min
-//             cell), stored with the row as (key32, row) pairs: a bucket of 4 pairs is 32 B =
-//             one 256-bit load that yields the row directly.  Load <= 0.125 (~0.2% spill).
-//             Used whenever the map fits the local frame.
+//             cell); a bucket of 8 keys is 32 B = one 256-bit load.  Load <= 0.25.  The probe
+//             returns the slot; the record sits at the same slot (it carries the row).
 //   kmode 0 — the reference's packed int64 keys in 64 B buckets of 8 (two 256-bit loads,
-//             load <= 0.25) and a parallel row array.
+//             load <= 0.25); the probe returns the slot, a parallel array gives the row and
+//             records are row-indexed.
 // The local key is built from decode(pack(floor)) — the reference's own key round trip —
 // so aliasing of out-of-range indices behaves exactly as the reference's packed keys.
-constexpr int kBucket64 = 8;
-constexpr int kBucket32 = 4;
+constexpr int kBucket = 8;
 constexpr unsigned kEmpty32 = 0xffffffffu;
 
 struct Query {
@@ -144,7 +162,7 @@ struct Query {
   bool inside;     // kmode 1: cell lies in the map's local frame (else certainly a miss)
 };
 struct ProbeGroup {
-  long long k[kBucket64];  // kmode 0: 8 keys; kmode 1: k[0..3] = (key32 | row << 32)
+  long long k[kBucket];  // kmode 0: 8 keys; kmode 1: k[0..3] hold 8 packed 32-bit keys
 };
 
 __device__ __forceinline__ void ld256(const void* p, long long& a, long long& b, long long& c,
@@ -181,42 +199,38 @@ __device__ __forceinline__ Query make_query(const MapView& mv, double fx, double
 __device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned bucket, int kmode) {
   ProbeGroup g;
   if (kmode) {
-    ld256(mv.kv32 + (size_t)bucket * kBucket32, g.k[0], g.k[1], g.k[2], g.k[3]);
+    ld256(mv.keys32 + (size_t)bucket * kBucket, g.k[0], g.k[1], g.k[2], g.k[3]);
   } else {
-    const long long* p = mv.keys + (size_t)bucket * kBucket64;
+    const long long* p = mv.keys + (size_t)bucket * kBucket;
     ld256(p, g.k[0], g.k[1], g.k[2], g.k[3]);
     ld256(p + 4, g.k[4], g.k[5], g.k[6], g.k[7]);
   }
   return g;
 }
 
-// 1 found (`hit` = row for kmode 1, slot for kmode 0), 0 missing, -1 next bucket
+// 1 found (`slot` set), 0 missing, -1 next bucket
 __device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& g,
-                                          unsigned bucket, const Query& q, int& hit,
+                                          unsigned bucket, const Query& q, int& slot,
                                           int kmode) {
   int found = -1;
   bool empty = false;
   if (kmode) {
 #pragma unroll
-    for (int j = kBucket32 - 1; j >= 0; --j) {
-      const unsigned kj = (unsigned)((unsigned long long)g.k[j] & 0xffffffffull);
-      if (kj == q.k32) found = (int)((unsigned long long)g.k[j] >> 32);
+    for (int j = kBucket - 1; j >= 0; --j) {
+      const unsigned kj = (unsigned)((unsigned long long)g.k[j >> 1] >> (32 * (j & 1)));
+      if (kj == q.k32) found = j;
       empty |= (kj == kEmpty32);
-    }
-    if (found >= 0) {
-      hit = found;
-      return 1;
     }
   } else {
 #pragma unroll
-    for (int j = kBucket64 - 1; j >= 0; --j) {
+    for (int j = kBucket - 1; j >= 0; --j) {
       if (g.k[j] == q.key) found = j;
       empty |= (g.k[j] == mv.empty_key);
     }
-    if (found >= 0) {
-      hit = (int)(bucket * kBucket64 + found);
-      return 1;
-    }
+  }
+  if (found >= 0) {
+    slot = (int)(bucket * kBucket + found);
+    return 1;
   }
   return empty ? 0 : -1;
 }
@@ -225,20 +239,24 @@ __device__ __forceinline__ unsigned next_bucket(unsigned b, const MapView& mv) {
   return (b + 1) & mv.mask;  // mask = #buckets - 1
 }
 
-// probe result -> reference row
-__device__ __forceinline__ int hit_row(const MapView& mv, int hit, int kmode) {
-  return kmode ? hit : __ldg(mv.rows + hit);
+// probe result (slot) -> index of the voxel record to gather
+__device__ __forceinline__ int rec_index(const MapView& mv, int slot, int kmode) {
+  return kmode ? slot : __ldg(mv.rows + slot);
+}
+// probe result (slot) -> reference row
+__device__ __forceinline__ int slot_row(const MapView& mv, int slot, int kmode) {
+  return kmode ? (int)__ldg(&mv.recs[slot].row) : __ldg(mv.rows + slot);
 }
 
-// full lookup: reference row or -1
+// full lookup: slot or -1
 __device__ __forceinline__ int probe_query(const MapView& mv, const Query& q) {
   if (mv.m == 0 || !q.inside) return -1;
   unsigned b = q.bucket;
   for (;;) {
     const ProbeGroup g = probe_load(mv, b, mv.kmode);
-    int hit = -1;
-    const int r = probe_scan(mv, g, b, q, hit, mv.kmode);
-    if (r >= 0) return r ? hit_row(mv, hit, mv.kmode) : -1;
+    int slot = -1;
+    const int r = probe_scan(mv, g, b, q, slot, mv.kmode);
+    if (r >= 0) return r ? slot : -1;
     b = next_bucket(b, mv);
   }
 }

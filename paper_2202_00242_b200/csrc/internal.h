@@ -55,8 +55,8 @@ struct vg_map {
   int log2cap = 0;
   long long* pkeys = nullptr;     // kmode 0 probe keys (capacity)
   int* prows = nullptr;           // kmode 0 row per slot (capacity)
-  uint2* pkv32 = nullptr;         // kmode 1 (key32, row) slots (capacity)
-  vg::VoxelRec* recs = nullptr;   // m records, row-indexed
+  unsigned* pkeys32 = nullptr;    // kmode 1 keys (capacity)
+  vg::VoxelRec* recs = nullptr;   // kmode 1: capacity, slot-indexed; kmode 0: m, row-indexed
   long long empty_key = 0;
   int kmode = 0;
   int bx = 0, by = 0, bz = 0, ex = 0, ey = 0, ez = 0;
@@ -69,7 +69,7 @@ struct vg_map {
     vg::MapView v;
     v.keys = pkeys;
     v.rows = prows;
-    v.kv32 = pkv32;
+    v.keys32 = pkeys32;
     v.recs = recs;
     v.empty_key = empty_key;
     v.kmode = kmode;
@@ -81,13 +81,8 @@ struct vg_map {
     v.ez = ez;
     v.res = res;
     v.inv_res = 1.0 / res;
-    if (kmode) {
-      v.mask = (capacity / vg::kBucket32) - 1;
-      v.shift = 32 - (log2cap - 2);
-    } else {
-      v.mask = (capacity / vg::kBucket64) - 1;
-      v.shift = 64 - (log2cap - 3);
-    }
+    v.mask = (capacity / vg::kBucket) - 1;
+    v.shift = (kmode ? 32 : 64) - (log2cap - 3);
     v.m = (int)m;
     int e2 = 0;
     v.pow2 = (std::frexp(res, &e2) == 0.5) ? 1 : 0;
@@ -112,6 +107,8 @@ struct vg_batch {
   int2* hits = nullptr;               // compacted (point, slot) hits, per-item regions
   int* hit_counts = nullptr;          // num_items
   vg::AccDesc* descs = nullptr;       // num_items (K4a -> K4b)
+  vg::ItemHdr* hdrs = nullptr;        // num_items (fused kernel headers; T refreshed per step)
+  int* work_counter = nullptr;        // fused kernel dynamic item counter
   long long hit_capacity = 0;
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;
@@ -151,6 +148,7 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                  const double* T_dev, long long* rows, double* moved, double* d, double* w,
                  double* wd, double* partial_cost, long long* partial_inl, int nblocks);
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
+int launch_spread_T(vg_ctx* ctx, vg_batch* b);  // FactorDev.T -> ItemHdr.T (explicit-T mode)
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);

@@ -312,7 +312,8 @@ __device__ __forceinline__ void q_matrix(Quat q, double* R) {
 #undef A_
 #undef S_
 
-__global__ void k_compose(FactorDev* __restrict__ factors, int F, const double* __restrict__ poses) {
+__global__ void k_compose(FactorDev* __restrict__ factors, int F, const double* __restrict__ poses,
+                          ItemHdr* __restrict__ hdrs) {
   const int fi = blockIdx.x * blockDim.x + threadIdx.x;
   if (fi >= F) return;
   FactorDev& f = factors[fi];
@@ -334,6 +335,16 @@ __global__ void k_compose(FactorDev* __restrict__ factors, int F, const double* 
   f.T[9] = __dadd_rn(tt[0], tinv[0]);
   f.T[10] = __dadd_rn(tt[1], tinv[1]);
   f.T[11] = __dadd_rn(tt[2], tinv[2]);
+  for (int it = 0; it < f.item_count; ++it)
+    for (int q = 0; q < 12; ++q) hdrs[f.item_begin + it].T[q] = f.T[q];
+}
+
+__global__ void k_spread_T(const FactorDev* __restrict__ factors, int F, ItemHdr* __restrict__ hdrs) {
+  const int fi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (fi >= F) return;
+  const FactorDev& f = factors[fi];
+  for (int it = 0; it < f.item_count; ++it)
+    for (int q = 0; q < 12; ++q) hdrs[f.item_begin + it].T[q] = f.T[q];
 }
 
 // ---- K3: transform + lookup (GaussianVoxelMap.lookup / overlap_rate) ----------------------
@@ -352,7 +363,8 @@ __global__ void k_lookup(CloudView cv, MapView mv, const double* __restrict__ Tp
     const Query q = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
                                floor_div(y, mv.res, mv.inv_res, mv.pow2),
                                floor_div(z, mv.res, mv.inv_res, mv.pow2), mv.kmode);
-    const long long row = probe_query(mv, q);
+    const int slot = probe_query(mv, q);
+    const long long row = slot < 0 ? -1 : slot_row(mv, slot, mv.kmode);
     if (rows) rows[i] = row;
     local += (row >= 0);
   }
@@ -384,16 +396,16 @@ __global__ void k_terms(CloudView cv, MapView mv, const double* __restrict__ Tp,
     const Query q = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
                                floor_div(y, mv.res, mv.inv_res, mv.pow2),
                                floor_div(z, mv.res, mv.inv_res, mv.pow2), mv.kmode);
-    const int row = probe_query(mv, q);
-    if (row < 0) {
+    const int slot = probe_query(mv, q);
+    if (slot < 0) {
       rows[i] = -1;
       for (int k = 0; k < 3; ++k) dout[3 * i + k] = 0.0, wdout[3 * i + k] = 0.0;
       for (int k = 0; k < 9; ++k) wout[9 * i + k] = 0.0;
       continue;
     }
-    rows[i] = row;
+    rows[i] = slot_row(mv, slot, mv.kmode);
     PointTerms o;
-    point_terms(R, cv, i, mv.recs + row, x, y, z, t, o);
+    point_terms(R, cv, i, mv.recs + rec_index(mv, slot, mv.kmode), x, y, z, t, o);
     const int sym[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};
     for (int k = 0; k < 3; ++k) dout[3 * i + k] = o.d[k], wdout[3 * i + k] = o.wd[k];
     for (int k = 0; k < 9; ++k) wout[9 * i + k] = o.W[sym[k]];
@@ -454,7 +466,16 @@ int launch_terms(vg_ctx* ctx, const CloudView& cv, const MapView& mv, const doub
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev) {
   if (b->F == 0) return 0;
   k_compose<<<grid_for(b->F, 128, 1 << 30), 128, 0, ctx->stream>>>(b->factors, (int)b->F,
-                                                                   poses_dev);
+                                                                   poses_dev, b->hdrs);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_spread_T(vg_ctx* ctx, vg_batch* b) {
+  if (b->F == 0) return 0;
+  k_spread_T<<<grid_for(b->F, 128, 1 << 30), 128, 0, ctx->stream>>>(b->factors, (int)b->F,
+                                                                    b->hdrs);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;

@@ -88,15 +88,41 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
   cnt_out[cidx] = cnt;
 }
 
-// one thread per cell: write the dense 128 B record (fp64 Gaussian) and insert key -> row
-// into the bucketized hash (home bucket first, then the next bucket; CAS on the key field).
+// one thread per cell: insert key into the bucketized hash (home bucket first, then the next
+// bucket; CAS on the key), then write the 128 B record (fp64 Gaussian + reference row) at the
+// slot (kmode 1) or at the row with a slot -> row entry (kmode 0).
 __global__ void k_hash_insert(const long long* __restrict__ keys, const double* __restrict__ means,
                               const double* __restrict__ covs, int m, MapView mv,
                               long long* __restrict__ pkeys, int* __restrict__ prows,
-                              uint2* __restrict__ pkv32, VoxelRec* __restrict__ recs) {
+                              unsigned* __restrict__ pkeys32, VoxelRec* __restrict__ recs) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   const long long key = keys[r];
+  size_t h = 0;
+  if (mv.kmode) {
+    const long long dx = (key >> 42) - kKeyOffset;
+    const long long dy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
+    const long long dz = (key & ((1LL << 21) - 1)) - kKeyOffset;
+    const unsigned k32 =
+        (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
+    bool placed = false;
+    for (unsigned b = (k32 * 0x9E3779B9u) >> mv.shift; !placed; b = (b + 1) & mv.mask)
+      for (int j = 0; j < kBucket && !placed; ++j) {
+        h = (size_t)b * kBucket + j;
+        placed = atomicCAS(pkeys32 + h, kEmpty32, k32) == kEmpty32;
+      }
+  } else {
+    bool placed = false;
+    for (unsigned b = slot_of(key, mv.shift); !placed; b = (b + 1) & mv.mask)
+      for (int j = 0; j < kBucket && !placed; ++j) {
+        h = (size_t)b * kBucket + j;
+        const unsigned long long prev =
+            atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
+                      (unsigned long long)mv.empty_key, (unsigned long long)key);
+        placed = prev == (unsigned long long)mv.empty_key;
+      }
+    prows[h] = r;
+  }
   VoxelRec v;
   v.mean[0] = means[3 * r];
   v.mean[1] = means[3 * r + 1];
@@ -108,38 +134,10 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
   v.cov[3] = C[4];
   v.cov[4] = C[5];
   v.cov[5] = C[8];
+  v.row = r;
 #pragma unroll
-  for (int k = 0; k < 7; ++k) v.pad[k] = 0.0;
-  recs[r] = v;
-  if (mv.kmode) {
-    const long long dx = (key >> 42) - kKeyOffset;
-    const long long dy = ((key >> 21) & ((1LL << 21) - 1)) - kKeyOffset;
-    const long long dz = (key & ((1LL << 21) - 1)) - kKeyOffset;
-    const unsigned k32 =
-        (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
-    for (unsigned b = (k32 * 0x9E3779B9u) >> mv.shift;; b = (b + 1) & mv.mask) {
-      for (int j = 0; j < kBucket32; ++j) {
-        uint2* sl = pkv32 + (size_t)b * kBucket32 + j;
-        if (atomicCAS(&sl->x, kEmpty32, k32) == kEmpty32) {
-          sl->y = (unsigned)r;
-          return;
-        }
-      }
-    }
-  } else {
-    for (unsigned b = slot_of(key, mv.shift);; b = (b + 1) & mv.mask) {
-      for (int j = 0; j < kBucket64; ++j) {
-        const size_t h = (size_t)b * kBucket64 + j;
-        const unsigned long long prev =
-            atomicCAS(reinterpret_cast<unsigned long long*>(pkeys + h),
-                      (unsigned long long)mv.empty_key, (unsigned long long)key);
-        if (prev == (unsigned long long)mv.empty_key) {
-          prows[h] = r;
-          return;
-        }
-      }
-    }
-  }
+  for (int k = 0; k < 6; ++k) v.pad[k] = 0.0;
+  recs[mv.kmode ? h : (size_t)r] = v;
 }
 
 __global__ void k_fill(long long* __restrict__ p, long long v, unsigned n) {
@@ -211,15 +209,15 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
     for (size_t i = 0; i < hk.size() && hk[i] == empty; ++i) ++empty;
   }
   map->empty_key = empty;
-  // capacity: kmode 1 pow2 >= 8m slots in 4-slot buckets, kmode 0 pow2 >= 4m in 8-slot ones
-  int l2 = map->kmode ? 2 : 3;
-  while ((1LL << l2) < (map->kmode ? 8 : 4) * map->m) ++l2;
+  // capacity: pow2 >= 4m slots in 8-slot buckets (load <= 0.25)
+  int l2 = 3;
+  while ((1LL << l2) < 4 * map->m) ++l2;
   map->capacity = 1u << l2;
   map->log2cap = l2;
   const int gfill = (int)std::min<unsigned>((map->capacity + 255) / 256, 148 * 16);
   if (map->kmode) {
-    VG_CUDA(cudaMallocAsync((void**)&map->pkv32, sizeof(uint2) * (size_t)map->capacity, ctx->stream));
-    VG_CUDA(cudaMemsetAsync(map->pkv32, 0xff, sizeof(uint2) * (size_t)map->capacity, ctx->stream));
+    VG_CUDA(cudaMallocAsync((void**)&map->pkeys32, sizeof(unsigned) * (size_t)map->capacity, ctx->stream));
+    VG_CUDA(cudaMemsetAsync(map->pkeys32, 0xff, sizeof(unsigned) * (size_t)map->capacity, ctx->stream));
   } else {
     VG_CUDA(cudaMallocAsync((void**)&map->pkeys, sizeof(long long) * (size_t)map->capacity, ctx->stream));
     VG_CUDA(cudaMallocAsync((void**)&map->prows, sizeof(int) * (size_t)map->capacity, ctx->stream));
@@ -228,10 +226,12 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
     VG_CUDA(cudaGetLastError());
   }
   if (map->m == 0) return 0;
-  VG_CUDA(cudaMallocAsync((void**)&map->recs, sizeof(VoxelRec) * (size_t)map->m, ctx->stream));
+  VG_CUDA(cudaMallocAsync((void**)&map->recs,
+                          sizeof(VoxelRec) * (size_t)(map->kmode ? map->capacity : map->m),
+                          ctx->stream));
   k_hash_insert<<<(int)((map->m + 127) / 128), 128, 0, ctx->stream>>>(
       map->keys, map->means, map->covs, (int)map->m, map->view(), map->pkeys, map->prows,
-      map->pkv32, map->recs);
+      map->pkeys32, map->recs);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
