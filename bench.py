@@ -51,6 +51,15 @@ def parse():
     return ap.parse_args()
 
 
+def traffic_record():
+    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01_traffic.json)."""
+    p = ROOT / "profiles" / "r01_traffic.json"
+    try:
+        return int(json.loads(p.read_text())["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -316,7 +325,7 @@ def run_ours(args):
                     "ms_per_step": statistics.median(e2e_ms)},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic_record(),
                          "kernel": "K4 = k_lookup_items (K4a) + k_accumulate<0> (K4b)",
                          "kernel_ms": statistics.mean(k4_ms),
                          "bytes_per_corr": BYTES_PER_CORR, "peak_kind": peak_kind},
