@@ -839,6 +839,11 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
     const char* e = getenv("VGICP_FUSED_WS");
     return e ? atoi(e) : 0;
   }();
+  static const int use_sg = [] {
+    const char* e = getenv("VGICP_SRCGROUP");  // 1 (default): source-grouped kernel if eligible
+    return e ? atoi(e) : 1;
+  }();
+  if (use_sg && b->num_groups > 0 && kmode != 2) return launch_srcgroup(ctx, b, kmode);
   if (use_ws && kmode != 2) return launch_fused_ws(ctx, b, kmode);
   static const int chunks_env = [] {
     const char* e = getenv("VGICP_CHUNKS");

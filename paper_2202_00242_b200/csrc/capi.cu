@@ -433,6 +433,13 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
                      [&](int64_t a, int64_t b) { return fac[a].cloud < fac[b].cloud; });
   std::vector<ItemDev> items;
   long long npts = 0, hoff = 0;
+  // source groups for the source-grouped kernel (K4s): every source fits in shared memory,
+  // every point is fp32-exact and every map uses 32-bit local keys
+  bool grouped = F > 0;
+  for (int64_t f = 0; f < F && grouped; ++f) {
+    const vg_cloud* c = specs[f].source;
+    grouped = c->n <= srcgroup_max_points() && c->exact32 && specs[f].target->kmode == 1;
+  }
   for (int64_t f : order) {
     const long long n = specs[f].source->n;
     npts += n;
@@ -469,6 +476,43 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     n32 += maps[i]->kmode;
   }
   b->key_mode = n32 == (int)maps.size() ? 1 : (n32 == 0 ? 0 : 2);
+  // groups in order of first appearance of their source in the caller's factor order
+  std::vector<SrcGroup> groups;
+  std::vector<int> group_factors;
+  if (grouped) {
+    std::vector<int> first(clouds.size(), -1), count(clouds.size(), 0);
+    std::vector<int> order_g;
+    for (int64_t f = 0; f < F; ++f) {
+      const int c = fac[f].cloud;
+      if (first[c] < 0) {
+        first[c] = (int)order_g.size();
+        order_g.push_back(c);
+      }
+      ++count[c];
+    }
+    std::vector<int> start(order_g.size() + 1, 0);
+    for (size_t gi = 0; gi < order_g.size(); ++gi) start[gi + 1] = start[gi] + count[order_g[gi]];
+    group_factors.resize(F);
+    std::vector<int> fill(order_g.size(), 0);
+    for (int64_t f = 0; f < F; ++f) {
+      const int gi = first[fac[f].cloud];
+      group_factors[start[gi] + fill[gi]++] = (int)f;
+    }
+    for (size_t gi = 0; gi < order_g.size(); ++gi) {
+      const CloudView& c = cv[order_g[gi]];
+      SrcGroup g;
+      g.a = c.a;
+      g.c0 = c.c0;
+      g.c1 = c.c1;
+      g.c2 = c.c2;
+      g.n = (int)c.n;
+      g.fbegin = start[gi];
+      g.fcount = count[order_g[gi]];
+      g.pad = 0;
+      groups.push_back(g);
+    }
+  }
+  b->num_groups = (int)groups.size();
   std::vector<ItemHdr> hdrs(items.size());
   for (size_t i = 0; i < items.size(); ++i) {
     ItemHdr& h = hdrs[i];
@@ -501,7 +545,11 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
       (rc = h2d(ctx, b->items, items.data(), sizeof(ItemDev) * items.size())) ||
       (rc = h2d(ctx, b->clouds, cv.data(), sizeof(CloudView) * cv.size())) ||
       (rc = h2d(ctx, b->maps, mv.data(), sizeof(MapView) * mv.size())) ||
-      (rc = h2d(ctx, b->hdrs, hdrs.data(), sizeof(ItemHdr) * hdrs.size()))) {
+      (rc = h2d(ctx, b->hdrs, hdrs.data(), sizeof(ItemHdr) * hdrs.size())) ||
+      (rc = dalloc(ctx, &b->groups, groups.size())) ||
+      (rc = dalloc(ctx, &b->group_factors, group_factors.size())) ||
+      (rc = h2d(ctx, b->groups, groups.data(), sizeof(SrcGroup) * groups.size())) ||
+      (rc = h2d(ctx, b->group_factors, group_factors.data(), sizeof(int) * group_factors.size()))) {
     vg_batch_destroy(b);
     return rc;
   }
@@ -531,6 +579,8 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->hit_counts);
   dfree(ctx, b->descs);
   dfree(ctx, b->hdrs);
+  dfree(ctx, b->groups);
+  dfree(ctx, b->group_factors);
   dfree(ctx, b->work_counter);
   dfree(ctx, b->out);
   dfree(ctx, b->poses);

@@ -109,6 +109,9 @@ struct vg_batch {
   vg::AccDesc* descs = nullptr;       // num_items (K4a -> K4b)
   vg::ItemHdr* hdrs = nullptr;        // num_items (fused kernel headers; T refreshed per step)
   int* work_counter = nullptr;        // fused kernel dynamic item counter
+  vg::SrcGroup* groups = nullptr;     // source groups (source-grouped kernel), or null
+  int* group_factors = nullptr;       // factor indices grouped by source
+  int num_groups = 0;                 // > 0 when the batch qualifies for K4s
   long long hit_capacity = 0;
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;
@@ -149,7 +152,9 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                  double* wd, double* partial_cost, long long* partial_inl, int nblocks);
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
 int launch_spread_T(vg_ctx* ctx, vg_batch* b);  // FactorDev.T -> ItemHdr.T (explicit-T mode)
-int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b
+int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b (or K4s)
+int launch_srcgroup(vg_ctx* ctx, vg_batch* b, int kmode);    // K4s
+int srcgroup_max_points();
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);
 int launch_cov(vg_ctx* ctx, const vg_cloud* cloud, const long long* nbrs_dev, int k,
