@@ -87,36 +87,55 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
       pz = a.z;
     }
   };
-  double nx, ny, nz;
-  load_pt(it.begin + lane, nx, ny, nz);
-  for (int base = it.begin; base < it.end; base += 32) {
-    const int i = base + lane;
-    const double px = nx, py = ny, pz = nz;
-    load_pt(i + 32, nx, ny, nz);
+  // transform + key of point i (clamped into the item), probe of its home bucket
+  auto make_q = [&](double px, double py, double pz) {
     // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
     const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
     const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
     const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
-    const Query qy = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                                floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                                floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
-    int slot = -1;  // becomes the reference row of the hit
-    if (i < it.end && mv.m && qy.inside) {
-      unsigned bk = qy.bucket;
-      ProbeGroup pg = probe_load(mv, bk, kmode);
+    return make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                      floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                      floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
+  };
+  // Two-deep software pipeline per lane: the probe of iteration k+1 is in flight while
+  // iteration k's probe is resolved, and the point of iteration k+2 is being loaded.
+  double px, py, pz, nx, ny, nz;
+  load_pt(it.begin + lane, px, py, pz);
+  load_pt(it.begin + 32 + lane, nx, ny, nz);
+  Query q0 = make_q(px, py, pz);
+  bool live0 = it.begin + lane < it.end && mv.m && q0.inside;
+  ProbeGroup g0;
+  if (live0) g0 = probe_load(mv, q0.bucket, kmode);
+  for (int base = it.begin; base < it.end; base += 32) {
+    const int i = base + lane;
+    // issue iteration k+1
+    const Query q1 = make_q(nx, ny, nz);
+    const bool live1 = i + 32 < it.end && mv.m && q1.inside;
+    ProbeGroup g1;
+    if (live1) g1 = probe_load(mv, q1.bucket, kmode);
+    load_pt(i + 64, nx, ny, nz);
+    // resolve iteration k
+    int slot = -1;
+    if (live0) {
+      unsigned bk = q0.bucket;
       int r;
-      while ((r = probe_scan(mv, pg, bk, qy, slot, kmode)) < 0) {
+      while ((r = probe_scan(mv, g0, bk, q0, slot, kmode)) < 0) {
         bk = next_bucket(bk, mv);
-        pg = probe_load(mv, bk, kmode);
+        g0 = probe_load(mv, bk, kmode);
       }
       if (r == 1) slot = rec_index(mv, slot, kmode);
+      else slot = -1;
       // warm L2 with the record line K4b will gather for this hit
       if (r == 1 && prefetch_recs)
         asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(mv.recs + slot));
     }
+    // misses contribute nothing (registration.py:150-156)
     const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
     if (slot >= 0) out[cnt + __popc(m & lt_mask)] = make_int2(i, slot);
     cnt += __popc(m);
+    q0 = q1;
+    live0 = live1;
+    g0 = g1;
   }
   if (lane == 0) {
     counts[w] = cnt;
@@ -730,7 +749,15 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
   const ItemDev* it = b->items + off;
   int* hc = b->hit_counts + off;
   AccDesc* dd = b->descs + off;
-  if (b->key_mode == 1)
+  static const int lblocks = [] {
+    const char* e = getenv("VGICP_LOOKUP_BLOCKS");
+    return e ? atoi(e) : 3;
+  }();
+  if (b->key_mode == 1 && lblocks == 2)
+    k_lookup_items<1, 2><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                           b->maps, b->hits, hc, p2, dd,
+                                                           prefetch);
+  else if (b->key_mode == 1)
     k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                            b->maps, b->hits, hc, p2, dd,
                                                            prefetch);
@@ -840,8 +867,10 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
     return e ? atoi(e) : 0;
   }();
   static const int use_sg = [] {
-    const char* e = getenv("VGICP_SRCGROUP");  // 1 (default): source-grouped kernel if eligible
-    return e ? atoi(e) : 1;
+    // 1: source-grouped warp-specialised kernel for eligible batches (experimental; measured
+    // 2.3x slower than K4a + K4b on config 5)
+    const char* e = getenv("VGICP_SRCGROUP");
+    return e ? atoi(e) : 0;
   }();
   if (use_sg && b->num_groups > 0 && kmode != 2) return launch_srcgroup(ctx, b, kmode);
   if (use_ws && kmode != 2) return launch_fused_ws(ctx, b, kmode);

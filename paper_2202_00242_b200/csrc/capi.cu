@@ -476,39 +476,65 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     n32 += maps[i]->kmode;
   }
   b->key_mode = n32 == (int)maps.size() ? 1 : (n32 == 0 ? 0 : 2);
-  // groups in order of first appearance of their source in the caller's factor order
+  // Source groups, ordered for L2 locality: a breadth-first walk of the bipartite graph
+  // (source -> its target maps -> the other sources of those maps), the Cuthill-McKee idea,
+  // so sources processed concurrently by different SMs share most of their target maps.
   std::vector<SrcGroup> groups;
   std::vector<int> group_factors;
   if (grouped) {
-    std::vector<int> first(clouds.size(), -1), count(clouds.size(), 0);
+    const int nc = (int)clouds.size(), nm = (int)maps.size();
+    std::vector<std::vector<int>> fac_of_cloud(nc), clouds_of_map(nm);
+    for (int64_t f = 0; f < F; ++f) {
+      fac_of_cloud[fac[f].cloud].push_back((int)f);
+      clouds_of_map[fac[f].map].push_back(fac[f].cloud);
+    }
     std::vector<int> order_g;
-    for (int64_t f = 0; f < F; ++f) {
-      const int c = fac[f].cloud;
-      if (first[c] < 0) {
-        first[c] = (int)order_g.size();
+    std::vector<char> seen_c(nc, 0), seen_m(nm, 0);
+    for (int64_t f0 = 0; f0 < F; ++f0) {  // every connected component, in caller order
+      const int c0 = fac[f0].cloud;
+      if (seen_c[c0]) continue;
+      std::vector<int> queue{c0};
+      seen_c[c0] = 1;
+      for (size_t qi = 0; qi < queue.size(); ++qi) {
+        const int c = queue[qi];
         order_g.push_back(c);
+        for (int f : fac_of_cloud[c]) {
+          const int m = fac[f].map;
+          if (seen_m[m]) continue;
+          seen_m[m] = 1;
+          for (int c2 : clouds_of_map[m])
+            if (!seen_c[c2]) {
+              seen_c[c2] = 1;
+              queue.push_back(c2);
+            }
+        }
       }
-      ++count[c];
     }
-    std::vector<int> start(order_g.size() + 1, 0);
-    for (size_t gi = 0; gi < order_g.size(); ++gi) start[gi + 1] = start[gi] + count[order_g[gi]];
-    group_factors.resize(F);
-    std::vector<int> fill(order_g.size(), 0);
-    for (int64_t f = 0; f < F; ++f) {
-      const int gi = first[fac[f].cloud];
-      group_factors[start[gi] + fill[gi]++] = (int)f;
+    static const int bfs = [] {
+      const char* e = getenv("VGICP_GROUP_BFS");  // 0: caller order of first appearance
+      return e ? atoi(e) : 1;
+    }();
+    if (!bfs) {
+      order_g.clear();
+      std::vector<char> seen(nc, 0);
+      for (int64_t f = 0; f < F; ++f)
+        if (!seen[fac[f].cloud]) {
+          seen[fac[f].cloud] = 1;
+          order_g.push_back(fac[f].cloud);
+        }
     }
-    for (size_t gi = 0; gi < order_g.size(); ++gi) {
-      const CloudView& c = cv[order_g[gi]];
+    for (int c : order_g) {
       SrcGroup g;
-      g.a = c.a;
-      g.c0 = c.c0;
-      g.c1 = c.c1;
-      g.c2 = c.c2;
-      g.n = (int)c.n;
-      g.fbegin = start[gi];
-      g.fcount = count[order_g[gi]];
+      const CloudView& cvw = cv[c];
+      g.a = cvw.a;
+      g.c0 = cvw.c0;
+      g.c1 = cvw.c1;
+      g.c2 = cvw.c2;
+      g.n = (int)cvw.n;
+      g.fbegin = (int)group_factors.size();
+      g.fcount = (int)fac_of_cloud[c].size();
       g.pad = 0;
+      for (int f : fac_of_cloud[c]) group_factors.push_back(f);
       groups.push_back(g);
     }
   }
