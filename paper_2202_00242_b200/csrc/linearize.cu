@@ -151,12 +151,10 @@ __device__ __forceinline__ void store_sym6(double* out, const double* A, const d
     }
 }
 
-__global__ void k_finalize(const FactorDev* __restrict__ factors, int F,
-                           const double* __restrict__ partials, int mode,
-                           double* __restrict__ out) {
-  const int fi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (fi >= F) return;
-  const FactorDev& f = factors[fi];
+// one factor; LINEARIZE records go to `o92` (shared memory staging), others straight to out
+__device__ __forceinline__ void finalize_one(const FactorDev& f, int fi,
+                                             const double* __restrict__ partials, int mode,
+                                             double* __restrict__ out, double* o92) {
   if (mode == 1 || mode == 3) {
     double c = 0.0, n = 0.0;
     for (int it = 0; it < f.item_count; ++it) {
@@ -181,7 +179,7 @@ __global__ void k_finalize(const FactorDev* __restrict__ factors, int F,
     for (int k = 0; k < 29; ++k) o[k] = s[k];
     return;
   }
-  double* o = out + (size_t)fi * 92;
+  double* o = o92;
   const double cost = s[27], inliers = s[28];
   if (inliers < (double)f.min_inliers) {  // DegenerateConstraint -> zero blocks
     for (int k = 0; k < 90; ++k) o[k] = 0.0;
@@ -259,6 +257,31 @@ __global__ void k_finalize(const FactorDev* __restrict__ factors, int F,
       else v = RtS[3 * (r - 3) + (c - 3)];
       hij[6 * r + c] = -2.0 * v;
     }
+}
+
+constexpr int kFinBlock = 64;
+constexpr int kFinStride = 93;  // odd stride: conflict-free staging rows
+
+// K5: per-factor fixed-order sum of item partials + fp64 adjoint expansion.  LINEARIZE
+// records (92 doubles) are staged in shared memory and written out contiguously.
+__global__ void __launch_bounds__(kFinBlock)
+    k_finalize(const FactorDev* __restrict__ factors, int F, const double* __restrict__ partials,
+               int mode, double* __restrict__ out) {
+  __shared__ double sh[kFinBlock * kFinStride];
+  const int f0 = blockIdx.x * kFinBlock;
+  const int fi = f0 + threadIdx.x;
+  if (mode != 0) {
+    if (fi < F) finalize_one(factors[fi], fi, partials, mode, out, nullptr);
+    return;
+  }
+  if (fi < F) finalize_one(factors[fi], fi, partials, mode, out, sh + threadIdx.x * kFinStride);
+  __syncthreads();
+  const int nf = min(kFinBlock, F - f0);
+  double* dst = out + (size_t)f0 * 92;
+  for (int k = threadIdx.x; k < nf * 92; k += kFinBlock) {
+    const int r = k / 92;
+    dst[k] = sh[r * kFinStride + (k - r * 92)];
+  }
 }
 
 // ---- pose composition on the device (geometry.py:47-144,231-237) ------------------------
@@ -483,8 +506,8 @@ int launch_spread_T(vg_ctx* ctx, vg_batch* b) {
 
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev) {
   if (b->F == 0) return 0;
-  k_finalize<<<grid_for(b->F, 128, 1 << 30), 128, 0, ctx->stream>>>(b->factors, (int)b->F,
-                                                                    b->partials, mode, out_dev);
+  k_finalize<<<(int)((b->F + kFinBlock - 1) / kFinBlock), kFinBlock, 0, ctx->stream>>>(
+      b->factors, (int)b->F, b->partials, mode, out_dev);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
