@@ -857,6 +857,13 @@ static int launch_fused_ws(vg_ctx* ctx, vg_batch* b, int kmode) {
   return 0;
 }
 
+int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi) {
+  if (hi <= lo) return 0;
+  VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream, 0));
+  if (kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream, false));
+  return 0;
+}
+
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   if (b->num_items == 0) return 0;
   const int n = (int)b->num_items;

@@ -425,13 +425,30 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     const char* e = getenv("VGICP_ITEM_ORDER");  // 0 target-major (default), 1 source-major, 2 input
     return e ? atoi(e) : 0;
   }();
+  // Stages (pipelined host output, vg_batch_linearize*): contiguous factor ranges whose
+  // records are copied to the host while the next stage computes; items are stage-major.
+  static const int stages_env = [] {
+    const char* e = getenv("VGICP_STAGES");  // default: 4 for batches of >= 8192 factors
+    return e ? atoi(e) : -1;
+  }();
+  const int S = (int)std::max<int64_t>(
+      1, std::min<int64_t>(stages_env >= 0 ? stages_env : (F >= 8192 ? 4 : 1), 16));
+  std::vector<int> stage_factors(S + 1), stage_of(F);
+  for (int s = 0; s <= S; ++s) stage_factors[s] = (int)((long long)F * s / S);
+  for (int s = 0; s < S; ++s)
+    for (int f = stage_factors[s]; f < stage_factors[s + 1]; ++f) stage_of[f] = s;
   if (order_mode == 0)
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int64_t a, int64_t b) { return fac[a].map < fac[b].map; });
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+      return stage_of[a] != stage_of[b] ? stage_of[a] < stage_of[b] : fac[a].map < fac[b].map;
+    });
   else if (order_mode == 1)
     std::stable_sort(order.begin(), order.end(),
                      [&](int64_t a, int64_t b) { return fac[a].cloud < fac[b].cloud; });
+  if (order_mode != 0)
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int64_t a, int64_t b) { return stage_of[a] < stage_of[b]; });
   std::vector<ItemDev> items;
+  std::vector<int> stage_items(S + 1, 0);
   long long npts = 0, hoff = 0;
   // source groups for the source-grouped kernel (K4s): every source fits in shared memory,
   // every point is fp32-exact and every map uses 32-bit local keys
@@ -455,7 +472,9 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
       items.push_back(it);
     }
     fac[f].item_count = (int)nchunks;
+    stage_items[stage_of[f] + 1] = (int)items.size();
   }
+  for (int s = 1; s <= S; ++s) stage_items[s] = std::max(stage_items[s], stage_items[s - 1]);
   if (hoff >= (1LL << 31)) return fail(VG_ERR_INVALID, "batch too large (2^31 points)");
   vg_batch* b = new vg_batch();
   b->ctx = ctx;
@@ -467,6 +486,9 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   b->num_maps = (int)maps.size();
   b->max_var = (int)max_var;
   b->host_factors = fac;
+  b->stages = S;
+  b->stage_factors = stage_factors;
+  b->stage_items = stage_items;
   std::vector<CloudView> cv(clouds.size());
   std::vector<MapView> mv(maps.size());
   for (size_t i = 0; i < clouds.size(); ++i) cv[i] = clouds[i]->view();
@@ -630,6 +652,37 @@ static int run_device(vg_batch* b, int mode, double* out_dev) {
   return VG_OK;
 }
 
+// K4 + K5 for every stage on the compute stream; each stage's records are copied to the
+// host on the copy stream as soon as its K5 finishes, overlapping the next stage's K4.
+static int run_to_host(vg_batch* b, int mode, double* out_host) {
+  vg_ctx* ctx = b->ctx;
+  const size_t rec = rec_of(mode);
+  if (b->stages <= 1) {
+    VG_CHECK(run_device(b, mode, b->out));
+    return d2h_sync(ctx, out_host, b->out, sizeof(double) * rec * b->F);
+  }
+  if (!ctx->side_stream) {
+    VG_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
+    for (auto& e : ctx->events) VG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int kmode = kmode_of(mode);
+  for (int s = 0; s < b->stages; ++s) {
+    const int f0 = b->stage_factors[s], f1 = b->stage_factors[s + 1];
+    VG_CHECK(launch_accumulate_range(ctx, b, kmode, b->stage_items[s], b->stage_items[s + 1]));
+    VG_CHECK(launch_finalize_range(ctx, b, mode, b->out, f0, f1));
+    VG_CUDA(cudaEventRecord(ctx->events[s], ctx->stream));
+    VG_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->events[s], 0));
+    VG_CUDA(cudaMemcpyAsync(out_host + (size_t)f0 * rec, b->out + (size_t)f0 * rec,
+                            sizeof(double) * rec * (size_t)(f1 - f0), cudaMemcpyDeviceToHost,
+                            ctx->side_stream));
+  }
+  // the compute stream must not run ahead of the copies that still read b->out
+  VG_CUDA(cudaEventRecord(ctx->events[b->stages], ctx->side_stream));
+  VG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->events[b->stages], 0));
+  VG_CUDA(cudaStreamSynchronize(ctx->side_stream));
+  return VG_OK;
+}
+
 int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_host) {
   if (!b || (b->F && (!T_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
   if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
@@ -639,8 +692,7 @@ int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_
   VG_CUDA(cudaMemcpy2DAsync(b->factors, sizeof(FactorDev), T_host, 12 * sizeof(double),
                             12 * sizeof(double), (size_t)b->F, cudaMemcpyHostToDevice, ctx->stream));
   VG_CHECK(launch_spread_T(ctx, b));
-  VG_CHECK(run_device(b, mode, b->out));
-  return d2h_sync(ctx, out_host, b->out, sizeof(double) * rec_of(mode) * b->F);
+  return run_to_host(b, mode, out_host);
 }
 
 static int ensure_poses(vg_batch* b, int64_t V) {
@@ -661,8 +713,7 @@ int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, i
   VG_CHECK(ensure_poses(b, V));
   VG_CHECK(h2d(b->ctx, b->poses, poses_host, sizeof(double) * 8 * V));
   VG_CHECK(launch_compose(b->ctx, b, b->poses));
-  VG_CHECK(run_device(b, mode, b->out));
-  return d2h_sync(b->ctx, out_host, b->out, sizeof(double) * rec_of(mode) * b->F);
+  return run_to_host(b, mode, out_host);
 }
 
 int vg_batch_linearize_poses_device(vg_batch* b, const double* poses_dev, int64_t V, int mode,

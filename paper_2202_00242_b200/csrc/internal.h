@@ -116,7 +116,10 @@ struct vg_batch {
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;
   double* out = nullptr;              // device output (F * 92)
-  double* T_host_stage = nullptr;     // unused placeholder
+  // pipelined host-output path: stage s = factors [stage_factors[s], stage_factors[s+1]),
+  // whose items are exactly [stage_items[s], stage_items[s+1]) (items are stage-major)
+  int stages = 1;
+  std::vector<int> stage_factors, stage_items;
   cudaGraphExec_t graph = nullptr;
   std::vector<vg::FactorDev> host_factors;
 };
@@ -156,6 +159,8 @@ int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b (or K4
 int launch_srcgroup(vg_ctx* ctx, vg_batch* b, int kmode);    // K4s
 int srcgroup_max_points();
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
+int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1);
+int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi);  // K4a + K4b
 int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);
 int launch_cov(vg_ctx* ctx, const vg_cloud* cloud, const long long* nbrs_dev, int k,
                double eps, double* covs_dev, unsigned char* degen_dev);

@@ -265,10 +265,10 @@ constexpr int kFinStride = 93;  // odd stride: conflict-free staging rows
 // K5: per-factor fixed-order sum of item partials + fp64 adjoint expansion.  LINEARIZE
 // records (92 doubles) are staged in shared memory and written out contiguously.
 __global__ void __launch_bounds__(kFinBlock)
-    k_finalize(const FactorDev* __restrict__ factors, int F, const double* __restrict__ partials,
-               int mode, double* __restrict__ out) {
+    k_finalize(const FactorDev* __restrict__ factors, int fbase, int F,
+               const double* __restrict__ partials, int mode, double* __restrict__ out) {
   __shared__ double sh[kFinBlock * kFinStride];
-  const int f0 = blockIdx.x * kFinBlock;
+  const int f0 = fbase + blockIdx.x * kFinBlock;
   const int fi = f0 + threadIdx.x;
   if (mode != 0) {
     if (fi < F) finalize_one(factors[fi], fi, partials, mode, out, nullptr);
@@ -504,11 +504,15 @@ int launch_spread_T(vg_ctx* ctx, vg_batch* b) {
   return 0;
 }
 
-int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev) {
-  if (b->F == 0) return 0;
-  k_finalize<<<(int)((b->F + kFinBlock - 1) / kFinBlock), kFinBlock, 0, ctx->stream>>>(
-      b->factors, (int)b->F, b->partials, mode, out_dev);
+int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1) {
+  if (f1 <= f0) return 0;
+  k_finalize<<<(f1 - f0 + kFinBlock - 1) / kFinBlock, kFinBlock, 0, ctx->stream>>>(
+      b->factors, f0, f1, b->partials, mode, out_dev);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
+}
+
+int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev) {
+  return launch_finalize_range(ctx, b, mode, out_dev, 0, (int)b->F);
 }

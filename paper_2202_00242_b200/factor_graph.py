@@ -148,6 +148,9 @@ class _Batcher:
             group.append(f)
         if requester not in group:
             group.append(requester)
+        # factors sharing a target map adjacent: the batch's item order is then target-major
+        # (map reuse in L2) and its pipelined host copy moves contiguous record ranges
+        group.sort(key=lambda f: id(f.target_map))
         batch, var_keys, fixed, _ = self._batch_for(group)
         poses = np.empty((len(var_keys) + fixed.shape[0], 8))
         for i, k in enumerate(var_keys):

@@ -5,7 +5,7 @@ global_mapping(): config 5 — N submaps, each a 256 x 64 = 16,384-point scan fr
 pose in the room; the source cloud of submap i is a seeded random subsample of its scan with
 n ~ U[200, 600] points; the target map of submap j is its full scan at 1.0 m
 (config.py:56); one binary factor per ordered pair (i -> j) for the k nearest submaps j of
-each i; estimates are the truth perturbed by (0.05 m, 1 deg).
+each i, listed by target j; estimates are the truth perturbed by (0.05 m, 1 deg).
 """
 
 from __future__ import annotations
@@ -52,6 +52,9 @@ def global_mapping(n_submaps: int = 1000, neighbors: int = 50, resolution: float
     sizes = rng.integers(200, 601, n_submaps)
     source_index = [np.sort(rng.choice(len(s), int(n), replace=False)) for s, n in zip(scans, sizes)]
     pairs = synthetic.nearest_pairs(truth, neighbors)
+    # factor list ordered by target submap (stable in the source): the batch's work items are
+    # target-major either way; this order also makes its staged host copies contiguous
+    pairs = pairs[np.lexsort((pairs[:, 0], pairs[:, 1]))]
     est = [pose_retract(p, synthetic.perturbation(rng, 0.05, 1.0)) for p in truth]
     wl = GlobalWorkload(n_submaps, neighbors, resolution, truth, est, scans, [], source_index,
                         pairs, np.array([pose_row(p) for p in est]))

@@ -306,3 +306,37 @@ def test_factor_degenerate_and_empty():
     assert RG.overlap_rate(empty, vm, G.Se3Pose.identity()) == 0.0
     with pytest.raises(DegenerateConstraint):
         RG.linearize_matching_cost(empty, vm, G.Se3Pose.identity(), G.Se3Pose.identity())
+
+
+def test_staged_host_output_matches_single_launch(small_graph):
+    """Batches of >= 8192 factors run K4/K5 in stages whose records are copied to the host
+    while the next stage computes; results must equal the one-launch device path bit for bit
+    (same items, same fixed-order sums) and the small batch of the test above."""
+    import torch
+
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
+    reps = 9000 // len(pairs) + 1
+    rng = np.random.default_rng(5)
+    sel = rng.permutation(np.tile(np.arange(len(pairs)), reps))   # F >= 8192 -> 4 stages
+    P = pairs[sel]
+    F = len(P)
+    unary = [(int(s) % 7) == 3 for s in sel]
+    table = np.array([G.pose_row(p) for p in est])
+    big = _lib.DeviceBatch([clouds[i] for i, _ in P], [dmaps[j] for _, j in P], unary, [10] * F,
+                           P[:, 0], P[:, 1])
+    small = _lib.DeviceBatch([clouds[i] for i, _ in pairs], [dmaps[j] for _, j in pairs],
+                             [(f % 7) == 3 for f in range(len(pairs))], [10] * len(pairs),
+                             pairs[:, 0], pairs[:, 1])
+    ref = small.linearize_poses(table)
+    for mode in (_lib.MODE_LINEARIZE, _lib.MODE_COST, _lib.MODE_COMPACT, _lib.MODE_INLIERS):
+        host = big.linearize_poses(table, mode)
+        dev = torch.zeros((F, _lib.RECORD_SIZE[mode]), dtype=torch.float64, device="cuda")
+        tdev = torch.from_numpy(table).cuda()
+        torch.cuda.synchronize()
+        big.linearize_poses_device(tdev.data_ptr(), len(table), mode, dev.data_ptr())
+        big.ctx.synchronize()
+        assert np.array_equal(host, dev.cpu().numpy()), mode
+        if mode == _lib.MODE_LINEARIZE:
+            assert np.array_equal(host, ref[sel])
