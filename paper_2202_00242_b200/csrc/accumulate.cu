@@ -30,7 +30,8 @@ namespace vg {
 constexpr int kLookupWarps = 8;
 
 // KM: 1 = every map of the batch uses 32-bit local keys, 0 = all int64, 2 = mixed (runtime)
-template <int KM, int kMinBlocks>
+// P2: every map of the batch has a power-of-two resolution (x * (1/res) is exact)
+template <int KM, int kMinBlocks, int P2 = 0>
 __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     k_lookup_items(const ItemDev* __restrict__ items, int n_items,
                    const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
@@ -93,9 +94,10 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
     const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
     const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
-    return make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                      floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                      floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
+    const double fx = P2 ? floor(x * mv.inv_res) : floor_div(x, mv.res, mv.inv_res, mv.pow2);
+    const double fy = P2 ? floor(y * mv.inv_res) : floor_div(y, mv.res, mv.inv_res, mv.pow2);
+    const double fz = P2 ? floor(z * mv.inv_res) : floor_div(z, mv.res, mv.inv_res, mv.pow2);
+    return KM == 1 ? make_query_local(mv, fx, fy, fz) : make_query(mv, fx, fy, fz, kmode);
   };
   // Two-deep software pipeline per lane: the probe of iteration k+1 is in flight while
   // iteration k's probe is resolved, and the point of iteration k+2 is being loaded.
@@ -145,6 +147,109 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     }
   }
   if (descs && lane == 0) descs[w].n = cnt;
+}
+
+// K4a, batched variant: each lane resolves U points per iteration (U independent point loads,
+// then U independent bucket probes in flight), sub-rounds compacted in point order.
+template <int KM, int U, int kMinBlocks>
+__global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
+    k_lookup_batch(const ItemDev* __restrict__ items, int n_items,
+                   const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
+                   const MapView* __restrict__ maps, int2* __restrict__ hits,
+                   int* __restrict__ counts, double* __restrict__ partials2,
+                   AccDesc* __restrict__ descs) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
+  if (w >= n_items) return;
+  const ItemDev it = items[w];
+  const FactorDev* f = factors + it.factor;
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(f->T + k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = __ldg(f->T + 9 + k);
+  const CloudView cv = clouds[__ldg(&f->cloud)];
+  const MapView mv = maps[__ldg(&f->map)];
+  const int kmode = KM == 2 ? mv.kmode : KM;
+  if (descs) {
+    AccDesc& d = descs[w];
+    double tv = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+      if (lane == k) tv = R[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      if (lane == 9 + k) tv = t[k];
+    if (lane < 12) d.T[lane] = tv;
+    else if (lane == 12) d.a = cv.a;
+    else if (lane == 13) d.xyz64 = cv.xyz64;
+    else if (lane == 14) d.c0 = cv.c0;
+    else if (lane == 15) d.c1 = cv.c1;
+    else if (lane == 16) d.c2 = cv.c2;
+    else if (lane == 17) d.recs = mv.recs;
+    else if (lane == 18) d.hoff = it.hoff;
+  }
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int2* out = hits + it.hoff;
+  int cnt = 0;
+  const int last = it.end - 1;
+  for (int base = it.begin; base < it.end; base += 32 * U) {
+    double px[U], py[U], pz[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int ic = min(base + 32 * u + lane, last);
+      if (cv.xyz64) {
+        px[u] = __ldg(cv.xyz64 + 3 * (size_t)ic);
+        py[u] = __ldg(cv.xyz64 + 3 * (size_t)ic + 1);
+        pz[u] = __ldg(cv.xyz64 + 3 * (size_t)ic + 2);
+      } else {
+        const float4 a = __ldg(cv.a + ic);
+        px[u] = a.x;
+        py[u] = a.y;
+        pz[u] = a.z;
+      }
+    }
+    Query q[U];
+    bool live[U];
+    ProbeGroup g[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
+      const double x = fma(R[0], px[u], fma(R[1], py[u], R[2] * pz[u])) + t[0];
+      const double y = fma(R[3], px[u], fma(R[4], py[u], R[5] * pz[u])) + t[1];
+      const double z = fma(R[6], px[u], fma(R[7], py[u], R[8] * pz[u])) + t[2];
+      q[u] = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
+                        floor_div(y, mv.res, mv.inv_res, mv.pow2),
+                        floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
+      live[u] = base + 32 * u + lane < it.end && mv.m && q[u].inside;
+      if (live[u]) g[u] = probe_load(mv, q[u].bucket, kmode);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int slot = -1;
+      if (live[u]) {
+        unsigned bk = q[u].bucket;
+        int r;
+        while ((r = probe_scan(mv, g[u], bk, q[u], slot, kmode)) < 0) {
+          bk = next_bucket(bk, mv);
+          g[u] = probe_load(mv, bk, kmode);
+        }
+        slot = r == 1 ? rec_index(mv, slot, kmode) : -1;
+      }
+      // misses contribute nothing (registration.py:150-156)
+      const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
+      if (slot >= 0) out[cnt + __popc(m & lt_mask)] = make_int2(base + 32 * u + lane, slot);
+      cnt += __popc(m);
+    }
+  }
+  if (lane == 0) {
+    counts[w] = cnt;
+    if (partials2) {
+      partials2[2 * (size_t)w] = 0.0;
+      partials2[2 * (size_t)w + 1] = (double)cnt;
+    }
+    if (descs) descs[w].n = cnt;
+  }
 }
 
 // ---- K4b ------------------------------------------------------------------------------------
@@ -353,9 +458,13 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   }
   // hit entries are prefetched one iteration ahead of their gather; the loads are
   // unconditional (index clamped) so their first use is the next iteration's gather
-  int2 nxt[ILP];
+  // two iterations of lead: the entries of round r + kAhead + ILP are loaded at iteration r - ILP
+  int2 nxt[ILP], nxt2[ILP];
 #pragma unroll
-  for (int u = 0; u < ILP; ++u) nxt[u] = __ldg(hl + min((kAhead + u) * 32 + lane, klast));
+  for (int u = 0; u < ILP; ++u) {
+    nxt[u] = __ldg(hl + min((kAhead + u) * 32 + lane, klast));
+    nxt2[u] = __ldg(hl + min((kAhead + ILP + u) * 32 + lane, klast));
+  }
   for (int r = 0; r < rounds; r += ILP) {
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
@@ -363,8 +472,10 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
       issue_round(cv, mv, sm, ri, nxt[u], dbg == 1 ? 0 : (ILP > 1 ? 32 : n - ri * 32), lane);
     }
 #pragma unroll
-    for (int u = 0; u < ILP; ++u)
-      nxt[u] = __ldg(hl + min((r + ILP + kAhead + u) * 32 + lane, klast));
+    for (int u = 0; u < ILP; ++u) {
+      nxt[u] = nxt2[u];
+      nxt2[u] = __ldg(hl + min((r + 2 * ILP + kAhead + u) * 32 + lane, klast));
+    }
     cp_async_wait<kAhead>();
     __syncwarp();
     if (dbg != 2) {
@@ -753,7 +864,35 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
     const char* e = getenv("VGICP_LOOKUP_BLOCKS");
     return e ? atoi(e) : 3;
   }();
-  if (b->key_mode == 1 && lblocks == 2)
+  static const int lu = [] {
+    const char* e = getenv("VGICP_LOOKUP_U");  // 0: two-deep pipelined K4a; 2/4: batched
+    return e ? atoi(e) : 0;
+  }();
+  if (b->key_mode == 1 && lu > 0) {
+    if (lu == 2 && lblocks == 4)
+      k_lookup_batch<1, 2, 4><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                                b->maps, b->hits, hc, p2, dd);
+    else if (lu == 2)
+      k_lookup_batch<1, 2, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                                b->maps, b->hits, hc, p2, dd);
+    else if (lu == 4 && lblocks == 2)
+      k_lookup_batch<1, 4, 2><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                                b->maps, b->hits, hc, p2, dd);
+    else if (lu == 4)
+      k_lookup_batch<1, 4, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                                b->maps, b->hits, hc, p2, dd);
+    else
+      k_lookup_batch<1, 8, 2><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                                b->maps, b->hits, hc, p2, dd);
+  } else if (b->key_mode == 1 && b->all_pow2 && lblocks == 4)
+    k_lookup_items<1, 4, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                              b->maps, b->hits, hc, p2, dd,
+                                                              prefetch);
+  else if (b->key_mode == 1 && b->all_pow2 && lblocks == 3)
+    k_lookup_items<1, 3, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+                                                              b->maps, b->hits, hc, p2, dd,
+                                                              prefetch);
+  else if (b->key_mode == 1 && lblocks == 2)
     k_lookup_items<1, 2><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                            b->maps, b->hits, hc, p2, dd,
                                                            prefetch);

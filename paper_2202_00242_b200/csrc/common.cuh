@@ -208,6 +208,25 @@ __device__ __forceinline__ Query make_query(const MapView& mv, double fx, double
   return q;
 }
 
+// kmode 1 fast path: for |floor| < 2^20 the reference's pack/unpack round trip is the
+// identity, so the local key comes straight from the floors; otherwise defer to make_query
+// (which reproduces the reference's aliasing of out-of-range indices).
+__device__ __forceinline__ Query make_query_local(const MapView& mv, double fx, double fy,
+                                                  double fz) {
+  if (fmax(fabs(fx), fmax(fabs(fy), fabs(fz))) < 1048576.0) {
+    Query q;
+    q.key = 0;
+    const unsigned lx = (unsigned)(__double2int_rz(fx) - mv.bx);
+    const unsigned ly = (unsigned)(__double2int_rz(fy) - mv.by);
+    const unsigned lz = (unsigned)(__double2int_rz(fz) - mv.bz);
+    q.inside = lx < (unsigned)mv.ex && ly < (unsigned)mv.ey && lz < (unsigned)mv.ez;
+    q.k32 = lx | (ly << 11) | (lz << 22);
+    q.bucket = (q.k32 * 0x9E3779B9u) >> mv.shift;
+    return q;
+  }
+  return make_query(mv, fx, fy, fz, 1);
+}
+
 __device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned bucket, int kmode) {
   ProbeGroup g;
   if (kmode) {
