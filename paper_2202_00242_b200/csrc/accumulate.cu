@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     k_accumulate(const AccDesc* __restrict__ descs, int n_items, const int2* __restrict__ hits,
                  double* __restrict__ partials, int dbg) {
   static_assert(kStages >= 2 * ILP || (ILP == 1 && kStages >= 2), "stage reuse hazard");
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int w = blockIdx.x * kAccWarps + wib;
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 #pragma unroll
   for (int r = 0; r < kAhead; ++r) {
     const int k = r * 32 + lane;
-    issue_round(cv, mv, sm, r, hl[min(k, klast)], dbg == 1 ? 0 : (ILP > 1 ? 32 : n - r * 32),
+    issue_round(cv, mv, sm, r, hl[min(k, klast)], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - r * 32),
                 lane);
   }
   // hit entries are prefetched one iteration ahead of their gather; the loads are
@@ -469,7 +470,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
       const int ri = r + kAhead + u;
-      issue_round(cv, mv, sm, ri, nxt[u], dbg == 1 ? 0 : (ILP > 1 ? 32 : n - ri * 32), lane);
+      issue_round(cv, mv, sm, ri, nxt[u], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - ri * 32), lane);
     }
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     }
     cp_async_wait<kAhead>();
     __syncwarp();
-    if (dbg != 2) {
+    if (!(dbg & 2)) {
       if (ILP == 1) {  // branch over padding lanes
         if (r * 32 + lane < n) hit_math<MODE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
       } else {  // branch-free so the ILP rounds interleave; padding lanes replay valid data
@@ -514,6 +515,170 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 }
 
 
+// ---- K4b, persistent form ---------------------------------------------------------------------
+// Same per-round pipeline and math as k_accumulate, but each warp loops over items claimed
+// from a counter, and the NEXT item's descriptor (160 B) and hit list (<= 4 KB) are brought
+// into shared memory by TMA bulk copies (cp.async.bulk, mbarrier completion) while the
+// current item computes.  This removes the two dependent global latencies of every item's
+// prologue (descriptor, then hit entries) and the per-round hit-entry loads from the loop.
+// Only the first kPreHits entries are staged (3 rounds): later rounds' entries are loaded
+// from global two rounds ahead.  Staging whole hit lists would take the shared memory the
+// L1 needs for the lane-own point/covariance gathers (measured: +20% K4b time).
+constexpr int kPreHits = 96;
+template <int kStages>
+struct PersistSmem {
+  AccSmem<kStages> acc;
+  int2 hit[2][kPreHits];
+  AccDesc desc[2];
+  unsigned long long bar[2];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "BW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra BW_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int MODE, int kStages, int kMinBlocks>
+__global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
+    k_acc_persist(const ItemDev* __restrict__ items, const AccDesc* __restrict__ descs,
+                  int n_items, const int2* __restrict__ hits, double* __restrict__ partials,
+                  int* __restrict__ counter, int dbg) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  PersistSmem<kStages>& ps = reinterpret_cast<PersistSmem<kStages>*>(smem_raw)[wib];
+  AccSmem<kStages>& sm = ps.acc;
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ps.bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ps.bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  // lane 0 claims items and issues the bulk copies of item `it` into buffer `b`
+  auto prefetch = [&](int it, const ItemDev& d, int b) {
+    const unsigned hb = (unsigned)min(((d.end - d.begin) + 1) & ~1, kPreHits) * 8u;
+    bar_expect_tx(&ps.bar[b], (unsigned)sizeof(AccDesc) + hb);
+    bulk_g2s(&ps.desc[b], descs + it, (unsigned)sizeof(AccDesc), &ps.bar[b]);
+    if (hb) bulk_g2s(&ps.hit[b][0], hits + d.hoff, hb, &ps.bar[b]);
+  };
+  // items are dealt round-robin (w, w + G, ...): a shared claim counter serialises ~60k
+  // same-address atomics at one L2 slice
+  const int G = gridDim.x * kAccWarps;
+  int next_claim = blockIdx.x * kAccWarps + wib;
+  auto claim = [&]() {
+    const int v = next_claim;
+    next_claim += G;
+    return v;
+  };
+  (void)counter;
+  int cur = claim();
+  if (cur >= n_items) return;
+  if (lane == 0) prefetch(cur, items[cur], 0);
+  int nxt = claim();
+  ItemDev inxt = items[min(nxt, n_items - 1)];
+  unsigned phase = 0;  // bit b: parity of buffer b's next completion
+  int b = 0;
+  for (;;) {
+    if (lane == 0 && nxt < n_items) prefetch(nxt, inxt, b ^ 1);
+    const int nn = nxt < n_items ? claim() : n_items;
+    const ItemDev inn = items[min(nn, n_items - 1)];
+    bar_wait(&ps.bar[b], (phase >> b) & 1u);
+    phase ^= 1u << b;
+    const AccDesc& dsc = ps.desc[b];
+    const int2* hs = &ps.hit[b][0];
+    const int n = dsc.n;
+    const int2* hl = hits + dsc.hoff;
+    double R[9], t[3];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = dsc.T[k];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[k] = dsc.T[9 + k];
+    CloudView cv;
+    cv.a = dsc.a;
+    cv.xyz64 = dsc.xyz64;
+    cv.c0 = dsc.c0;
+    cv.c1 = dsc.c1;
+    cv.c2 = dsc.c2;
+    cv.n = 0;
+    MapView mv;
+    mv.recs = dsc.recs;
+    const bool f64pts = cv.xyz64 != nullptr;
+    double acc[28];
+#pragma unroll
+    for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+    const int rounds = (n + 31) / 32;
+    constexpr int kAhead = kStages - 1;
+    const int klast = n > 0 ? n - 1 : 0;
+    if (n > 0) {
+      static_assert(kAhead + 2 <= kPreHits / 32, "prologue entries must be staged");
+#pragma unroll
+      for (int r = 0; r < kAhead; ++r)
+        issue_round(cv, mv, sm, r, hs[min(r * 32 + lane, klast)], (dbg & 1) ? 0 : n - r * 32, lane);
+      int2 nxt = hs[min(kAhead * 32 + lane, klast)];
+      int2 nxt2 = hs[min((kAhead + 1) * 32 + lane, klast)];
+      for (int r = 0; r < rounds; ++r) {
+        const int ri = r + kAhead;
+        issue_round(cv, mv, sm, ri, nxt, (dbg & 1) ? 0 : n - ri * 32, lane);
+        nxt = nxt2;
+        nxt2 = __ldg(hl + min((ri + 2) * 32 + lane, klast));
+        cp_async_wait<kAhead>();
+        __syncwarp();
+        if (r * 32 + lane < n && !(dbg & 2))
+          hit_math<MODE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
+        __syncwarp();
+      }
+      cp_async_wait<0>();
+    }
+    if (MODE == 1) {
+      double c = acc[27];
+#pragma unroll
+      for (int s2 = 16; s2 >= 1; s2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s2);
+      if (lane == 0) {
+        partials[2 * (size_t)cur] = c;
+        partials[2 * (size_t)cur + 1] = (double)n;
+      }
+    } else {
+      double v[32];
+#pragma unroll
+      for (int k = 0; k < 28; ++k) v[k] = acc[k];
+      v[28] = lane == 0 ? (double)n : 0.0;
+      v[29] = 0.0;
+      v[30] = 0.0;
+      v[31] = 0.0;
+      partials[(size_t)cur * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
+    }
+    __syncwarp();  // buffer b is refilled two items from now
+    if (nxt >= n_items) break;
+    cur = nxt;
+    nxt = nn;
+    inxt = inn;
+    b ^= 1;
+  }
+}
+
 // ---- K4ws: warp-specialised persistent fused lookup + accumulate ---------------------------
 // One CTA per SM, 16 warps = 8 producer/consumer pairs.  A producer warp claims items
 // (dynamic, in target-major order), resolves the correspondences of the item's points
@@ -548,9 +713,6 @@ struct __align__(16) PairSmem {
   int2 hits[kMaxChunk];
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -928,12 +1090,51 @@ static int launch_acc_kernel(vg_ctx* ctx, K kern, size_t smem, const AccDesc* d,
   return 0;
 }
 
+template <class K>
+static int launch_persist_kernel(vg_ctx* ctx, vg_batch* b, K kern, int min_blocks, int off,
+                                 int cnt, double* partials, cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) VG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const size_t smem = sizeof(PersistSmem<2>) * kAccWarps;
+  VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  VG_CUDA(cudaMemsetAsync(b->work_counter, 0, sizeof(int), st));
+  static int occ = -1;
+  if (occ < 0) {
+    VG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kAccWarps * 32, smem));
+    if (getenv("VGICP_DEBUG_OCC")) fprintf(stderr, "k_acc_persist: %d CTAs/SM, %zu B smem\n", occ, smem);
+  }
+  min_blocks = std::max(1, std::min(min_blocks, occ));
+  const int grid = std::max(1, std::min(sms * min_blocks, (cnt + kAccWarps - 1) / kAccWarps));
+  static const int dbg = [] {
+    const char* e = getenv("VGICP_K4B_DEBUG");
+    return e ? atoi(e) : 0;
+  }();
+  kern<<<grid, kAccWarps * 32, smem, st>>>(b->items + off, b->descs + off, cnt, b->hits, partials,
+                                           b->work_counter, dbg);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
 static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
                             cudaStream_t st, bool shared_sm) {
   static const int variant = [] {
     const char* e = getenv("VGICP_ACC_VARIANT");
     return e ? atoi(e) : 0;
   }();
+  static const int persist = [] {
+    // 1: persistent K4b with TMA item prefetch (measured equal to the one-item-per-warp
+    // kernel on config 5: 0.385 vs 0.382 ms; kept as an option)
+    const char* e = getenv("VGICP_ACC_PERSIST");
+    return e ? atoi(e) : 0;
+  }();
+  if (persist) {
+    if (kmode == 1)
+      return launch_persist_kernel(ctx, b, k_acc_persist<1, 2, 3>, 3, off, cnt,
+                                   b->partials + 2 * (size_t)off, st);
+    return launch_persist_kernel(ctx, b, k_acc_persist<0, 2, 3>, 3, off, cnt,
+                                 b->partials + (size_t)off * kPartialStride, st);
+  }
   const AccDesc* d = b->descs + off;
   if (kmode == 1)
     return launch_acc_kernel(ctx, k_accumulate<1, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
