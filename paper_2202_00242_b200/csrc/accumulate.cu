@@ -150,6 +150,133 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
   if (descs && lane == 0) descs[w].n = cnt;
 }
 
+// K4a fast path: every map uses 32-bit local keys and a power-of-two resolution, every
+// source point is fp32-exact.  The item header (T_ij + views, refreshed by K-compose) is read
+// in one dependent step instead of item -> factor -> cloud/map views.
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
+    k_lookup_fast(const ItemHdr* __restrict__ hdrs, int n_items, int2* __restrict__ hits,
+                  int* __restrict__ counts, double* __restrict__ partials2,
+                  AccDesc* __restrict__ descs) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
+  if (w >= n_items) return;
+  const ItemHdr* h = hdrs + w;
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(h->T + k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = __ldg(h->T + 9 + k);
+  const float4* pa = (const float4*)__ldg((const unsigned long long*)&h->a);
+  const unsigned* keys32 = (const unsigned*)__ldg((const unsigned long long*)&h->mv.keys32);
+  const double inv_res = __ldg(&h->mv.inv_res);
+  const int shift = __ldg(&h->mv.shift);
+  const unsigned mask = __ldg(&h->mv.mask);
+  const int m = __ldg(&h->mv.m);
+  const int bx = __ldg(&h->mv.bx), by = __ldg(&h->mv.by), bz = __ldg(&h->mv.bz);
+  const int ex = __ldg(&h->mv.ex), ey = __ldg(&h->mv.ey), ez = __ldg(&h->mv.ez);
+  const int begin = __ldg(&h->begin), end = __ldg(&h->end), hoff = __ldg(&h->hoff);
+  if (descs) {
+    AccDesc& d = descs[w];
+    if (lane < 12) d.T[lane] = __ldg(h->T + lane);
+    else if (lane == 12) d.a = pa;
+    else if (lane == 13) d.xyz64 = nullptr;
+    else if (lane == 14) d.c0 = (const double2*)__ldg((const unsigned long long*)&h->c0);
+    else if (lane == 15) d.c1 = (const double2*)__ldg((const unsigned long long*)&h->c1);
+    else if (lane == 16) d.c2 = (const double2*)__ldg((const unsigned long long*)&h->c2);
+    else if (lane == 17) d.recs = (const VoxelRec*)__ldg((const unsigned long long*)&h->mv.recs);
+    else if (lane == 18) d.hoff = hoff;
+  }
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int2* out = hits + hoff;
+  int cnt = 0;
+  const int last = end - 1;
+  struct Q {
+    unsigned k32, bucket;
+    bool live;
+  };
+  auto make_q = [&](float4 a, int i) {
+    const double px = a.x, py = a.y, pz = a.z;
+    // points @ R^T + t (registration.py:148); floor(p / res) exact for power-of-two res
+    const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
+    const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
+    const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
+    const double fx = floor(x * inv_res), fy = floor(y * inv_res), fz = floor(z * inv_res);
+    Q q;
+    q.live = false;
+    q.k32 = 0;
+    q.bucket = 0;
+    if (fmax(fabs(fx), fmax(fabs(fy), fabs(fz))) < 1048576.0) {
+      // |floor| < 2^20: the reference's pack/unpack round trip is the identity
+      const unsigned lx = (unsigned)(__double2int_rz(fx) - bx);
+      const unsigned ly = (unsigned)(__double2int_rz(fy) - by);
+      const unsigned lz = (unsigned)(__double2int_rz(fz) - bz);
+      q.live = lx < (unsigned)ex && ly < (unsigned)ey && lz < (unsigned)ez;
+      q.k32 = lx | (ly << 11) | (lz << 22);
+    } else {
+      MapView mv;
+      mv.bx = bx; mv.by = by; mv.bz = bz; mv.ex = ex; mv.ey = ey; mv.ez = ez; mv.shift = shift;
+      const Query qq = make_query(mv, fx, fy, fz, 1);
+      q.live = qq.inside;
+      q.k32 = qq.k32;
+    }
+    q.bucket = (q.k32 * 0x9E3779B9u) >> shift;
+    q.live = q.live && i < end && m > 0;
+    return q;
+  };
+  auto load256 = [&](unsigned bucket, long long (&g)[4]) {
+    ld256(keys32 + (size_t)bucket * kBucket, g[0], g[1], g[2], g[3]);
+  };
+  float4 a0 = __ldg(pa + min(begin + lane, last));
+  float4 a1 = __ldg(pa + min(begin + 32 + lane, last));
+  Q q0 = make_q(a0, begin + lane);
+  long long g0[4] = {0, 0, 0, 0};
+  if (q0.live) load256(q0.bucket, g0);
+  for (int base = begin; base < end; base += 32) {
+    const int i = base + lane;
+    const Q q1 = make_q(a1, i + 32);
+    long long g1[4] = {0, 0, 0, 0};
+    if (q1.live) load256(q1.bucket, g1);
+    a1 = __ldg(pa + min(i + 64, last));
+    int slot = -1;
+    if (q0.live) {
+      unsigned bk = q0.bucket;
+      for (;;) {
+        int found = -1;
+        bool empty = false;
+#pragma unroll
+        for (int j = kBucket - 1; j >= 0; --j) {
+          const unsigned kj = (unsigned)((unsigned long long)g0[j >> 1] >> (32 * (j & 1)));
+          if (kj == q0.k32) found = j;
+          empty |= (kj == kEmpty32);
+        }
+        if (found >= 0) {
+          slot = (int)(bk * kBucket + found);
+          break;
+        }
+        if (empty) break;
+        bk = (bk + 1) & mask;
+        load256(bk, g0);
+      }
+    }
+    // misses contribute nothing (registration.py:150-156)
+    const unsigned mb = __ballot_sync(0xffffffffu, slot >= 0);
+    if (slot >= 0) out[cnt + __popc(mb & lt_mask)] = make_int2(i, slot);
+    cnt += __popc(mb);
+    q0 = q1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g0[k] = g1[k];
+  }
+  if (lane == 0) {
+    counts[w] = cnt;
+    if (partials2) {
+      partials2[2 * (size_t)w] = 0.0;
+      partials2[2 * (size_t)w + 1] = (double)cnt;
+    }
+    if (descs) descs[w].n = cnt;
+  }
+}
+
 // K4a, batched variant: each lane resolves U points per iteration (U independent point loads,
 // then U independent bucket probes in flight), sub-rounds compacted in point order.
 template <int KM, int U, int kMinBlocks>
@@ -1030,7 +1157,16 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
     const char* e = getenv("VGICP_LOOKUP_U");  // 0: two-deep pipelined K4a; 2/4: batched
     return e ? atoi(e) : 0;
   }();
-  if (b->key_mode == 1 && lu > 0) {
+  static const int fast = [] {
+    const char* e = getenv("VGICP_LOOKUP_FAST");
+    return e ? atoi(e) : 1;
+  }();
+  if (fast && b->key_mode == 1 && b->all_pow2 && b->all_f32) {
+    if (lblocks != 3)  // 4 CTAs/SM measured fastest (0.196 vs 0.203 ms at 3)
+      k_lookup_fast<4><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
+    else
+      k_lookup_fast<3><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
+  } else if (b->key_mode == 1 && lu > 0) {
     if (lu == 2 && lblocks == 4)
       k_lookup_batch<1, 2, 4><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                                 b->maps, b->hits, hc, p2, dd);
@@ -1151,6 +1287,9 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
                                cnt, b->hits, p, st);
     case 3:
       return launch_acc_kernel(ctx, k_accumulate<0, 4, 3, 2>, sizeof(AccSmem<4>) * kAccWarps, d,
+                               cnt, b->hits, p, st);
+    case 4:
+      return launch_acc_kernel(ctx, k_accumulate<0, 2, 4, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
                                cnt, b->hits, p, st);
     default:
       return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d,

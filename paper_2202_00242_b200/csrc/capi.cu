@@ -500,6 +500,8 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   b->key_mode = n32 == (int)maps.size() ? 1 : (n32 == 0 ? 0 : 2);
   b->all_pow2 = 1;
   for (const MapView& m : mv) b->all_pow2 &= m.pow2 ? 1 : 0;
+  b->all_f32 = 1;
+  for (const CloudView& c : cv) b->all_f32 &= c.xyz64 ? 0 : 1;
   // Source groups, ordered for L2 locality: a breadth-first walk of the bipartite graph
   // (source -> its target maps -> the other sources of those maps), the Cuthill-McKee idea,
   // so sources processed concurrently by different SMs share most of their target maps.
