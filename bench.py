@@ -52,8 +52,9 @@ def parse():
 
 
 def traffic_record():
-    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01_traffic.json)."""
-    p = ROOT / "profiles" / "r01_traffic.json"
+    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01b_traffic.json,
+    written by tools/launch_traffic.py from profiles/r01b_launches.csv)."""
+    p = ROOT / "profiles" / "r01b_traffic.json"
     try:
         return int(json.loads(p.read_text())["dram_bytes_per_launch"])
     except Exception:
@@ -326,7 +327,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_record(),
-                         "kernel": "K4 = k_lookup_items (K4a) + k_accumulate<0> (K4b)",
+                         "kernel": "K4 = k_lookup_fast (K4a) + k_accumulate<0> (K4b)",
                          "kernel_ms": statistics.mean(k4_ms),
                          "bytes_per_corr": BYTES_PER_CORR, "peak_kind": peak_kind},
             "clocks": clocks,

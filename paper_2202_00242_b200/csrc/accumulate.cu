@@ -1149,10 +1149,11 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
   const ItemDev* it = b->items + off;
   int* hc = b->hit_counts + off;
   AccDesc* dd = b->descs + off;
-  static const int lblocks = [] {
+  static const int lblocks_env = [] {
     const char* e = getenv("VGICP_LOOKUP_BLOCKS");
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 0;
   }();
+  const int lblocks = lblocks_env ? lblocks_env : 3;
   static const int lu = [] {
     const char* e = getenv("VGICP_LOOKUP_U");  // 0: two-deep pipelined K4a; 2/4: batched
     return e ? atoi(e) : 0;
@@ -1162,7 +1163,7 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
     return e ? atoi(e) : 1;
   }();
   if (fast && b->key_mode == 1 && b->all_pow2 && b->all_f32) {
-    if (lblocks != 3)  // 4 CTAs/SM measured fastest (0.196 vs 0.203 ms at 3)
+    if (lblocks_env != 3)  // 4 CTAs/SM measured fastest (0.196 vs 0.203 ms at 3)
       k_lookup_fast<4><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
     else
       k_lookup_fast<3><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
