@@ -82,7 +82,8 @@ int vg_pack_voxel_keys(vg_ctx* ctx, const double* xyz, int64_t n, double resolut
 
 /* ---- clouds (Frame: preprocess.py:46-60) ----------------------------------------------- */
 /* xyz: n x 3; cov: n x 3 x 3 or NULL.  Points exactly representable in fp32 take the fast
- * 36 B/point fp32 SoA path; any other input keeps an fp64 copy so voxel keys stay exact. */
+ * fast path: 64 B/point SoA in HBM (float4 xyz + the covariance as three fp64 double2 rows);
+ * any other input also keeps an fp64 xyz copy so voxel keys stay exact. */
 int vg_cloud_create(vg_ctx* ctx, const double* xyz, const double* cov, int64_t n,
                     vg_cloud** out);
 int vg_cloud_info(const vg_cloud* cloud, int64_t* n, int32_t* has_cov, int32_t* exact_fp32);

@@ -190,7 +190,8 @@ def context(device: int | None = None) -> Context:
 
 
 class DeviceCloud:
-    """Device copy of a Frame's points (+ covariances): 36 B/point fp32 SoA in HBM."""
+    """Device copy of a Frame's points (+ covariances): 64 B/point SoA in HBM (float4 xyz,
+    fp64 covariance rows); non-fp32-exact points keep an extra fp64 xyz copy."""
 
     def __init__(self, points, covs=None, ctx: Context | None = None):
         ctx = ctx or context()

@@ -1,12 +1,13 @@
-// linearize.cu — K3 lookup, K3t per-point terms, K4 fused VGICP linearize / cost, K5 finalize,
-// and the on-device pose composition T_ij = T_j^-1 T_i.
+// linearize.cu — K3 lookup, K3t per-point terms (the per-factor API), K5 finalize, and the
+// on-device pose composition T_ij = T_j^-1 T_i (K4a/K4b, the batched path, are in
+// accumulate.cu).
 //
 // Reference: registration.py:146-157 (match_terms), :207-248 (linearize_from_terms),
 // :251-269 (linearize_matching_cost), factor_graph.py:253-308 (MatchingCostFactor).
 //
-// Per correspondence the kernel reads the source Gaussian (fp32 xyz + fp64 covariance, SoA,
-// coalesced) and one 96 B hash slot carrying the voxel Gaussian, and does all math in
-// registers, in fp64:
+// Per correspondence the kernels read the source Gaussian (fp32 xyz + fp64 covariance, SoA)
+// and one voxel record (fp64 mean + covariance) found through the hash, and do all math in
+// fp64:
 //   x = R p + t -> key (bit-exact floor) -> probe -> d = mu' - x -> W = (C' + R C R^T)^-1
 //   (adjugate) -> accumulate the 6x6 target-frame block about the source origin (29 values,
 //   H_ii, H_ij, H_jj, b_i, b_j are exact fp64 adjoint transforms of it, so
