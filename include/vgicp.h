@@ -153,6 +153,26 @@ int vg_batch_graph_capture(vg_batch* batch, const double* poses_dev, int64_t num
                            int mode, double* out_dev);
 int vg_batch_graph_launch(vg_batch* batch);
 
+/* ---- normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536) ------------
+ * Sums every factor's blocks into the block-sparse system the LM solves,
+ * on the device and in a fixed order (factor order per block), so only the system crosses
+ * PCIe.  Variables are pose-table rows 0 .. num_vars-1; rows >= num_vars are constants (the
+ * fixed targets of unary factors), whose blocks are dropped as the reference's unary factors
+ * do (factor_graph.py:296-297).  Factors below their min_inliers contribute nothing
+ * (:282-291).  Output (doubles): [0] cost, [1] factors contributing, then
+ *   diag  num_vars x 21  upper triangle (row-major) of each variable's 6x6 H block,
+ *   grad  num_vars x 6   g,
+ *   pairs P x 36          H block (a, b), row-major, for each variable pair a < b
+ * with the pair list from vg_batch_assemble_pairs().  6-dof blocks: a caller with 15-dof
+ * frame-state keys embeds them top-left (factor_graph.py:292-308). */
+int vg_batch_assemble_setup(vg_batch* batch, int64_t num_vars, int64_t* num_pairs,
+                            int64_t* out_doubles);
+int vg_batch_assemble_pairs(const vg_batch* batch, int32_t* pairs_out /* P x 2 */);
+int vg_batch_assemble_poses(vg_batch* batch, const double* poses_host, int64_t num_poses,
+                            double* out_host);
+int vg_batch_assemble_poses_device(vg_batch* batch, const double* poses_dev,
+                                   int64_t num_poses, double* out_dev);
+
 /* ---- preprocessing (preprocess.py:122-164) --------------------------------------------- */
 /* replaces knn_search (preprocess.py:122-139): exact k nearest (self included), ordered by
  * (squared distance, index).  Returns VG_ERR_TOO_SPARSE when n < k. */

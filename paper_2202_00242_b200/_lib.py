@@ -81,6 +81,10 @@ _SIGNATURES = {
     "vg_batch_finalize_device": ([c_void_p, c_int, c_void_p], c_int),
     "vg_batch_graph_capture": ([c_void_p, c_void_p, c_int64, c_int, c_void_p], c_int),
     "vg_batch_graph_launch": ([c_void_p], c_int),
+    "vg_batch_assemble_setup": ([c_void_p, c_int64, _P_I64, _P_I64], c_int),
+    "vg_batch_assemble_pairs": ([c_void_p, POINTER(c_int32)], c_int),
+    "vg_batch_assemble_poses": ([c_void_p, _P_D, c_int64, _P_D], c_int),
+    "vg_batch_assemble_poses_device": ([c_void_p, c_void_p, c_int64, c_void_p], c_int),
     "vg_knn": ([c_void_p, c_void_p, c_int32, _P_I64], c_int),
     "vg_covariances": ([c_void_p, c_void_p, _P_I64, c_int32, c_double, _P_D, _P_U8], c_int),
     "vg_cloud_estimate_covariances": ([c_void_p, c_void_p, c_int32, c_double, _P_I64, _P_D,
@@ -338,3 +342,72 @@ class DeviceBatch:
 
     def launch_graph(self) -> None:
         check(self.ctx.lib.vg_batch_graph_launch(self.handle))
+
+    # ---- normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536) ----------
+    def assemble_setup(self, num_vars: int) -> np.ndarray:
+        """Variables are pose-table rows < num_vars; returns the (P, 2) variable pairs whose
+        off-diagonal blocks the assembly produces."""
+        P, total = c_int64(), c_int64()
+        check(self.ctx.lib.vg_batch_assemble_setup(self.handle, int(num_vars), ctypes.byref(P),
+                                                   ctypes.byref(total)), "vg_batch_assemble_setup")
+        pairs = np.empty((int(P.value), 2), dtype=np.int32)
+        if P.value:
+            check(self.ctx.lib.vg_batch_assemble_pairs(
+                self.handle, pairs.ctypes.data_as(POINTER(c_int32))), "vg_batch_assemble_pairs")
+        self.asm_vars = int(num_vars)
+        self.asm_pairs = pairs
+        self.asm_size = int(total.value)
+        return pairs
+
+    def assemble_poses(self, poses: np.ndarray, out: np.ndarray | None = None) -> "NormalEquations":
+        poses = f64(poses).reshape(-1, 8)
+        if out is None:
+            out = np.empty(self.asm_size)
+        check(self.ctx.lib.vg_batch_assemble_poses(self.handle, dptr(poses), poses.shape[0],
+                                                   dptr(out)), "vg_batch_assemble_poses")
+        return NormalEquations.from_flat(out, self.asm_vars, self.asm_pairs)
+
+    def assemble_poses_device(self, poses_dev_ptr: int, num_poses: int, out_dev_ptr: int) -> None:
+        check(self.ctx.lib.vg_batch_assemble_poses_device(
+            self.handle, c_void_p(poses_dev_ptr), int(num_poses), c_void_p(out_dev_ptr)),
+            "vg_batch_assemble_poses_device")
+
+
+_UPPER6 = np.triu_indices(6)
+
+
+class NormalEquations:
+    """Block-sparse H, g and cost of a batch's factors (vg_batch_assemble_*): 6x6 diagonal
+    blocks per variable, the gradient per variable, and H blocks (a, b) for pairs a < b."""
+
+    def __init__(self, cost, count, diag, grad, pairs, off):
+        self.cost, self.count = cost, count
+        self.diag, self.grad, self.pairs, self.off = diag, grad, pairs, off
+
+    @classmethod
+    def from_flat(cls, flat: np.ndarray, V: int, pairs: np.ndarray) -> "NormalEquations":
+        P = len(pairs)
+        up = flat[2:2 + 21 * V].reshape(V, 21)
+        diag = np.zeros((V, 6, 6))
+        diag[:, _UPPER6[0], _UPPER6[1]] = up
+        diag[:, _UPPER6[1], _UPPER6[0]] = up
+        grad = flat[2 + 21 * V:2 + 27 * V].reshape(V, 6).copy()
+        off = flat[2 + 27 * V:2 + 27 * V + 36 * P].reshape(P, 6, 6).copy()
+        return cls(float(flat[0]), int(flat[1]), diag, grad, pairs, off)
+
+    def dense(self, offsets=None, dim=None):
+        """Dense H, g; variable v's 6x6 block at rows offsets[v]:offsets[v]+6 (default 6v)."""
+        V = len(self.diag)
+        offsets = np.arange(V) * 6 if offsets is None else np.asarray(offsets)
+        dim = 6 * V if dim is None else dim
+        h = np.zeros((dim, dim))
+        g = np.zeros(dim)
+        rows = offsets[:, None] + np.arange(6)          # (V, 6); blocks are disjoint
+        h[rows[:, :, None], rows[:, None, :]] += self.diag
+        g[rows] += self.grad
+        if len(self.pairs):
+            ra = rows[self.pairs[:, 0]]
+            rb = rows[self.pairs[:, 1]]
+            h[ra[:, :, None], rb[:, None, :]] += self.off
+            h[rb[:, :, None], ra[:, None, :]] += self.off.transpose(0, 2, 1)
+        return h, g

@@ -636,6 +636,9 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->work_counter);
   dfree(ctx, b->out);
   dfree(ctx, b->poses);
+  dfree(ctx, b->asm_begin);
+  dfree(ctx, b->asm_codes);
+  dfree(ctx, b->asm_out);
   cudaStreamSynchronize(ctx->stream);
   delete b;
   return VG_OK;
@@ -746,6 +749,114 @@ int vg_batch_accumulate_device(vg_batch* b, int mode) {
 int vg_batch_finalize_device(vg_batch* b, int mode, double* out_dev) {
   if (!b || !out_dev || mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad arguments");
   return launch_finalize(b->ctx, b, mode, out_dev);
+}
+
+int vg_batch_assemble_setup(vg_batch* b, int64_t num_vars, int64_t* num_pairs,
+                            int64_t* out_doubles) {
+  if (!b || num_vars <= 0 || num_vars >= (1LL << 28))
+    return fail(VG_ERR_INVALID, "invalid assembly arguments");
+  vg_ctx* ctx = b->ctx;
+  const long long V = num_vars, F = b->F;
+  // contributions per unit, in factor order (factor_graph.py:529-535 adds blocks in order)
+  std::vector<std::vector<int>> diag((size_t)V);
+  std::vector<std::pair<long long, int>> pc;  // (pair key, code), stable-sorted below
+  for (long long f = 0; f < F; ++f) {
+    const FactorDev& d = b->host_factors[f];
+    const long long vs = d.var_source, vt = d.var_target;
+    const bool unary = d.flags & 1;
+    if (vs < 0 || (!unary && vt < 0))
+      return fail(VG_ERR_INVALID, "factor without pose-table variables");
+    if (f >= (1LL << 28)) return fail(VG_ERR_INVALID, "too many factors for assembly");
+    const int code = (int)f * 8;
+    if (vs < V) diag[vs].push_back(code + 0);
+    if (unary || vt >= V) continue;  // constant target: only the source blocks
+    if (vs == vt) {
+      diag[vs].push_back(code + 4);
+      diag[vs].push_back(code + 1);
+      continue;
+    }
+    diag[vt].push_back(code + 1);
+    if (vs < V) {
+      const long long a = std::min(vs, vt), c = std::max(vs, vt);
+      pc.push_back({a * V + c, code + (vs < vt ? 2 : 3)});
+    }
+  }
+  std::stable_sort(pc.begin(), pc.end(),
+                   [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) {
+                     return x.first < y.first;
+                   });
+  std::vector<int> begin, codes, pairs;
+  begin.reserve(V + pc.size() + 2);
+  for (long long v = 0; v < V; ++v) {
+    begin.push_back((int)codes.size());
+    codes.insert(codes.end(), diag[v].begin(), diag[v].end());
+  }
+  for (size_t i = 0; i < pc.size(); ++i) {
+    if (i == 0 || pc[i].first != pc[i - 1].first) {
+      begin.push_back((int)codes.size());
+      pairs.push_back((int)(pc[i].first / V));
+      pairs.push_back((int)(pc[i].first % V));
+    }
+    codes.push_back(pc[i].second);
+  }
+  begin.push_back((int)codes.size());
+  const long long P = (long long)pairs.size() / 2;
+  const long long total = 2 + V * 27 + P * 36;
+  dfree(ctx, b->asm_begin);
+  dfree(ctx, b->asm_codes);
+  dfree(ctx, b->asm_out);
+  b->asm_begin = nullptr;
+  b->asm_codes = nullptr;
+  b->asm_out = nullptr;
+  b->asm_vars = -1;
+  VG_CHECK(dalloc(ctx, &b->asm_begin, begin.size()));
+  VG_CHECK(dalloc(ctx, &b->asm_codes, std::max<size_t>(codes.size(), 1)));
+  VG_CHECK(dalloc(ctx, &b->asm_out, (size_t)total));
+  VG_CHECK(h2d(ctx, b->asm_begin, begin.data(), sizeof(int) * begin.size()));
+  if (!codes.empty()) VG_CHECK(h2d(ctx, b->asm_codes, codes.data(), sizeof(int) * codes.size()));
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  b->asm_vars = V;
+  b->asm_pairs_n = P;
+  b->asm_pairs = pairs;
+  if (num_pairs) *num_pairs = P;
+  if (out_doubles) *out_doubles = total;
+  return VG_OK;
+}
+
+int vg_batch_assemble_pairs(const vg_batch* b, int32_t* pairs_out) {
+  if (!b || b->asm_vars < 0) return fail(VG_ERR_INVALID, "assembly not set up");
+  if (b->asm_pairs_n && !pairs_out) return fail(VG_ERR_INVALID, "null argument");
+  if (b->asm_pairs_n) memcpy(pairs_out, b->asm_pairs.data(), sizeof(int32_t) * b->asm_pairs.size());
+  return VG_OK;
+}
+
+static int run_assemble(vg_batch* b, const double* poses_dev, int64_t V, double* out_dev) {
+  if (b->asm_vars < 0) return fail(VG_ERR_INVALID, "assembly not set up (vg_batch_assemble_setup)");
+  if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  vg_ctx* ctx = b->ctx;
+  if (b->F) {
+    VG_CHECK(launch_compose(ctx, b, poses_dev));
+    VG_CHECK(launch_accumulate(ctx, b, kmode_of(VG_MODE_LINEARIZE)));
+    VG_CHECK(launch_finalize(ctx, b, VG_MODE_LINEARIZE, b->out));
+  }
+  return launch_assemble(ctx, b, b->out, out_dev);
+}
+
+int vg_batch_assemble_poses_device(vg_batch* b, const double* poses_dev, int64_t V,
+                                   double* out_dev) {
+  if (!b || !poses_dev || !out_dev) return fail(VG_ERR_INVALID, "null argument");
+  return run_assemble(b, poses_dev, V, out_dev);
+}
+
+int vg_batch_assemble_poses(vg_batch* b, const double* poses_host, int64_t V, double* out_host) {
+  if (!b || !poses_host || !out_host) return fail(VG_ERR_INVALID, "null argument");
+  if (b->asm_vars < 0) return fail(VG_ERR_INVALID, "assembly not set up (vg_batch_assemble_setup)");
+  if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  VG_CHECK(ensure_poses(b, V));
+  VG_CHECK(h2d(b->ctx, b->poses, poses_host, sizeof(double) * 8 * V));
+  VG_CHECK(run_assemble(b, b->poses, V, b->asm_out));
+  const size_t total = 2 + (size_t)b->asm_vars * 27 + (size_t)b->asm_pairs_n * 36;
+  return d2h_sync(b->ctx, out_host, b->asm_out, sizeof(double) * total);
 }
 
 int vg_batch_graph_capture(vg_batch* b, const double* poses_dev, int64_t V, int mode,

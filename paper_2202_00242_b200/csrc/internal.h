@@ -124,6 +124,13 @@ struct vg_batch {
   std::vector<int> stage_factors, stage_items;
   cudaGraphExec_t graph = nullptr;
   std::vector<vg::FactorDev> host_factors;
+  // normal-equation assembly (vg_batch_assemble_*): CSR of contributions per output unit
+  long long asm_vars = -1;            // variables (pose-table rows < asm_vars); -1: not set up
+  long long asm_pairs_n = 0;
+  std::vector<int> asm_pairs;         // P x 2 (a < b)
+  int* asm_begin = nullptr;           // units + 1
+  int* asm_codes = nullptr;           // factor * 8 + role
+  double* asm_out = nullptr;          // device output (host-buffer entry point)
 };
 
 // error plumbing (capi.cu)
@@ -162,6 +169,7 @@ int launch_srcgroup(vg_ctx* ctx, vg_batch* b, int kmode);    // K4s
 int srcgroup_max_points();
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1);
+int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev);  // K6
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi);  // K4a + K4b
 int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);
 int launch_cov(vg_ctx* ctx, const vg_cloud* cloud, const long long* nbrs_dev, int k,

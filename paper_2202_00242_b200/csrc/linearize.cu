@@ -285,6 +285,97 @@ __global__ void __launch_bounds__(kFinBlock)
   }
 }
 
+// ---- K6: block-sparse normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536)
+// One warp per output unit: unit u < V is variable u's diagonal block (21, upper) + gradient
+// (6); V <= u < V + P is the H block of variable pair u - V (36); unit V + P is the cost.
+// A unit's contributions are listed in factor order (CSR, code = factor * 8 + role), and each
+// lane sums its element in that order from 0.0, so the result is the reference's sequential
+// per-block sum.  Roles: 0 source block (H_ii, b_i), 1 target block (H_jj, b_j), 2 H_ij as is,
+// 3 H_ij transposed, 4 H_ij + H_ij^T (a factor whose two keys are the same variable).
+// Records of factors below min_inliers have zero blocks (K5), so they add exact zeros.
+__constant__ unsigned char kUpperRow[21] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1,
+                                            2, 2, 2, 2, 3, 3, 3, 4, 4, 5};
+__constant__ unsigned char kUpperCol[21] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5,
+                                            2, 3, 4, 5, 3, 4, 5, 4, 5, 5};
+
+__device__ __forceinline__ double asm_value(const double* __restrict__ r, int role, int k) {
+  // k: element index of the unit (diag: 0..20 H upper, 21..26 g; pair: 0..35)
+  switch (role) {
+    case 0: return k < 21 ? __ldg(r + k) : __ldg(r + 78 + (k - 21));
+    case 1: return k < 21 ? __ldg(r + 57 + k) : __ldg(r + 84 + (k - 21));
+    case 2: return __ldg(r + 21 + k);
+    case 3: return __ldg(r + 21 + 6 * (k % 6) + k / 6);
+    default: {
+      if (k >= 21) return 0.0;
+      const int a = kUpperRow[k], c = kUpperCol[k];
+      return __ldg(r + 21 + 6 * a + c) + __ldg(r + 21 + 6 * c + a);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128)
+    k_assemble(const double* __restrict__ rec, const FactorDev* __restrict__ factors, int F,
+               const int* __restrict__ begin, const int* __restrict__ codes, int V, int P,
+               double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (u > V + P) return;
+  if (u == V + P) {  // cost of the factors that pass their inlier gate, and their count
+    double c = 0.0, n = 0.0;
+    for (int f = lane; f < F; f += 32) {
+      const double* r = rec + (size_t)f * 92;
+      if (__ldg(r + 91) >= (double)__ldg(&factors[f].min_inliers)) {
+        c += __ldg(r + 90);
+        n += 1.0;
+      }
+    }
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      c += __shfl_xor_sync(0xffffffffu, c, s);
+      n += __shfl_xor_sync(0xffffffffu, n, s);
+    }
+    if (lane == 0) {
+      out[0] = c;
+      out[1] = n;
+    }
+    return;
+  }
+  const int k0 = __ldg(begin + u), k1 = __ldg(begin + u + 1);
+  const bool diag = u < V;
+  const int nel = diag ? 27 : 36;
+  double acc0 = 0.0, acc1 = 0.0;  // elements lane and lane + 32
+  const bool has0 = lane < nel, has1 = lane + 32 < nel;
+  // four contributions in flight per step; additions stay in contribution order
+  for (int k = k0; k < k1; k += 4) {
+    double v0[4], v1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v0[q] = 0.0;
+      v1[q] = 0.0;
+      if (k + q < k1) {
+        const int code = __ldg(codes + k + q);
+        const double* r = rec + (size_t)(code >> 3) * 92;
+        if (has0) v0[q] = asm_value(r, code & 7, lane);
+        if (has1) v1[q] = asm_value(r, code & 7, lane + 32);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (k + q < k1) {
+        acc0 += v0[q];
+        acc1 += v1[q];
+      }
+  }
+  if (diag) {
+    if (lane < 21) out[2 + (size_t)u * 21 + lane] = acc0;
+    else if (lane < 27) out[2 + (size_t)V * 21 + (size_t)u * 6 + (lane - 21)] = acc0;
+  } else {
+    double* o = out + 2 + (size_t)V * 27 + (size_t)(u - V) * 36;
+    o[lane] = acc0;
+    if (has1) o[lane + 32] = acc1;
+  }
+}
+
 // ---- pose composition on the device (geometry.py:47-144,231-237) ------------------------
 // Mirrors Rotation's quaternion arithmetic operation for operation without FMA contraction,
 // so T_ij matches pose_compose(pose_inverse(t_j), t_i) to the last bit except for numpy's
@@ -516,4 +607,14 @@ int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, i
 
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev) {
   return launch_finalize_range(ctx, b, mode, out_dev, 0, (int)b->F);
+}
+
+int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev) {
+  const int units = (int)(b->asm_vars + b->asm_pairs_n + 1);
+  k_assemble<<<(units + 3) / 4, 128, 0, ctx->stream>>>(rec, b->factors, (int)b->F, b->asm_begin,
+                                                       b->asm_codes, (int)b->asm_vars,
+                                                       (int)b->asm_pairs_n, out_dev);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
 }

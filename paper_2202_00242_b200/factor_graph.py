@@ -163,6 +163,41 @@ class _Batcher:
             f._store(values, mode, rec)
 
 
+    def assemble(self, group, values, var_keys) -> "_lib.NormalEquations":
+        """Device-assembled normal equations of `group` over the graph variables `var_keys`
+        (FactorGraph._assemble_dense, factor_graph.py:522-536)."""
+        sig = ("asm", tuple(f._serial for f in group), tuple(var_keys))
+        hit = self._batches.get(sig)
+        if hit is None:
+            index = {k: i for i, k in enumerate(var_keys)}
+            fixed_rows, vs, vt = [], [], []
+            for f in group:
+                vs.append(index[f.keys[0]])
+                if f.unary:
+                    vt.append(len(var_keys) + len(fixed_rows))
+                    fixed_rows.append(pose_row(f.fixed_target_pose))
+                else:
+                    vt.append(index[f.keys[1]])
+            batch = _lib.DeviceBatch([device_cloud(f.source) for f in group],
+                                     [_as_device_map(f.target_map) for f in group],
+                                     [f.unary for f in group], [f.min_inliers for f in group],
+                                     vs, vt)
+            batch.assemble_setup(len(var_keys))
+            hit = (batch, np.array(fixed_rows).reshape(-1, 8), [weakref.ref(f) for f in group])
+            self._batches[sig] = hit
+            while len(self._batches) > 8:
+                self._batches.popitem(last=False)
+        self._batches.move_to_end(sig)
+        batch, fixed, _ = hit
+        poses = np.empty((len(var_keys) + fixed.shape[0], 8))
+        for i, k in enumerate(var_keys):
+            poses[i] = pose_row(_pose_of(k.kind, values[k]))
+        if fixed.shape[0]:
+            poses[len(var_keys):] = fixed
+        self.evaluations += 1
+        return batch.assemble_poses(poses)
+
+
 _BATCHER = _Batcher()
 
 
@@ -339,11 +374,27 @@ class FactorGraph:
             off += k.dim
         return out, off
 
+    #: sum the matching factors' blocks on the device (vg_batch_assemble_*) instead of per
+    #: factor on the host; results agree to fp64 rounding (block sums in factor order)
+    device_assembly = True
+
     def _assemble_dense(self, values, slices, dim):
         h = np.zeros((dim, dim))
         g = np.zeros(dim)
         cost = 0.0
-        for f in self.factors:
+        factors = self.factors
+        if self.device_assembly:
+            gpu = [f for f in factors if isinstance(f, MatchingCostFactor) and not f._empty]
+            if gpu:
+                keys = list(self.values)
+                ne = _BATCHER.assemble(gpu, values, keys)
+                hd, gd = ne.dense([slices[k].start for k in keys], dim)
+                h += hd
+                g += gd
+                cost += ne.cost
+                factors = [f for f in factors
+                           if not (isinstance(f, MatchingCostFactor) and not f._empty)]
+        for f in factors:
             lin = f.linearize(values)
             cost += lin.cost
             sls = [slices[k] for k in lin.keys]

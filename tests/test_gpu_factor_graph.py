@@ -113,3 +113,44 @@ def test_unary_factor_in_graph():
     res = g.optimize_lm()
     err = G.pose_local(res.estimates[submap_key(0)], true)
     assert np.linalg.norm(err) < 1e-3
+
+
+def test_device_assembly_matches_per_factor_assembly():
+    """FactorGraph._assemble_dense with the matching factors summed on the device
+    (vg_batch_assemble_poses) equals the reference's per-factor scatter, and the LM reaches
+    the same estimate either way."""
+    rng = np.random.default_rng(17)
+    pts, covs = plane_cloud(rng)
+    vmap = RG.build_voxelmap(make_frame(pts, covs), 0.5)
+    g = FactorGraph()
+    rels = []
+    for i in range(6):
+        rel = G.Se3Pose(G.so3_exp(rng.uniform(-0.04, 0.04, 3)), rng.uniform(-0.1, 0.1, 3))
+        rels.append(rel)
+        g.add_variable(submap_key(i), G.pose_retract(rel, rng.uniform(-0.01, 0.01, 6)))
+    g.add_factor(PriorFactor(submap_key(0), rels[0], np.full(6, 1e6)))
+    for i in range(6):
+        for j in range(6):
+            if i != j and (i + j) % 2:
+                src = make_frame(G.pose_apply(G.pose_inverse(rels[i]), pts), covs)
+                tgt = RG.build_voxelmap(make_frame(G.pose_apply(G.pose_inverse(rels[j]), pts),
+                                                   covs), 0.5)
+                g.add_factor(MatchingCostFactor(submap_key(i), src, tgt, key_target=submap_key(j)))
+    g.add_factor(MatchingCostFactor(submap_key(3), make_frame(
+        G.pose_apply(G.pose_inverse(rels[3]), pts), covs), vmap, fixed_target_pose=G.Se3Pose.identity()))
+    slices, dim = g._slices()
+    g.device_assembly = True
+    h_d, g_d, c_d = g._assemble_dense(g.values, slices, dim)
+    g.device_assembly = False
+    h_h, g_h, c_h = g._assemble_dense(g.values, slices, dim)
+    assert np.allclose(h_d, h_h, rtol=1e-12, atol=1e-8)
+    assert np.allclose(g_d, g_h, rtol=1e-12, atol=1e-8)
+    assert abs(c_d - c_h) <= 1e-12 * abs(c_h)
+    g.device_assembly = True
+    a = g.optimize_lm()
+    g2 = FactorGraph()
+    g2.values, g2.factors = dict(g.values), list(g.factors)
+    g2.device_assembly = False
+    b = g2.optimize_lm()
+    for k in a.estimates:
+        assert np.linalg.norm(G.pose_local(a.estimates[k], b.estimates[k])) < 1e-6

@@ -340,3 +340,66 @@ def test_staged_host_output_matches_single_launch(small_graph):
         assert np.array_equal(host, dev.cpu().numpy()), mode
         if mode == _lib.MODE_LINEARIZE:
             assert np.array_equal(host, ref[sel])
+
+
+def test_device_normal_equations_match_host_assembly(small_graph):
+    """vg_batch_assemble_*: every block is the factor-order sum of the factors' blocks,
+    bit for bit (same additions as a sequential host sum), unary targets are constants, and
+    the dense form matches the reference's _assemble_dense scatter (factor_graph.py:522-536)."""
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
+    F, V = len(pairs), len(est)
+    unary = [(f % 7) == 3 for f in range(F)]
+    fixed = [G.pose_row(G.pose_retract(poses[j], np.full(6, 0.01))) for _, j in pairs]
+    vs = pairs[:, 0].copy()
+    vt = np.array([V + f if unary[f] else pairs[f, 1] for f in range(F)])
+    table = np.vstack([np.array([G.pose_row(p) for p in est]), np.array(fixed)])
+    batch = _lib.DeviceBatch([clouds[i] for i, _ in pairs], [dmaps[j] for _, j in pairs], unary,
+                             [10] * F, vs, vt)
+    prs = batch.assemble_setup(V)
+    rec = batch.linearize_poses(table)
+    ne = batch.assemble_poses(table)
+    # host: sequential sums in factor order
+    diag = np.zeros((V, 21))
+    grad = np.zeros((V, 6))
+    off = {tuple(p): np.zeros(36) for p in prs}
+    cost, count = 0.0, 0
+    for f in range(F):
+        r = rec[f]
+        if r[91] >= 10:
+            cost += r[90]
+            count += 1
+        diag[vs[f]] += r[0:21]
+        grad[vs[f]] += r[78:84]
+        if unary[f]:
+            continue
+        diag[vt[f]] += r[57:78]
+        grad[vt[f]] += r[84:90]
+        a, b = min(vs[f], vt[f]), max(vs[f], vt[f])
+        blk = r[21:57] if vs[f] < vt[f] else r[21:57].reshape(6, 6).T.ravel()
+        off[(a, b)] += blk
+    iu = np.triu_indices(6)
+    assert np.array_equal(ne.diag[:, iu[0], iu[1]], diag)
+    assert np.array_equal(ne.grad, grad)
+    assert set(map(tuple, prs)) == set(off) and np.all(prs[:, 0] < prs[:, 1])
+    for p, blk in zip(prs, ne.off):
+        assert np.array_equal(blk.ravel(), off[tuple(p)])
+    assert ne.count == count and abs(ne.cost - cost) <= 1e-12 * abs(cost)
+    # dense form vs the reference's per-factor scatter of the unpacked linearizations
+    h_ref = np.zeros((6 * V, 6 * V))
+    g_ref = np.zeros(6 * V)
+    for f in range(F):
+        lin = RG.unpack_record(rec[f], unary[f])
+        i = vs[f]
+        h_ref[6 * i:6 * i + 6, 6 * i:6 * i + 6] += lin.h_ii
+        g_ref[6 * i:6 * i + 6] += lin.b_i
+        if unary[f]:
+            continue
+        j = vt[f]
+        h_ref[6 * j:6 * j + 6, 6 * j:6 * j + 6] += lin.h_jj
+        h_ref[6 * i:6 * i + 6, 6 * j:6 * j + 6] += lin.h_ij
+        h_ref[6 * j:6 * j + 6, 6 * i:6 * i + 6] += lin.h_ij.T
+        g_ref[6 * j:6 * j + 6] += lin.b_j
+    h, g = ne.dense()
+    assert np.allclose(h, h_ref, rtol=1e-12, atol=1e-9) and np.allclose(g, g_ref, rtol=1e-12, atol=1e-9)
