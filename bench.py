@@ -297,6 +297,26 @@ def run_ours(args):
         d2h = len(wl.pairs) * REC * 8
     e2e_value = total_points / (statistics.median(e2e_ms) / 1e3)
 
+    # ---- e2e of the normal equations: the same linearization, summed into
+    # the block-sparse H/g on the device, only the system crosses PCIe ----
+    ne_line = None
+    if world == 1:
+        pairs = batch.assemble_setup(V)
+        ne_out = torch.empty(batch.asm_size, dtype=torch.float64).pin_memory().numpy()
+        ne_ms = []
+        for k in range(args.e2e_steps + 2):
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            batch.assemble_poses(poses_np, out=ne_out, unpack=False)
+            if k >= 2:
+                ne_ms.append((time.perf_counter() - a) * 1e3)
+        ne_line = {"value": total_points / (statistics.median(ne_ms) / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(poses_host.numel() * 8),
+                   "d2h_bytes_per_step": int(batch.asm_size * 8),
+                   "ms_per_step": statistics.median(ne_ms), "variables": int(V),
+                   "pairs": int(len(pairs)),
+                   "api": "DeviceBatch.assemble_poses (vg_batch_assemble_poses)"}
+
     # ---- roofline of the dominant kernel (K4) ----
     peak, peak_kind = hbm_peak()
     k4_avg_s = statistics.mean(k4_ms) / 1e3
@@ -324,6 +344,7 @@ def run_ours(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": statistics.median(e2e_ms)},
+            "e2e_normal_equations": ne_line,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_record(),

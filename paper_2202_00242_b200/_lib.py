@@ -359,13 +359,16 @@ class DeviceBatch:
         self.asm_size = int(total.value)
         return pairs
 
-    def assemble_poses(self, poses: np.ndarray, out: np.ndarray | None = None) -> "NormalEquations":
+    def assemble_poses(self, poses: np.ndarray, out: np.ndarray | None = None,
+                       unpack: bool = True):
+        """Normal equations at the pose table; `unpack=False` returns the flat C-ABI layout
+        (cost, count, diag V x 21, grad V x 6, pair blocks P x 36) in `out`."""
         poses = f64(poses).reshape(-1, 8)
         if out is None:
             out = np.empty(self.asm_size)
         check(self.ctx.lib.vg_batch_assemble_poses(self.handle, dptr(poses), poses.shape[0],
                                                    dptr(out)), "vg_batch_assemble_poses")
-        return NormalEquations.from_flat(out, self.asm_vars, self.asm_pairs)
+        return NormalEquations.from_flat(out, self.asm_vars, self.asm_pairs) if unpack else out
 
     def assemble_poses_device(self, poses_dev_ptr: int, num_poses: int, out_dev_ptr: int) -> None:
         check(self.ctx.lib.vg_batch_assemble_poses_device(

@@ -639,6 +639,9 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->asm_begin);
   dfree(ctx, b->asm_codes);
   dfree(ctx, b->asm_out);
+  dfree(ctx, b->asm_partial);
+  dfree(ctx, b->asm_done);
+  dfree(ctx, b->asm_gcost);
   cudaStreamSynchronize(ctx->stream);
   delete b;
   return VG_OK;
@@ -812,6 +815,10 @@ int vg_batch_assemble_setup(vg_batch* b, int64_t num_vars, int64_t* num_pairs,
   VG_CHECK(dalloc(ctx, &b->asm_begin, begin.size()));
   VG_CHECK(dalloc(ctx, &b->asm_codes, std::max<size_t>(codes.size(), 1)));
   VG_CHECK(dalloc(ctx, &b->asm_out, (size_t)total));
+  if (!b->asm_partial) VG_CHECK(dalloc(ctx, &b->asm_partial, 2 * 128));
+  if (!b->asm_done) VG_CHECK(dalloc(ctx, &b->asm_done, 1));
+  if (!b->asm_gcost && F) VG_CHECK(dalloc(ctx, &b->asm_gcost, (size_t)F));
+  VG_CUDA(cudaMemsetAsync(b->asm_done, 0, sizeof(unsigned), ctx->stream));
   VG_CHECK(h2d(ctx, b->asm_begin, begin.data(), sizeof(int) * begin.size()));
   if (!codes.empty()) VG_CHECK(h2d(ctx, b->asm_codes, codes.data(), sizeof(int) * codes.size()));
   VG_CUDA(cudaStreamSynchronize(ctx->stream));

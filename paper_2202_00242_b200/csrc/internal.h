@@ -131,6 +131,9 @@ struct vg_batch {
   int* asm_begin = nullptr;           // units + 1
   int* asm_codes = nullptr;           // factor * 8 + role
   double* asm_out = nullptr;          // device output (host-buffer entry point)
+  double* asm_partial = nullptr;      // per-CTA cost partials of k_assemble_cost
+  unsigned* asm_done = nullptr;       // its arrival counter (reset by the last CTA)
+  double2* asm_gcost = nullptr;       // per-factor (gated cost, 1 if gated in), written by K5
 };
 
 // error plumbing (capi.cu)

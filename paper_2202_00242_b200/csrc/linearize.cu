@@ -267,7 +267,8 @@ constexpr int kFinStride = 93;  // odd stride: conflict-free staging rows
 // records (92 doubles) are staged in shared memory and written out contiguously.
 __global__ void __launch_bounds__(kFinBlock)
     k_finalize(const FactorDev* __restrict__ factors, int fbase, int F,
-               const double* __restrict__ partials, int mode, double* __restrict__ out) {
+               const double* __restrict__ partials, int mode, double* __restrict__ out,
+               double2* __restrict__ gcost) {
   __shared__ double sh[kFinBlock * kFinStride];
   const int f0 = fbase + blockIdx.x * kFinBlock;
   const int fi = f0 + threadIdx.x;
@@ -275,7 +276,15 @@ __global__ void __launch_bounds__(kFinBlock)
     if (fi < F) finalize_one(factors[fi], fi, partials, mode, out, nullptr);
     return;
   }
-  if (fi < F) finalize_one(factors[fi], fi, partials, mode, out, sh + threadIdx.x * kFinStride);
+  if (fi < F) {
+    const double* o = sh + threadIdx.x * kFinStride;
+    finalize_one(factors[fi], fi, partials, mode, out, sh + threadIdx.x * kFinStride);
+    // gated cost + count per factor for the normal-equation assembly (factor_graph.py:271-275)
+    if (gcost) {
+      const bool in = o[91] >= (double)factors[fi].min_inliers;
+      gcost[fi] = make_double2(in ? o[90] : 0.0, in ? 1.0 : 0.0);
+    }
+  }
   __syncthreads();
   const int nf = min(kFinBlock, F - f0);
   double* dst = out + (size_t)f0 * 92;
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(kFinBlock)
 
 // ---- K6: block-sparse normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536)
 // One warp per output unit: unit u < V is variable u's diagonal block (21, upper) + gradient
-// (6); V <= u < V + P is the H block of variable pair u - V (36); unit V + P is the cost.
+// (6); V <= u < V + P is the H block of variable pair u - V (36).  The cost is k_assemble_cost.
 // A unit's contributions are listed in factor order (CSR, code = factor * 8 + role), and each
 // lane sums its element in that order from 0.0, so the result is the reference's sequential
 // per-block sum.  Roles: 0 source block (H_ii, b_i), 1 target block (H_jj, b_j), 2 H_ij as is,
@@ -319,52 +328,37 @@ __global__ void __launch_bounds__(128)
                double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (u > V + P) return;
-  if (u == V + P) {  // cost of the factors that pass their inlier gate, and their count
-    double c = 0.0, n = 0.0;
-    for (int f = lane; f < F; f += 32) {
-      const double* r = rec + (size_t)f * 92;
-      if (__ldg(r + 91) >= (double)__ldg(&factors[f].min_inliers)) {
-        c += __ldg(r + 90);
-        n += 1.0;
-      }
-    }
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-      c += __shfl_xor_sync(0xffffffffu, c, s);
-      n += __shfl_xor_sync(0xffffffffu, n, s);
-    }
-    if (lane == 0) {
-      out[0] = c;
-      out[1] = n;
-    }
-    return;
-  }
+  if (u >= V + P) return;
   const int k0 = __ldg(begin + u), k1 = __ldg(begin + u + 1);
   const bool diag = u < V;
   const int nel = diag ? 27 : 36;
   double acc0 = 0.0, acc1 = 0.0;  // elements lane and lane + 32
   const bool has0 = lane < nel, has1 = lane + 32 < nel;
-  // four contributions in flight per step; additions stay in contribution order
-  for (int k = k0; k < k1; k += 4) {
-    double v0[4], v1[4];
+  // 32 codes per coalesced load, eight contributions' values in flight per step; the
+  // additions stay in contribution order
+  for (int kb = k0; kb < k1; kb += 32) {
+    const int my_code = kb + lane < k1 ? __ldg(codes + kb + lane) : 0;
+    const int nk = min(32, k1 - kb);
+    for (int j = 0; j < nk; j += 8) {
+      double v0[8], v1[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      v0[q] = 0.0;
-      v1[q] = 0.0;
-      if (k + q < k1) {
-        const int code = __ldg(codes + k + q);
-        const double* r = rec + (size_t)(code >> 3) * 92;
-        if (has0) v0[q] = asm_value(r, code & 7, lane);
-        if (has1) v1[q] = asm_value(r, code & 7, lane + 32);
+      for (int q = 0; q < 8; ++q) {
+        const int code = __shfl_sync(0xffffffffu, my_code, (j + q) & 31);
+        v0[q] = 0.0;
+        v1[q] = 0.0;
+        if (j + q < nk) {
+          const double* r = rec + (size_t)(code >> 3) * 92;
+          if (has0) v0[q] = asm_value(r, code & 7, lane);
+          if (has1) v1[q] = asm_value(r, code & 7, lane + 32);
+        }
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (j + q < nk) {
+          acc0 += v0[q];
+          acc1 += v1[q];
+        }
     }
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (k + q < k1) {
-        acc0 += v0[q];
-        acc1 += v1[q];
-      }
   }
   if (diag) {
     if (lane < 21) out[2 + (size_t)u * 21 + lane] = acc0;
@@ -599,7 +593,7 @@ int launch_spread_T(vg_ctx* ctx, vg_batch* b) {
 int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1) {
   if (f1 <= f0) return 0;
   k_finalize<<<(f1 - f0 + kFinBlock - 1) / kFinBlock, kFinBlock, 0, ctx->stream>>>(
-      b->factors, f0, f1, b->partials, mode, out_dev);
+      b->factors, f0, f1, b->partials, mode, out_dev, mode == 0 ? b->asm_gcost : nullptr);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
@@ -609,12 +603,67 @@ int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev) {
   return launch_finalize_range(ctx, b, mode, out_dev, 0, (int)b->F);
 }
 
+namespace vg {
+// cost and count of the factors that pass their inlier gate (K5 writes them per factor to
+// asm_gcost, coalesced): kCostBlocks CTAs each sum a
+// fixed contiguous factor range (strided per thread, fixed tree), the last CTA to finish adds
+// the partials in block order (deterministic)
+constexpr int kCostThreads = 256;
+constexpr int kCostBlocks = 128;
+__global__ void __launch_bounds__(kCostThreads)
+    k_assemble_cost(const double2* __restrict__ gcost, int F, double* __restrict__ partial,
+                    unsigned* __restrict__ done, double* __restrict__ out) {
+  __shared__ double sc[kCostThreads], sn[kCostThreads];
+  __shared__ bool last;
+  const int t = threadIdx.x;
+  const int per = (F + kCostBlocks - 1) / kCostBlocks;
+  const int f0 = blockIdx.x * per, f1 = min(F, f0 + per);
+  double c = 0.0, n = 0.0;
+  for (int f = f0 + t; f < f1; f += kCostThreads) {
+    const double2 v = __ldg(gcost + f);
+    c += v.x;
+    n += v.y;
+  }
+  sc[t] = c;
+  sn[t] = n;
+  __syncthreads();
+  for (int s = kCostThreads / 2; s >= 1; s >>= 1) {
+    if (t < s) {
+      sc[t] += sc[t + s];
+      sn[t] += sn[t + s];
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    partial[2 * blockIdx.x] = sc[0];
+    partial[2 * blockIdx.x + 1] = sn[0];
+    __threadfence();
+    last = atomicAdd(done, 1u) == kCostBlocks - 1;
+  }
+  __syncthreads();
+  if (last && t == 0) {
+    __threadfence();
+    double cc = 0.0, nn = 0.0;
+    for (int b = 0; b < kCostBlocks; ++b) {
+      cc += __ldcg(partial + 2 * b);
+      nn += __ldcg(partial + 2 * b + 1);
+    }
+    out[0] = cc;
+    out[1] = nn;
+    *done = 0u;  // ready for the next launch
+  }
+}
+}  // namespace vg
+
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev) {
-  const int units = (int)(b->asm_vars + b->asm_pairs_n + 1);
-  k_assemble<<<(units + 3) / 4, 128, 0, ctx->stream>>>(rec, b->factors, (int)b->F, b->asm_begin,
+  const int units = (int)(b->asm_vars + b->asm_pairs_n);
+  if (units > 0)
+    k_assemble<<<(units + 3) / 4, 128, 0, ctx->stream>>>(rec, b->factors, (int)b->F, b->asm_begin,
                                                        b->asm_codes, (int)b->asm_vars,
                                                        (int)b->asm_pairs_n, out_dev);
-  ctx->launches++;
+  k_assemble_cost<<<kCostBlocks, kCostThreads, 0, ctx->stream>>>(
+      b->asm_gcost, (int)b->F, b->asm_partial, b->asm_done, out_dev);
+  ctx->launches += 2;
   VG_CUDA(cudaGetLastError());
   return 0;
 }

@@ -60,7 +60,14 @@ def main():
     res["finalize_ms"] = timeit(lambda: b.finalize_device(0, out.data_ptr()), False)
     b.finalize_device(3, out.data_ptr())
     torch.cuda.synchronize()
-    res["inliers_total"] = float(out[:, 1].sum().item()) if False else None
+    # normal-equation assembly (K6 + cost): full assemble step minus the linearize step
+    b.assemble_setup(poses.shape[0])
+    ne = torch.empty(b.asm_size, dtype=torch.float64, device="cuda")
+    res["step_linearize_ms"] = timeit(
+        lambda: b.linearize_poses_device(poses.data_ptr(), poses.shape[0], 0, out.data_ptr()), True)
+    res["step_assemble_ms"] = timeit(
+        lambda: b.assemble_poses_device(poses.data_ptr(), poses.shape[0], ne.data_ptr()), True)
+    res["assemble_only_ms"] = res["step_assemble_ms"] - res["step_linearize_ms"]
     print(json.dumps(res))
 
 
