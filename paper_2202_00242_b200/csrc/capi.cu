@@ -385,10 +385,10 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   std::vector<FactorDev> fac(F);
   // dedupe clouds and maps (sort by handle address)
   std::vector<std::pair<const void*, int64_t>> ck(F), mk(F);
+  bool all_covs = true;  // without covariances a batch serves VG_MODE_INLIERS only
   for (int64_t f = 0; f < F; ++f) {
     if (!specs[f].source || !specs[f].target) return fail(VG_ERR_INVALID, "factor without cloud/map");
-    if (!specs[f].source->has_cov && specs[f].source->n > 0)
-      return fail(VG_ERR_INVALID, "source frame has no covariances");
+    if (!specs[f].source->has_cov && specs[f].source->n > 0) all_covs = false;
     ck[f] = {specs[f].source, f};
     mk[f] = {specs[f].target, f};
   }
@@ -486,6 +486,7 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   b->num_maps = (int)maps.size();
   b->max_var = (int)max_var;
   b->host_factors = fac;
+  b->all_covs = all_covs;
   b->stages = S;
   b->stage_factors = stage_factors;
   b->stage_items = stage_items;
@@ -656,6 +657,13 @@ static int kmode_of(int mode) {
   return mode == VG_MODE_COST ? 1 : mode == VG_MODE_INLIERS ? 2 : 0;
 }
 
+static int check_mode(const vg_batch* b, int mode) {
+  if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
+  if (mode != VG_MODE_INLIERS && !b->all_covs)
+    return fail(VG_ERR_INVALID, "source frame has no covariances");
+  return VG_OK;
+}
+
 static int run_device(vg_batch* b, int mode, double* out_dev) {
   VG_CHECK(launch_accumulate(b->ctx, b, kmode_of(mode)));
   VG_CHECK(launch_finalize(b->ctx, b, mode, out_dev));
@@ -695,7 +703,7 @@ static int run_to_host(vg_batch* b, int mode, double* out_host) {
 
 int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_host) {
   if (!b || (b->F && (!T_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
-  if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
+  VG_CHECK(check_mode(b, mode));
   if (b->F == 0) return VG_OK;
   vg_ctx* ctx = b->ctx;
   // scatter T_ij into the 128 B factor records (dst pitch 128, src pitch 96)
@@ -717,7 +725,7 @@ static int ensure_poses(vg_batch* b, int64_t V) {
 int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, int mode,
                              double* out_host) {
   if (!b || (b->F && (!poses_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
-  if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
+  VG_CHECK(check_mode(b, mode));
   if (b->F == 0) return VG_OK;
   if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
   VG_CHECK(ensure_poses(b, V));
@@ -729,7 +737,7 @@ int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, i
 int vg_batch_linearize_poses_device(vg_batch* b, const double* poses_dev, int64_t V, int mode,
                                     double* out_dev) {
   if (!b || !out_dev) return fail(VG_ERR_INVALID, "null argument");
-  if (mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad mode");
+  VG_CHECK(check_mode(b, mode));
   if (b->F == 0) return VG_OK;
   if (poses_dev) {
     if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
@@ -745,7 +753,8 @@ int vg_batch_compose_device(vg_batch* b, const double* poses_dev, int64_t V) {
 }
 
 int vg_batch_accumulate_device(vg_batch* b, int mode) {
-  if (!b || mode < 0 || mode > 3) return fail(VG_ERR_INVALID, "bad arguments");
+  if (!b) return fail(VG_ERR_INVALID, "bad arguments");
+  VG_CHECK(check_mode(b, mode));
   return launch_accumulate(b->ctx, b, kmode_of(mode));
 }
 
@@ -840,6 +849,7 @@ int vg_batch_assemble_pairs(const vg_batch* b, int32_t* pairs_out) {
 static int run_assemble(vg_batch* b, const double* poses_dev, int64_t V, double* out_dev) {
   if (b->asm_vars < 0) return fail(VG_ERR_INVALID, "assembly not set up (vg_batch_assemble_setup)");
   if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  VG_CHECK(check_mode(b, VG_MODE_LINEARIZE));
   vg_ctx* ctx = b->ctx;
   if (b->F) {
     VG_CHECK(launch_compose(ctx, b, poses_dev));

@@ -101,6 +101,7 @@ struct vg_batch {
   int key_mode = 2;                   // 1: all maps 32-bit local keys, 0: all int64, 2: mixed
   int all_pow2 = 0;                   // every map's resolution is a power of two
   int all_f32 = 0;                    // every source point is fp32-exact (no xyz64 copy)
+  bool all_covs = true;               // every source has covariances (else INLIERS mode only)
   vg::FactorDev* factors = nullptr;   // F
   vg::ItemDev* items = nullptr;       // num_items (ordered by target map, then factor)
   vg::CloudView* clouds = nullptr;    // num_clouds

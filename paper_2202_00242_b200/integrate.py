@@ -6,7 +6,8 @@
     undo()
 
 Every replaced name keeps the reference's signature, argument meaning and exceptions
-(registration.py:29-269, preprocess.py:68-164, factor_graph.py:209-308).  Modules that
+(registration.py:29-269, preprocess.py:68-164, factor_graph.py:209-308); the keyframe overlap
+matrix of OdometryEstimator (odometry.py:396-403) becomes one batched lookup launch.  Modules that
 imported a name with ``from .registration import ...`` (factor_graph.py:49-55,
 odometry.py:21-46) get their module-level binding replaced too; the reference's
 FactorGraph, LM solver, IMU factors and odometry logic are untouched and call the drop-in
@@ -57,6 +58,19 @@ REPLACEMENTS = {
 }
 
 
+def _overlap_matrix(self):
+    """OdometryEstimator._overlap_matrix (odometry.py:396-403) as one batched launch."""
+    kfs = self.keyframes
+    return _rg.overlap_matrix([kf.frame for kf in kfs], [kf.voxelmap for kf in kfs],
+                              [kf.pose() for kf in kfs])
+
+
+# methods of reference classes whose per-pair loops become one batched GPU call
+METHOD_REPLACEMENTS = {
+    "odometry": {"OdometryEstimator": {"_overlap_matrix": _overlap_matrix}},
+}
+
+
 def _module(pkg, sub):
     if isinstance(pkg, str):
         name = f"{pkg}.{sub}"
@@ -81,6 +95,16 @@ def patch(pkg="limapper"):
             if hasattr(mod, name):
                 saved.append((mod, name, getattr(mod, name)))
                 setattr(mod, name, obj)
+    for sub, classes in METHOD_REPLACEMENTS.items():
+        mod = _module(pkg, sub) if not hasattr(pkg, sub) else getattr(pkg, sub)
+        for cname, methods in classes.items():
+            cls = getattr(mod, cname, None) if mod is not None else None
+            if cls is None:
+                continue
+            for name, fn in methods.items():
+                if name in vars(cls):
+                    saved.append((cls, name, vars(cls)[name]))
+                    setattr(cls, name, fn)
 
     def undo():
         for mod, name, obj in reversed(saved):

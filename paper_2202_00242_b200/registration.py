@@ -237,6 +237,56 @@ def overlap_rate(frame, vmap, t_ij) -> float:
     return float(hits[0]) / len(frame)
 
 
+# overlap batches, keyed by the identities of their device clouds and maps
+_overlap_cache: "OrderedDict[tuple, _lib.DeviceBatch]" = OrderedDict()
+
+
+def _overlap_cloud(frame):
+    # reuse the factor path's upload when the frame carries covariances
+    return device_cloud(frame, with_covs=getattr(frame, "covs", None) is not None)
+
+
+def overlap_rates(frames, vmaps, t_ijs) -> np.ndarray:
+    """overlap_rate (registration.py:168-173) for many (frame, map, T_ij) triples in one
+    launch (VG_MODE_INLIERS: K4a lookups + hit counts only).  Empty inputs give 0.0."""
+    n = len(frames)
+    out = np.zeros(n)
+    idx = [k for k in range(n) if len(frames[k]) and len(vmaps[k])]
+    if not idx:
+        return out
+    clouds = [_overlap_cloud(frames[k]) for k in idx]
+    maps = [_as_device_map(vmaps[k]) for k in idx]
+    key = tuple((id(c), id(m)) for c, m in zip(clouds, maps))
+    b = _overlap_cache.get(key)
+    if b is None or any(x is not c for x, c in zip(b._keep[0], clouds)) \
+            or any(x is not m for x, m in zip(b._keep[1], maps)):
+        b = _lib.DeviceBatch(clouds, maps, [False] * len(idx), [0] * len(idx))
+        _overlap_cache[key] = b
+        while len(_overlap_cache) > 16:
+            _overlap_cache.popitem(last=False)
+    else:
+        _overlap_cache.move_to_end(key)
+    T = np.stack([transform12(t_ijs[k]) for k in idx])
+    rec = b.linearize(T, _lib.MODE_INLIERS)
+    out[idx] = rec[:, 1] / np.array([len(frames[k]) for k in idx], dtype=float)
+    return out
+
+
+def overlap_matrix(frames, vmaps, poses) -> np.ndarray:
+    """out[i, j] = overlap_rate(frames[i], vmaps[j], T_j^-1 T_i) for i != j, 0 on the
+    diagonal: the keyframe overlap matrix of odometry.py:396-403 in one launch."""
+    m = len(frames)
+    out = np.zeros((m, m))
+    pairs = [(i, j) for i in range(m) for j in range(m) if i != j]
+    if not pairs:
+        return out
+    rates = overlap_rates([frames[i] for i, _ in pairs], [vmaps[j] for _, j in pairs],
+                          [pose_compose(pose_inverse(poses[j]), poses[i]) for i, j in pairs])
+    for (i, j), r in zip(pairs, rates):
+        out[i, j] = r
+    return out
+
+
 @dataclass(frozen=True)
 class MatchingCostLinearization:
     """Gauss-Newton blocks of the matching cost (registration.py:176-191)."""

@@ -403,3 +403,27 @@ def test_device_normal_equations_match_host_assembly(small_graph):
         g_ref[6 * j:6 * j + 6] += lin.b_j
     h, g = ne.dense()
     assert np.allclose(h, h_ref, rtol=1e-12, atol=1e-9) and np.allclose(g, g_ref, rtol=1e-12, atol=1e-9)
+
+
+def test_overlap_rates_and_keyframe_matrix(small_graph):
+    """Batched overlap_rate / keyframe overlap matrix (odometry.py:396-403) equal the oracle's
+    per-pair overlap_rate exactly (integer hit counts / n); empty inputs give 0."""
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    frames = [make_frame(s, c) for s, c in srcs[:6]]
+    vmaps = [RG.build_voxelmap(make_frame(s, c), 1.0) for s, c in zip(scans[:6], covs[:6])]
+    m = RG.overlap_matrix(frames, vmaps, est[:6])
+    for i in range(6):
+        assert m[i, i] == 0.0
+        for j in range(6):
+            if i == j:
+                continue
+            tij = G.pose_compose(G.pose_inverse(est[j]), est[i])
+            ref = O.overlap_rate(srcs[i][0], maps[j], tij.rotation.matrix(), tij.translation)
+            assert m[i, j] == ref
+            assert RG.overlap_rate(frames[i], vmaps[j], tij) == ref
+    # frames without covariances work for overlap (lookups only); empty frames give 0
+    bare = make_frame(srcs[0][0], None)
+    empty = make_frame(np.zeros((0, 3)), np.zeros((0, 3, 3)))
+    r = RG.overlap_rates([bare, empty], [vmaps[1], vmaps[1]],
+                         [G.pose_compose(G.pose_inverse(est[1]), est[0])] * 2)
+    assert r[0] == m[0, 1] and r[1] == 0.0

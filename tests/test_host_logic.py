@@ -106,12 +106,20 @@ def test_integrate_patch_replaces_and_restores():
                                            unrelated=sentinel),
         factor_graph=types.SimpleNamespace(MatchingCostFactor=sentinel),
         preprocess=types.SimpleNamespace(knn_search=sentinel),
-        odometry=types.SimpleNamespace(overlap_rate=sentinel))
+        odometry=types.SimpleNamespace(overlap_rate=sentinel, OdometryEstimator=None))
+
+    class OdometryEstimator:
+        def _overlap_matrix(self):
+            return "reference loop"
+
+    pkg.odometry.OdometryEstimator = OdometryEstimator
     undo = integrate.patch(pkg)
+    assert OdometryEstimator._overlap_matrix is integrate._overlap_matrix
     assert pkg.registration.build_voxelmap is registration.build_voxelmap
     assert pkg.factor_graph.MatchingCostFactor is factor_graph.MatchingCostFactor
     assert pkg.odometry.overlap_rate is registration.overlap_rate
     assert pkg.registration.unrelated is sentinel
     undo()
+    assert OdometryEstimator()._overlap_matrix() == "reference loop"
     assert pkg.registration.build_voxelmap is sentinel
     assert pkg.preprocess.knn_search is sentinel
