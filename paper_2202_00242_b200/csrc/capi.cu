@@ -457,11 +457,21 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     const vg_cloud* c = specs[f].source;
     grouped = c->n <= srcgroup_max_points() && c->exact32 && specs[f].target->kmode == 1;
   }
+  // item size: up to kMaxChunk points, smaller when the batch is too small to give every
+  // K4a warp slot of the GPU (148 SMs x 32) about one item
+  long long total_pts = 0;
+  for (int64_t f = 0; f < F; ++f) total_pts += specs[f].source->n;
+  static int sms = 0;
+  if (!sms && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device) != cudaSuccess)
+    sms = 148;
+  const long long want = (long long)sms * 32;
+  long long chunk = ((total_pts + want - 1) / want + 31) / 32 * 32;
+  chunk = std::max<long long>(64, std::min<long long>(kMaxChunk, chunk));
   for (int64_t f : order) {
     const long long n = specs[f].source->n;
     npts += n;
     fac[f].item_begin = (int)items.size();
-    long long nchunks = std::max<long long>(1, (n + kMaxChunk - 1) / kMaxChunk);
+    long long nchunks = std::max<long long>(1, (n + chunk - 1) / chunk);
     for (long long c = 0; c < nchunks; ++c) {
       ItemDev it;
       it.factor = (int)f;
@@ -623,6 +633,9 @@ int vg_batch_destroy(vg_batch* b) {
   if (!b) return VG_OK;
   vg_ctx* ctx = b->ctx;
   if (b->graph) cudaGraphExecDestroy(b->graph);
+  if (b->hgraph) cudaGraphExecDestroy(b->hgraph);
+  if (b->h_poses) cudaFreeHost(b->h_poses);
+  if (b->h_out) cudaFreeHost(b->h_out);
   dfree(ctx, b->factors);
   dfree(ctx, b->items);
   dfree(ctx, b->clouds);
@@ -722,12 +735,66 @@ static int ensure_poses(vg_batch* b, int64_t V) {
   return VG_OK;
 }
 
+// Small batches through the host API are launch-latency bound: the pose-table upload,
+// K-compose, K4a, K4b, K5 and the record download are captured once into a CUDA graph over
+// pinned staging buffers owned by the batch, so a call is two host memcpys + one launch.
+static constexpr size_t kSmallHostBytes = 1 << 20;
+
+static int run_small_host(vg_batch* b, const double* poses_host, int64_t V, int mode,
+                          double* out_host) {
+  vg_ctx* ctx = b->ctx;
+  const size_t out_bytes = sizeof(double) * rec_of(mode) * b->F;
+  const size_t pose_bytes = sizeof(double) * 8 * V;
+  if (!b->hgraph || b->hgraph_mode != mode || b->hgraph_V != V) {
+    if (b->hgraph) cudaGraphExecDestroy(b->hgraph);
+    b->hgraph = nullptr;
+    if (b->h_poses) cudaFreeHost(b->h_poses);
+    if (b->h_out) cudaFreeHost(b->h_out);
+    b->h_poses = b->h_out = nullptr;
+    VG_CUDA(cudaMallocHost((void**)&b->h_poses, pose_bytes));
+    VG_CUDA(cudaMallocHost((void**)&b->h_out, out_bytes));
+    VG_CHECK(ensure_poses(b, V));
+    VG_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaGraph_t g;
+    const long long l0 = ctx->launches;
+    VG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e1 = cudaMemcpyAsync(b->poses, b->h_poses, pose_bytes, cudaMemcpyHostToDevice,
+                                     ctx->stream);
+    int rc = e1 == cudaSuccess ? launch_compose(ctx, b, b->poses) : VG_ERR_CUDA;
+    if (!rc) rc = run_device(b, mode, b->out);
+    cudaError_t e2 = rc ? cudaSuccess
+                        : cudaMemcpyAsync(b->h_out, b->out, out_bytes, cudaMemcpyDeviceToHost,
+                                          ctx->stream);
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    b->hgraph_launches = ctx->launches - l0;
+    ctx->launches = l0;
+    if (rc) return rc;
+    if (e1 != cudaSuccess) return vg_cuda_fail(e1, "cudaMemcpyAsync (capture)");
+    if (e2 != cudaSuccess) return vg_cuda_fail(e2, "cudaMemcpyAsync (capture)");
+    if (e != cudaSuccess) return vg_cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&b->hgraph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return vg_cuda_fail(e, "cudaGraphInstantiate");
+    b->hgraph_mode = mode;
+    b->hgraph_V = V;
+  }
+  memcpy(b->h_poses, poses_host, pose_bytes);
+  VG_CUDA(cudaGraphLaunch(b->hgraph, ctx->stream));
+  ctx->launches += b->hgraph_launches;
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  memcpy(out_host, b->h_out, out_bytes);
+  return VG_OK;
+}
+
 int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, int mode,
                              double* out_host) {
   if (!b || (b->F && (!poses_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
   VG_CHECK(check_mode(b, mode));
   if (b->F == 0) return VG_OK;
   if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  if (b->stages <= 1 && sizeof(double) * rec_of(mode) * b->F <= kSmallHostBytes &&
+      sizeof(double) * 8 * V <= kSmallHostBytes && !getenv("VGICP_NO_HOST_GRAPH"))
+    return run_small_host(b, poses_host, V, mode, out_host);
   VG_CHECK(ensure_poses(b, V));
   VG_CHECK(h2d(b->ctx, b->poses, poses_host, sizeof(double) * 8 * V));
   VG_CHECK(launch_compose(b->ctx, b, b->poses));
@@ -885,9 +952,12 @@ int vg_batch_graph_capture(vg_batch* b, const double* poses_dev, int64_t V, int 
     b->graph = nullptr;
   }
   cudaGraph_t g;
+  const long long l0 = ctx->launches;
   VG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   int rc = vg_batch_linearize_poses_device(b, poses_dev, V, mode, out_dev);
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  b->graph_launches = ctx->launches - l0;
+  ctx->launches = l0;
   if (rc) return rc;
   if (e != cudaSuccess) return vg_cuda_fail(e, "cudaStreamEndCapture");
   e = cudaGraphInstantiate(&b->graph, g, 0);
@@ -899,7 +969,7 @@ int vg_batch_graph_capture(vg_batch* b, const double* poses_dev, int64_t V, int 
 int vg_batch_graph_launch(vg_batch* b) {
   if (!b || !b->graph) return fail(VG_ERR_INVALID, "no captured graph");
   VG_CUDA(cudaGraphLaunch(b->graph, b->ctx->stream));
-  b->ctx->launches += 3;
+  b->ctx->launches += b->graph_launches;
   return VG_OK;
 }
 

@@ -124,6 +124,14 @@ struct vg_batch {
   int stages = 1;
   std::vector<int> stage_factors, stage_items;
   cudaGraphExec_t graph = nullptr;
+  long long graph_launches = 0;
+  // small-batch host path: graph over pinned staging (see run_small_host in capi.cu)
+  cudaGraphExec_t hgraph = nullptr;
+  long long hgraph_launches = 0;
+  int hgraph_mode = -1;
+  long long hgraph_V = -1;
+  double* h_poses = nullptr;
+  double* h_out = nullptr;
   std::vector<vg::FactorDev> host_factors;
   // normal-equation assembly (vg_batch_assemble_*): CSR of contributions per output unit
   long long asm_vars = -1;            // variables (pose-table rows < asm_vars); -1: not set up

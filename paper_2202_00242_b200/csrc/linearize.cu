@@ -152,6 +152,8 @@ __device__ __forceinline__ void store_sym6(double* out, const double* A, const d
     }
 }
 
+__device__ __forceinline__ void expand_record(const FactorDev& f, const double* s, double* o);
+
 // one factor; LINEARIZE records go to `o92` (shared memory staging), others straight to out
 __device__ __forceinline__ void finalize_one(const FactorDev& f, int fi,
                                              const double* __restrict__ partials, int mode,
@@ -180,7 +182,12 @@ __device__ __forceinline__ void finalize_one(const FactorDev& f, int fi,
     for (int k = 0; k < 29; ++k) o[k] = s[k];
     return;
   }
-  double* o = o92;
+  expand_record(f, s, o92);
+}
+
+// fp64 adjoint expansion of one factor's 29 sums (H' 21, b' 6, cost, inliers) into the
+// 92-double record, with min_inliers gating (factor_graph.py:282-291)
+__device__ __forceinline__ void expand_record(const FactorDev& f, const double* s, double* o) {
   const double cost = s[27], inliers = s[28];
   if (inliers < (double)f.min_inliers) {  // DegenerateConstraint -> zero blocks
     for (int k = 0; k < 90; ++k) o[k] = 0.0;
@@ -292,6 +299,49 @@ __global__ void __launch_bounds__(kFinBlock)
     const int r = k / 92;
     dst[k] = sh[r * kFinStride + (k - r * 92)];
   }
+}
+
+// K5, warp per factor (batches with few factors or many items per factor): lane k sums value
+// k over the factor's items in item order — the same additions as k_finalize's per-thread
+// loop, so the records are bit-identical — then lane 0 expands and the warp writes out.
+constexpr int kFinWarps = 4;
+__global__ void __launch_bounds__(kFinWarps * 32)
+    k_finalize_warp(const FactorDev* __restrict__ factors, int fbase, int F,
+                    const double* __restrict__ partials, int mode, double* __restrict__ out,
+                    double2* __restrict__ gcost) {
+  __shared__ double sh[kFinWarps][32 + 92];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int fi = fbase + blockIdx.x * kFinWarps + w;
+  if (fi >= F) return;
+  const FactorDev& f = factors[fi];
+  const int ib = f.item_begin, ic = f.item_count;
+  if (mode == 1 || mode == 3) {
+    if (lane < 2) {
+      double v = 0.0;
+      for (int it = 0; it < ic; ++it) v += partials[2 * (size_t)(ib + it) + lane];
+      out[2 * (size_t)fi + lane] = v;
+    }
+    return;
+  }
+  double v = 0.0;
+  if (lane < 29)
+    for (int it = 0; it < ic; ++it) v += partials[(size_t)(ib + it) * kPartialStride + lane];
+  if (mode == 2) {
+    if (lane < 29) out[(size_t)fi * 29 + lane] = v;
+    return;
+  }
+  double* sw = sh[w];
+  sw[lane] = v;
+  __syncwarp();
+  if (lane == 0) {
+    expand_record(f, sw, sw + 32);
+    if (gcost) {
+      const bool in = sw[32 + 91] >= (double)f.min_inliers;
+      gcost[fi] = make_double2(in ? sw[32 + 90] : 0.0, in ? 1.0 : 0.0);
+    }
+  }
+  __syncwarp();
+  for (int k = lane; k < 92; k += 32) out[(size_t)fi * 92 + k] = sw[32 + k];
 }
 
 // ---- K6: block-sparse normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536)
@@ -592,6 +642,14 @@ int launch_spread_T(vg_ctx* ctx, vg_batch* b) {
 
 int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1) {
   if (f1 <= f0) return 0;
+  // few factors or long item lists: a warp per factor sums the items in parallel lanes
+  if (b->F < 4096 || b->num_items > 4 * b->F) {
+    k_finalize_warp<<<(f1 - f0 + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, ctx->stream>>>(
+        b->factors, f0, f1, b->partials, mode, out_dev, mode == 0 ? b->asm_gcost : nullptr);
+    ctx->launches++;
+    VG_CUDA(cudaGetLastError());
+    return 0;
+  }
   k_finalize<<<(f1 - f0 + kFinBlock - 1) / kFinBlock, kFinBlock, 0, ctx->stream>>>(
       b->factors, f0, f1, b->partials, mode, out_dev, mode == 0 ? b->asm_gcost : nullptr);
   ctx->launches++;

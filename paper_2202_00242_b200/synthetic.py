@@ -102,3 +102,14 @@ def config1_scans(n_az: int = 256, n_el: int = 64):
     source = scan(p_i, dirs, np.random.default_rng(1))
     xi = perturbation(np.random.default_rng(3), 0.1, 5.0)
     return source, target, pose_retract(p_i, xi), p_j
+
+
+def circle_trajectory(count: int, step: float = 0.4, center=(0.11, 0.13, 0.0)) -> list:
+    """`count` poses `step` metres apart on a circle in the room, yaw along the tangent."""
+    radius = max(count * step / (2 * math.pi), 3.0)
+    poses = []
+    for k in range(count):
+        a = k * step / radius
+        t = [center[0] + radius * math.cos(a), center[1] + radius * math.sin(a), center[2]]
+        poses.append(yaw_pose(a + math.pi / 2, t))
+    return poses

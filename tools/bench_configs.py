@@ -1,0 +1,166 @@
+#!/usr/bin/env python
+"""Single-GPU BASELINE configs other than the headline one: 1 (single binary factor),
+3 (odometry window, unary + 3 resolutions) and 4 (local mapping, 4,950 factors).
+
+One JSON line per config, with the fields of bench.py's line: device-resident linearization
+step (compose + K4a + K4b + K5 replayed as one CUDA graph; CUDA events on the launching
+stream, L2 flushed between steps; K4 timed separately with stream launches), e2e through DeviceBatch.linearize_poses with pinned host buffers, K4's fraction of the
+HBM roofline (84 B/correspondence), and the CPU oracle on all host cores over a
+bounded factor sample.  Config 5 is bench.py itself.
+
+    python tools/bench_configs.py [--configs 1,3,4] [--steps 50] > profiles/r01_configs.jsonl
+"""
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+from paper_2202_00242_b200 import _lib, workloads  # noqa: E402
+
+BUILDERS = {1: workloads.single_factor, 3: workloads.odometry_window, 4: workloads.local_mapping}
+
+
+def cpu_sample(wl, max_points=2_000_000):
+    """Oracle inputs for the first factors up to ~max_points correspondences."""
+    from oracle import vgicp_oracle as O
+
+    fids, pts = [], 0
+    for f in range(len(wl.clouds)):
+        if fids and pts + len(wl.host_sources[f][0]) > max_points:
+            break
+        fids.append(f)
+        pts += len(wl.host_sources[f][0])
+    maps, cache = {}, {}
+    for f in fids:
+        tp, tc, res = wl.host_targets[f]
+        key = (id(tp), res)
+        if key not in cache:
+            cache[key] = O.build_voxelmap(tp, tc, res)
+        maps[f] = cache[key]
+    R, t = O.relative_transforms(wl.pose_table, wl.var_source[fids], wl.var_target[fids])
+    sample = {"pairs": np.array([(f, f) for f in fids]), "maps": maps,
+              "sources": {f: wl.host_sources[f] for f in fids},
+              "R": np.zeros((max(fids) + 1, 3, 3)), "t": np.zeros((max(fids) + 1, 3)),
+              "points": pts}
+    sample["R"][fids] = R
+    sample["t"][fids] = t
+    return sample, len(fids)
+
+
+def run(cfg, args, ctx, stream):
+    wl = BUILDERS[cfg]()
+    batch = wl.batch(ctx=ctx)
+    ctx.set_stream(stream.cuda_stream)
+    V = wl.pose_table.shape[0]
+    F = len(wl.clouds)
+    REC = _lib.RECORD_SIZE[_lib.MODE_LINEARIZE]
+    poses = torch.from_numpy(wl.pose_table).cuda()
+    out = torch.zeros((F, REC), dtype=torch.float64, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+
+    def step(ev=None):
+        if ev:
+            ev[0].record()
+        batch.compose_device(poses.data_ptr(), V)
+        if ev:
+            ev[1].record()
+        batch.accumulate_device(_lib.MODE_LINEARIZE)
+        if ev:
+            ev[2].record()
+        batch.finalize_device(_lib.MODE_LINEARIZE, out.data_ptr())
+        if ev:
+            ev[3].record()
+
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    with bench.ClockSampler(0) as clk:
+        for k in range(args.steps):
+            flush.zero_()
+            step(evs[k])
+        torch.cuda.synchronize()
+    step_ms = [e[0].elapsed_time(e[3]) for e in evs]
+    k4_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    ms = statistics.median(step_ms)
+    if not args.no_graph:
+        # the step as one CUDA graph launch (small configs are launch-latency bound)
+        batch.capture_graph(poses.data_ptr(), V, _lib.MODE_LINEARIZE, out.data_ptr())
+        for _ in range(3):
+            batch.launch_graph()
+        gms = []
+        for k in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            batch.launch_graph()
+            e1.record()
+            torch.cuda.synchronize()
+            gms.append(e0.elapsed_time(e1))
+        ms = statistics.median(gms)
+    # e2e: host pose table in, host records out (pinned)
+    poses_h = torch.from_numpy(wl.pose_table.copy()).pin_memory().numpy()
+    out_h = torch.empty((F, REC), dtype=torch.float64).pin_memory().numpy()
+    e2e = []
+    for k in range(args.steps + 2):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        batch.linearize_poses(poses_h, _lib.MODE_LINEARIZE, out=out_h)
+        if k >= 2:
+            e2e.append((time.perf_counter() - a) * 1e3)
+    peak, kind = bench.hbm_peak()
+    achieved = bench.BYTES_PER_CORR * wl.num_points / (statistics.median(k4_ms) / 1e3) / 1e9
+    cpu = None
+    if not args.no_cpu:
+        from oracle import cpu_baseline
+
+        sample, nf = cpu_sample(wl)
+        rate, sec, procs = cpu_baseline.time_sample(sample, steps=2, warmup=1)
+        cpu = {"value": rate, "unit": bench.UNIT, "cores": procs, "kind": "port",
+               "sample": f"first {nf} factors, {sample['points']} correspondences per pass, "
+                         f"oracle linearization (unary factors evaluated as binary), "
+                         f"{procs}-process fork pool, 2 passes"}
+    cfgd = dict(wl.config)
+    cfgd.update({"workload": wl.name, "corr_per_step": wl.num_points,
+                 "l2": "flushed between timed steps (256 MB write)",
+                 "step": "one CUDA graph (compose + K4a + K4b + K5)" if not args.no_graph
+                 else "stream launches"})
+    return {"metric": bench.METRIC, "value": wl.num_points / (ms / 1e3), "unit": bench.UNIT,
+            "n_gpus": 1, "steps": args.steps, "ms_per_step": ms, "higher_is_better": True,
+            "dtype": "f32+f64", "data": "synthetic", "config": cfgd,
+            "e2e": {"value": wl.num_points / (statistics.median(e2e) / 1e3), "unit": bench.UNIT,
+                    "h2d_bytes_per_step": int(wl.pose_table.nbytes),
+                    "d2h_bytes_per_step": int(F * REC * 8),
+                    "ms_per_step": statistics.median(e2e)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "kernel": "K4 (K4a + K4b)",
+                         "kernel_ms": statistics.median(k4_ms),
+                         "bytes_per_corr": bench.BYTES_PER_CORR, "peak_kind": kind},
+            "clocks": clk.summary(), "cpu_baseline": cpu}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,3,4")
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true")
+    args = ap.parse_args()
+    ctx = _lib.context(0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    for c in (int(x) for x in args.configs.split(",")):
+        print(json.dumps(run(c, args, ctx, stream)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
