@@ -300,6 +300,38 @@ def run_ours(args):
     # ---- e2e of the normal equations: the same linearization, summed into
     # the block-sparse H/g on the device, only the system crosses PCIe ----
     ne_line = None
+    if world > 1:
+        # every rank assembles its shard in the global pair layout; one NCCL sum-reduction
+        # puts the per-pose-pair H/b blocks on the solver rank, which copies them to the host
+        gp = sharding.global_pairs(wl.pairs[:, 0], wl.pairs[:, 1], np.zeros(len(wl.pairs), bool),
+                                   V)
+        batch.assemble_setup(V, gp)
+        ne_dev = torch.empty(batch.asm_size, dtype=torch.float64, device="cuda")
+        ne_host = torch.empty(batch.asm_size, dtype=torch.float64).pin_memory()
+        ne_ms = []
+        for k in range(args.e2e_steps + 2):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a = time.perf_counter()
+            if rank == 0:
+                poses_dev.copy_(poses_host, non_blocking=True)
+            sharding.broadcast_poses(poses_dev, 0)
+            batch.assemble_poses_device(poses_dev.data_ptr(), V, ne_dev.data_ptr())
+            sharding.reduce_normal_equations(ne_dev, 0)
+            if rank == 0:
+                ne_host.copy_(ne_dev, non_blocking=False)
+            torch.cuda.synchronize()
+            dt = torch.tensor([(time.perf_counter() - a) * 1e3], dtype=torch.float64,
+                              device="cuda")
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            if k >= 2:
+                ne_ms.append(float(dt.item()))
+        ne_line = {"value": total_points / (statistics.median(ne_ms) / 1e3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(poses_host.numel() * 8),
+                   "d2h_bytes_per_step": int(batch.asm_size * 8),
+                   "ms_per_step": statistics.median(ne_ms), "variables": int(V),
+                   "pairs": int(len(gp)),
+                   "api": "DeviceBatch.assemble_poses_device + NCCL reduce (sharding)"}
     if world == 1:
         pairs = batch.assemble_setup(V)
         ne_out = torch.empty(batch.asm_size, dtype=torch.float64).pin_memory().numpy()

@@ -167,6 +167,11 @@ int vg_batch_graph_launch(vg_batch* batch);
  * frame-state keys embeds them top-left (factor_graph.py:292-308). */
 int vg_batch_assemble_setup(vg_batch* batch, int64_t num_vars, int64_t* num_pairs,
                             int64_t* out_doubles);
+/* same with a caller-given pair list (sorted, unique, a < b): every rank of a sharded graph
+ * passes the global list, so the per-rank systems share one layout and one sum-reduction
+ * combines them.  Pairs of this batch missing from the list: VG_ERR_INVALID. */
+int vg_batch_assemble_setup_pairs(vg_batch* batch, int64_t num_vars, const int32_t* pairs,
+                                  int64_t num_pairs, int64_t* out_doubles);
 int vg_batch_assemble_pairs(const vg_batch* batch, int32_t* pairs_out /* P x 2 */);
 int vg_batch_assemble_poses(vg_batch* batch, const double* poses_host, int64_t num_poses,
                             double* out_host);

@@ -82,6 +82,8 @@ _SIGNATURES = {
     "vg_batch_graph_capture": ([c_void_p, c_void_p, c_int64, c_int, c_void_p], c_int),
     "vg_batch_graph_launch": ([c_void_p], c_int),
     "vg_batch_assemble_setup": ([c_void_p, c_int64, _P_I64, _P_I64], c_int),
+    "vg_batch_assemble_setup_pairs": ([c_void_p, c_int64, POINTER(c_int32), c_int64, _P_I64],
+                                      c_int),
     "vg_batch_assemble_pairs": ([c_void_p, POINTER(c_int32)], c_int),
     "vg_batch_assemble_poses": ([c_void_p, _P_D, c_int64, _P_D], c_int),
     "vg_batch_assemble_poses_device": ([c_void_p, c_void_p, c_int64, c_void_p], c_int),
@@ -344,16 +346,25 @@ class DeviceBatch:
         check(self.ctx.lib.vg_batch_graph_launch(self.handle))
 
     # ---- normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536) ----------
-    def assemble_setup(self, num_vars: int) -> np.ndarray:
+    def assemble_setup(self, num_vars: int, pairs: np.ndarray | None = None) -> np.ndarray:
         """Variables are pose-table rows < num_vars; returns the (P, 2) variable pairs whose
-        off-diagonal blocks the assembly produces."""
+        off-diagonal blocks the assembly produces — the batch's own pairs, or `pairs` (a
+        sorted global list shared by all ranks of a sharded graph)."""
         P, total = c_int64(), c_int64()
-        check(self.ctx.lib.vg_batch_assemble_setup(self.handle, int(num_vars), ctypes.byref(P),
-                                                   ctypes.byref(total)), "vg_batch_assemble_setup")
-        pairs = np.empty((int(P.value), 2), dtype=np.int32)
-        if P.value:
-            check(self.ctx.lib.vg_batch_assemble_pairs(
-                self.handle, pairs.ctypes.data_as(POINTER(c_int32))), "vg_batch_assemble_pairs")
+        if pairs is None:
+            check(self.ctx.lib.vg_batch_assemble_setup(self.handle, int(num_vars),
+                                                       ctypes.byref(P), ctypes.byref(total)),
+                  "vg_batch_assemble_setup")
+            pairs = np.empty((int(P.value), 2), dtype=np.int32)
+            if P.value:
+                check(self.ctx.lib.vg_batch_assemble_pairs(
+                    self.handle, pairs.ctypes.data_as(POINTER(c_int32))),
+                    "vg_batch_assemble_pairs")
+        else:
+            pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+            check(self.ctx.lib.vg_batch_assemble_setup_pairs(
+                self.handle, int(num_vars), pairs.ctypes.data_as(POINTER(c_int32)), len(pairs),
+                ctypes.byref(total)), "vg_batch_assemble_setup_pairs")
         self.asm_vars = int(num_vars)
         self.asm_pairs = pairs
         self.asm_size = int(total.value)

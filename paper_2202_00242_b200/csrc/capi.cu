@@ -830,8 +830,22 @@ int vg_batch_finalize_device(vg_batch* b, int mode, double* out_dev) {
   return launch_finalize(b->ctx, b, mode, out_dev);
 }
 
+static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, int64_t given_P,
+                          int64_t* num_pairs, int64_t* out_doubles);
+
 int vg_batch_assemble_setup(vg_batch* b, int64_t num_vars, int64_t* num_pairs,
                             int64_t* out_doubles) {
+  return assemble_setup(b, num_vars, nullptr, -1, num_pairs, out_doubles);
+}
+
+int vg_batch_assemble_setup_pairs(vg_batch* b, int64_t num_vars, const int32_t* pairs,
+                                  int64_t num_pairs, int64_t* out_doubles) {
+  if (num_pairs < 0 || (num_pairs && !pairs)) return fail(VG_ERR_INVALID, "invalid pair list");
+  return assemble_setup(b, num_vars, pairs, num_pairs, nullptr, out_doubles);
+}
+
+static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, int64_t given_P,
+                          int64_t* num_pairs, int64_t* out_doubles) {
   if (!b || num_vars <= 0 || num_vars >= (1LL << 28))
     return fail(VG_ERR_INVALID, "invalid assembly arguments");
   vg_ctx* ctx = b->ctx;
@@ -870,13 +884,32 @@ int vg_batch_assemble_setup(vg_batch* b, int64_t num_vars, int64_t* num_pairs,
     begin.push_back((int)codes.size());
     codes.insert(codes.end(), diag[v].begin(), diag[v].end());
   }
-  for (size_t i = 0; i < pc.size(); ++i) {
-    if (i == 0 || pc[i].first != pc[i - 1].first) {
+  if (given) {
+    // caller's (global) pair list, e.g. the same on every rank so blocks can be summed with
+    // one reduction; pairs this batch does not touch stay zero
+    size_t k = 0;
+    for (int64_t p = 0; p < given_P; ++p) {
+      const long long a = given[2 * p], c = given[2 * p + 1];
+      if (a < 0 || c >= V || a >= c || (p && a * V + c <= (long long)given[2 * p - 2] * V + given[2 * p - 1]))
+        return fail(VG_ERR_INVALID, "pair list must be sorted, unique, a < b < num_vars");
       begin.push_back((int)codes.size());
-      pairs.push_back((int)(pc[i].first / V));
-      pairs.push_back((int)(pc[i].first % V));
+      pairs.push_back((int)a);
+      pairs.push_back((int)c);
+      for (; k < pc.size() && pc[k].first == a * V + c; ++k) codes.push_back(pc[k].second);
+      if (k < pc.size() && pc[k].first < a * V + c)
+        return fail(VG_ERR_INVALID, "a factor's variable pair is missing from the pair list");
     }
-    codes.push_back(pc[i].second);
+    if (k != pc.size())
+      return fail(VG_ERR_INVALID, "a factor's variable pair is missing from the pair list");
+  } else {
+    for (size_t i = 0; i < pc.size(); ++i) {
+      if (i == 0 || pc[i].first != pc[i - 1].first) {
+        begin.push_back((int)codes.size());
+        pairs.push_back((int)(pc[i].first / V));
+        pairs.push_back((int)(pc[i].first % V));
+      }
+      codes.push_back(pc[i].second);
+    }
   }
   begin.push_back((int)codes.size());
   const long long P = (long long)pairs.size() / 2;

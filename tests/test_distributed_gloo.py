@@ -103,3 +103,71 @@ def test_lpt_balance_large():
         loads = sharding.shard_loads(w, sharding.lpt_shards(w, n))
         assert loads.max() / loads.min() < 1.0005
         assert sum(len(s) for s in sharding.lpt_shards(w, n)) == 50000
+
+
+def assemble_np(rec, vs, vt, unary, V, pairs):
+    """NumPy model of vg_batch_assemble_* (K6): flat [cost, count, diag V x 21, grad V x 6,
+    pair blocks P x 36], block sums in factor order."""
+    index = {(int(a), int(b)): k for k, (a, b) in enumerate(pairs)}
+    diag, grad = np.zeros((V, 21)), np.zeros((V, 6))
+    off = np.zeros((len(pairs), 36))
+    cost = count = 0.0
+    for f in range(len(rec)):
+        r = rec[f]
+        if r[91] >= 10:
+            cost += r[90]
+            count += 1
+        diag[vs[f]] += r[0:21]
+        grad[vs[f]] += r[78:84]
+        if unary[f]:
+            continue
+        diag[vt[f]] += r[57:78]
+        grad[vt[f]] += r[84:90]
+        a, b = min(vs[f], vt[f]), max(vs[f], vt[f])
+        off[index[(a, b)]] += r[21:57] if vs[f] < vt[f] else r[21:57].reshape(6, 6).T.ravel()
+    return np.concatenate([[cost, count], diag.ravel(), grad.ravel(), off.ravel()])
+
+
+def _ne_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(5)
+    V, F = 9, 60
+    vs = rng.integers(0, V, F)
+    vt = (vs + rng.integers(1, V, F)) % V
+    unary = rng.uniform(size=F) < 0.2
+    rec = rng.normal(size=(F, 92))
+    rec[:, 91] = rng.integers(0, 40, F)
+    pairs = sharding.global_pairs(vs, vt, unary, V)
+    shards = sharding.lpt_shards(rng.integers(200, 600, F), world)
+    mine = shards[rank]
+    flat = torch.from_numpy(assemble_np(rec[mine], vs[mine], vt[mine], unary[mine], V, pairs))
+    sharding.reduce_normal_equations(flat, dst=0)
+    if rank == 0:
+        ref = assemble_np(rec, vs, vt, unary, V, pairs)
+        q.put(float(np.max(np.abs(flat.numpy() - ref) / np.maximum(np.abs(ref), 1.0))))
+    dist.destroy_process_group()
+
+
+def test_two_rank_normal_equations_reduce_matches_single_process():
+    """Per-rank normal equations in the global pair layout (sharding.global_pairs), summed
+    onto the solver rank, equal the single-process assembly to fp64 rounding."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ne_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert err < 1e-12
+
+
+def test_global_pairs_layout():
+    vs = np.array([0, 2, 1, 3, 2, 0])
+    vt = np.array([1, 0, 0, 9, 2, 3])
+    unary = np.array([False, False, False, False, False, True])
+    assert sharding.global_pairs(vs, vt, unary, 4).tolist() == [[0, 1], [0, 2]]

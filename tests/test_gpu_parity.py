@@ -433,3 +433,34 @@ def test_overlap_rates_and_keyframe_matrix(small_graph):
     r = RG.overlap_rates([bare, empty], [vmaps[1], vmaps[1]],
                          [G.pose_compose(G.pose_inverse(est[1]), est[0])] * 2)
     assert r[0] == m[0, 1] and r[1] == 0.0
+
+
+def test_sharded_normal_equations_share_the_global_layout(small_graph):
+    """Two factor shards assembled in the global pair layout (vg_batch_assemble_setup_pairs,
+    what every rank of a sharded graph does before the sum-reduction) add up to the
+    single-batch system."""
+    from paper_2202_00242_b200 import sharding
+
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
+    F, V = len(pairs), len(est)
+    table = np.array([G.pose_row(p) for p in est])
+    unary = np.zeros(F, bool)
+    gp = sharding.global_pairs(pairs[:, 0], pairs[:, 1], unary, V)
+
+    def system(ids, layout):
+        b = _lib.DeviceBatch([clouds[pairs[f, 0]] for f in ids], [dmaps[pairs[f, 1]] for f in ids],
+                             [False] * len(ids), [10] * len(ids), pairs[ids, 0], pairs[ids, 1])
+        b.assemble_setup(V, layout)
+        return b.assemble_poses(table, unpack=False)
+
+    full = system(np.arange(F), None)
+    shards = sharding.lpt_shards(np.ones(F), 2)
+    parts = [system(s, gp) for s in shards]
+    assert full.shape == parts[0].shape == parts[1].shape
+    tot = parts[0] + parts[1]
+    assert np.allclose(tot, full, rtol=1e-12, atol=1e-9 * np.abs(full).max())
+    # a layout missing one of the batch's pairs is rejected
+    with pytest.raises(Exception):
+        system(np.arange(F), gp[1:])
