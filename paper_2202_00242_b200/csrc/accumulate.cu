@@ -6,7 +6,7 @@
 //
 // K4a — one warp per (factor, <=512-point chunk) item, light on registers so many warps hide
 //   the two dependent memory latencies of a lookup (source point, then the probed key
-//   bucket).  x = R p + t (fp64) -> key (bit-exact floor) -> one 32 B bucket of 8 local keys.
+//   bucket).  x = R p + t (fp64) -> key (bit-exact floor) -> one 16 B bucket of 4 local keys.
 //   Hits are written as (point, row) pairs into the item's region of a batch-wide hit list
 //   with a warp ballot, preserving point order.  Misses contribute nothing (:150-156).
 // K4b — one warp per item over its compacted hits, so every lane of the expensive fp64 path
@@ -224,19 +224,23 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     q.live = q.live && i < end && m > 0;
     return q;
   };
-  auto load256 = [&](unsigned bucket, long long (&g)[4]) {
-    ld256(keys32 + (size_t)bucket * kBucket, g[0], g[1], g[2], g[3]);
+  auto load_bucket = [&](unsigned bucket, unsigned (&g)[4]) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(keys32 + (size_t)bucket * kBucket32));
+    g[0] = v.x;
+    g[1] = v.y;
+    g[2] = v.z;
+    g[3] = v.w;
   };
   float4 a0 = __ldg(pa + min(begin + lane, last));
   float4 a1 = __ldg(pa + min(begin + 32 + lane, last));
   Q q0 = make_q(a0, begin + lane);
-  long long g0[4] = {0, 0, 0, 0};
-  if (q0.live) load256(q0.bucket, g0);
+  unsigned g0[4] = {0, 0, 0, 0};
+  if (q0.live) load_bucket(q0.bucket, g0);
   for (int base = begin; base < end; base += 32) {
     const int i = base + lane;
     const Q q1 = make_q(a1, i + 32);
-    long long g1[4] = {0, 0, 0, 0};
-    if (q1.live) load256(q1.bucket, g1);
+    unsigned g1[4] = {0, 0, 0, 0};
+    if (q1.live) load_bucket(q1.bucket, g1);
     a1 = __ldg(pa + min(i + 64, last));
     int slot = -1;
     if (q0.live) {
@@ -245,18 +249,17 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
         int found = -1;
         bool empty = false;
 #pragma unroll
-        for (int j = kBucket - 1; j >= 0; --j) {
-          const unsigned kj = (unsigned)((unsigned long long)g0[j >> 1] >> (32 * (j & 1)));
-          if (kj == q0.k32) found = j;
-          empty |= (kj == kEmpty32);
+        for (int j = kBucket32 - 1; j >= 0; --j) {
+          if (g0[j] == q0.k32) found = j;
+          empty |= (g0[j] == kEmpty32);
         }
         if (found >= 0) {
-          slot = (int)(bk * kBucket + found);
+          slot = (int)(bk * kBucket32 + found);
           break;
         }
         if (empty) break;
         bk = (bk + 1) & mask;
-        load256(bk, g0);
+        load_bucket(bk, g0);
       }
     }
     // misses contribute nothing (registration.py:150-156)

@@ -157,14 +157,16 @@ __device__ __forceinline__ unsigned slot_of(long long key, int shift) {
 // before spilling to the next one, so a lookup resolves in its home bucket unless that
 // bucket is full.  Two key encodings:
 //   kmode 1 — 32-bit cell-local keys (lx | ly << 11 | lz << 22 relative to the map's min
-//             cell); a bucket of 8 keys is 32 B = one 256-bit load.  Load <= 0.25.  The probe
-//             returns the slot; the record sits at the same slot (it carries the row).
+//             cell); a bucket of 4 keys is 16 B = one 128-bit load.  Load <= 0.25, so ~0.4% of
+//             buckets overflow into the next one.  The probe returns the slot; the record sits
+//             at the same slot (it carries the row).
 //   kmode 0 — the reference's packed int64 keys in 64 B buckets of 8 (two 256-bit loads,
 //             load <= 0.25); the probe returns the slot, a parallel array gives the row and
 //             records are row-indexed.
 // The local key is built from decode(pack(floor)) — the reference's own key round trip —
 // so aliasing of out-of-range indices behaves exactly as the reference's packed keys.
-constexpr int kBucket = 8;
+constexpr int kBucket = 8;    // kmode 0: int64 keys, 64 B buckets
+constexpr int kBucket32 = 4;  // kmode 1: 32-bit keys, 16 B buckets (one 128-bit load)
 constexpr unsigned kEmpty32 = 0xffffffffu;
 
 struct Query {
@@ -230,7 +232,9 @@ __device__ __forceinline__ Query make_query_local(const MapView& mv, double fx, 
 __device__ __forceinline__ ProbeGroup probe_load(const MapView& mv, unsigned bucket, int kmode) {
   ProbeGroup g;
   if (kmode) {
-    ld256(mv.keys32 + (size_t)bucket * kBucket, g.k[0], g.k[1], g.k[2], g.k[3]);
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(mv.keys32 + (size_t)bucket * kBucket32));
+    g.k[0] = (long long)((unsigned long long)v.x | ((unsigned long long)v.y << 32));
+    g.k[1] = (long long)((unsigned long long)v.z | ((unsigned long long)v.w << 32));
   } else {
     const long long* p = mv.keys + (size_t)bucket * kBucket;
     ld256(p, g.k[0], g.k[1], g.k[2], g.k[3]);
@@ -247,7 +251,7 @@ __device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& g
   bool empty = false;
   if (kmode) {
 #pragma unroll
-    for (int j = kBucket - 1; j >= 0; --j) {
+    for (int j = kBucket32 - 1; j >= 0; --j) {
       const unsigned kj = (unsigned)((unsigned long long)g.k[j >> 1] >> (32 * (j & 1)));
       if (kj == q.k32) found = j;
       empty |= (kj == kEmpty32);
@@ -260,7 +264,7 @@ __device__ __forceinline__ int probe_scan(const MapView& mv, const ProbeGroup& g
     }
   }
   if (found >= 0) {
-    slot = (int)(bucket * kBucket + found);
+    slot = (int)(bucket * (kmode ? kBucket32 : kBucket) + found);
     return 1;
   }
   return empty ? 0 : -1;

@@ -81,8 +81,8 @@ struct vg_map {
     v.ez = ez;
     v.res = res;
     v.inv_res = 1.0 / res;
-    v.mask = (capacity / vg::kBucket) - 1;
-    v.shift = (kmode ? 32 : 64) - (log2cap - 3);
+    v.mask = (capacity / (kmode ? vg::kBucket32 : vg::kBucket)) - 1;
+    v.shift = kmode ? 32 - (log2cap - 2) : 64 - (log2cap - 3);
     v.m = (int)m;
     int e2 = 0;
     v.pow2 = (std::frexp(res, &e2) == 0.5) ? 1 : 0;

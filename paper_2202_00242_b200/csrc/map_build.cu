@@ -107,8 +107,8 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
         (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
     bool placed = false;
     for (unsigned b = (k32 * 0x9E3779B9u) >> mv.shift; !placed; b = (b + 1) & mv.mask)
-      for (int j = 0; j < kBucket && !placed; ++j) {
-        h = (size_t)b * kBucket + j;
+      for (int j = 0; j < kBucket32 && !placed; ++j) {
+        h = (size_t)b * kBucket32 + j;
         placed = atomicCAS(pkeys32 + h, kEmpty32, k32) == kEmpty32;
       }
   } else {
@@ -209,7 +209,7 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
     for (size_t i = 0; i < hk.size() && hk[i] == empty; ++i) ++empty;
   }
   map->empty_key = empty;
-  // capacity: pow2 >= 4m slots in 8-slot buckets (load <= 0.25)
+  // capacity: pow2 >= 4m slots (load <= 0.25) in 8-slot (kmode 0) / 4-slot (kmode 1) buckets
   int l2 = 3;
   while ((1LL << l2) < 4 * map->m) ++l2;
   map->capacity = 1u << l2;

@@ -5,7 +5,7 @@
 // processed by one CTA while the source cloud sits in shared memory:
 //   * the source points and fp64 covariances are loaded once per CTA pass (cp.async) instead
 //     of once per factor and per hit — per correspondence the L2 traffic drops to the hash
-//     probe (one 32 B bucket) plus, on a hit, the voxel record (80 B);
+//     probe (one 16 B bucket) plus, on a hit, the voxel record (80 B);
 //   * 12 producer warps transform points straight out of shared memory, probe the target
 //     map's hash (4 lookups in flight per lane: only the probe latency remains), compact the
 //     hits and stream them as rounds of 32 into their own 3-slot ring: point indices plus the
