@@ -392,6 +392,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
@@ -407,14 +408,17 @@ __device__ __forceinline__ void cp_async_wait() {
 // banks, so 8 lanes of a 16 B shared-memory read hit 8 distinct 4-bank groups: conflict free)
 constexpr int kRecUnits = 5;
 constexpr int kRecStride = 5;
-struct AccStage {
-  float4 pt[2][32];
+// PT: 16 B point units per lane — 2 (fp64 xyz possible) or 1 (every point fp32-exact)
+template <int PT>
+struct AccStageT {
+  float4 pt[PT][32];
   float4 cov[3][32];
   float4 rec[32][kRecStride];
 };
-template <int kStages>
+using AccStage = AccStageT<2>;
+template <int kStages, int PT = 2>
 struct AccSmem {
-  AccStage stage[kStages];
+  AccStageT<PT> stage[kStages];
 };
 
 // Gather one round (32 hits; the last round of an item pads with replays of its last hit) into
@@ -423,18 +427,18 @@ struct AccSmem {
 // records are gathered cooperatively: each cp.async instruction covers 32 consecutive 16 B
 // units of 6-7 records instead of one unit of 32 records, cutting L1 wavefronts ~4x.
 // Always commits one group so every lane has the same number of outstanding groups.
-template <int kStages>
+template <int kStages, int PT = 2>
 __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& mv,
-                                            AccSmem<kStages>& sm, int round, int2 e, int nvalid,
-                                            int lane) {
-  AccStage& st = sm.stage[round % kStages];
+                                            AccSmem<kStages, PT>& sm, int round, int2 e,
+                                            int nvalid, int lane) {
+  AccStageT<PT>& st = sm.stage[round % kStages];
   if (lane < nvalid) {
-    if (cv.xyz64) {
+    if (PT == 2 && cv.xyz64) {
       const double* p = cv.xyz64 + 3 * (size_t)e.x;
       double* d = reinterpret_cast<double*>(&st.pt[0][lane]);
       cp_async8(d, p);
       cp_async8(d + 1, p + 1);
-      cp_async8(reinterpret_cast<double*>(&st.pt[1][lane]), p + 2);
+      cp_async8(reinterpret_cast<double*>(&st.pt[PT - 1][lane]), p + 2);
     } else {
       cp_async16(&st.pt[0][lane], cv.a + e.x);
     }
@@ -455,16 +459,16 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
 
 // per-hit fp64 math of K4b on one staged hit: moved point, residual, fused covariance and its
 // inverse, cost, and the target-frame Jacobian blocks about the source origin
-template <int MODE>
-__device__ __forceinline__ void hit_math(const AccStage& st, int lane, bool f64pts,
+template <int MODE, int PT = 2>
+__device__ __forceinline__ void hit_math(const AccStageT<PT>& st, int lane, bool f64pts,
                                          const double (&R)[9], const double (&t)[3],
                                          double scale, double (&acc)[28]) {
   double px, py, pz;
-  if (f64pts) {
+  if (PT == 2 && f64pts) {
     const double* d = reinterpret_cast<const double*>(&st.pt[0][lane]);
     px = d[0];
     py = d[1];
-    pz = reinterpret_cast<const double*>(&st.pt[1][lane])[0];
+    pz = reinterpret_cast<const double*>(&st.pt[PT - 1][lane])[0];
   } else {
     const float4 a = st.pt[0][lane];
     px = a.x;
@@ -542,7 +546,7 @@ __device__ __forceinline__ void hit_math(const AccStage& st, int lane, bool f64p
 // K4b.  ILP rounds of 32 hits are computed per iteration (ILP = 2 gives each lane two
 // independent fp64 dependency chains); kStages >= 2 * ILP staged rounds keep the gathers of
 // the next kStages - ILP rounds in flight during the math.
-template <int MODE, int kStages, int kMinBlocks, int ILP>
+template <int MODE, int kStages, int kMinBlocks, int ILP, int PT = 2>
 __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     k_accumulate(const AccDesc* __restrict__ descs, int n_items, const int2* __restrict__ hits,
                  double* __restrict__ partials, int dbg) {
@@ -552,7 +556,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   const int wib = threadIdx.x >> 5;
   const int w = blockIdx.x * kAccWarps + wib;
   if (w >= n_items) return;
-  AccSmem<kStages>& sm = reinterpret_cast<AccSmem<kStages>*>(smem_raw)[wib];
+  AccSmem<kStages, PT>& sm = reinterpret_cast<AccSmem<kStages, PT>*>(smem_raw)[wib];
   const AccDesc* dsc = descs + w;
   const int n = __ldg(&dsc->n);
   const int2* hl = hits + __ldg(&dsc->hoff);
@@ -570,7 +574,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   cv.n = 0;
   MapView mv;
   mv.recs = (const VoxelRec*)__ldg((const unsigned long long*)&dsc->recs);
-  const bool f64pts = cv.xyz64 != nullptr;
+  const bool f64pts = PT == 2 && cv.xyz64 != nullptr;
 
   double acc[28];
 #pragma unroll
@@ -584,7 +588,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 #pragma unroll
   for (int r = 0; r < kAhead; ++r) {
     const int k = r * 32 + lane;
-    issue_round(cv, mv, sm, r, hl[min(k, klast)], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - r * 32),
+    issue_round<kStages, PT>(cv, mv, sm, r, hl[min(k, klast)], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - r * 32),
                 lane);
   }
   // hit entries are prefetched one iteration ahead of their gather; the loads are
@@ -600,7 +604,8 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
       const int ri = r + kAhead + u;
-      issue_round(cv, mv, sm, ri, nxt[u], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - ri * 32), lane);
+      issue_round<kStages, PT>(cv, mv, sm, ri, nxt[u], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - ri * 32),
+                               lane);
     }
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
@@ -611,11 +616,12 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     __syncwarp();
     if (!(dbg & 2)) {
       if (ILP == 1) {  // branch over padding lanes
-        if (r * 32 + lane < n) hit_math<MODE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
+        if (r * 32 + lane < n)
+          hit_math<MODE, PT>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
       } else {  // branch-free so the ILP rounds interleave; padding lanes replay valid data
 #pragma unroll
         for (int u = 0; u < ILP; ++u)
-          hit_math<MODE>(sm.stage[(r + u) % kStages], lane, f64pts, R, t,
+          hit_math<MODE, PT>(sm.stage[(r + u) % kStages], lane, f64pts, R, t,
                          (r + u) * 32 + lane < n ? 1.0 : 0.0, acc);
       }
     }
@@ -1295,10 +1301,25 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
     case 4:
       return launch_acc_kernel(ctx, k_accumulate<0, 2, 4, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
                                cnt, b->hits, p, st);
+    case 5:  // fp32 points: ILP 2 with 4 stages at 3 CTAs/SM (smaller stages fit)
+      if (b->all_f32)
+        return launch_acc_kernel(ctx, k_accumulate<0, 4, 3, 2, 1>,
+                                 sizeof(AccSmem<4, 1>) * kAccWarps, d, cnt, b->hits, p, st);
+      break;
+    case 6:  // fp32 points: 3 stages
+      if (b->all_f32)
+        return launch_acc_kernel(ctx, k_accumulate<0, 3, 3, 1, 1>,
+                                 sizeof(AccSmem<3, 1>) * kAccWarps, d, cnt, b->hits, p, st);
+      break;
+
     default:
-      return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
-                               cnt, b->hits, p, st);
+      break;
   }
+  if (b->all_f32)  // every point fp32-exact: one 16 B point unit per lane (more L1 left)
+    return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1, 1>, sizeof(AccSmem<2, 1>) * kAccWarps,
+                             d, cnt, b->hits, p, st);
+  return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d, cnt,
+                           b->hits, p, st);
 }
 
 // K4a + K4b.  Experiment knobs (measured slower on config 5, kept off): VGICP_CHUNKS > 1
