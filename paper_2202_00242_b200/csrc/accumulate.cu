@@ -457,6 +457,12 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
   cp_async_commit();
 }
 
+template <int MODE>
+__device__ __forceinline__ void hit_core(double px, double py, double pz, double2 s0,
+                                         double2 s1, double2 s2, const float4* rec,
+                                         const double (&R)[9], const double (&t)[3],
+                                         double scale, double (&acc)[28]);
+
 // per-hit fp64 math of K4b on one staged hit: moved point, residual, fused covariance and its
 // inverse, cost, and the target-frame Jacobian blocks about the source origin
 template <int MODE, int PT = 2>
@@ -478,11 +484,20 @@ __device__ __forceinline__ void hit_math(const AccStageT<PT>& st, int lane, bool
   const double2 s0 = *reinterpret_cast<const double2*>(&st.cov[0][lane]);
   const double2 s1 = *reinterpret_cast<const double2*>(&st.cov[1][lane]);
   const double2 s2 = *reinterpret_cast<const double2*>(&st.cov[2][lane]);
-  const double2 m01 = *reinterpret_cast<const double2*>(&st.rec[lane][0]);
-  const double2 m2c0 = *reinterpret_cast<const double2*>(&st.rec[lane][1]);
-  const double2 c12 = *reinterpret_cast<const double2*>(&st.rec[lane][2]);
-  const double2 c34 = *reinterpret_cast<const double2*>(&st.rec[lane][3]);
-  const double v5 = reinterpret_cast<const double*>(&st.rec[lane][4])[0];
+  hit_core<MODE>(px, py, pz, s0, s1, s2, st.rec[lane], R, t, scale, acc);
+}
+
+// the math of one hit from its source point, source covariance rows and staged voxel record
+template <int MODE>
+__device__ __forceinline__ void hit_core(double px, double py, double pz, double2 s0,
+                                         double2 s1, double2 s2, const float4* rec,
+                                         const double (&R)[9], const double (&t)[3],
+                                         double scale, double (&acc)[28]) {
+  const double2 m01 = *reinterpret_cast<const double2*>(&rec[0]);
+  const double2 m2c0 = *reinterpret_cast<const double2*>(&rec[1]);
+  const double2 c12 = *reinterpret_cast<const double2*>(&rec[2]);
+  const double2 c34 = *reinterpret_cast<const double2*>(&rec[3]);
+  const double v5 = reinterpret_cast<const double*>(&rec[4])[0];
   // moved point (registration.py:148) and residual d = mu' - moved (:152)
   const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
   const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
