@@ -464,3 +464,41 @@ def test_sharded_normal_equations_share_the_global_layout(small_graph):
     # a layout missing one of the batch's pairs is rejected
     with pytest.raises(Exception):
         system(np.arange(F), gp[1:])
+
+
+@pytest.mark.parametrize("res,wide", [(0.3, False), (1.0, True)])
+def test_batch_general_paths_vs_oracle(small_graph, res, wide):
+    """Batches off the fast path: a non-power-of-two resolution (IEEE-division key fallback,
+    generic K4a), maps whose cells exceed the 32-bit local key frame (a far outlier point:
+    int64 keys, kmode 0), and non-fp32 source points (fp64 staging in K4b)."""
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    sel = pairs[:8]
+    table = np.array([G.pose_row(p) for p in est])
+    R, t = O.relative_transforms(table, sel[:, 0], sel[:, 1])
+    rng = np.random.default_rng(9)
+    for jitter in (False, True):
+        clouds, dmaps, refs = [], [], []
+        for f, (i, j) in enumerate(sel):
+            pts = srcs[i][0] + (rng.normal(scale=1e-9, size=srcs[i][0].shape) if jitter else 0.0)
+            tp, tc = scans[j], covs[j]
+            if wide and f % 2 == 0:  # a cell 3 km away: the key extent no longer fits 11 bits
+                # (every other map: the batch mixes 32-bit and int64 key tables)
+                tp = np.vstack([tp, [[3000.25, 0.25, 0.25]]])
+                tc = np.concatenate([tc, np.eye(3)[None] * 0.01])
+            clouds.append(_lib.DeviceCloud(pts, srcs[i][1]))
+            dmaps.append(_lib.DeviceMap.build(_lib.DeviceCloud(tp, tc), res))
+            refs.append((pts, O.build_voxelmap(tp, tc, res)))
+        batch = _lib.DeviceBatch(clouds, dmaps, [False] * len(sel), [10] * len(sel),
+                                 sel[:, 0], sel[:, 1])
+        out = batch.linearize_poses(table)
+        checked = 0
+        for f in range(len(sel)):
+            pts, vmap = refs[f]
+            try:
+                ref = O.linearize(pts, srcs[sel[f, 0]][1], vmap, R[f], t[f])
+            except ValueError:
+                assert out[f][91] < 10
+                continue
+            assert_lin(RG.unpack_record(out[f], False), ref, False)
+            checked += 1
+        assert checked >= len(sel) // 2
