@@ -11,8 +11,9 @@
 //   with a warp ballot, preserving point order.  Misses contribute nothing (:150-156).
 // K4b — one warp per item over its compacted hits, so every lane of the expensive fp64 path
 //   does useful work.  Each round of 32 hits gathers the source point (16 B), source
-//   covariance (48 B) and voxel record (80 B) with cp.async into a 3-stage shared-memory
-//   pipeline, so the gathers of rounds r+1, r+2 are in flight while round r computes.
+//   covariance (48 B) and voxel record (80 B) with cp.async into a 2-stage shared-memory
+//   pipeline, so the gathers of round r+1 are in flight while round r computes (hit entries
+//   are loaded two rounds ahead).
 //   The per-item 29-value partial (target-frame 6x6 about the source origin)
 //   is reduced across the warp in a fixed order.
 #include <cuda_runtime.h>
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
                    const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
                    const MapView* __restrict__ maps, int2* __restrict__ hits,
                    int* __restrict__ counts, double* __restrict__ partials2,
-                   AccDesc* __restrict__ descs, int prefetch_recs) {
+                   AccDesc* __restrict__ descs) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
   if (w >= n_items) return;
@@ -128,9 +129,6 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
       }
       if (r == 1) slot = rec_index(mv, slot, kmode);
       else slot = -1;
-      // warm L2 with the record line K4b will gather for this hit
-      if (r == 1 && prefetch_recs)
-        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(mv.recs + slot));
     }
     // misses contribute nothing (registration.py:150-156)
     const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
@@ -280,113 +278,8 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
   }
 }
 
-// K4a, batched variant: each lane resolves U points per iteration (U independent point loads,
-// then U independent bucket probes in flight), sub-rounds compacted in point order.
-template <int KM, int U, int kMinBlocks>
-__global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
-    k_lookup_batch(const ItemDev* __restrict__ items, int n_items,
-                   const FactorDev* __restrict__ factors, const CloudView* __restrict__ clouds,
-                   const MapView* __restrict__ maps, int2* __restrict__ hits,
-                   int* __restrict__ counts, double* __restrict__ partials2,
-                   AccDesc* __restrict__ descs) {
-  const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
-  if (w >= n_items) return;
-  const ItemDev it = items[w];
-  const FactorDev* f = factors + it.factor;
-  double R[9], t[3];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) R[k] = __ldg(f->T + k);
-#pragma unroll
-  for (int k = 0; k < 3; ++k) t[k] = __ldg(f->T + 9 + k);
-  const CloudView cv = clouds[__ldg(&f->cloud)];
-  const MapView mv = maps[__ldg(&f->map)];
-  const int kmode = KM == 2 ? mv.kmode : KM;
-  if (descs) {
-    AccDesc& d = descs[w];
-    double tv = 0.0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k)
-      if (lane == k) tv = R[k];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-      if (lane == 9 + k) tv = t[k];
-    if (lane < 12) d.T[lane] = tv;
-    else if (lane == 12) d.a = cv.a;
-    else if (lane == 13) d.xyz64 = cv.xyz64;
-    else if (lane == 14) d.c0 = cv.c0;
-    else if (lane == 15) d.c1 = cv.c1;
-    else if (lane == 16) d.c2 = cv.c2;
-    else if (lane == 17) d.recs = mv.recs;
-    else if (lane == 18) d.hoff = it.hoff;
-  }
-  const unsigned lt_mask = (1u << lane) - 1u;
-  int2* out = hits + it.hoff;
-  int cnt = 0;
-  const int last = it.end - 1;
-  for (int base = it.begin; base < it.end; base += 32 * U) {
-    double px[U], py[U], pz[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int ic = min(base + 32 * u + lane, last);
-      if (cv.xyz64) {
-        px[u] = __ldg(cv.xyz64 + 3 * (size_t)ic);
-        py[u] = __ldg(cv.xyz64 + 3 * (size_t)ic + 1);
-        pz[u] = __ldg(cv.xyz64 + 3 * (size_t)ic + 2);
-      } else {
-        const float4 a = __ldg(cv.a + ic);
-        px[u] = a.x;
-        py[u] = a.y;
-        pz[u] = a.z;
-      }
-    }
-    Query q[U];
-    bool live[U];
-    ProbeGroup g[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
-      const double x = fma(R[0], px[u], fma(R[1], py[u], R[2] * pz[u])) + t[0];
-      const double y = fma(R[3], px[u], fma(R[4], py[u], R[5] * pz[u])) + t[1];
-      const double z = fma(R[6], px[u], fma(R[7], py[u], R[8] * pz[u])) + t[2];
-      q[u] = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                        floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                        floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
-      live[u] = base + 32 * u + lane < it.end && mv.m && q[u].inside;
-      if (live[u]) g[u] = probe_load(mv, q[u].bucket, kmode);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      int slot = -1;
-      if (live[u]) {
-        unsigned bk = q[u].bucket;
-        int r;
-        while ((r = probe_scan(mv, g[u], bk, q[u], slot, kmode)) < 0) {
-          bk = next_bucket(bk, mv);
-          g[u] = probe_load(mv, bk, kmode);
-        }
-        slot = r == 1 ? rec_index(mv, slot, kmode) : -1;
-      }
-      // misses contribute nothing (registration.py:150-156)
-      const unsigned m = __ballot_sync(0xffffffffu, slot >= 0);
-      if (slot >= 0) out[cnt + __popc(m & lt_mask)] = make_int2(base + 32 * u + lane, slot);
-      cnt += __popc(m);
-    }
-  }
-  if (lane == 0) {
-    counts[w] = cnt;
-    if (partials2) {
-      partials2[2 * (size_t)w] = 0.0;
-      partials2[2 * (size_t)w + 1] = (double)cnt;
-    }
-    if (descs) descs[w].n = cnt;
-  }
-}
-
 // ---- K4b ------------------------------------------------------------------------------------
 constexpr int kAccWarps = 4;
-// stage layout (16 B units x 32 lanes): p0 p1 (point), c0 c1 c2 (source cov), r0..r4 (record)
-constexpr int kStageUnits = 10;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -666,571 +559,31 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 }
 
 
-// ---- K4b, persistent form ---------------------------------------------------------------------
-// Same per-round pipeline and math as k_accumulate, but each warp loops over items claimed
-// from a counter, and the NEXT item's descriptor (160 B) and hit list (<= 4 KB) are brought
-// into shared memory by TMA bulk copies (cp.async.bulk, mbarrier completion) while the
-// current item computes.  This removes the two dependent global latencies of every item's
-// prologue (descriptor, then hit entries) and the per-round hit-entry loads from the loop.
-// Only the first kPreHits entries are staged (3 rounds): later rounds' entries are loaded
-// from global two rounds ahead.  Staging whole hit lists would take the shared memory the
-// L1 needs for the lane-own point/covariance gathers (measured: +20% K4b time).
-constexpr int kPreHits = 96;
-template <int kStages>
-struct PersistSmem {
-  AccSmem<kStages> acc;
-  int2 hit[2][kPreHits];
-  AccDesc desc[2];
-  unsigned long long bar[2];
-};
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "BW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra BW_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-template <int MODE, int kStages, int kMinBlocks>
-__global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
-    k_acc_persist(const ItemDev* __restrict__ items, const AccDesc* __restrict__ descs,
-                  int n_items, const int2* __restrict__ hits, double* __restrict__ partials,
-                  int* __restrict__ counter, int dbg) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
-  PersistSmem<kStages>& ps = reinterpret_cast<PersistSmem<kStages>*>(smem_raw)[wib];
-  AccSmem<kStages>& sm = ps.acc;
-  if (lane == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ps.bar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ps.bar[1])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
-  // lane 0 claims items and issues the bulk copies of item `it` into buffer `b`
-  auto prefetch = [&](int it, const ItemDev& d, int b) {
-    const unsigned hb = (unsigned)min(((d.end - d.begin) + 1) & ~1, kPreHits) * 8u;
-    bar_expect_tx(&ps.bar[b], (unsigned)sizeof(AccDesc) + hb);
-    bulk_g2s(&ps.desc[b], descs + it, (unsigned)sizeof(AccDesc), &ps.bar[b]);
-    if (hb) bulk_g2s(&ps.hit[b][0], hits + d.hoff, hb, &ps.bar[b]);
-  };
-  // items are dealt round-robin (w, w + G, ...): a shared claim counter serialises ~60k
-  // same-address atomics at one L2 slice
-  const int G = gridDim.x * kAccWarps;
-  int next_claim = blockIdx.x * kAccWarps + wib;
-  auto claim = [&]() {
-    const int v = next_claim;
-    next_claim += G;
-    return v;
-  };
-  (void)counter;
-  int cur = claim();
-  if (cur >= n_items) return;
-  if (lane == 0) prefetch(cur, items[cur], 0);
-  int nxt = claim();
-  ItemDev inxt = items[min(nxt, n_items - 1)];
-  unsigned phase = 0;  // bit b: parity of buffer b's next completion
-  int b = 0;
-  for (;;) {
-    if (lane == 0 && nxt < n_items) prefetch(nxt, inxt, b ^ 1);
-    const int nn = nxt < n_items ? claim() : n_items;
-    const ItemDev inn = items[min(nn, n_items - 1)];
-    bar_wait(&ps.bar[b], (phase >> b) & 1u);
-    phase ^= 1u << b;
-    const AccDesc& dsc = ps.desc[b];
-    const int2* hs = &ps.hit[b][0];
-    const int n = dsc.n;
-    const int2* hl = hits + dsc.hoff;
-    double R[9], t[3];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) R[k] = dsc.T[k];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) t[k] = dsc.T[9 + k];
-    CloudView cv;
-    cv.a = dsc.a;
-    cv.xyz64 = dsc.xyz64;
-    cv.c0 = dsc.c0;
-    cv.c1 = dsc.c1;
-    cv.c2 = dsc.c2;
-    cv.n = 0;
-    MapView mv;
-    mv.recs = dsc.recs;
-    const bool f64pts = cv.xyz64 != nullptr;
-    double acc[28];
-#pragma unroll
-    for (int k = 0; k < 28; ++k) acc[k] = 0.0;
-    const int rounds = (n + 31) / 32;
-    constexpr int kAhead = kStages - 1;
-    const int klast = n > 0 ? n - 1 : 0;
-    if (n > 0) {
-      static_assert(kAhead + 2 <= kPreHits / 32, "prologue entries must be staged");
-#pragma unroll
-      for (int r = 0; r < kAhead; ++r)
-        issue_round(cv, mv, sm, r, hs[min(r * 32 + lane, klast)], (dbg & 1) ? 0 : n - r * 32, lane);
-      int2 nxt = hs[min(kAhead * 32 + lane, klast)];
-      int2 nxt2 = hs[min((kAhead + 1) * 32 + lane, klast)];
-      for (int r = 0; r < rounds; ++r) {
-        const int ri = r + kAhead;
-        issue_round(cv, mv, sm, ri, nxt, (dbg & 1) ? 0 : n - ri * 32, lane);
-        nxt = nxt2;
-        nxt2 = __ldg(hl + min((ri + 2) * 32 + lane, klast));
-        cp_async_wait<kAhead>();
-        __syncwarp();
-        if (r * 32 + lane < n && !(dbg & 2))
-          hit_math<MODE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
-        __syncwarp();
-      }
-      cp_async_wait<0>();
-    }
-    if (MODE == 1) {
-      double c = acc[27];
-#pragma unroll
-      for (int s2 = 16; s2 >= 1; s2 >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s2);
-      if (lane == 0) {
-        partials[2 * (size_t)cur] = c;
-        partials[2 * (size_t)cur + 1] = (double)n;
-      }
-    } else {
-      double v[32];
-#pragma unroll
-      for (int k = 0; k < 28; ++k) v[k] = acc[k];
-      v[28] = lane == 0 ? (double)n : 0.0;
-      v[29] = 0.0;
-      v[30] = 0.0;
-      v[31] = 0.0;
-      partials[(size_t)cur * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
-    }
-    __syncwarp();  // buffer b is refilled two items from now
-    if (nxt >= n_items) break;
-    cur = nxt;
-    nxt = nn;
-    inxt = inn;
-    b ^= 1;
-  }
-}
-
-// ---- K4ws: warp-specialised persistent fused lookup + accumulate ---------------------------
-// One CTA per SM, 16 warps = 8 producer/consumer pairs.  A producer warp claims items
-// (dynamic, in target-major order), resolves the correspondences of the item's points
-// (4 lookups in flight per lane), compacts the hits in shared memory and streams them as
-// rounds of <= 32 hits into its consumer's 4-slot ring: each slot receives the round's
-// source points / covariances and voxel records by cp.async (records gathered
-// cooperatively), plus the item's T_ij and round flags; completion is signalled through an
-// mbarrier (cp.async.mbarrier.arrive), so the consumer never waits on global memory.  The
-// consumer warp runs the fp64 math of a full round at a time (the math saturates the fp64
-// pipe with 4-8 warps/SM, tools/microbench/mathbench.cu) and reduces each item's 29-value
-// partial in a fixed order.  Registers: 512 threads x 128.
-constexpr int kPairs = 8;
-constexpr int kRing = 4;
-constexpr int kLookupU = 4;
-
-enum : int { kFlagFirst = 1, kFlagLast = 2, kFlagEnd = 4, kFlagF64 = 8 };
-
-struct __align__(16) SlotMeta {
-  double T[12];
-  int item;
-  int nvalid;
-  int flags;
-  int total;
-};
-
-struct __align__(16) PairSmem {
-  AccStage slot[kRing];
-  SlotMeta meta[kRing];
-  unsigned long long full[kRing];
-  unsigned long long empty[kRing];
-  ItemHdr hdr;
-  int2 hits[kMaxChunk];
-};
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cp_async(unsigned long long* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-// LOOKUP = 1: producers resolve correspondences themselves (fully fused);
-// LOOKUP = 0: producers stream the compacted hit lists K4a wrote (descs/hits).
-template <int MODE, int KM, int LOOKUP>
-__global__ void __launch_bounds__(2 * kPairs * 32, 1)
-    k_fused_ws(const ItemHdr* __restrict__ hdrs, const AccDesc* __restrict__ descs,
-               const int2* __restrict__ hit_list, int n_items, int* __restrict__ work_counter,
-               double* __restrict__ partials) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  PairSmem* pairs = reinterpret_cast<PairSmem*>(smem_raw);
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  if (threadIdx.x < kPairs * kRing) {
-    PairSmem& ps = pairs[threadIdx.x / kRing];
-    mbar_init(&ps.full[threadIdx.x % kRing], 33);  // 32 cp.async arrivals + 1 metadata arrive
-    mbar_init(&ps.empty[threadIdx.x % kRing], 1);
-  }
-  __syncthreads();
-
-  if (warp < kPairs) {
-    // ================================ producer ================================
-    PairSmem& ps = pairs[warp];
-    const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned k = 0;  // ring cursor
-    int item = 0;
-    if (lane == 0) item = atomicAdd(work_counter, 1);
-    item = __shfl_sync(0xffffffffu, item, 0);
-    // header of the next item is loaded into registers while the current one is processed
-    // LOOKUP: 256 B ItemHdr (16 lanes x 16 B); else 160 B AccDesc (10 lanes x 16 B)
-    constexpr int kHdrLanes = LOOKUP ? 16 : (int)(sizeof(AccDesc) / 16);
-    auto hdr_src = [&](int it) -> const int4* {
-      return LOOKUP ? reinterpret_cast<const int4*>(hdrs + it)
-                    : reinterpret_cast<const int4*>(descs + it);
-    };
-    int4 hreg = make_int4(0, 0, 0, 0);
-    if (item < n_items && lane < kHdrLanes) hreg = __ldg(hdr_src(item) + lane);
-    for (;;) {
-      if (item >= n_items) {  // tell the consumer to stop
-        const unsigned slot = k % kRing;
-        mbar_wait(&ps.empty[slot], ((k / kRing) & 1) ^ 1);
-        if (lane == 0) ps.meta[slot].flags = kFlagEnd;
-        __syncwarp();
-        mbar_arrive_cp_async(&ps.full[slot]);
-        if (lane == 0) mbar_arrive(&ps.full[slot]);
-        break;
-      }
-      if (lane < kHdrLanes) reinterpret_cast<int4*>(&ps.hdr)[lane] = hreg;
-      int next = 0;
-      if (lane == 0) next = atomicAdd(work_counter, 1);
-      next = __shfl_sync(0xffffffffu, next, 0);
-      __syncwarp();
-      if (next < n_items && lane < kHdrLanes) hreg = __ldg(hdr_src(next) + lane);
-      if (!LOOKUP) {
-        // ---- stream K4a's hit list: the descriptor holds T, the gather pointers, n, hoff
-        const AccDesc& dd = *reinterpret_cast<const AccDesc*>(&ps.hdr);
-        const int nh = dd.n;
-        const int2* hl = hit_list + dd.hoff;
-        const int rounds = nh > 0 ? (nh + 31) / 32 : 1;
-        const int klast = nh > 0 ? nh - 1 : 0;
-        CloudView cv;
-        cv.a = dd.a;
-        cv.xyz64 = dd.xyz64;
-        cv.c0 = dd.c0;
-        cv.c1 = dd.c1;
-        cv.c2 = dd.c2;
-        cv.n = 0;
-        const VoxelRec* recs = dd.recs;
-        int2 e = __ldg(hl + min(lane, klast));
-        for (int r = 0; r < rounds; ++r, ++k) {
-          const int2 en = __ldg(hl + min((r + 1) * 32 + lane, klast));  // next round's entry
-          const unsigned slot = k % kRing;
-          mbar_wait(&ps.empty[slot], ((k / kRing) & 1) ^ 1);
-          SlotMeta& md = ps.meta[slot];
-          if (lane < 12) md.T[lane] = dd.T[lane];
-          if (lane == 12) md.item = item;
-          if (lane == 13) md.nvalid = max(0, min(32, nh - r * 32));
-          if (lane == 14)
-            md.flags = (r == 0 ? kFlagFirst : 0) | (r == rounds - 1 ? kFlagLast : 0) |
-                       (cv.xyz64 ? kFlagF64 : 0);
-          if (lane == 15) md.total = nh;
-          AccStage& st = ps.slot[slot];
-          const int nvalid = max(0, min(32, nh - r * 32));
-          if (lane < nvalid) {
-            if (cv.xyz64) {
-              const double* q = cv.xyz64 + 3 * (size_t)e.x;
-              double* d8 = reinterpret_cast<double*>(&st.pt[0][lane]);
-              cp_async8(d8, q);
-              cp_async8(d8 + 1, q + 1);
-              cp_async8(reinterpret_cast<double*>(&st.pt[1][lane]), q + 2);
-            } else {
-              cp_async16(&st.pt[0][lane], cv.a + e.x);
-            }
-            cp_async16(&st.cov[0][lane], cv.c0 + e.x);
-            cp_async16(&st.cov[1][lane], cv.c1 + e.x);
-            cp_async16(&st.cov[2][lane], cv.c2 + e.x);
-          }
-#pragma unroll
-          for (int c = 0; c < kRecUnits; ++c) {
-            const int u = c * 32 + lane;
-            const int q = u / kRecUnits, j = u - q * kRecUnits;
-            const int row = __shfl_sync(0xffffffffu, e.y, q);
-            if (q < nvalid)
-              cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(recs + row) + 16 * j);
-          }
-          __syncwarp();
-          mbar_arrive_cp_async(&ps.full[slot]);
-          if (lane == 0) mbar_arrive(&ps.full[slot]);
-          e = en;
-        }
-        item = next;
-        continue;
-      }
-      const ItemHdr& h = ps.hdr;
-      double R[9], t[3];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) R[q] = h.T[q];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) t[q] = h.T[9 + q];
-      const MapView& mv = h.mv;
-      const float4* pa = h.a;
-      const double* p64 = h.xyz64;
-      const int begin = h.begin, end = h.end;
-      const int kmode = KM == 2 ? mv.kmode : KM;
-      // ---- lookups: kLookupU points per lane in flight
-      int nh = 0;
-      for (int base = begin; base < end; base += 32 * kLookupU) {
-        Query qy[kLookupU];
-        ProbeGroup pg[kLookupU];
-        bool live[kLookupU];
-#pragma unroll
-        for (int u = 0; u < kLookupU; ++u) {
-          const int i = base + 32 * u + lane;
-          live[u] = i < end;
-          const int ic = min(i, end - 1);
-          double px, py, pz;
-          if (p64) {
-            px = p64[3 * (size_t)ic];
-            py = p64[3 * (size_t)ic + 1];
-            pz = p64[3 * (size_t)ic + 2];
-          } else {
-            const float4 a = __ldg(pa + ic);
-            px = a.x;
-            py = a.y;
-            pz = a.z;
-          }
-          // points @ R^T + t (registration.py:148), keys (preprocess.py:68-70)
-          const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
-          const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
-          const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
-          qy[u] = make_query(mv, floor_div(x, mv.res, mv.inv_res, mv.pow2),
-                             floor_div(y, mv.res, mv.inv_res, mv.pow2),
-                             floor_div(z, mv.res, mv.inv_res, mv.pow2), kmode);
-          live[u] = live[u] && mv.m && qy[u].inside;
-          if (live[u]) pg[u] = probe_load(mv, qy[u].bucket, kmode);
-        }
-#pragma unroll
-        for (int u = 0; u < kLookupU; ++u) {
-          int row = -1;
-          if (live[u]) {
-            unsigned bk = qy[u].bucket;
-            int r;
-            while ((r = probe_scan(mv, pg[u], bk, qy[u], row, kmode)) < 0) {
-              bk = next_bucket(bk, mv);
-              pg[u] = probe_load(mv, bk, kmode);
-            }
-            if (r == 1) row = rec_index(mv, row, kmode);
-            if (r != 1) row = -1;
-          }
-          const unsigned m = __ballot_sync(0xffffffffu, row >= 0);
-          if (row >= 0) ps.hits[nh + __popc(m & lt_mask)] = make_int2(base + 32 * u + lane, row);
-          nh += __popc(m);
-        }
-      }
-      __syncwarp();
-      // ---- stream the hits to the consumer, one round (<= 32 hits) per ring slot
-      const int rounds = nh > 0 ? (nh + 31) / 32 : 1;
-      CloudView cv;
-      cv.a = pa;
-      cv.xyz64 = p64;
-      cv.c0 = h.c0;
-      cv.c1 = h.c1;
-      cv.c2 = h.c2;
-      cv.n = 0;
-      for (int r = 0; r < rounds; ++r, ++k) {
-        const unsigned slot = k % kRing;
-        mbar_wait(&ps.empty[slot], ((k / kRing) & 1) ^ 1);
-        SlotMeta& md = ps.meta[slot];
-        if (lane < 12) md.T[lane] = h.T[lane];
-        if (lane == 12) md.item = item;
-        if (lane == 13) md.nvalid = min(32, nh - r * 32);
-        if (lane == 14)
-          md.flags = (r == 0 ? kFlagFirst : 0) | (r == rounds - 1 ? kFlagLast : 0) |
-                     (p64 ? kFlagF64 : 0);
-        if (lane == 15) md.total = nh;
-        const int kh = r * 32 + lane;
-        const int2 e = ps.hits[min(kh, max(nh - 1, 0))];
-        // gather into the slot (the AccStage layout K4b uses)
-        AccStage& st = ps.slot[slot];
-        const int nvalid = max(0, min(32, nh - r * 32));
-        if (lane < nvalid) {
-          if (p64) {
-            const double* q = p64 + 3 * (size_t)e.x;
-            double* dd = reinterpret_cast<double*>(&st.pt[0][lane]);
-            cp_async8(dd, q);
-            cp_async8(dd + 1, q + 1);
-            cp_async8(reinterpret_cast<double*>(&st.pt[1][lane]), q + 2);
-          } else {
-            cp_async16(&st.pt[0][lane], pa + e.x);
-          }
-          cp_async16(&st.cov[0][lane], cv.c0 + e.x);
-          cp_async16(&st.cov[1][lane], cv.c1 + e.x);
-          cp_async16(&st.cov[2][lane], cv.c2 + e.x);
-        }
-#pragma unroll
-        for (int c = 0; c < kRecUnits; ++c) {
-          const int u = c * 32 + lane;
-          const int q = u / kRecUnits, j = u - q * kRecUnits;
-          const int row = __shfl_sync(0xffffffffu, e.y, q);
-          if (q < nvalid)
-            cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(mv.recs + row) + 16 * j);
-        }
-        __syncwarp();  // metadata stores of all lanes before lane 0's release-arrive
-        mbar_arrive_cp_async(&ps.full[slot]);
-        if (lane == 0) mbar_arrive(&ps.full[slot]);
-      }
-      item = next;
-    }
-  } else {
-    // ================================ consumer ================================
-    PairSmem& ps = pairs[warp - kPairs];
-    double acc[28];
-#pragma unroll
-    for (int q = 0; q < 28; ++q) acc[q] = 0.0;
-    for (unsigned k = 0;; ++k) {
-      const unsigned slot = k % kRing;
-      mbar_wait(&ps.full[slot], (k / kRing) & 1);
-      const SlotMeta& md = ps.meta[slot];
-      const int flags = md.flags;
-      if (flags & kFlagEnd) break;
-      const int nvalid = md.nvalid, item = md.item, total = md.total;
-      double R[9], t[3];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) R[q] = md.T[q];
-#pragma unroll
-      for (int q = 0; q < 3; ++q) t[q] = md.T[9 + q];
-      if (flags & kFlagFirst) {
-#pragma unroll
-        for (int q = 0; q < 28; ++q) acc[q] = 0.0;
-      }
-      if (lane < nvalid)
-        hit_math<MODE>(ps.slot[slot], lane, (flags & kFlagF64) != 0, R, t, 1.0, acc);
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ps.empty[slot]);  // slot data fully consumed
-      if (flags & kFlagLast) {
-        if (MODE == 1) {
-          double c = acc[27];
-#pragma unroll
-          for (int q = 16; q >= 1; q >>= 1) c += __shfl_xor_sync(0xffffffffu, c, q);
-          if (lane == 0) {
-            partials[2 * (size_t)item] = c;
-            partials[2 * (size_t)item + 1] = (double)total;
-          }
-        } else {
-          double v[32];
-#pragma unroll
-          for (int q = 0; q < 28; ++q) v[q] = acc[q];
-          v[28] = lane == 0 ? (double)total : 0.0;
-          v[29] = 0.0;
-          v[30] = 0.0;
-          v[31] = 0.0;
-          partials[(size_t)item * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
-        }
-      }
-    }
-  }
-}
-
 }  // namespace vg
 
 using namespace vg;
 
 static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
-                               cudaStream_t st, int prefetch) {
+                               cudaStream_t st) {
   const int lb = (cnt + kLookupWarps - 1) / kLookupWarps;
   double* p2 = kmode == 2 ? b->partials + 2 * (size_t)off : nullptr;
   const ItemDev* it = b->items + off;
   int* hc = b->hit_counts + off;
   AccDesc* dd = b->descs + off;
-  static const int lblocks_env = [] {
-    const char* e = getenv("VGICP_LOOKUP_BLOCKS");
-    return e ? atoi(e) : 0;
-  }();
-  const int lblocks = lblocks_env ? lblocks_env : 3;
-  static const int lu = [] {
-    const char* e = getenv("VGICP_LOOKUP_U");  // 0: two-deep pipelined K4a; 2/4: batched
-    return e ? atoi(e) : 0;
-  }();
-  static const int fast = [] {
-    const char* e = getenv("VGICP_LOOKUP_FAST");
-    return e ? atoi(e) : 1;
-  }();
-  if (fast && b->key_mode == 1 && b->all_pow2 && b->all_f32) {
-    if (lblocks_env != 3)  // 4 CTAs/SM measured fastest (0.196 vs 0.203 ms at 3)
-      k_lookup_fast<4><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
-    else
-      k_lookup_fast<3><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
-  } else if (b->key_mode == 1 && lu > 0) {
-    if (lu == 2 && lblocks == 4)
-      k_lookup_batch<1, 2, 4><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                                b->maps, b->hits, hc, p2, dd);
-    else if (lu == 2)
-      k_lookup_batch<1, 2, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                                b->maps, b->hits, hc, p2, dd);
-    else if (lu == 4 && lblocks == 2)
-      k_lookup_batch<1, 4, 2><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                                b->maps, b->hits, hc, p2, dd);
-    else if (lu == 4)
-      k_lookup_batch<1, 4, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                                b->maps, b->hits, hc, p2, dd);
-    else
-      k_lookup_batch<1, 8, 2><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                                b->maps, b->hits, hc, p2, dd);
-  } else if (b->key_mode == 1 && b->all_pow2 && lblocks == 4)
-    k_lookup_items<1, 4, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                              b->maps, b->hits, hc, p2, dd,
-                                                              prefetch);
-  else if (b->key_mode == 1 && b->all_pow2 && lblocks == 3)
+  if (b->key_mode == 1 && b->all_pow2 && b->all_f32)  // fast path, 4 CTAs/SM
+    k_lookup_fast<4><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
+  else if (b->key_mode == 1 && b->all_pow2)
     k_lookup_items<1, 3, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                              b->maps, b->hits, hc, p2, dd,
-                                                              prefetch);
-  else if (b->key_mode == 1 && lblocks == 2)
-    k_lookup_items<1, 2><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                           b->maps, b->hits, hc, p2, dd,
-                                                           prefetch);
+                                                              b->maps, b->hits, hc, p2, dd);
   else if (b->key_mode == 1)
     k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                           b->maps, b->hits, hc, p2, dd,
-                                                           prefetch);
+                                                           b->maps, b->hits, hc, p2, dd);
   else if (b->key_mode == 0)
     k_lookup_items<0, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                           b->maps, b->hits, hc, p2, dd,
-                                                           prefetch);
+                                                           b->maps, b->hits, hc, p2, dd);
   else
     k_lookup_items<2, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
-                                                           b->maps, b->hits, hc, p2, dd,
-                                                           prefetch);
+                                                           b->maps, b->hits, hc, p2, dd);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
@@ -1251,85 +604,13 @@ static int launch_acc_kernel(vg_ctx* ctx, K kern, size_t smem, const AccDesc* d,
   return 0;
 }
 
-template <class K>
-static int launch_persist_kernel(vg_ctx* ctx, vg_batch* b, K kern, int min_blocks, int off,
-                                 int cnt, double* partials, cudaStream_t st) {
-  static int sms = 0;
-  if (!sms) VG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-  const size_t smem = sizeof(PersistSmem<2>) * kAccWarps;
-  VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  VG_CUDA(cudaMemsetAsync(b->work_counter, 0, sizeof(int), st));
-  static int occ = -1;
-  if (occ < 0) {
-    VG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kAccWarps * 32, smem));
-    if (getenv("VGICP_DEBUG_OCC")) fprintf(stderr, "k_acc_persist: %d CTAs/SM, %zu B smem\n", occ, smem);
-  }
-  min_blocks = std::max(1, std::min(min_blocks, occ));
-  const int grid = std::max(1, std::min(sms * min_blocks, (cnt + kAccWarps - 1) / kAccWarps));
-  static const int dbg = [] {
-    const char* e = getenv("VGICP_K4B_DEBUG");
-    return e ? atoi(e) : 0;
-  }();
-  kern<<<grid, kAccWarps * 32, smem, st>>>(b->items + off, b->descs + off, cnt, b->hits, partials,
-                                           b->work_counter, dbg);
-  ctx->launches++;
-  VG_CUDA(cudaGetLastError());
-  return 0;
-}
-
 static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
-                            cudaStream_t st, bool shared_sm) {
-  static const int variant = [] {
-    const char* e = getenv("VGICP_ACC_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  static const int persist = [] {
-    // 1: persistent K4b with TMA item prefetch (measured equal to the one-item-per-warp
-    // kernel on config 5: 0.385 vs 0.382 ms; kept as an option)
-    const char* e = getenv("VGICP_ACC_PERSIST");
-    return e ? atoi(e) : 0;
-  }();
-  if (persist) {
-    if (kmode == 1)
-      return launch_persist_kernel(ctx, b, k_acc_persist<1, 2, 3>, 3, off, cnt,
-                                   b->partials + 2 * (size_t)off, st);
-    return launch_persist_kernel(ctx, b, k_acc_persist<0, 2, 3>, 3, off, cnt,
-                                 b->partials + (size_t)off * kPartialStride, st);
-  }
+                            cudaStream_t st) {
   const AccDesc* d = b->descs + off;
   if (kmode == 1)
     return launch_acc_kernel(ctx, k_accumulate<1, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
                              cnt, b->hits, b->partials + 2 * (size_t)off, st);
   double* p = b->partials + (size_t)off * kPartialStride;
-  (void)shared_sm;
-  // variants (stages, min CTAs/SM, ILP): 0 = (2,3,1), 1 = (4,2,2), 2 = (3,3,1), 3 = (4,3,2)
-  switch (variant) {
-    case 1:
-      return launch_acc_kernel(ctx, k_accumulate<0, 4, 2, 2>, sizeof(AccSmem<4>) * kAccWarps, d,
-                               cnt, b->hits, p, st);
-    case 2:
-      return launch_acc_kernel(ctx, k_accumulate<0, 3, 3, 1>, sizeof(AccSmem<3>) * kAccWarps, d,
-                               cnt, b->hits, p, st);
-    case 3:
-      return launch_acc_kernel(ctx, k_accumulate<0, 4, 3, 2>, sizeof(AccSmem<4>) * kAccWarps, d,
-                               cnt, b->hits, p, st);
-    case 4:
-      return launch_acc_kernel(ctx, k_accumulate<0, 2, 4, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
-                               cnt, b->hits, p, st);
-    case 5:  // fp32 points: ILP 2 with 4 stages at 3 CTAs/SM (smaller stages fit)
-      if (b->all_f32)
-        return launch_acc_kernel(ctx, k_accumulate<0, 4, 3, 2, 1>,
-                                 sizeof(AccSmem<4, 1>) * kAccWarps, d, cnt, b->hits, p, st);
-      break;
-    case 6:  // fp32 points: 3 stages
-      if (b->all_f32)
-        return launch_acc_kernel(ctx, k_accumulate<0, 3, 3, 1, 1>,
-                                 sizeof(AccSmem<3, 1>) * kAccWarps, d, cnt, b->hits, p, st);
-      break;
-
-    default:
-      break;
-  }
   if (b->all_f32)  // every point fp32-exact: one 16 B point unit per lane (more L1 left)
     return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1, 1>, sizeof(AccSmem<2, 1>) * kAccWarps,
                              d, cnt, b->hits, p, st);
@@ -1337,83 +618,14 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
                            b->hits, p, st);
 }
 
-// K4a + K4b.  Experiment knobs (measured slower on config 5, kept off): VGICP_CHUNKS > 1
-// alternates K4a/K4b over item chunks; VGICP_PREFETCH=1 makes K4a prefetch record lines to L2.
-static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
-                               cudaStream_t st, int prefetch);
-
-static int launch_fused_ws(vg_ctx* ctx, vg_batch* b, int kmode) {
-  const int n = (int)b->num_items;
-  static int sms = 0;
-  if (!sms) VG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-  const size_t smem = sizeof(PairSmem) * kPairs;
-  VG_CUDA(cudaMemsetAsync(b->work_counter, 0, sizeof(int), ctx->stream));
-  const int grid = std::min(sms, (n + 7) / 8);
-  auto go = [&](auto kern) -> int {
-    VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, 2 * kPairs * 32, smem, ctx->stream>>>(b->hdrs, b->descs, b->hits, n,
-                                                       b->work_counter, b->partials);
-    return 0;
-  };
-  static const int ws_mode = [] {
-    const char* e = getenv("VGICP_FUSED_WS");  // 1: K4a + streaming WS kernel, 2: fully fused
-    return e ? atoi(e) : 1;
-  }();
-  int rc;
-  if (ws_mode == 2) {
-    if (b->key_mode == 1)
-      rc = kmode == 1 ? go(k_fused_ws<1, 1, 1>) : go(k_fused_ws<0, 1, 1>);
-    else
-      rc = kmode == 1 ? go(k_fused_ws<1, 2, 1>) : go(k_fused_ws<0, 2, 1>);
-  } else {
-    VG_CHECK(launch_lookup_range(ctx, b, kmode, 0, n, ctx->stream, 0));
-    VG_CUDA(cudaMemsetAsync(b->work_counter, 0, sizeof(int), ctx->stream));
-    rc = kmode == 1 ? go(k_fused_ws<1, 1, 0>) : go(k_fused_ws<0, 1, 0>);
-  }
-  if (rc) return rc;
-  ctx->launches++;
-  VG_CUDA(cudaGetLastError());
-  return 0;
-}
-
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi) {
   if (hi <= lo) return 0;
-  VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream, 0));
-  if (kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream, false));
+  VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
+  if (kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
   return 0;
 }
 
+// K4a + K4b over the whole batch (DESIGN.md §9 lists the alternatives that measured slower)
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
-  if (b->num_items == 0) return 0;
-  const int n = (int)b->num_items;
-  static const int use_ws = [] {
-    // 0 (default): K4a + K4b; 1: K4a + streaming warp-specialised kernel; 2: fully fused
-    // warp-specialised kernel (both measured slower on config 5, kept for experiments)
-    const char* e = getenv("VGICP_FUSED_WS");
-    return e ? atoi(e) : 0;
-  }();
-  static const int use_sg = [] {
-    // 1: source-grouped warp-specialised kernel for eligible batches (experimental; measured
-    // 2.3x slower than K4a + K4b on config 5)
-    const char* e = getenv("VGICP_SRCGROUP");
-    return e ? atoi(e) : 0;
-  }();
-  if (use_sg && b->num_groups > 0 && kmode != 2) return launch_srcgroup(ctx, b, kmode);
-  if (use_ws && kmode != 2) return launch_fused_ws(ctx, b, kmode);
-  static const int chunks_env = [] {
-    const char* e = getenv("VGICP_CHUNKS");
-    return e ? atoi(e) : 1;
-  }();
-  static const int prefetch_env = [] {
-    const char* e = getenv("VGICP_PREFETCH");
-    return e ? atoi(e) : 0;
-  }();
-  const int chunks = (kmode == 2 || n < 4096) ? 1 : std::max(1, std::min(chunks_env, 256));
-  const int prefetch = kmode != 2 && prefetch_env;
-  for (int c = 0; c < chunks; ++c) {
-    const int lo = (int)((long long)n * c / chunks), hi = (int)((long long)n * (c + 1) / chunks);
-    VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream, prefetch));
-    if (kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream, false));
-  }
-  return 0;
+  return launch_accumulate_range(ctx, b, kmode, 0, (int)b->num_items);
 }

@@ -450,13 +450,6 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   std::vector<ItemDev> items;
   std::vector<int> stage_items(S + 1, 0);
   long long npts = 0, hoff = 0;
-  // source groups for the source-grouped kernel (K4s): every source fits in shared memory,
-  // every point is fp32-exact and every map uses 32-bit local keys
-  bool grouped = F > 0;
-  for (int64_t f = 0; f < F && grouped; ++f) {
-    const vg_cloud* c = specs[f].source;
-    grouped = c->n <= srcgroup_max_points() && c->exact32 && specs[f].target->kmode == 1;
-  }
   // item size: up to kMaxChunk points, smaller when the batch is too small to give every
   // K4a warp slot of the GPU (148 SMs x 32) about one item
   long long total_pts = 0;
@@ -513,69 +506,6 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   for (const MapView& m : mv) b->all_pow2 &= m.pow2 ? 1 : 0;
   b->all_f32 = 1;
   for (const CloudView& c : cv) b->all_f32 &= c.xyz64 ? 0 : 1;
-  // Source groups, ordered for L2 locality: a breadth-first walk of the bipartite graph
-  // (source -> its target maps -> the other sources of those maps), the Cuthill-McKee idea,
-  // so sources processed concurrently by different SMs share most of their target maps.
-  std::vector<SrcGroup> groups;
-  std::vector<int> group_factors;
-  if (grouped) {
-    const int nc = (int)clouds.size(), nm = (int)maps.size();
-    std::vector<std::vector<int>> fac_of_cloud(nc), clouds_of_map(nm);
-    for (int64_t f = 0; f < F; ++f) {
-      fac_of_cloud[fac[f].cloud].push_back((int)f);
-      clouds_of_map[fac[f].map].push_back(fac[f].cloud);
-    }
-    std::vector<int> order_g;
-    std::vector<char> seen_c(nc, 0), seen_m(nm, 0);
-    for (int64_t f0 = 0; f0 < F; ++f0) {  // every connected component, in caller order
-      const int c0 = fac[f0].cloud;
-      if (seen_c[c0]) continue;
-      std::vector<int> queue{c0};
-      seen_c[c0] = 1;
-      for (size_t qi = 0; qi < queue.size(); ++qi) {
-        const int c = queue[qi];
-        order_g.push_back(c);
-        for (int f : fac_of_cloud[c]) {
-          const int m = fac[f].map;
-          if (seen_m[m]) continue;
-          seen_m[m] = 1;
-          for (int c2 : clouds_of_map[m])
-            if (!seen_c[c2]) {
-              seen_c[c2] = 1;
-              queue.push_back(c2);
-            }
-        }
-      }
-    }
-    static const int bfs = [] {
-      const char* e = getenv("VGICP_GROUP_BFS");  // 0: caller order of first appearance
-      return e ? atoi(e) : 1;
-    }();
-    if (!bfs) {
-      order_g.clear();
-      std::vector<char> seen(nc, 0);
-      for (int64_t f = 0; f < F; ++f)
-        if (!seen[fac[f].cloud]) {
-          seen[fac[f].cloud] = 1;
-          order_g.push_back(fac[f].cloud);
-        }
-    }
-    for (int c : order_g) {
-      SrcGroup g;
-      const CloudView& cvw = cv[c];
-      g.a = cvw.a;
-      g.c0 = cvw.c0;
-      g.c1 = cvw.c1;
-      g.c2 = cvw.c2;
-      g.n = (int)cvw.n;
-      g.fbegin = (int)group_factors.size();
-      g.fcount = (int)fac_of_cloud[c].size();
-      g.pad = 0;
-      for (int f : fac_of_cloud[c]) group_factors.push_back(f);
-      groups.push_back(g);
-    }
-  }
-  b->num_groups = (int)groups.size();
   std::vector<ItemHdr> hdrs(items.size());
   for (size_t i = 0; i < items.size(); ++i) {
     ItemHdr& h = hdrs[i];
@@ -602,17 +532,12 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
       (rc = dalloc(ctx, &b->hit_counts, items.size())) ||
       (rc = dalloc(ctx, &b->descs, items.size())) ||
       (rc = dalloc(ctx, &b->hdrs, items.size())) ||
-      (rc = dalloc(ctx, &b->work_counter, 1)) ||
       (rc = dalloc(ctx, &b->out, (size_t)F * VG_REC_LINEARIZE)) ||
       (rc = h2d(ctx, b->factors, fac.data(), sizeof(FactorDev) * F)) ||
       (rc = h2d(ctx, b->items, items.data(), sizeof(ItemDev) * items.size())) ||
       (rc = h2d(ctx, b->clouds, cv.data(), sizeof(CloudView) * cv.size())) ||
       (rc = h2d(ctx, b->maps, mv.data(), sizeof(MapView) * mv.size())) ||
-      (rc = h2d(ctx, b->hdrs, hdrs.data(), sizeof(ItemHdr) * hdrs.size())) ||
-      (rc = dalloc(ctx, &b->groups, groups.size())) ||
-      (rc = dalloc(ctx, &b->group_factors, group_factors.size())) ||
-      (rc = h2d(ctx, b->groups, groups.data(), sizeof(SrcGroup) * groups.size())) ||
-      (rc = h2d(ctx, b->group_factors, group_factors.data(), sizeof(int) * group_factors.size()))) {
+      (rc = h2d(ctx, b->hdrs, hdrs.data(), sizeof(ItemHdr) * hdrs.size()))) {
     vg_batch_destroy(b);
     return rc;
   }
@@ -645,9 +570,6 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->hit_counts);
   dfree(ctx, b->descs);
   dfree(ctx, b->hdrs);
-  dfree(ctx, b->groups);
-  dfree(ctx, b->group_factors);
-  dfree(ctx, b->work_counter);
   dfree(ctx, b->out);
   dfree(ctx, b->poses);
   dfree(ctx, b->asm_begin);

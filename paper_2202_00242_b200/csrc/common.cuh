@@ -79,18 +79,6 @@ struct __align__(16) ItemHdr {
 };
 static_assert(sizeof(ItemHdr) == 256, "item header must be 256 B");
 
-// Source group for the source-grouped kernel: one source cloud and the factors reading it.
-struct __align__(16) SrcGroup {
-  const float4* a;
-  const double2* c0;
-  const double2* c1;
-  const double2* c2;
-  int n;        // source points
-  int fbegin;   // range in the batch's group_factors array
-  int fcount;
-  int pad;
-};
-
 // Per-factor record resident in HBM (128 B).  T = T_ij (R row-major, t), fp64.
 struct __align__(16) FactorDev {
   double T[12];

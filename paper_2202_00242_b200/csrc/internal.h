@@ -110,11 +110,7 @@ struct vg_batch {
   int2* hits = nullptr;               // compacted (point, slot) hits, per-item regions
   int* hit_counts = nullptr;          // num_items
   vg::AccDesc* descs = nullptr;       // num_items (K4a -> K4b)
-  vg::ItemHdr* hdrs = nullptr;        // num_items (fused kernel headers; T refreshed per step)
-  int* work_counter = nullptr;        // fused kernel dynamic item counter
-  vg::SrcGroup* groups = nullptr;     // source groups (source-grouped kernel), or null
-  int* group_factors = nullptr;       // factor indices grouped by source
-  int num_groups = 0;                 // > 0 when the batch qualifies for K4s
+  vg::ItemHdr* hdrs = nullptr;        // num_items (K4a fast-path headers; T refreshed per step)
   long long hit_capacity = 0;
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;
@@ -177,8 +173,6 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
 int launch_spread_T(vg_ctx* ctx, vg_batch* b);  // FactorDev.T -> ItemHdr.T (explicit-T mode)
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b (or K4s)
-int launch_srcgroup(vg_ctx* ctx, vg_batch* b, int kmode);    // K4s
-int srcgroup_max_points();
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1);
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev);  // K6
