@@ -8,11 +8,22 @@
 // correctly rounded ops: the association numpy's einsum uses (checked bit for bit against
 // the reference in tests/golden).
 //
+// Clouds of >= kKnnGridMin points use an exact uniform-grid search instead (k_knn_grid): the
+// cloud is counting-sorted into cells of side h, and each query scans Chebyshev rings of cells
+// around its own until the k-th best squared distance is below the distance to any unscanned
+// cell; the same d2 expression and (d2, index) order give the brute-force result.
+//
 // estimate_covariances (preprocess.py:142-164): sample covariance / k, fp64 Jacobi
 // eigen-decomposition, smallest-eigenvalue direction n, C = I - (1 - eps) n n^T (identical
 // to V diag(eps, 1, 1) V^T), degenerate (lambda_max < 1e-12) -> eps * I.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "internal.h"
@@ -84,6 +95,142 @@ __global__ void __launch_bounds__(kKnnTile)
     for (int j = 0; j < KM; ++j)
       if (j >= KM - k) out[(size_t)q * k + (j - (KM - k))] = id[j];
   }
+}
+
+// ---- exact grid kNN ------------------------------------------------------------------------
+struct KnnGrid {
+  double ox, oy, oz;  // grid origin (cloud minimum)
+  double h, inv_h;    // cell side
+  int dx, dy, dz;     // cells per axis
+};
+
+__device__ __forceinline__ int knn_cell_axis(double v, double o, double inv_h, int d) {
+  const int c = (int)floor((v - o) * inv_h);
+  return min(max(c, 0), d - 1);
+}
+
+__global__ void k_bbox(const double* __restrict__ xyz, int n, double* __restrict__ out) {
+  __shared__ double smin[3][256], smax[3][256];
+  double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int a = 0; a < 3; ++a) {
+      const double v = xyz[3 * (size_t)i + a];
+      lo[a] = fmin(lo[a], v);
+      hi[a] = fmax(hi[a], v);
+    }
+  for (int a = 0; a < 3; ++a) {
+    smin[a][threadIdx.x] = lo[a];
+    smax[a][threadIdx.x] = hi[a];
+  }
+  __syncthreads();
+  for (int s = blockDim.x / 2; s >= 1; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int a = 0; a < 3; ++a) {
+        smin[a][threadIdx.x] = fmin(smin[a][threadIdx.x], smin[a][threadIdx.x + s]);
+        smax[a][threadIdx.x] = fmax(smax[a][threadIdx.x], smax[a][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int a = 0; a < 3; ++a) {
+      out[6 * blockIdx.x + a] = smin[a][0];
+      out[6 * blockIdx.x + 3 + a] = smax[a][0];
+    }
+}
+
+__global__ void k_knn_cell_count(const double* __restrict__ xyz, int n, KnnGrid g,
+                                 int* __restrict__ cell, int* __restrict__ counts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cx = knn_cell_axis(xyz[3 * (size_t)i], g.ox, g.inv_h, g.dx);
+  const int cy = knn_cell_axis(xyz[3 * (size_t)i + 1], g.oy, g.inv_h, g.dy);
+  const int cz = knn_cell_axis(xyz[3 * (size_t)i + 2], g.oz, g.inv_h, g.dz);
+  const int c = (cx * g.dy + cy) * g.dz + cz;
+  cell[i] = c;
+  atomicAdd(counts + c, 1);
+}
+
+// scatter into cell order (order inside a cell is irrelevant: selection is by (d2, index))
+__global__ void k_knn_scatter(const double* __restrict__ xyz, int n, const int* __restrict__ cell,
+                              const int* __restrict__ start, int* __restrict__ fill,
+                              double4* __restrict__ sorted) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = cell[i];
+  const int pos = start[c] + atomicAdd(fill + c, 1);
+  sorted[pos] = make_double4(xyz[3 * (size_t)i], xyz[3 * (size_t)i + 1], xyz[3 * (size_t)i + 2],
+                             __hiloint2double(0, i));
+}
+
+template <int KM>
+__global__ void __launch_bounds__(128)
+    k_knn_grid(const double4* __restrict__ sorted, int n, int k, KnnGrid g,
+               const int* __restrict__ start, long long* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  // queries in cell order: neighbouring threads scan the same cells
+  const double4 qp = sorted[t];
+  const double qx = qp.x, qy = qp.y, qz = qp.z;
+  const int q = __double2loint(qp.w);
+  double d[KM];
+  int id[KM];
+#pragma unroll
+  for (int j = 0; j < KM; ++j) {
+    const bool pad = j < KM - k;
+    d[j] = pad ? -DBL_MAX : DBL_MAX;
+    id[j] = pad ? -1 : INT_MAX;
+  }
+  auto consider = [&](int pos) {
+    const double4 p = sorted[pos];
+    const double ex = __dsub_rn(p.x, qx), ey = __dsub_rn(p.y, qy), ez = __dsub_rn(p.z, qz);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ez, ez)), __dmul_rn(ey, ey));
+    const int ci = __double2loint(p.w);
+    if (knn_less(d2, ci, d[KM - 1], id[KM - 1])) {
+      d[KM - 1] = d2;
+      id[KM - 1] = ci;
+#pragma unroll
+      for (int s = KM - 1; s > 0; --s) {
+        if (knn_less(d[s], id[s], d[s - 1], id[s - 1])) {
+          const double td = d[s];
+          d[s] = d[s - 1];
+          d[s - 1] = td;
+          const int ti = id[s];
+          id[s] = id[s - 1];
+          id[s - 1] = ti;
+        }
+      }
+    }
+  };
+  const int cx = knn_cell_axis(qx, g.ox, g.inv_h, g.dx);
+  const int cy = knn_cell_axis(qy, g.oy, g.inv_h, g.dy);
+  const int cz = knn_cell_axis(qz, g.oz, g.inv_h, g.dz);
+  const int rmax = max(max(g.dx, g.dy), g.dz);
+  for (int R = 0;; ++R) {
+    // the shell of cells at Chebyshev distance R
+    for (int ix = max(cx - R, 0); ix <= min(cx + R, g.dx - 1); ++ix) {
+      const bool xe = ix == cx - R || ix == cx + R;
+      for (int iy = max(cy - R, 0); iy <= min(cy + R, g.dy - 1); ++iy) {
+        const bool ye = iy == cy - R || iy == cy + R;
+        const int base = (ix * g.dy + iy) * g.dz;
+        if (xe || ye) {
+          const int z0 = max(cz - R, 0), z1 = min(cz + R, g.dz - 1);
+          for (int pos = start[base + z0]; pos < start[base + z1 + 1]; ++pos) consider(pos);
+        } else {
+          if (cz - R >= 0)
+            for (int pos = start[base + cz - R]; pos < start[base + cz - R + 1]; ++pos) consider(pos);
+          if (R > 0 && cz + R < g.dz)
+            for (int pos = start[base + cz + R]; pos < start[base + cz + R + 1]; ++pos) consider(pos);
+        }
+      }
+    }
+    // every unscanned point is farther than R * h (up to the rounding of the cell
+    // assignment, hence the margin); ties at the bound are scanned too
+    const double bound = (R - 1e-6) * g.h;
+    if (R >= rmax || (R > 0 && d[KM - 1] < bound * bound)) break;
+  }
+#pragma unroll
+  for (int j = 0; j < KM; ++j)
+    if (j >= KM - k) out[(size_t)q * k + (j - (KM - k))] = id[j];
 }
 
 // cyclic Jacobi on a symmetric 3x3 (fp64); a is destroyed, v receives eigenvectors (columns)
@@ -170,9 +317,96 @@ __global__ void k_cov(const double* __restrict__ xyz, const long long* __restric
 
 using namespace vg;
 
+static constexpr int kKnnGridMin = 4096;
+
+// exact grid kNN: bbox -> cell side (about one cell per point, at most 4 n cells) -> counting
+// sort into cells -> ring search per query
+static int launch_knn_grid(vg_ctx* ctx, const vg_cloud* cl, int k, long long* nbrs_dev) {
+  const int n = (int)cl->n;
+  cudaStream_t st = ctx->stream;
+  const int bb_blocks = 64;
+  double* dbb = nullptr;
+  VG_CUDA(cudaMallocAsync((void**)&dbb, sizeof(double) * 6 * bb_blocks, st));
+  k_bbox<<<bb_blocks, 256, 0, st>>>(cl->xyz64, n, dbb);
+  std::vector<double> hb(6 * bb_blocks);
+  VG_CUDA(cudaMemcpyAsync(hb.data(), dbb, sizeof(double) * 6 * bb_blocks, cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaStreamSynchronize(st));
+  VG_CUDA(cudaFreeAsync(dbb, st));
+  double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+  for (int b = 0; b < bb_blocks; ++b)
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = std::min(lo[a], hb[6 * b + a]);
+      hi[a] = std::max(hi[a], hb[6 * b + 3 + a]);
+    }
+  double ext[3], emax = 0.0;
+  for (int a = 0; a < 3; ++a) {
+    ext[a] = hi[a] - lo[a];
+    emax = std::max(emax, ext[a]);
+  }
+  if (!(emax > 0.0) || !std::isfinite(emax)) return -1;  // degenerate cloud: brute force
+  const double floor_e = emax * 1e-3;
+  double h = std::cbrt(std::max(ext[0], floor_e) * std::max(ext[1], floor_e) *
+                       std::max(ext[2], floor_e) / n);
+  KnnGrid g;
+  long long cells = 0;
+  for (int it = 0; it < 64; ++it, h *= 1.25) {
+    g.dx = (int)std::min(ext[0] / h, 1e6) + 1;
+    g.dy = (int)std::min(ext[1] / h, 1e6) + 1;
+    g.dz = (int)std::min(ext[2] / h, 1e6) + 1;
+    cells = (long long)g.dx * g.dy * g.dz;
+    if (cells <= 4LL * n) break;
+  }
+  if (cells > 4LL * n) return -1;
+  g.ox = lo[0];
+  g.oy = lo[1];
+  g.oz = lo[2];
+  g.h = h;
+  g.inv_h = 1.0 / h;
+  int *cell = nullptr, *counts = nullptr, *start = nullptr, *fill = nullptr;
+  double4* sorted = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, start, (int)cells + 1, st);
+  VG_CUDA(cudaMallocAsync((void**)&cell, sizeof(int) * n, st));
+  VG_CUDA(cudaMallocAsync((void**)&counts, sizeof(int) * (cells + 1), st));
+  VG_CUDA(cudaMallocAsync((void**)&start, sizeof(int) * (cells + 1), st));
+  VG_CUDA(cudaMallocAsync((void**)&fill, sizeof(int) * cells, st));
+  VG_CUDA(cudaMallocAsync((void**)&sorted, sizeof(double4) * n, st));
+  VG_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), st));
+  VG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * (cells + 1), st));
+  VG_CUDA(cudaMemsetAsync(fill, 0, sizeof(int) * cells, st));
+  k_knn_cell_count<<<(n + 255) / 256, 256, 0, st>>>(cl->xyz64, n, g, cell, counts);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, counts, start, (int)cells + 1, st);
+  k_knn_scatter<<<(n + 255) / 256, 256, 0, st>>>(cl->xyz64, n, cell, start, fill, sorted);
+  const int blocks = (n + 127) / 128;
+  if (k <= 8)
+    k_knn_grid<8><<<blocks, 128, 0, st>>>(sorted, n, k, g, start, nbrs_dev);
+  else if (k <= 16)
+    k_knn_grid<16><<<blocks, 128, 0, st>>>(sorted, n, k, g, start, nbrs_dev);
+  else
+    k_knn_grid<32><<<blocks, 128, 0, st>>>(sorted, n, k, g, start, nbrs_dev);
+  ctx->launches += 5;
+  VG_CUDA(cudaGetLastError());
+  VG_CUDA(cudaFreeAsync(cell, st));
+  VG_CUDA(cudaFreeAsync(counts, st));
+  VG_CUDA(cudaFreeAsync(start, st));
+  VG_CUDA(cudaFreeAsync(fill, st));
+  VG_CUDA(cudaFreeAsync(sorted, st));
+  VG_CUDA(cudaFreeAsync(tmp, st));
+  return 0;
+}
+
 int launch_knn(vg_ctx* ctx, const vg_cloud* cl, int k, long long* nbrs_dev) {
   const int n = (int)cl->n;
   if (n == 0) return 0;
+  static const int grid_env = [] {
+    const char* e = getenv("VGICP_KNN_GRID");  // 0: always brute force
+    return e ? atoi(e) : 1;
+  }();
+  if (grid_env && n >= kKnnGridMin && k <= 32) {
+    const int rc = launch_knn_grid(ctx, cl, k, nbrs_dev);
+    if (rc != -1) return rc;  // -1: grid not applicable (degenerate extent), brute force below
+  }
   const int blocks = (n + kKnnTile - 1) / kKnnTile;
   if (k <= 8)
     k_knn<8><<<blocks, kKnnTile, 0, ctx->stream>>>(cl->xyz64, n, k, nbrs_dev);

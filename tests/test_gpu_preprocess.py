@@ -105,3 +105,38 @@ def test_fused_knn_covariances_vs_oracle():
     assert ok.mean() > 0.99
     np.testing.assert_allclose(out.covs[ok], ref[ok], rtol=0, atol=1e-6)
     assert np.array_equal(out.degenerate, degen)
+
+
+def _brute_knn(pts, k, chunk=512):
+    """(d2, index)-ordered brute force with the reference's d2 association (dx²+dz²)+dy²."""
+    out = np.empty((len(pts), k), np.int64)
+    idx = np.arange(len(pts))
+    for a in range(0, len(pts), chunk):
+        q = pts[a:a + chunk]
+        d = pts[None, :, :] - q[:, None, :]
+        sq = d * d
+        d2 = (sq[..., 0] + sq[..., 2]) + sq[..., 1]
+        order = np.lexsort((np.broadcast_to(idx, d2.shape), d2), axis=1)
+        out[a:a + chunk] = order[:, :k]
+    return out
+
+
+@pytest.mark.parametrize("case", ["lattice_ties", "clusters_outliers", "flat"])
+def test_grid_knn_exact_on_hard_clouds(case):
+    """Clouds >= 4096 points take the grid kNN: exact (d2, index) order, including exact
+    distance ties (integer lattice), duplicates, far outliers and a degenerate (flat) extent."""
+    rng = np.random.default_rng(3)
+    if case == "lattice_ties":
+        g = np.stack(np.meshgrid(np.arange(20), np.arange(20), np.arange(12), indexing="ij"), -1)
+        pts = g.reshape(-1, 3).astype(float) * 0.5
+        pts = np.vstack([pts, pts[:300]])                      # exact duplicates
+    elif case == "clusters_outliers":
+        centers = rng.uniform(-30, 30, (12, 3))
+        pts = np.vstack([c + rng.normal(scale=0.2, size=(400, 3)) for c in centers])
+        pts = np.vstack([pts, rng.uniform(-500, 500, (20, 3))])  # isolated far points
+    else:
+        pts = np.column_stack([rng.uniform(-5, 5, 5000), rng.uniform(-5, 5, 5000), np.zeros(5000)])
+    pts = pts.astype(np.float32).astype(np.float64)
+    assert len(pts) >= 4096
+    ours = P.knn_search(P.make_frame(pts), 10)
+    assert np.array_equal(ours, _brute_knn(pts, 10))
