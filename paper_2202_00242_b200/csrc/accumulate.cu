@@ -29,7 +29,11 @@
 namespace vg {
 
 // ---- K4a ------------------------------------------------------------------------------------
-constexpr int kLookupWarps = 8;
+// One warp per CTA for K4a and K4b: an SM slot is released as soon as its item finishes
+// (with 4-8 warp CTAs the slot waits for the CTA's slowest item; measured 12% slower for K4a,
+// 7% for K4b).  Residency is set through the min-CTAs launch bound: 32 (K4a fast path,
+// 64 registers), 24 (K4a generic), 12 (K4b, <= 170 registers).
+constexpr int kLookupWarps = 1;
 
 // KM: 1 = every map of the batch uses 32-bit local keys, 0 = all int64, 2 = mixed (runtime)
 // P2: every map of the batch has a power-of-two resolution (x * (1/res) is exact)
@@ -279,7 +283,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
 }
 
 // ---- K4b ------------------------------------------------------------------------------------
-constexpr int kAccWarps = 4;
+constexpr int kAccWarps = 1;  // see kLookupWarps
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -570,19 +574,19 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
   const ItemDev* it = b->items + off;
   int* hc = b->hit_counts + off;
   AccDesc* dd = b->descs + off;
-  if (b->key_mode == 1 && b->all_pow2 && b->all_f32)  // fast path, 4 CTAs/SM
-    k_lookup_fast<4><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
+  if (b->key_mode == 1 && b->all_pow2 && b->all_f32)  // fast path
+    k_lookup_fast<32><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
   else if (b->key_mode == 1 && b->all_pow2)
-    k_lookup_items<1, 3, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+    k_lookup_items<1, 24, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                               b->maps, b->hits, hc, p2, dd);
   else if (b->key_mode == 1)
-    k_lookup_items<1, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+    k_lookup_items<1, 24><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                            b->maps, b->hits, hc, p2, dd);
   else if (b->key_mode == 0)
-    k_lookup_items<0, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+    k_lookup_items<0, 24><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                            b->maps, b->hits, hc, p2, dd);
   else
-    k_lookup_items<2, 3><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
+    k_lookup_items<2, 24><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                            b->maps, b->hits, hc, p2, dd);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
@@ -608,13 +612,13 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
                             cudaStream_t st) {
   const AccDesc* d = b->descs + off;
   if (kmode == 1)
-    return launch_acc_kernel(ctx, k_accumulate<1, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
+    return launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
                              cnt, b->hits, b->partials + 2 * (size_t)off, st);
   double* p = b->partials + (size_t)off * kPartialStride;
   if (b->all_f32)  // every point fp32-exact: one 16 B point unit per lane (more L1 left)
-    return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1, 1>, sizeof(AccSmem<2, 1>) * kAccWarps,
+    return launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1>, sizeof(AccSmem<2, 1>) * kAccWarps,
                              d, cnt, b->hits, p, st);
-  return launch_acc_kernel(ctx, k_accumulate<0, 2, 3, 1>, sizeof(AccSmem<2>) * kAccWarps, d, cnt,
+  return launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1>, sizeof(AccSmem<2>) * kAccWarps, d, cnt,
                            b->hits, p, st);
 }
 
