@@ -52,9 +52,9 @@ def parse():
 
 
 def traffic_record():
-    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01b_traffic.json,
-    written by tools/launch_traffic.py from profiles/r01b_launches.csv)."""
-    p = ROOT / "profiles" / "r01b_traffic.json"
+    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01c_traffic.json,
+    written by tools/launch_traffic.py from profiles/r01c_launches.csv)."""
+    p = ROOT / "profiles" / "r01c_traffic.json"
     try:
         return int(json.loads(p.read_text())["dram_bytes_per_launch"])
     except Exception:
