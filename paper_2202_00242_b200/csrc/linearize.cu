@@ -372,12 +372,13 @@ __device__ __forceinline__ double asm_value(const double* __restrict__ r, int ro
   }
 }
 
-__global__ void __launch_bounds__(128)
+constexpr int kAsmWarps = 1;  // one-warp CTAs: the long diagonal units do not hold CTA slots
+__global__ void __launch_bounds__(kAsmWarps * 32)
     k_assemble(const double* __restrict__ rec, const FactorDev* __restrict__ factors, int F,
                const int* __restrict__ begin, const int* __restrict__ codes, int V, int P,
                double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int u = blockIdx.x * kAsmWarps + (threadIdx.x >> 5);
   if (u >= V + P) return;
   const int k0 = __ldg(begin + u), k1 = __ldg(begin + u + 1);
   const bool diag = u < V;
@@ -716,7 +717,7 @@ __global__ void __launch_bounds__(kCostThreads)
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev) {
   const int units = (int)(b->asm_vars + b->asm_pairs_n);
   if (units > 0)
-    k_assemble<<<(units + 3) / 4, 128, 0, ctx->stream>>>(rec, b->factors, (int)b->F, b->asm_begin,
+    k_assemble<<<(units + kAsmWarps - 1) / kAsmWarps, kAsmWarps * 32, 0, ctx->stream>>>(rec, b->factors, (int)b->F, b->asm_begin,
                                                        b->asm_codes, (int)b->asm_vars,
                                                        (int)b->asm_pairs_n, out_dev);
   k_assemble_cost<<<kCostBlocks, kCostThreads, 0, ctx->stream>>>(
