@@ -354,7 +354,7 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
   cp_async_commit();
 }
 
-template <int MODE>
+template <int MODE, int PLANE>
 __device__ __forceinline__ void hit_core(double px, double py, double pz, double2 s0,
                                          double2 s1, double2 s2, const float4* rec,
                                          const double (&R)[9], const double (&t)[3],
@@ -362,7 +362,7 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
 
 // per-hit fp64 math of K4b on one staged hit: moved point, residual, fused covariance and its
 // inverse, cost, and the target-frame Jacobian blocks about the source origin
-template <int MODE, int PT = 2>
+template <int MODE, int PT = 2, int PLANE = 0>
 __device__ __forceinline__ void hit_math(const AccStageT<PT>& st, int lane, bool f64pts,
                                          const double (&R)[9], const double (&t)[3],
                                          double scale, double (&acc)[28]) {
@@ -381,11 +381,12 @@ __device__ __forceinline__ void hit_math(const AccStageT<PT>& st, int lane, bool
   const double2 s0 = *reinterpret_cast<const double2*>(&st.cov[0][lane]);
   const double2 s1 = *reinterpret_cast<const double2*>(&st.cov[1][lane]);
   const double2 s2 = *reinterpret_cast<const double2*>(&st.cov[2][lane]);
-  hit_core<MODE>(px, py, pz, s0, s1, s2, st.rec[lane], R, t, scale, acc);
+  hit_core<MODE, PLANE>(px, py, pz, s0, s1, s2, st.rec[lane], R, t, scale, acc);
 }
 
-// the math of one hit from its source point, source covariance rows and staged voxel record
-template <int MODE>
+// the math of one hit from its source point, source covariance rows (PLANE: the plane form
+// (n0, n1), (n2, kappa), (alpha, 0), map_build.cu) and staged voxel record
+template <int MODE, int PLANE>
 __device__ __forceinline__ void hit_core(double px, double py, double pz, double2 s0,
                                          double2 s1, double2 s2, const float4* rec,
                                          const double (&R)[9], const double (&t)[3],
@@ -401,6 +402,21 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
   const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
   const double d0 = m01.x - x, d1 = m01.y - y, d2 = m2c0.x - z;
   // F = C' + R C R^T (:153)
+  double fa, fb, fc, fd, fe, ff;
+  if (PLANE) {
+    // R C R^T = alpha I - kappa m m^T, m = R n
+    const double n0 = s0.x, n1 = s0.y, n2 = s1.x, kappa = s1.y, alpha = s2.x;
+    const double m0 = fma(R[0], n0, fma(R[1], n1, R[2] * n2));
+    const double m1 = fma(R[3], n0, fma(R[4], n1, R[5] * n2));
+    const double m2 = fma(R[6], n0, fma(R[7], n1, R[8] * n2));
+    const double km0 = kappa * m0, km1 = kappa * m1, km2 = kappa * m2;
+    fa = fma(-km0, m0, m2c0.y + alpha);
+    fb = fma(-km0, m1, c12.x);
+    fc = fma(-km0, m2, c12.y);
+    fd = fma(-km1, m1, c34.x + alpha);
+    fe = fma(-km1, m2, c34.y);
+    ff = fma(-km2, m2, v5 + alpha);
+  } else {
   const double C00 = s0.x, C01 = s0.y, C02 = s1.x, C11 = s1.y, C12 = s2.x, C22 = s2.y;
   double A[9];
 #pragma unroll
@@ -413,8 +429,13 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
   auto arT = [&](int a_, int c_) {
     return fma(A[3 * a_], R[3 * c_], fma(A[3 * a_ + 1], R[3 * c_ + 1], A[3 * a_ + 2] * R[3 * c_ + 2]));
   };
-  const double fa = m2c0.y + arT(0, 0), fb = c12.x + arT(0, 1), fc = c12.y + arT(0, 2);
-  const double fd = c34.x + arT(1, 1), fe = c34.y + arT(1, 2), ff = v5 + arT(2, 2);
+  fa = m2c0.y + arT(0, 0);
+  fb = c12.x + arT(0, 1);
+  fc = c12.y + arT(0, 2);
+  fd = c34.x + arT(1, 1);
+  fe = c34.y + arT(1, 2);
+  ff = v5 + arT(2, 2);
+  }
   // W = F^-1 (:113-130)
   const double i00 = fma(fd, ff, -fe * fe), i01 = fma(fc, fe, -fb * ff),
                i02 = fma(fb, fe, -fc * fd), i11 = fma(fa, ff, -fc * fc),
@@ -458,7 +479,7 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
 // K4b.  ILP rounds of 32 hits are computed per iteration (ILP = 2 gives each lane two
 // independent fp64 dependency chains); kStages >= 2 * ILP staged rounds keep the gathers of
 // the next kStages - ILP rounds in flight during the math.
-template <int MODE, int kStages, int kMinBlocks, int ILP, int PT = 2>
+template <int MODE, int kStages, int kMinBlocks, int ILP, int PT = 2, int PLANE = 0>
 __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     k_accumulate(const AccDesc* __restrict__ descs, int n_items, const int2* __restrict__ hits,
                  double* __restrict__ partials, int dbg) {
@@ -529,11 +550,11 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     if (!(dbg & 2)) {
       if (ILP == 1) {  // branch over padding lanes
         if (r * 32 + lane < n)
-          hit_math<MODE, PT>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
+          hit_math<MODE, PT, PLANE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
       } else {  // branch-free so the ILP rounds interleave; padding lanes replay valid data
 #pragma unroll
         for (int u = 0; u < ILP; ++u)
-          hit_math<MODE, PT>(sm.stage[(r + u) % kStages], lane, f64pts, R, t,
+          hit_math<MODE, PT, PLANE>(sm.stage[(r + u) % kStages], lane, f64pts, R, t,
                          (r + u) * 32 + lane < n ? 1.0 : 0.0, acc);
       }
     }
@@ -611,15 +632,22 @@ static int launch_acc_kernel(vg_ctx* ctx, K kern, size_t smem, const AccDesc* d,
 static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
                             cudaStream_t st) {
   const AccDesc* d = b->descs + off;
-  if (kmode == 1)
-    return launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1>, sizeof(AccSmem<2>) * kAccWarps, d,
-                             cnt, b->hits, b->partials + 2 * (size_t)off, st);
+  const size_t s2 = sizeof(AccSmem<2>) * kAccWarps, s1 = sizeof(AccSmem<2, 1>) * kAccWarps;
+  if (kmode == 1) {
+    double* p = b->partials + 2 * (size_t)off;
+    return b->all_plane
+               ? launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1, 2, 1>, s2, d, cnt, b->hits, p, st)
+               : launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1>, s2, d, cnt, b->hits, p, st);
+  }
   double* p = b->partials + (size_t)off * kPartialStride;
-  if (b->all_f32)  // every point fp32-exact: one 16 B point unit per lane (more L1 left)
-    return launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1>, sizeof(AccSmem<2, 1>) * kAccWarps,
-                             d, cnt, b->hits, p, st);
-  return launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1>, sizeof(AccSmem<2>) * kAccWarps, d, cnt,
-                           b->hits, p, st);
+  // PT = 1: every point fp32-exact, one 16 B point unit per lane (more L1 left)
+  if (b->all_f32)
+    return b->all_plane
+               ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1, 1>, s1, d, cnt, b->hits, p, st)
+               : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1>, s1, d, cnt, b->hits, p, st);
+  return b->all_plane
+             ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 2, 1>, s2, d, cnt, b->hits, p, st)
+             : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1>, s2, d, cnt, b->hits, p, st);
 }
 
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi) {

@@ -193,6 +193,9 @@ int vg_cloud_destroy(vg_cloud* c) {
   dfree(ctx, c->c2);
   dfree(ctx, c->xyz64);
   dfree(ctx, c->cov64);
+  dfree(ctx, c->p0);
+  dfree(ctx, c->p1);
+  dfree(ctx, c->p2);
   delete c;
   return VG_OK;
 }
@@ -496,6 +499,21 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   std::vector<CloudView> cv(clouds.size());
   std::vector<MapView> mv(maps.size());
   for (size_t i = 0; i < clouds.size(); ++i) cv[i] = clouds[i]->view();
+  // plane-form covariances for every source: the batch's views (read by K4a, which hands
+  // them to K4b) carry the plane parameters instead of the covariance rows
+  int all_plane = !clouds.empty() && all_covs;
+  for (const vg_cloud* c : clouds) all_plane &= (c->plane || c->n == 0) ? 1 : 0;
+  static const int plane_env = [] {
+    const char* e = getenv("VGICP_PLANE");  // 0: always the general covariance form
+    return e ? atoi(e) : 1;
+  }();
+  all_plane &= plane_env ? 1 : 0;
+  if (all_plane)
+    for (size_t i = 0; i < clouds.size(); ++i) {
+      cv[i].c0 = clouds[i]->p0;
+      cv[i].c1 = clouds[i]->p1;
+      cv[i].c2 = clouds[i]->p2;
+    }
   int n32 = 0;
   for (size_t i = 0; i < maps.size(); ++i) {
     mv[i] = maps[i]->view();
@@ -504,6 +522,7 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   b->key_mode = n32 == (int)maps.size() ? 1 : (n32 == 0 ? 0 : 2);
   b->all_pow2 = 1;
   for (const MapView& m : mv) b->all_pow2 &= m.pow2 ? 1 : 0;
+  b->all_plane = all_plane;
   b->all_f32 = 1;
   for (const CloudView& c : cv) b->all_f32 &= c.xyz64 ? 0 : 1;
   std::vector<ItemHdr> hdrs(items.size());

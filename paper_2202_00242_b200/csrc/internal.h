@@ -35,6 +35,10 @@ struct vg_cloud {
   double2* c2 = nullptr;
   double* xyz64 = nullptr;  // always kept: fp64 points (map build, kNN)
   double* cov64 = nullptr;  // n*9 fp64 covariances (bit-exact map build), or null
+  double2* p0 = nullptr;    // plane form alpha I - kappa n n^T of every covariance (map_build.cu)
+  double2* p1 = nullptr;
+  double2* p2 = nullptr;
+  bool plane = false;       // every covariance has the plane form
   vg::CloudView view() const {
     vg::CloudView v;
     v.a = a;
@@ -101,6 +105,8 @@ struct vg_batch {
   int key_mode = 2;                   // 1: all maps 32-bit local keys, 0: all int64, 2: mixed
   int all_pow2 = 0;                   // every map's resolution is a power of two
   int all_f32 = 0;                    // every source point is fp32-exact (no xyz64 copy)
+  int all_plane = 0;                  // every source covariance has the plane form (c0..c2 of
+                                      // the batch's cloud views then point at p0..p2)
   bool all_covs = true;               // every source has covariances (else INLIERS mode only)
   vg::FactorDev* factors = nullptr;   // F
   vg::ItemDev* items = nullptr;       // num_items (ordered by target map, then factor)

@@ -10,6 +10,9 @@
 #include <climits>
 #include <vector>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
@@ -46,6 +49,60 @@ __global__ void k_cloud_pack(const double* __restrict__ xyz, const double* __res
       c1[i] = make_double2(C[2], C[4]);
       c2[i] = make_double2(C[5], C[8]);
     }
+  }
+}
+
+// Plane form of a source covariance: C = alpha I - kappa n n^T (|n| = 1), which every
+// covariance estimate_covariances makes (V diag(eps, 1, 1) V^T = I - (1 - eps) n n^T;
+// degenerate: eps I), so R C R^T = alpha I - kappa (R n)(R n)^T costs 21 fp64 ops per
+// correspondence in K4b instead of 45.  alpha and kappa follow from the trace and the
+// Frobenius norm (alpha is the double eigenvalue), n from the largest column of
+// alpha I - C; a point is accepted when the reconstruction matches C to 1e-12, otherwise the
+// cloud keeps the general form.  Layout: p0 = (n0, n1), p1 = (n2, kappa), p2 = (alpha, 0).
+__global__ void k_plane_fit(const double* __restrict__ cov, long long n, double2* __restrict__ p0,
+                            double2* __restrict__ p1, double2* __restrict__ p2,
+                            unsigned* __restrict__ fails) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double* C = cov + 9 * i;
+    // fit the symmetric part (V diag V^T is symmetric only to the last bit); the acceptance
+    // test below checks all nine entries
+    const double a00 = C[0], a11 = C[4], a22 = C[8];
+    const double a01 = 0.5 * (C[1] + C[3]), a02 = 0.5 * (C[2] + C[6]), a12 = 0.5 * (C[5] + C[7]);
+    bool ok = true;
+    double alpha = 0.0, kappa = 0.0, n0 = 1.0, n1 = 0.0, n2 = 0.0;
+    if (a01 == 0.0 && a02 == 0.0 && a12 == 0.0 && a00 == a11 && a11 == a22 && C[1] == 0.0 &&
+        C[2] == 0.0 && C[5] == 0.0) {
+      alpha = a00;  // isotropic (degenerate neighbourhoods: eps I)
+    } else {
+      const double t = a00 + a11 + a22;
+      const double q = a00 * a00 + a11 * a11 + a22 * a22 + 2.0 * (a01 * a01 + a02 * a02 + a12 * a12);
+      alpha = (4.0 * t + sqrt(fmax(24.0 * q - 8.0 * t * t, 0.0))) / 12.0;
+      kappa = 3.0 * alpha - t;
+      const double m[3][3] = {{alpha - a00, -a01, -a02}, {-a01, alpha - a11, -a12},
+                              {-a02, -a12, alpha - a22}};
+      int k = 0;
+      if (m[1][1] > m[k][k]) k = 1;
+      if (m[2][2] > m[k][k]) k = 2;
+      if (!(kappa > 0.0) || !(m[k][k] > 0.0)) {
+        ok = false;
+      } else {
+        const double sc = 1.0 / sqrt(kappa * m[k][k]);
+        n0 = m[0][k] * sc;
+        n1 = m[1][k] * sc;
+        n2 = m[2][k] * sc;
+        const double nv[3] = {n0, n1, n2};
+        double r = 0.0;
+        for (int a = 0; a < 3; ++a)
+          for (int b = 0; b < 3; ++b)
+            r = fmax(r, fabs((a == b ? alpha : 0.0) - kappa * nv[a] * nv[b] - C[3 * a + b]));
+        ok = r <= 1e-12 * fmax(1.0, fabs(alpha));
+      }
+    }
+    if (!ok) atomicAdd(fails, 1u);
+    p0[i] = make_double2(n0, n1);
+    p1[i] = make_double2(n2, kappa);
+    p2[i] = make_double2(alpha, 0.0);
   }
 }
 
@@ -166,11 +223,32 @@ int launch_pack_keys(vg_ctx* ctx, const double* xyz_dev, long long n, double res
 }
 
 int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cl) {
+  cl->plane = false;
   if (cl->n == 0) return 0;
   k_cloud_pack<<<grid1(cl->n, 256), 256, 0, ctx->stream>>>(cl->xyz64, cl->cov64, cl->n, cl->a,
                                                            cl->c0, cl->c1, cl->c2);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
+  if (!cl->cov64) return 0;
+  if (!cl->p0) {
+    VG_CUDA(cudaMallocAsync((void**)&cl->p0, sizeof(double2) * cl->n, ctx->stream));
+    VG_CUDA(cudaMallocAsync((void**)&cl->p1, sizeof(double2) * cl->n, ctx->stream));
+    VG_CUDA(cudaMallocAsync((void**)&cl->p2, sizeof(double2) * cl->n, ctx->stream));
+  }
+  unsigned* dfail = nullptr;
+  unsigned hfail = 1;
+  VG_CUDA(cudaMallocAsync((void**)&dfail, sizeof(unsigned), ctx->stream));
+  VG_CUDA(cudaMemsetAsync(dfail, 0, sizeof(unsigned), ctx->stream));
+  k_plane_fit<<<grid1(cl->n, 256), 256, 0, ctx->stream>>>(cl->cov64, cl->n, cl->p0, cl->p1,
+                                                          cl->p2, dfail);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  VG_CUDA(cudaMemcpyAsync(&hfail, dfail, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CUDA(cudaStreamSynchronize(ctx->stream));
+  VG_CUDA(cudaFreeAsync(dfail, ctx->stream));
+  cl->plane = hfail == 0;
+  if (getenv("VGICP_DEBUG_PLANE"))
+    fprintf(stderr, "plane fit: %lld points, %u not in plane form\n", cl->n, hfail);
   return 0;
 }
 

@@ -502,3 +502,38 @@ def test_batch_general_paths_vs_oracle(small_graph, res, wide):
             assert_lin(RG.unpack_record(out[f], False), ref, False)
             checked += 1
         assert checked >= len(sel) // 2
+
+
+def test_general_source_covariances_vs_oracle(small_graph):
+    """Source covariances that are not of the plane form alpha I - kappa n n^T (random SPD)
+    take K4b's general R C R^T path; plane-form ones (everything estimate_covariances makes)
+    take the 21-op path.  Both match the oracle."""
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    sel = pairs[:10]
+    table = np.array([G.pose_row(p) for p in est])
+    R, t = O.relative_transforms(table, sel[:, 0], sel[:, 1])
+    rng = np.random.default_rng(12)
+    dmaps = {j: _lib.DeviceMap.build(_lib.DeviceCloud(scans[j], covs[j]), 1.0)
+             for j in np.unique(sel[:, 1])}
+    for general in (False, True):
+        clouds, ccovs = [], []
+        for i, _ in sel:
+            c = srcs[i][1]
+            if general:
+                a = rng.normal(scale=0.3, size=(len(c), 3, 3))
+                c = c + np.einsum("nij,nkj->nik", a, a) * 0.1   # SPD, not plane form
+            clouds.append(_lib.DeviceCloud(srcs[i][0], c))
+            ccovs.append(c)
+        batch = _lib.DeviceBatch(clouds, [dmaps[j] for j in sel[:, 1]], [False] * len(sel),
+                                 [10] * len(sel), sel[:, 0], sel[:, 1])
+        out = batch.linearize_poses(table)
+        checked = 0
+        for f, (i, j) in enumerate(sel):
+            try:
+                ref = O.linearize(srcs[i][0], ccovs[f], maps[j], R[f], t[f])
+            except ValueError:
+                assert out[f][91] < 10
+                continue
+            assert_lin(RG.unpack_record(out[f], False), ref, False)
+            checked += 1
+        assert checked >= len(sel) // 2
