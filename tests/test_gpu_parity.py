@@ -505,9 +505,9 @@ def test_batch_general_paths_vs_oracle(small_graph, res, wide):
 
 
 def test_general_source_covariances_vs_oracle(small_graph):
-    """Source covariances that are not of the plane form alpha I - kappa n n^T (random SPD)
-    take K4b's general R C R^T path; plane-form ones (everything estimate_covariances makes)
-    take the 21-op path.  Both match the oracle."""
+    """Source covariances of the plane form alpha I - kappa n n^T (everything
+    estimate_covariances makes, alpha = 1; and alpha = 2) take K4b's 21-op path, general SPD
+    ones the R C R^T path; all match the oracle."""
     poses, est, scans, covs, maps, srcs, pairs = small_graph
     sel = pairs[:10]
     table = np.array([G.pose_row(p) for p in est])
@@ -515,11 +515,13 @@ def test_general_source_covariances_vs_oracle(small_graph):
     rng = np.random.default_rng(12)
     dmaps = {j: _lib.DeviceMap.build(_lib.DeviceCloud(scans[j], covs[j]), 1.0)
              for j in np.unique(sel[:, 1])}
-    for general in (False, True):
+    for form in ("unit plane", "scaled plane", "general"):
         clouds, ccovs = [], []
         for i, _ in sel:
             c = srcs[i][1]
-            if general:
+            if form == "scaled plane":  # 2 (I - kappa n n^T): plane form with alpha = 2
+                c = 2.0 * c
+            elif form == "general":
                 a = rng.normal(scale=0.3, size=(len(c), 3, 3))
                 c = c + np.einsum("nij,nkj->nik", a, a) * 0.1   # SPD, not plane form
             clouds.append(_lib.DeviceCloud(srcs[i][0], c))
