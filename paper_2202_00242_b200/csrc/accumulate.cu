@@ -203,22 +203,25 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
     const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
     const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
-    const double fx = floor(x * inv_res), fy = floor(y * inv_res), fz = floor(z * inv_res);
+    const double qx = x * inv_res, qy = y * inv_res, qz = z * inv_res;
+    // floor in the convert (F2I.FLOOR, saturating), range-checked as integers
+    const int ix = __double2int_rd(qx), iy = __double2int_rd(qy), iz = __double2int_rd(qz);
     Q q;
     q.live = false;
     q.k32 = 0;
     q.bucket = 0;
-    if (fmax(fabs(fx), fmax(fabs(fy), fabs(fz))) < 1048576.0) {
+    if ((unsigned)(ix + 1048575) < 2097151u && (unsigned)(iy + 1048575) < 2097151u &&
+        (unsigned)(iz + 1048575) < 2097151u) {
       // |floor| < 2^20: the reference's pack/unpack round trip is the identity
-      const unsigned lx = (unsigned)(__double2int_rz(fx) - bx);
-      const unsigned ly = (unsigned)(__double2int_rz(fy) - by);
-      const unsigned lz = (unsigned)(__double2int_rz(fz) - bz);
+      const unsigned lx = (unsigned)(ix - bx);
+      const unsigned ly = (unsigned)(iy - by);
+      const unsigned lz = (unsigned)(iz - bz);
       q.live = lx < (unsigned)ex && ly < (unsigned)ey && lz < (unsigned)ez;
       q.k32 = lx | (ly << 11) | (lz << 22);
     } else {
       MapView mv;
       mv.bx = bx; mv.by = by; mv.bz = bz; mv.ex = ex; mv.ey = ey; mv.ez = ez; mv.shift = shift;
-      const Query qq = make_query(mv, fx, fy, fz, 1);
+      const Query qq = make_query(mv, floor(qx), floor(qy), floor(qz), 1);
       q.live = qq.inside;
       q.k32 = qq.k32;
     }
