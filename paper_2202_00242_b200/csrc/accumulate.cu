@@ -399,11 +399,12 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
   const double2 c12 = *reinterpret_cast<const double2*>(&rec[2]);
   const double2 c34 = *reinterpret_cast<const double2*>(&rec[3]);
   const double v5 = reinterpret_cast<const double*>(&rec[4])[0];
-  // moved point (registration.py:148) and residual d = mu' - moved (:152)
-  const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
-  const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
-  const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
-  const double d0 = m01.x - x, d1 = m01.y - y, d2 = m2c0.x - z;
+  // moved point (registration.py:148) and residual d = mu' - moved (:152); the lever arm
+  // about the source origin is x' = R p
+  const double vx = fma(R[0], px, fma(R[1], py, R[2] * pz));
+  const double vy = fma(R[3], px, fma(R[4], py, R[5] * pz));
+  const double vz = fma(R[6], px, fma(R[7], py, R[8] * pz));
+  const double d0 = m01.x - (vx + t[0]), d1 = m01.y - (vy + t[1]), d2 = m2c0.x - (vz + t[2]);
   // F = C' + R C R^T (:153)
   double fa, fb, fc, fd, fe, ff;
   if (PLANE) {
@@ -439,43 +440,54 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
   fe = c34.y + arT(1, 2);
   ff = v5 + arT(2, 2);
   }
-  // W = F^-1 (:113-130)
+  // W = F^-1 = adj(F) / det(F) (:113-130).  W itself is never formed: every accumulated
+  // term is linear in W, so the terms use the adjugate I and are scaled by s = scale / det
+  // in their accumulating FMA.  `scale` is 0 for padding lanes (which replay a valid hit),
+  // so padding contributes exact zeros without a branch.
   const double i00 = fma(fd, ff, -fe * fe), i01 = fma(fc, fe, -fb * ff),
                i02 = fma(fb, fe, -fc * fd), i11 = fma(fa, ff, -fc * fc),
                i12 = fma(fb, fc, -fa * fe), i22 = fma(fa, fd, -fb * fb);
-  // `scale` is 0 for padding lanes (which replay a valid hit): W, Wd and every accumulated
-  // term are linear in it, so padding contributes exact zeros without a branch
-  const double inv = rcp64(fma(fa, i00, fma(fb, i01, fc * i02))) * scale;
-  const double W00 = i00 * inv, W01 = i01 * inv, W02 = i02 * inv, W11 = i11 * inv,
-               W12 = i12 * inv, W22 = i22 * inv;
-  const double wd0 = fma(W00, d0, fma(W01, d1, W02 * d2));
-  const double wd1 = fma(W01, d0, fma(W11, d1, W12 * d2));
-  const double wd2 = fma(W02, d0, fma(W12, d1, W22 * d2));
-  acc[27] += fma(d0, wd0, fma(d1, wd1, d2 * wd2));  // cost (:156)
+  const double sw = rcp64(fma(fa, i00, fma(fb, i01, fc * i02))) * scale;
+  // I d  (W d = s I d)
+  const double wd0 = fma(i00, d0, fma(i01, d1, i02 * d2));
+  const double wd1 = fma(i01, d0, fma(i11, d1, i12 * d2));
+  const double wd2 = fma(i02, d0, fma(i12, d1, i22 * d2));
+  acc[27] = fma(fma(d0, wd0, fma(d1, wd1, d2 * wd2)), sw, acc[27]);  // cost (:156)
   if (MODE == 0) {
-    const double vx = x - t[0], vy = y - t[1], vz = z - t[2];
-    // N = hat(x') W, P = N hat(x')^T, b' = [x' x Wd ; Wd]  (J' = [-hat(x') | I])
-    const double N00 = fma(-vz, W01, vy * W02), N01 = fma(-vz, W11, vy * W12),
-                 N02 = fma(-vz, W12, vy * W22);
-    const double N10 = fma(vz, W00, -vx * W02), N11 = fma(vz, W01, -vx * W12),
-                 N12 = fma(vz, W02, -vx * W22);
-    const double N20 = fma(-vy, W00, vx * W01), N21 = fma(-vy, W01, vx * W11),
-                 N22 = fma(-vy, W02, vx * W12);
-    acc[0] += fma(-vz, N01, vy * N02);
-    acc[1] += fma(vz, N00, -vx * N02);
-    acc[2] += fma(-vy, N00, vx * N01);
-    acc[3] += fma(vz, N10, -vx * N12);
-    acc[4] += fma(-vy, N10, vx * N11);
-    acc[5] += fma(-vy, N20, vx * N21);
-    acc[6] += N00; acc[7] += N01; acc[8] += N02;
-    acc[9] += N10; acc[10] += N11; acc[11] += N12;
-    acc[12] += N20; acc[13] += N21; acc[14] += N22;
-    acc[15] += W00; acc[16] += W01; acc[17] += W02;
-    acc[18] += W11; acc[19] += W12; acc[20] += W22;
-    acc[21] += fma(vy, wd2, -vz * wd1);
-    acc[22] += fma(vz, wd0, -vx * wd2);
-    acc[23] += fma(vx, wd1, -vy * wd0);
-    acc[24] += wd0; acc[25] += wd1; acc[26] += wd2;
+    // N = hat(x') W, P = N hat(x')^T, b' = [x' x Wd ; Wd]  (J' = [-hat(x') | I]), all / s
+    const double N00 = fma(-vz, i01, vy * i02), N01 = fma(-vz, i11, vy * i12),
+                 N02 = fma(-vz, i12, vy * i22);
+    const double N10 = fma(vz, i00, -vx * i02), N11 = fma(vz, i01, -vx * i12),
+                 N12 = fma(vz, i02, -vx * i22);
+    const double N20 = fma(-vy, i00, vx * i01), N21 = fma(-vy, i01, vx * i11),
+                 N22 = fma(-vy, i02, vx * i12);
+    acc[0] = fma(fma(-vz, N01, vy * N02), sw, acc[0]);
+    acc[1] = fma(fma(vz, N00, -vx * N02), sw, acc[1]);
+    acc[2] = fma(fma(-vy, N00, vx * N01), sw, acc[2]);
+    acc[3] = fma(fma(vz, N10, -vx * N12), sw, acc[3]);
+    acc[4] = fma(fma(-vy, N10, vx * N11), sw, acc[4]);
+    acc[5] = fma(fma(-vy, N20, vx * N21), sw, acc[5]);
+    acc[6] = fma(N00, sw, acc[6]);
+    acc[7] = fma(N01, sw, acc[7]);
+    acc[8] = fma(N02, sw, acc[8]);
+    acc[9] = fma(N10, sw, acc[9]);
+    acc[10] = fma(N11, sw, acc[10]);
+    acc[11] = fma(N12, sw, acc[11]);
+    acc[12] = fma(N20, sw, acc[12]);
+    acc[13] = fma(N21, sw, acc[13]);
+    acc[14] = fma(N22, sw, acc[14]);
+    acc[15] = fma(i00, sw, acc[15]);
+    acc[16] = fma(i01, sw, acc[16]);
+    acc[17] = fma(i02, sw, acc[17]);
+    acc[18] = fma(i11, sw, acc[18]);
+    acc[19] = fma(i12, sw, acc[19]);
+    acc[20] = fma(i22, sw, acc[20]);
+    acc[21] = fma(fma(vy, wd2, -vz * wd1), sw, acc[21]);
+    acc[22] = fma(fma(vz, wd0, -vx * wd2), sw, acc[22]);
+    acc[23] = fma(fma(vx, wd1, -vy * wd0), sw, acc[23]);
+    acc[24] = fma(wd0, sw, acc[24]);
+    acc[25] = fma(wd1, sw, acc[25]);
+    acc[26] = fma(wd2, sw, acc[26]);
   }
 }
 
