@@ -330,9 +330,9 @@ struct AccSmem {
 template <int kStages, int PT = 2>
 __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& mv,
                                             AccSmem<kStages, PT>& sm, int round, int2 e,
-                                            int nvalid, int lane) {
+                                            int nvalid, int lane, bool own = true) {
   AccStageT<PT>& st = sm.stage[round % kStages];
-  if (lane < nvalid) {
+  if (lane < nvalid && own) {
     if (PT == 2 && cv.xyz64) {
       const double* p = cv.xyz64 + 3 * (size_t)e.x;
       double* d = reinterpret_cast<double*>(&st.pt[0][lane]);
@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   for (int r = 0; r < kAhead; ++r) {
     const int k = r * 32 + lane;
     issue_round<kStages, PT>(cv, mv, sm, r, hl[min(k, klast)], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - r * 32),
-                lane);
+                lane, !(dbg & 4));
   }
   // hit entries are prefetched one iteration ahead of their gather; the loads are
   // unconditional (index clamped) so their first use is the next iteration's gather
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     for (int u = 0; u < ILP; ++u) {
       const int ri = r + kAhead + u;
       issue_round<kStages, PT>(cv, mv, sm, ri, nxt[u], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - ri * 32),
-                               lane);
+                               lane, !(dbg & 4));
     }
 #pragma unroll
     for (int u = 0; u < ILP; ++u) {
@@ -633,7 +633,8 @@ template <class K>
 static int launch_acc_kernel(vg_ctx* ctx, K kern, size_t smem, const AccDesc* d, int cnt,
                              const int2* hits, double* partials, cudaStream_t st) {
   static const int dbg = [] {
-    const char* e = getenv("VGICP_K4B_DEBUG");  // profiling only: 1 no gathers, 2 no math
+    // profiling only: 1 no gathers, 2 no math, 4 no lane-own point/covariance gathers
+    const char* e = getenv("VGICP_K4B_DEBUG");
     return e ? atoi(e) : 0;
   }();
   VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
