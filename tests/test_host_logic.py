@@ -123,3 +123,35 @@ def test_integrate_patch_replaces_and_restores():
     assert OdometryEstimator()._overlap_matrix() == "reference loop"
     assert pkg.registration.build_voxelmap is sentinel
     assert pkg.preprocess.knn_search is sentinel
+
+
+def test_normal_equations_flat_layout_and_dense():
+    """NormalEquations.from_flat / dense (the host side of vg_batch_assemble_*): the flat C-ABI
+    layout [cost, count, diag V x 21 (upper), grad V x 6, pairs P x 36] scatters into the dense
+    system the way the reference's _assemble_dense does (factor_graph.py:529-535)."""
+    from paper_2202_00242_b200._lib import NormalEquations
+
+    rng = np.random.default_rng(4)
+    V, pairs = 4, np.array([[0, 2], [1, 3]], np.int32)
+    full = [rng.normal(size=(6, 6)) for _ in range(V)]
+    full = [a + a.T for a in full]
+    iu = np.triu_indices(6)
+    off = rng.normal(size=(2, 6, 6))
+    grad = rng.normal(size=(V, 6))
+    flat = np.concatenate([[3.5, 7.0], np.concatenate([a[iu] for a in full]), grad.ravel(),
+                           off.ravel()])
+    ne = NormalEquations.from_flat(flat, V, pairs)
+    assert ne.cost == 3.5 and ne.count == 7
+    assert all(np.array_equal(ne.diag[v], full[v]) for v in range(V))
+    h, g = ne.dense(offsets=[0, 6, 12, 18], dim=24)
+    ref = np.zeros((24, 24))
+    for v in range(V):
+        ref[6 * v:6 * v + 6, 6 * v:6 * v + 6] += full[v]
+    for (a, b), blk in zip(pairs, off):
+        ref[6 * a:6 * a + 6, 6 * b:6 * b + 6] += blk
+        ref[6 * b:6 * b + 6, 6 * a:6 * a + 6] += blk.T
+    assert np.array_equal(h, ref) and np.array_equal(h, h.T)
+    assert np.array_equal(g, grad.ravel())
+    # 15-dof keys: blocks land top-left of each variable's slice
+    h15, _ = ne.dense(offsets=[0, 15, 30, 45], dim=60)
+    assert np.array_equal(h15[15:21, 45:51], off[1]) and not h15[21:30].any()
