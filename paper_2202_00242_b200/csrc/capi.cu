@@ -954,12 +954,11 @@ int vg_knn(vg_ctx* ctx, const vg_cloud* cloud, int32_t k, int64_t* nbrs_out) {
     return fail(VG_ERR_TOO_SPARSE, "frame has " + std::to_string(cloud->n) +
                                        " points, need at least " + std::to_string(k));
   if (cloud->n >= (1LL << 31)) return fail(VG_ERR_INVALID, "cloud too large");
+  DeviceTemps temps(ctx->stream);
   long long* dn = nullptr;
-  VG_CHECK(dalloc(ctx, &dn, (size_t)cloud->n * k));
+  VG_CUDA(temps.alloc(&dn, (size_t)cloud->n * k));
   VG_CHECK(launch_knn(ctx, cloud, k, dn));
-  int rc = d2h_sync(ctx, nbrs_out, dn, sizeof(long long) * cloud->n * k);
-  dfree(ctx, dn);
-  return rc;
+  return d2h_sync(ctx, nbrs_out, dn, sizeof(long long) * cloud->n * k);
 }
 
 int vg_covariances(vg_ctx* ctx, const vg_cloud* cloud, const int64_t* nbrs, int32_t k, double eps,
@@ -970,20 +969,17 @@ int vg_covariances(vg_ctx* ctx, const vg_cloud* cloud, const int64_t* nbrs, int3
   if (n == 0) return VG_OK;
   for (long long i = 0; i < n * k; ++i)
     if (nbrs[i] < 0 || nbrs[i] >= n) return fail(VG_ERR_INVALID, "neighbor index out of range");
+  DeviceTemps temps(ctx->stream);
   long long* dn = nullptr;
   double* dc = nullptr;
   unsigned char* dg = nullptr;
-  VG_CHECK(dalloc(ctx, &dn, (size_t)n * k));
-  VG_CHECK(dalloc(ctx, &dc, 9 * (size_t)n));
-  VG_CHECK(dalloc(ctx, &dg, (size_t)n));
+  VG_CUDA(temps.alloc(&dn, (size_t)n * k));
+  VG_CUDA(temps.alloc(&dc, 9 * (size_t)n));
+  VG_CUDA(temps.alloc(&dg, (size_t)n));
   VG_CHECK(h2d(ctx, dn, nbrs, sizeof(long long) * n * k));
   VG_CHECK(launch_cov(ctx, cloud, dn, k, eps, dc, dg));
   if (degen_out) VG_CUDA(cudaMemcpyAsync(degen_out, dg, n, cudaMemcpyDeviceToHost, ctx->stream));
-  int rc = d2h_sync(ctx, covs_out, dc, sizeof(double) * 9 * n);
-  dfree(ctx, dn);
-  dfree(ctx, dc);
-  dfree(ctx, dg);
-  return rc;
+  return d2h_sync(ctx, covs_out, dc, sizeof(double) * 9 * n);
 }
 
 int vg_cloud_estimate_covariances(vg_ctx* ctx, vg_cloud* cloud, int32_t k, double eps,
@@ -993,10 +989,11 @@ int vg_cloud_estimate_covariances(vg_ctx* ctx, vg_cloud* cloud, int32_t k, doubl
   if (n < k)
     return fail(VG_ERR_TOO_SPARSE, "frame has " + std::to_string(n) + " points, need at least " +
                                        std::to_string(k));
+  DeviceTemps temps(ctx->stream);
   long long* dn = nullptr;
   unsigned char* dg = nullptr;
-  VG_CHECK(dalloc(ctx, &dn, (size_t)n * k));
-  VG_CHECK(dalloc(ctx, &dg, (size_t)n));
+  VG_CUDA(temps.alloc(&dn, (size_t)n * k));
+  VG_CUDA(temps.alloc(&dg, (size_t)n));
   if (!cloud->cov64) {
     VG_CHECK(dalloc(ctx, &cloud->cov64, 9 * (size_t)n));
     VG_CHECK(dalloc(ctx, &cloud->c0, (size_t)n));
@@ -1011,8 +1008,6 @@ int vg_cloud_estimate_covariances(vg_ctx* ctx, vg_cloud* cloud, int32_t k, doubl
   if (covs_out) VG_CUDA(cudaMemcpyAsync(covs_out, cloud->cov64, 72 * n, cudaMemcpyDeviceToHost, ctx->stream));
   if (degen_out) VG_CUDA(cudaMemcpyAsync(degen_out, dg, n, cudaMemcpyDeviceToHost, ctx->stream));
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
-  dfree(ctx, dn);
-  dfree(ctx, dg);
   return VG_OK;
 }
 

@@ -147,6 +147,26 @@ struct vg_batch {
   double2* asm_gcost = nullptr;       // per-factor (gated cost, 1 if gated in), written by K5
 };
 
+// Stream-ordered device temporaries of one call, released on every exit path.
+struct DeviceTemps {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit DeviceTemps(cudaStream_t s) : st(s) {}
+  DeviceTemps(const DeviceTemps&) = delete;
+  DeviceTemps& operator=(const DeviceTemps&) = delete;
+  template <class T>
+  cudaError_t alloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) return cudaSuccess;
+    const cudaError_t e = cudaMallocAsync((void**)p, sizeof(T) * count, st);
+    if (e == cudaSuccess) ptrs.push_back((void*)*p);
+    return e;
+  }
+  ~DeviceTemps() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
 // error plumbing (capi.cu)
 void vg_set_error(const std::string& msg);
 int vg_cuda_fail(cudaError_t e, const char* what);

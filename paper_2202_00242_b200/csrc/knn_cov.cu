@@ -329,9 +329,11 @@ static int launch_knn_grid(vg_ctx* ctx, const vg_cloud* cl, int k, long long* nb
   VG_CUDA(cudaMallocAsync((void**)&dbb, sizeof(double) * 6 * bb_blocks, st));
   k_bbox<<<bb_blocks, 256, 0, st>>>(cl->xyz64, n, dbb);
   std::vector<double> hb(6 * bb_blocks);
-  VG_CUDA(cudaMemcpyAsync(hb.data(), dbb, sizeof(double) * 6 * bb_blocks, cudaMemcpyDeviceToHost, st));
+  const cudaError_t ebb =
+      cudaMemcpyAsync(hb.data(), dbb, sizeof(double) * 6 * bb_blocks, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dbb, st);
+  VG_CUDA(ebb);
   VG_CUDA(cudaStreamSynchronize(st));
-  VG_CUDA(cudaFreeAsync(dbb, st));
   double lo[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, hi[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
   for (int b = 0; b < bb_blocks; ++b)
     for (int a = 0; a < 3; ++a) {
@@ -366,13 +368,14 @@ static int launch_knn_grid(vg_ctx* ctx, const vg_cloud* cl, int k, long long* nb
   double4* sorted = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0;
+  DeviceTemps temps(st);
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, counts, start, (int)cells + 1, st);
-  VG_CUDA(cudaMallocAsync((void**)&cell, sizeof(int) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&counts, sizeof(int) * (cells + 1), st));
-  VG_CUDA(cudaMallocAsync((void**)&start, sizeof(int) * (cells + 1), st));
-  VG_CUDA(cudaMallocAsync((void**)&fill, sizeof(int) * cells, st));
-  VG_CUDA(cudaMallocAsync((void**)&sorted, sizeof(double4) * n, st));
-  VG_CUDA(cudaMallocAsync(&tmp, std::max<size_t>(tmp_bytes, 16), st));
+  VG_CUDA(temps.alloc(&cell, (size_t)n));
+  VG_CUDA(temps.alloc(&counts, (size_t)cells + 1));
+  VG_CUDA(temps.alloc(&start, (size_t)cells + 1));
+  VG_CUDA(temps.alloc(&fill, (size_t)cells));
+  VG_CUDA(temps.alloc(&sorted, (size_t)n));
+  VG_CUDA(temps.alloc((unsigned char**)&tmp, std::max<size_t>(tmp_bytes, 16)));
   VG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int) * (cells + 1), st));
   VG_CUDA(cudaMemsetAsync(fill, 0, sizeof(int) * cells, st));
   k_knn_cell_count<<<(n + 255) / 256, 256, 0, st>>>(cl->xyz64, n, g, cell, counts);
@@ -387,12 +390,6 @@ static int launch_knn_grid(vg_ctx* ctx, const vg_cloud* cl, int k, long long* nb
     k_knn_grid<32><<<blocks, 128, 0, st>>>(sorted, n, k, g, start, nbrs_dev);
   ctx->launches += 5;
   VG_CUDA(cudaGetLastError());
-  VG_CUDA(cudaFreeAsync(cell, st));
-  VG_CUDA(cudaFreeAsync(counts, st));
-  VG_CUDA(cudaFreeAsync(start, st));
-  VG_CUDA(cudaFreeAsync(fill, st));
-  VG_CUDA(cudaFreeAsync(sorted, st));
-  VG_CUDA(cudaFreeAsync(tmp, st));
   return 0;
 }
 

@@ -325,14 +325,15 @@ int launch_map_build(vg_ctx* ctx, const vg_cloud* cl, double res, vg_map* map) {
   int *idx = nullptr, *perm = nullptr, *counts = nullptr, *offsets = nullptr, *num_runs = nullptr;
   void* tmp = nullptr;
   size_t tmp_bytes = 0, t1 = 0, t2 = 0, t3 = 0;
-  VG_CUDA(cudaMallocAsync((void**)&keys, sizeof(long long) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&keys_sorted, sizeof(long long) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&ukeys, sizeof(long long) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&idx, sizeof(int) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&perm, sizeof(int) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&counts, sizeof(int) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&offsets, sizeof(int) * n, st));
-  VG_CUDA(cudaMallocAsync((void**)&num_runs, sizeof(int), st));
+  DeviceTemps temps(st);  // released on every exit path
+  VG_CUDA(temps.alloc(&keys, (size_t)n));
+  VG_CUDA(temps.alloc(&keys_sorted, (size_t)n));
+  VG_CUDA(temps.alloc(&ukeys, (size_t)n));
+  VG_CUDA(temps.alloc(&idx, (size_t)n));
+  VG_CUDA(temps.alloc(&perm, (size_t)n));
+  VG_CUDA(temps.alloc(&counts, (size_t)n));
+  VG_CUDA(temps.alloc(&offsets, (size_t)n));
+  VG_CUDA(temps.alloc(&num_runs, 1));
   k_pack_keys<<<grid1(n, 256), 256, 0, st>>>(cl->xyz64, n, res, keys, idx);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
@@ -341,7 +342,7 @@ int launch_map_build(vg_ctx* ctx, const vg_cloud* cl, double res, vg_map* map) {
   cub::DeviceScan::ExclusiveSum(nullptr, t3, counts, offsets, (int)n, st);
   tmp_bytes = t1 > t2 ? t1 : t2;
   tmp_bytes = tmp_bytes > t3 ? tmp_bytes : t3;
-  VG_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  VG_CUDA(temps.alloc((unsigned char**)&tmp, tmp_bytes));
   VG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st));
   VG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st));
   int m = 0;
@@ -359,14 +360,5 @@ int launch_map_build(vg_ctx* ctx, const vg_cloud* cl, double res, vg_map* map) {
                                                 map->means, map->covs, map->counts);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
-  cudaFreeAsync(keys, st);
-  cudaFreeAsync(keys_sorted, st);
-  cudaFreeAsync(ukeys, st);
-  cudaFreeAsync(idx, st);
-  cudaFreeAsync(perm, st);
-  cudaFreeAsync(counts, st);
-  cudaFreeAsync(offsets, st);
-  cudaFreeAsync(num_runs, st);
-  cudaFreeAsync(tmp, st);
   return launch_map_finish(ctx, map);
 }
