@@ -494,11 +494,14 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
 // K4b.  ILP rounds of 32 hits are computed per iteration (ILP = 2 gives each lane two
 // independent fp64 dependency chains); kStages >= 2 * ILP staged rounds keep the gathers of
 // the next kStages - ILP rounds in flight during the math.
-template <int MODE, int kStages, int kMinBlocks, int ILP, int PT = 2, int PLANE = 0>
+// K4b: one warp per item.  kStages staged rounds: the gathers of the next kStages - 1 rounds
+// are in flight while a round computes; hit entries are loaded two rounds ahead of their
+// gather (clamped index, so the loads are unconditional).
+template <int MODE, int kStages, int kMinBlocks, int PT = 2, int PLANE = 0>
 __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
     k_accumulate(const AccDesc* __restrict__ descs, int n_items, const int2* __restrict__ hits,
                  double* __restrict__ partials, int dbg) {
-  static_assert(kStages >= 2 * ILP || (ILP == 1 && kStages >= 2), "stage reuse hazard");
+  static_assert(kStages >= 2, "stage reuse hazard");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -527,59 +530,34 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   MapView mv;
   mv.recs = (const VoxelRec*)__ldg((const unsigned long long*)&dsc->recs);
   const bool f64pts = PT == 2 && cv.xyz64 != nullptr;
+  // profiling knobs (VGICP_K4B_DEBUG): 1 no gathers, 2 no math, 4 no lane-own gathers
+  const bool gather = !(dbg & 1), math = !(dbg & 2), own = !(dbg & 4);
 
   double acc[28];
 #pragma unroll
   for (int k = 0; k < 28; ++k) acc[k] = 0.0;
   const int rounds = (n + 31) / 32;
-  constexpr int kAhead = kStages - ILP;  // rounds in flight beyond the ones being computed
+  constexpr int kAhead = kStages - 1;
   const int klast = n > 0 ? n - 1 : 0;
-  // ILP > 1: every staged round is a full round of valid hits (rounds past the end replay hit
-  // n-1 and are masked by scale = 0), so the branch-free math never reads uninitialised data
   if (n > 0) {
 #pragma unroll
-  for (int r = 0; r < kAhead; ++r) {
-    const int k = r * 32 + lane;
-    issue_round<kStages, PT>(cv, mv, sm, r, hl[min(k, klast)], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - r * 32),
-                lane, !(dbg & 4));
-  }
-  // hit entries are prefetched one iteration ahead of their gather; the loads are
-  // unconditional (index clamped) so their first use is the next iteration's gather
-  // two iterations of lead: the entries of round r + kAhead + ILP are loaded at iteration r - ILP
-  int2 nxt[ILP], nxt2[ILP];
-#pragma unroll
-  for (int u = 0; u < ILP; ++u) {
-    nxt[u] = __ldg(hl + min((kAhead + u) * 32 + lane, klast));
-    nxt2[u] = __ldg(hl + min((kAhead + ILP + u) * 32 + lane, klast));
-  }
-  for (int r = 0; r < rounds; r += ILP) {
-#pragma unroll
-    for (int u = 0; u < ILP; ++u) {
-      const int ri = r + kAhead + u;
-      issue_round<kStages, PT>(cv, mv, sm, ri, nxt[u], (dbg & 1) ? 0 : (ILP > 1 ? 32 : n - ri * 32),
-                               lane, !(dbg & 4));
+    for (int r = 0; r < kAhead; ++r)
+      issue_round<kStages, PT>(cv, mv, sm, r, __ldg(hl + min(r * 32 + lane, klast)),
+                               gather ? n - r * 32 : 0, lane, own);
+    int2 nxt = __ldg(hl + min(kAhead * 32 + lane, klast));
+    int2 nxt2 = __ldg(hl + min((kAhead + 1) * 32 + lane, klast));
+    for (int r = 0; r < rounds; ++r) {
+      const int ri = r + kAhead;
+      issue_round<kStages, PT>(cv, mv, sm, ri, nxt, gather ? n - ri * 32 : 0, lane, own);
+      nxt = nxt2;
+      nxt2 = __ldg(hl + min((ri + 2) * 32 + lane, klast));
+      cp_async_wait<kAhead>();
+      __syncwarp();
+      if (math && r * 32 + lane < n)
+        hit_math<MODE, PT, PLANE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
+      __syncwarp();  // stage r % kStages is refilled by round r + kStages
     }
-#pragma unroll
-    for (int u = 0; u < ILP; ++u) {
-      nxt[u] = nxt2[u];
-      nxt2[u] = __ldg(hl + min((r + 2 * ILP + kAhead + u) * 32 + lane, klast));
-    }
-    cp_async_wait<kAhead>();
-    __syncwarp();
-    if (!(dbg & 2)) {
-      if (ILP == 1) {  // branch over padding lanes
-        if (r * 32 + lane < n)
-          hit_math<MODE, PT, PLANE>(sm.stage[r % kStages], lane, f64pts, R, t, 1.0, acc);
-      } else {  // branch-free so the ILP rounds interleave; padding lanes replay valid data
-#pragma unroll
-        for (int u = 0; u < ILP; ++u)
-          hit_math<MODE, PT, PLANE>(sm.stage[(r + u) % kStages], lane, f64pts, R, t,
-                         (r + u) * 32 + lane < n ? 1.0 : 0.0, acc);
-      }
-    }
-    __syncwarp();  // the stages of rounds r..r+ILP-1 are reused by later rounds
-  }
-  cp_async_wait<0>();
+    cp_async_wait<0>();
   }
 
   if (MODE == 1) {
@@ -653,21 +631,25 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
                             cudaStream_t st) {
   const AccDesc* d = b->descs + off;
   const size_t s2 = sizeof(AccSmem<2>) * kAccWarps, s1 = sizeof(AccSmem<2, 1>) * kAccWarps;
-  if (kmode == 1) {
+  if (kmode == 1) {  // cost only (LM candidate steps, factor_graph.py:591)
     double* p = b->partials + 2 * (size_t)off;
+    if (b->all_f32)
+      return b->all_plane
+                 ? launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1, 1>, s1, d, cnt, b->hits, p, st)
+                 : launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1, 0>, s1, d, cnt, b->hits, p, st);
     return b->all_plane
-               ? launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1, 2, 1>, s2, d, cnt, b->hits, p, st)
-               : launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1>, s2, d, cnt, b->hits, p, st);
+               ? launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 2, 1>, s2, d, cnt, b->hits, p, st)
+               : launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 2, 0>, s2, d, cnt, b->hits, p, st);
   }
   double* p = b->partials + (size_t)off * kPartialStride;
   // PT = 1: every point fp32-exact, one 16 B point unit per lane (more L1 left)
   if (b->all_f32)
     return b->all_plane
-               ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1, 1>, s1, d, cnt, b->hits, p, st)
-               : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1>, s1, d, cnt, b->hits, p, st);
+               ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1>, s1, d, cnt, b->hits, p, st)
+               : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 0>, s1, d, cnt, b->hits, p, st);
   return b->all_plane
-             ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 2, 1>, s2, d, cnt, b->hits, p, st)
-             : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1>, s2, d, cnt, b->hits, p, st);
+             ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 2, 1>, s2, d, cnt, b->hits, p, st)
+             : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 2, 0>, s2, d, cnt, b->hits, p, st);
 }
 
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi) {
