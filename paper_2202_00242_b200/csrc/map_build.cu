@@ -57,8 +57,8 @@ __global__ void k_cloud_pack(const double* __restrict__ xyz, const double* __res
 // degenerate: eps I), so R C R^T = alpha I - kappa (R n)(R n)^T costs 21 fp64 ops per
 // correspondence in K4b instead of 45.  alpha and kappa follow from the trace and the
 // Frobenius norm (alpha is the double eigenvalue), n from the largest column of
-// alpha I - C; a point is accepted when the reconstruction matches C to 1e-12, otherwise the
-// cloud keeps the general form.  Layout: p0 = (n0, n1), p1 = (n2, kappa), p2 = (alpha, 0).
+// alpha I - C; a point is accepted when the reconstruction matches C to 1e-13 of its largest
+// entry (the fit itself is accurate to ~1e-16), otherwise the cloud keeps the general form.  Layout: p0 = (n0, n1), p1 = (n2, kappa), p2 = (alpha, 0).
 __global__ void k_plane_fit(const double* __restrict__ cov, long long n, double2* __restrict__ p0,
                             double2* __restrict__ p1, double2* __restrict__ p2,
                             unsigned* __restrict__ fails) {
@@ -96,7 +96,10 @@ __global__ void k_plane_fit(const double* __restrict__ cov, long long n, double2
         for (int a = 0; a < 3; ++a)
           for (int b = 0; b < 3; ++b)
             r = fmax(r, fabs((a == b ? alpha : 0.0) - kappa * nv[a] * nv[b] - C[3 * a + b]));
-        ok = r <= 1e-12 * fmax(1.0, fabs(alpha));
+        // relative to the matrix scale, so scaled covariances are held to the same accuracy
+        double cmax = 0.0;
+        for (int a = 0; a < 9; ++a) cmax = fmax(cmax, fabs(C[a]));
+        ok = r <= 1e-13 * cmax;
       }
     }
     if (!ok) atomicAdd(fails, 1u);

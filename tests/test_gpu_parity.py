@@ -515,12 +515,14 @@ def test_general_source_covariances_vs_oracle(small_graph):
     rng = np.random.default_rng(12)
     dmaps = {j: _lib.DeviceMap.build(_lib.DeviceCloud(scans[j], covs[j]), 1.0)
              for j in np.unique(sel[:, 1])}
-    for form in ("unit plane", "scaled plane", "general"):
+    for form in ("unit plane", "scaled plane", "small plane", "general"):
         clouds, ccovs = [], []
         for i, _ in sel:
             c = srcs[i][1]
             if form == "scaled plane":  # 2 (I - kappa n n^T): plane form with alpha = 2
                 c = 2.0 * c
+            elif form == "small plane":  # alpha = 1e-3: the fit tolerance is relative
+                c = 1e-3 * c
             elif form == "general":
                 a = rng.normal(scale=0.3, size=(len(c), 3, 3))
                 c = c + np.einsum("nij,nkj->nik", a, a) * 0.1   # SPD, not plane form
