@@ -7,8 +7,8 @@ One step = one linearization of every factor of the graph: compose T_ij from the
 (K-compose), fused transform/lookup/fused-covariance/accumulate (K4), fixed-order finalize
 into the per-factor H_ii/H_ij/H_jj/b_i/b_j/cost records (K5).  Under torchrun the factors are
 LPT-sharded by point count across ranks (strong scaling of the fixed graph); each step
-broadcasts the pose table from the solver rank and gathers the per-factor blocks to it
-over NCCL.
+broadcasts the pose table from the solver rank, and every rank sums its shard into the
+global block-sparse normal equations (K6), which one NCCL reduction puts on the solver rank.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -204,13 +204,22 @@ def run_ours(args):
 
     poses_dev = torch.from_numpy(wl.pose_table).to("cuda")
     out_dev = torch.zeros((F_max, REC), dtype=torch.float64, device="cuda")
-    gather = ([torch.empty_like(out_dev) for _ in range(world)] if (world > 1 and rank == 0)
-              else None)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
 
     from paper_2202_00242_b200 import sharding
+
+    ne_dev = None
+    if world > 1:
+        # the exchange (north_star): every rank sums its shard's blocks into the
+        # global normal-equation layout (K6) and one NCCL reduction puts the per-pose-pair
+        # H/b blocks on the solver rank -- 8.2 MB instead of gathering 36.8 MB of records.
+        # N > 1 does strictly more device work per factor than N = 1 (K6).
+        gp = sharding.global_pairs(wl.pairs[:, 0], wl.pairs[:, 1],
+                                   np.zeros(len(wl.pairs), bool), V)
+        batch.assemble_setup(V, gp)
+        ne_dev = torch.empty(batch.asm_size, dtype=torch.float64, device="cuda")
 
     def step(e=None):
         if world > 1:
@@ -225,9 +234,8 @@ def run_ours(args):
             e[2].record()
         batch.finalize_device(_lib.MODE_LINEARIZE, out_dev.data_ptr())
         if world > 1:
-            sharding.gather_records(out_dev, gather, dst=0)
-            if rank == 0:  # solver rank: records back in global factor order
-                sharding.assemble_records(gather, shards, len(wl.pairs))
+            batch.assemble_records_device(out_dev.data_ptr(), ne_dev.data_ptr())
+            sharding.reduce_normal_equations(ne_dev, 0)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -262,8 +270,8 @@ def run_ours(args):
     # ---- e2e: through the public batch API with host buffers (H2D poses, D2H records) ----
     poses_host = torch.from_numpy(wl.pose_table.copy()).pin_memory()
     out_host = torch.empty((F_max, REC), dtype=torch.float64).pin_memory()
-    out_full_host = (torch.empty((len(wl.pairs), REC), dtype=torch.float64).pin_memory()
-                     if world > 1 and rank == 0 else None)
+    ne_host = (torch.empty(batch.asm_size, dtype=torch.float64).pin_memory()
+               if world > 1 else None)
     e2e_ms = []
     if world == 1:
         out_np = out_host.numpy()
@@ -285,8 +293,7 @@ def run_ours(args):
                 poses_dev.copy_(poses_host, non_blocking=True)
             step()
             if rank == 0:
-                full = sharding.assemble_records(gather, shards, len(wl.pairs))
-                out_full_host[: full.shape[0]].copy_(full, non_blocking=False)
+                ne_host.copy_(ne_dev, non_blocking=False)
             torch.cuda.synchronize()
             dt = torch.tensor([(time.perf_counter() - a) * 1e3], dtype=torch.float64,
                               device="cuda")
@@ -294,44 +301,12 @@ def run_ours(args):
             if k >= 2:
                 e2e_ms.append(float(dt.item()))
         h2d = poses_host.numel() * 8
-        d2h = len(wl.pairs) * REC * 8
+        d2h = batch.asm_size * 8
     e2e_value = total_points / (statistics.median(e2e_ms) / 1e3)
 
     # ---- e2e of the normal equations: the same linearization, summed into
     # the block-sparse H/g on the device, only the system crosses PCIe ----
     ne_line = None
-    if world > 1:
-        # every rank assembles its shard in the global pair layout; one NCCL sum-reduction
-        # puts the per-pose-pair H/b blocks on the solver rank, which copies them to the host
-        gp = sharding.global_pairs(wl.pairs[:, 0], wl.pairs[:, 1], np.zeros(len(wl.pairs), bool),
-                                   V)
-        batch.assemble_setup(V, gp)
-        ne_dev = torch.empty(batch.asm_size, dtype=torch.float64, device="cuda")
-        ne_host = torch.empty(batch.asm_size, dtype=torch.float64).pin_memory()
-        ne_ms = []
-        for k in range(args.e2e_steps + 2):
-            torch.cuda.synchronize()
-            dist.barrier()
-            a = time.perf_counter()
-            if rank == 0:
-                poses_dev.copy_(poses_host, non_blocking=True)
-            sharding.broadcast_poses(poses_dev, 0)
-            batch.assemble_poses_device(poses_dev.data_ptr(), V, ne_dev.data_ptr())
-            sharding.reduce_normal_equations(ne_dev, 0)
-            if rank == 0:
-                ne_host.copy_(ne_dev, non_blocking=False)
-            torch.cuda.synchronize()
-            dt = torch.tensor([(time.perf_counter() - a) * 1e3], dtype=torch.float64,
-                              device="cuda")
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-            if k >= 2:
-                ne_ms.append(float(dt.item()))
-        ne_line = {"value": total_points / (statistics.median(ne_ms) / 1e3), "unit": UNIT,
-                   "h2d_bytes_per_step": int(poses_host.numel() * 8),
-                   "d2h_bytes_per_step": int(batch.asm_size * 8),
-                   "ms_per_step": statistics.median(ne_ms), "variables": int(V),
-                   "pairs": int(len(gp)),
-                   "api": "DeviceBatch.assemble_poses_device + NCCL reduce (sharding)"}
     if world == 1:
         pairs = batch.assemble_setup(V)
         ne_out = torch.empty(batch.asm_size, dtype=torch.float64).pin_memory().numpy()

@@ -177,6 +177,10 @@ int vg_batch_assemble_poses(vg_batch* batch, const double* poses_host, int64_t n
                             double* out_host);
 int vg_batch_assemble_poses_device(vg_batch* batch, const double* poses_dev,
                                    int64_t num_poses, double* out_dev);
+/* K6 alone, over records the last vg_batch_finalize_device (VG_MODE_LINEARIZE) wrote:
+ * lets a caller time K-compose / K4 / K5 separately and still assemble (bench.py, N > 1) */
+int vg_batch_assemble_records_device(vg_batch* batch, const double* records_dev,
+                                     double* out_dev);
 
 /* ---- preprocessing (preprocess.py:122-164) --------------------------------------------- */
 /* replaces knn_search (preprocess.py:122-139): exact k nearest (self included), ordered by

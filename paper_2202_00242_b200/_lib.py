@@ -87,6 +87,7 @@ _SIGNATURES = {
     "vg_batch_assemble_pairs": ([c_void_p, POINTER(c_int32)], c_int),
     "vg_batch_assemble_poses": ([c_void_p, _P_D, c_int64, _P_D], c_int),
     "vg_batch_assemble_poses_device": ([c_void_p, c_void_p, c_int64, c_void_p], c_int),
+    "vg_batch_assemble_records_device": ([c_void_p, c_void_p, c_void_p], c_int),
     "vg_knn": ([c_void_p, c_void_p, c_int32, _P_I64], c_int),
     "vg_covariances": ([c_void_p, c_void_p, _P_I64, c_int32, c_double, _P_D, _P_U8], c_int),
     "vg_cloud_estimate_covariances": ([c_void_p, c_void_p, c_int32, c_double, _P_I64, _P_D,
@@ -380,6 +381,12 @@ class DeviceBatch:
         check(self.ctx.lib.vg_batch_assemble_poses(self.handle, dptr(poses), poses.shape[0],
                                                    dptr(out)), "vg_batch_assemble_poses")
         return NormalEquations.from_flat(out, self.asm_vars, self.asm_pairs) if unpack else out
+
+    def assemble_records_device(self, records_dev_ptr: int, out_dev_ptr: int) -> None:
+        """K6 over records written by finalize_device(MODE_LINEARIZE) on this batch."""
+        check(self.ctx.lib.vg_batch_assemble_records_device(
+            self.handle, c_void_p(records_dev_ptr), c_void_p(out_dev_ptr)),
+            "vg_batch_assemble_records_device")
 
     def assemble_poses_device(self, poses_dev_ptr: int, num_poses: int, out_dev_ptr: int) -> None:
         check(self.ctx.lib.vg_batch_assemble_poses_device(

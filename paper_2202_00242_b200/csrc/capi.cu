@@ -906,6 +906,12 @@ int vg_batch_assemble_poses_device(vg_batch* b, const double* poses_dev, int64_t
   return run_assemble(b, poses_dev, V, out_dev);
 }
 
+int vg_batch_assemble_records_device(vg_batch* b, const double* records_dev, double* out_dev) {
+  if (!b || !records_dev || !out_dev) return fail(VG_ERR_INVALID, "null argument");
+  if (b->asm_vars < 0) return fail(VG_ERR_INVALID, "assembly not set up (vg_batch_assemble_setup)");
+  return launch_assemble(b->ctx, b, records_dev, out_dev);
+}
+
 int vg_batch_assemble_poses(vg_batch* b, const double* poses_host, int64_t V, double* out_host) {
   if (!b || !poses_host || !out_host) return fail(VG_ERR_INVALID, "null argument");
   if (b->asm_vars < 0) return fail(VG_ERR_INVALID, "assembly not set up (vg_batch_assemble_setup)");

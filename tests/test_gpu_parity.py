@@ -589,3 +589,29 @@ def test_config5_full_size_sample_vs_oracle_and_invariants(config5):
         assert_lin(RG.unpack_record(host[f], False), ref, False)
         checked += 1
     assert checked >= 12
+
+
+def test_assemble_records_device_equals_assemble_poses(small_graph):
+    """K6 alone over finalize_device's records (what each rank runs in the sharded step) gives
+    the same system as the one-call assemble_poses."""
+    import torch
+
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
+    F, V = len(pairs), len(est)
+    table = np.array([G.pose_row(p) for p in est])
+    b = _lib.DeviceBatch([clouds[i] for i, _ in pairs], [dmaps[j] for _, j in pairs],
+                         [False] * F, [10] * F, pairs[:, 0], pairs[:, 1])
+    b.assemble_setup(V)
+    ref = b.assemble_poses(table, unpack=False)
+    tp = torch.from_numpy(table).cuda()
+    rec = torch.zeros((F, 92), dtype=torch.float64, device="cuda")
+    ne = torch.zeros(b.asm_size, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    b.compose_device(tp.data_ptr(), V)
+    b.accumulate_device(_lib.MODE_LINEARIZE)
+    b.finalize_device(_lib.MODE_LINEARIZE, rec.data_ptr())
+    b.assemble_records_device(rec.data_ptr(), ne.data_ptr())
+    b.ctx.synchronize()
+    assert np.array_equal(ne.cpu().numpy(), ref)
