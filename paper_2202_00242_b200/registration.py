@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _lib
 from .errors import DegenerateConstraint
-from .geometry import Gaussian3, Se3Pose, pose_compose, pose_inverse, transform12
+from .geometry import Gaussian3, Se3Pose, pose_compose, pose_inverse, pose_row, transform12
 from .preprocess import Frame, device_cloud
 
 MIN_INLIERS_DEFAULT = 10  # registration.py:26
@@ -246,6 +246,25 @@ def _overlap_cloud(frame):
     return device_cloud(frame, with_covs=getattr(frame, "covs", None) is not None)
 
 
+def _overlap_batch(frames, vmaps, idx, var_source=None, var_target=None):
+    clouds = [_overlap_cloud(frames[k]) for k in idx]
+    maps = [_as_device_map(vmaps[k]) for k in idx]
+    vs = None if var_source is None else [int(var_source[k]) for k in idx]
+    vt = None if var_target is None else [int(var_target[k]) for k in idx]
+    key = (tuple((id(c), id(m)) for c, m in zip(clouds, maps)),
+           None if vs is None else (tuple(vs), tuple(vt)))
+    b = _overlap_cache.get(key)
+    if b is None or any(x is not c for x, c in zip(b._keep[0], clouds)) \
+            or any(x is not m for x, m in zip(b._keep[1], maps)):
+        b = _lib.DeviceBatch(clouds, maps, [False] * len(idx), [0] * len(idx), vs, vt)
+        _overlap_cache[key] = b
+        while len(_overlap_cache) > 16:
+            _overlap_cache.popitem(last=False)
+    else:
+        _overlap_cache.move_to_end(key)
+    return b
+
+
 def overlap_rates(frames, vmaps, t_ijs) -> np.ndarray:
     """overlap_rate (registration.py:168-173) for many (frame, map, T_ij) triples in one
     launch (VG_MODE_INLIERS: K4a lookups + hit counts only).  Empty inputs give 0.0."""
@@ -254,18 +273,7 @@ def overlap_rates(frames, vmaps, t_ijs) -> np.ndarray:
     idx = [k for k in range(n) if len(frames[k]) and len(vmaps[k])]
     if not idx:
         return out
-    clouds = [_overlap_cloud(frames[k]) for k in idx]
-    maps = [_as_device_map(vmaps[k]) for k in idx]
-    key = tuple((id(c), id(m)) for c, m in zip(clouds, maps))
-    b = _overlap_cache.get(key)
-    if b is None or any(x is not c for x, c in zip(b._keep[0], clouds)) \
-            or any(x is not m for x, m in zip(b._keep[1], maps)):
-        b = _lib.DeviceBatch(clouds, maps, [False] * len(idx), [0] * len(idx))
-        _overlap_cache[key] = b
-        while len(_overlap_cache) > 16:
-            _overlap_cache.popitem(last=False)
-    else:
-        _overlap_cache.move_to_end(key)
+    b = _overlap_batch(frames, vmaps, idx)
     T = np.stack([transform12(t_ijs[k]) for k in idx])
     rec = b.linearize(T, _lib.MODE_INLIERS)
     out[idx] = rec[:, 1] / np.array([len(frames[k]) for k in idx], dtype=float)
@@ -274,16 +282,23 @@ def overlap_rates(frames, vmaps, t_ijs) -> np.ndarray:
 
 def overlap_matrix(frames, vmaps, poses) -> np.ndarray:
     """out[i, j] = overlap_rate(frames[i], vmaps[j], T_j^-1 T_i) for i != j, 0 on the
-    diagonal: the keyframe overlap matrix of odometry.py:396-403 in one launch."""
+    diagonal: the keyframe overlap matrix of odometry.py:396-403 in one launch (the relative
+    poses are composed on the device from the pose table, K-compose)."""
     m = len(frames)
     out = np.zeros((m, m))
-    pairs = [(i, j) for i in range(m) for j in range(m) if i != j]
+    pairs = [(i, j) for i in range(m) for j in range(m)
+             if i != j and len(frames[i]) and len(vmaps[j])]
     if not pairs:
         return out
-    rates = overlap_rates([frames[i] for i, _ in pairs], [vmaps[j] for _, j in pairs],
-                          [pose_compose(pose_inverse(poses[j]), poses[i]) for i, j in pairs])
-    for (i, j), r in zip(pairs, rates):
-        out[i, j] = r
+    fs = [frames[i] for i, _ in pairs]
+    ms_ = [vmaps[j] for _, j in pairs]
+    vs = [i for i, _ in pairs]
+    vt = [j for _, j in pairs]
+    b = _overlap_batch(fs, ms_, list(range(len(pairs))), vs, vt)
+    table = np.array([pose_row(p) for p in poses])
+    rec = b.linearize_poses(table, _lib.MODE_INLIERS)
+    for (i, j), r in zip(pairs, rec[:, 1]):
+        out[i, j] = r / len(frames[i])
     return out
 
 

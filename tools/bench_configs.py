@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Single-GPU BASELINE configs other than the headline one: 1 (single binary factor),
 2 (preprocessing: kNN covariances + 3 voxel maps of a 131k-point scan), 3 (odometry window,
-unary + 3 resolutions) and 4 (local mapping, 4,950 factors).
+unary + 3 resolutions), 4 (local mapping, 4,950 factors), and "6": the keyframe overlap
+matrix of the config-3 window (overlap gating).
 
 One JSON line per config, with the fields of bench.py's line: device-resident linearization
 step (compose + K4a + K4b + K5 replayed as one CUDA graph; CUDA events on the launching
@@ -202,9 +203,60 @@ def run_preprocess(args):
             "cpu_baseline": cpu}
 
 
+def run_overlap(args):
+    """The keyframe overlap matrix of config 3's window (odometry.py:396-403): every ordered
+    pair of the 23 frames (506 overlap_rate calls of 16,384 points each) in one
+    VG_MODE_INLIERS launch, vs the oracle's per-pair loop."""
+    from paper_2202_00242_b200 import registration as RG
+    from paper_2202_00242_b200 import synthetic
+    from paper_2202_00242_b200.preprocess import make_frame
+
+    dirs = synthetic.ray_table(256, 64)
+    traj = synthetic.circle_trajectory(23, step=0.4)
+    scans = [synthetic.scan(p, dirs, np.random.default_rng(900 + k)) for k, p in enumerate(traj)]
+    frames, vmaps = [], []
+    for sc in scans:
+        c = _lib.DeviceCloud(sc, None)
+        _, covs, _ = c.estimate_covariances(10, 1e-3, want_neighbors=False)
+        f = make_frame(sc, covs)
+        frames.append(f)
+        vmaps.append(RG.build_voxelmap(f, 1.0))
+    RG.overlap_matrix(frames, vmaps, traj)  # warm: uploads + batch
+    ms = []
+    for _ in range(max(5, args.steps // 5)):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        m = RG.overlap_matrix(frames, vmaps, traj)
+        ms.append((time.perf_counter() - a) * 1e3)
+    n = sum(len(scans[i]) for i in range(23) for j in range(23) if i != j)
+    cpu = None
+    if not args.no_cpu:
+        from oracle import vgicp_oracle as O
+        from paper_2202_00242_b200.geometry import pose_compose, pose_inverse
+
+        omaps = [(1.0, v.keys, v.means, v.covs, v.counts) for v in vmaps]
+        a = time.perf_counter()
+        for i in range(23):
+            for j in range(23):
+                if i != j:
+                    tij = pose_compose(pose_inverse(traj[j]), traj[i])
+                    O.overlap_rate(scans[i], omaps[j], tij.rotation.matrix(), tij.translation)
+        sec = time.perf_counter() - a
+        cpu = {"value": n / sec, "unit": "lookups/s", "cores": 1, "kind": "port",
+               "sample": f"the same 506 pairs once: {1e3 * sec:.0f} ms (single-threaded NumPy)"}
+    k = statistics.median(ms)
+    return {"metric": "voxel lookups/sec (keyframe overlap matrix)", "value": n / (k / 1e3),
+            "unit": "lookups/s", "n_gpus": 1, "ms_per_step": k, "higher_is_better": True,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "keyframe overlap matrix (config 3 window, odometry.py:396-403)",
+                       "frames": 23, "pairs": 506, "scan_points": 16384,
+                       "timing": "wall clock around registration.overlap_matrix (host API)"},
+            "cpu_baseline": cpu}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default="1,2,3,4")
+    ap.add_argument("--configs", default="1,2,3,4,6")  # 6: overlap matrix
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
@@ -214,7 +266,8 @@ def main():
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     for c in (int(x) for x in args.configs.split(",")):
-        line = run_preprocess(args) if c == 2 else run(c, args, ctx, stream)
+        line = (run_preprocess(args) if c == 2 else run_overlap(args) if c == 6
+                else run(c, args, ctx, stream))
         print(json.dumps(line), flush=True)
 
 
