@@ -27,7 +27,8 @@ class GaussianVoxelMap:
     """Per-voxel aggregate Gaussians (registration.py:29-71).
 
     Host arrays ``keys``/``means``/``covs``/``counts`` are the reference's sorted parallel
-    arrays; the device copy is a 64 B-slot open-addressing hash table whose value is the
+    arrays; the device copy is a bucketized open-addressing hash table (32-bit cell-local keys
+    in 16 B buckets, or int64 keys for maps beyond the local frame) whose records carry the
     reference row.  Maps built on the GPU export their host arrays lazily.
     """
 

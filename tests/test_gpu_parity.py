@@ -615,3 +615,23 @@ def test_assemble_records_device_equals_assemble_poses(small_graph):
     b.assemble_records_device(rec.data_ptr(), ne.data_ptr())
     b.ctx.synchronize()
     assert np.array_equal(ne.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_hash_stress_every_cell_and_misses(wide):
+    """A 150k-cell map (many overflowing 16 B buckets, and an int64-key map when `wide`):
+    every occupied cell's centre finds its reference row, and random points match the
+    oracle's binary search, including misses."""
+    rng = np.random.default_rng(77)
+    cells = np.unique(rng.integers(0, 200, (160000, 3)) * [1, 1, 1], axis=0)
+    if wide:
+        cells = np.vstack([cells, [[5000, 3, 3]]])
+    pts = (cells + 0.5) * 0.25
+    covs = np.broadcast_to(np.eye(3) * 0.01, (len(pts), 3, 3)).copy()
+    ref = O.build_voxelmap(pts, covs, 0.25)
+    vm = RG.build_voxelmap(make_frame(pts, covs), 0.25)
+    assert np.array_equal(vm.keys, ref[1])
+    rows = vm.lookup(pts)
+    assert np.array_equal(rows, O.lookup(ref, pts)) and np.all(rows >= 0)
+    q = rng.uniform(-1, 52, (200000, 3))
+    assert np.array_equal(vm.lookup(q), O.lookup(ref, q))
