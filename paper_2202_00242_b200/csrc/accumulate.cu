@@ -162,6 +162,8 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
                   AccDesc* __restrict__ descs) {
   const int lane = threadIdx.x & 31;
   const int w = blockIdx.x * kLookupWarps + (threadIdx.x >> 5);
+  pdl_release();
+  pdl_wait();  // item headers carry T_ij written by K-compose
   if (w >= n_items) return;
   const ItemHdr* h = hdrs + w;
   double R[9], t[3];
@@ -506,6 +508,8 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int w = blockIdx.x * kAccWarps + wib;
+  pdl_release();
+  pdl_wait();  // descriptors and hit lists written by K4a
   if (w >= n_items) return;
   AccSmem<kStages, PT>& sm = reinterpret_cast<AccSmem<kStages, PT>*>(smem_raw)[wib];
   const AccDesc* dsc = descs + w;
@@ -593,7 +597,8 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
   int* hc = b->hit_counts + off;
   AccDesc* dd = b->descs + off;
   if (b->key_mode == 1 && b->all_pow2 && b->all_f32)  // fast path
-    k_lookup_fast<32><<<lb, kLookupWarps * 32, 0, st>>>(b->hdrs + off, cnt, b->hits, hc, p2, dd);
+    VG_CUDA(launch_pdl(k_lookup_fast<32>, dim3(lb), dim3(kLookupWarps * 32), 0, st,
+                       (const ItemHdr*)(b->hdrs + off), cnt, b->hits, hc, p2, dd));
   else if (b->key_mode == 1 && b->all_pow2)
     k_lookup_items<1, 24, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
                                                               b->maps, b->hits, hc, p2, dd);
@@ -620,8 +625,8 @@ static int launch_acc_kernel(vg_ctx* ctx, K kern, size_t smem, const AccDesc* d,
     return e ? atoi(e) : 0;
   }();
   VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(cnt + kAccWarps - 1) / kAccWarps, kAccWarps * 32, smem, st>>>(d, cnt, hits, partials,
-                                                                        dbg);
+  VG_CUDA(launch_pdl(kern, dim3((cnt + kAccWarps - 1) / kAccWarps), dim3(kAccWarps * 32), smem,
+                     st, d, cnt, hits, partials, dbg));
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;

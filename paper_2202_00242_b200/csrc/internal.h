@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -146,6 +147,29 @@ struct vg_batch {
   unsigned* asm_done = nullptr;       // its arrival counter (reset by the last CTA)
   double2* asm_gcost = nullptr;       // per-factor (gated cost, 1 if gated in), written by K5
 };
+
+// Programmatic dependent launch: the kernel may be scheduled while its stream predecessor
+// drains (it waits in griddepcontrol.wait before touching the predecessor's results), hiding
+// the launch gap between the kernels of a step.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // Stream-ordered device temporaries of one call, released on every exit path.
 struct DeviceTemps {

@@ -279,6 +279,8 @@ __global__ void __launch_bounds__(kFinBlock)
   __shared__ double sh[kFinBlock * kFinStride];
   const int f0 = fbase + blockIdx.x * kFinBlock;
   const int fi = f0 + threadIdx.x;
+  pdl_release();
+  pdl_wait();  // item partials written by K4b
   if (mode != 0) {
     if (fi < F) finalize_one(factors[fi], fi, partials, mode, out, nullptr);
     return;
@@ -651,8 +653,9 @@ int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, i
     VG_CUDA(cudaGetLastError());
     return 0;
   }
-  k_finalize<<<(f1 - f0 + kFinBlock - 1) / kFinBlock, kFinBlock, 0, ctx->stream>>>(
-      b->factors, f0, f1, b->partials, mode, out_dev, mode == 0 ? b->asm_gcost : nullptr);
+  VG_CUDA(launch_pdl(k_finalize, dim3((f1 - f0 + kFinBlock - 1) / kFinBlock), dim3(kFinBlock), 0,
+                     ctx->stream, (const FactorDev*)b->factors, f0, f1, (const double*)b->partials,
+                     mode, out_dev, mode == 0 ? b->asm_gcost : (double2*)nullptr));
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
