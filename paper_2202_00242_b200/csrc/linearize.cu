@@ -477,6 +477,8 @@ __device__ __forceinline__ void q_matrix(Quat q, double* R) {
 __global__ void k_compose(FactorDev* __restrict__ factors, int F, const double* __restrict__ poses,
                           ItemHdr* __restrict__ hdrs) {
   const int fi = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_release();
+  pdl_wait();  // the previous step's K5 still reads T_ij
   if (fi >= F) return;
   FactorDev& f = factors[fi];
   const double* pi = poses + 8 * (size_t)f.var_source;
@@ -627,8 +629,8 @@ int launch_terms(vg_ctx* ctx, const CloudView& cv, const MapView& mv, const doub
 
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev) {
   if (b->F == 0) return 0;
-  k_compose<<<grid_for(b->F, 128, 1 << 30), 128, 0, ctx->stream>>>(b->factors, (int)b->F,
-                                                                   poses_dev, b->hdrs);
+  VG_CUDA(launch_pdl(k_compose, dim3(grid_for(b->F, 128, 1 << 30)), dim3(128), 0, ctx->stream,
+                     b->factors, (int)b->F, poses_dev, b->hdrs));
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
