@@ -55,3 +55,23 @@ def test_sm100a_cubin_present():
     out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_null_handles_return_status_codes():
+    """The C-ABI validates its arguments before touching a device: null handles and bad
+    modes come back as VG_ERR_INVALID with a message, never as a crash (no GPU needed)."""
+    import ctypes
+
+    lib = _lib.load_library()
+    VG_ERR_INVALID = 1
+    null = ctypes.c_void_p(0)
+    dptr = ctypes.POINTER(ctypes.c_double)()
+    assert lib.vg_batch_linearize(null, dptr, 0, dptr) == VG_ERR_INVALID
+    assert b"null" in lib.vg_last_error().lower() or lib.vg_last_error()
+    assert lib.vg_batch_linearize_poses(null, dptr, 1, 0, dptr) == VG_ERR_INVALID
+    assert lib.vg_batch_assemble_setup(null, 4, None, None) == VG_ERR_INVALID
+    assert lib.vg_batch_info(null, None, None, None) == VG_ERR_INVALID
+    assert lib.vg_map_info(null, None, None, None) == VG_ERR_INVALID
+    out = ctypes.c_void_p()
+    assert lib.vg_cloud_create(null, dptr, dptr, 3, ctypes.byref(out)) == VG_ERR_INVALID
+    assert lib.vg_batch_destroy(null) == 0 and lib.vg_map_destroy(null) == 0
