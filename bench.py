@@ -61,6 +61,16 @@ def traffic_record():
         return None
 
 
+def ncu_metrics():
+    """Per-kernel ncu digest of K4a/K4b from the committed capture (profiles/r01c_ncu_metrics.json,
+    tools/ncu_summary.py): L2/L1 hit rates and pipe use beside the roofline."""
+    p = ROOT / "profiles" / "r01c_ncu_metrics.json"
+    try:
+        return json.loads(p.read_text())
+    except Exception:
+        return None
+
+
 def hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -377,7 +387,8 @@ def run_ours(args):
                          "frac": achieved / peak, "traffic": traffic_record(),
                          "kernel": "K4 = k_lookup_fast (K4a) + k_accumulate<0> (K4b)",
                          "kernel_ms": statistics.mean(k4_ms),
-                         "bytes_per_corr": BYTES_PER_CORR, "peak_kind": peak_kind},
+                         "bytes_per_corr": BYTES_PER_CORR, "peak_kind": peak_kind,
+                         "ncu": ncu_metrics()},
             "clocks": clocks,
             "cpu_baseline": cpu,
         }

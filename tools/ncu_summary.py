@@ -20,12 +20,25 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
 STALLS = "smsp__pcsamp_warps_issue_stalled_"
 
 
-def main(path):
+def main(path, json_out=None):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr = rows[0]
+    summary = {}
     for r in rows[2:]:
+        d0 = dict(zip(hdr, r))
+        name = d0.get("Kernel Name", "").split("(")[0].replace("void ", "").strip()
+        summary.setdefault(name, {
+            "time_us": d0.get("gpu__time_duration.sum"),
+            "l2_hit_rate_pct": d0.get("lts__t_sector_hit_rate.pct"),
+            "l1_hit_rate_pct": d0.get("l1tex__t_sector_hit_rate.pct"),
+            "l1_throughput_pct": d0.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+            "fp64_pipe_pct": d0.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": d0.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "dram_read_mb": d0.get("dram__bytes_read.sum"),
+            "dram_write_mb": d0.get("dram__bytes_write.sum"),
+            "registers": d0.get("launch__registers_per_thread")})
         d = dict(zip(hdr, r))
         print("==", d.get("Kernel Name", "")[:90])
         for k in KEYS:
@@ -36,7 +49,13 @@ def main(path):
         tot = sum(st.values()) or 1.0
         top = sorted(st.items(), key=lambda kv: -kv[1])[:7]
         print("   stalls:", ", ".join(f"{k} {100 * v / tot:.0f}%" for k, v in top))
+    if json_out:
+        import json
+
+        with open(json_out, "w") as f:
+            json.dump({k: {m: float(v) if v not in (None, "") else None for m, v in d.items()}
+                       for k, d in summary.items()}, f, indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else None)
