@@ -7,11 +7,12 @@
 // K4a — one warp per (factor, <=512-point chunk) item, light on registers so many warps hide
 //   the two dependent memory latencies of a lookup (source point, then the probed key
 //   bucket).  x = R p + t (fp64) -> key (bit-exact floor) -> one 16 B bucket of 4 local keys.
-//   Hits are written as (point, row) pairs into the item's region of a batch-wide hit list
-//   with a warp ballot, preserving point order.  Misses contribute nothing (:150-156).
+//   Hits are written as (point, record) pairs into the item's region of a batch-wide hit
+//   list with a warp ballot, preserving point order.  Misses contribute nothing (:150-156).
 // K4b — one warp per item over its compacted hits, so every lane of the expensive fp64 path
 //   does useful work.  Each round of 32 hits gathers the source point (16 B), source
-//   covariance (48 B) and voxel record (80 B) with cp.async into a 2-stage shared-memory
+//   covariance or its plane form (48 B) and voxel record (80 B) with cp.async into a 2-stage
+//   shared-memory
 //   pipeline, so the gathers of round r+1 are in flight while round r computes (hit entries
 //   are loaded two rounds ahead).
 //   The per-item 29-value partial (target-frame 6x6 about the source origin)
@@ -305,7 +306,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// per-warp stage: own point (2 x 16 B, fp32 or fp64 xyz), own source covariance (3 x 16 B),
+// per-warp stage: own point (1-2 x 16 B, fp32 or fp64 xyz), own source covariance (3 x 16 B),
 // and 32 voxel records gathered cooperatively (5 x 16 B each; the 80 B lane stride is 20
 // banks, so 8 lanes of a 16 B shared-memory read hit 8 distinct 4-bank groups: conflict free)
 constexpr int kRecUnits = 5;
@@ -493,9 +494,6 @@ __device__ __forceinline__ void hit_core(double px, double py, double pz, double
   }
 }
 
-// K4b.  ILP rounds of 32 hits are computed per iteration (ILP = 2 gives each lane two
-// independent fp64 dependency chains); kStages >= 2 * ILP staged rounds keep the gathers of
-// the next kStages - ILP rounds in flight during the math.
 // K4b: one warp per item.  kStages staged rounds: the gathers of the next kStages - 1 rounds
 // are in flight while a round computes; hit entries are loaded two rounds ahead of their
 // gather (clamped index, so the loads are unconditional).
