@@ -12,9 +12,8 @@
 // K4b — one warp per item over its compacted hits, so every lane of the expensive fp64 path
 //   does useful work.  Each round of 32 hits gathers the source point (16 B), source
 //   covariance or its plane form (48 B) and voxel record (80 B) with cp.async into a 2-stage
-//   shared-memory
-//   pipeline, so the gathers of round r+1 are in flight while round r computes (hit entries
-//   are loaded two rounds ahead).
+//   shared-memory pipeline, so the gathers of round r+1 are in flight while round r computes
+//   (hit entries are loaded two rounds ahead).
 //   The per-item 29-value partial (target-frame 6x6 about the source origin)
 //   is reduced across the warp in a fixed order.
 #include <cuda_runtime.h>
