@@ -222,7 +222,7 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                  double* wd, double* partial_cost, long long* partial_inl, int nblocks);
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
 int launch_spread_T(vg_ctx* ctx, vg_batch* b);  // FactorDev.T -> ItemHdr.T (explicit-T mode)
-int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b (or K4s)
+int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b
 int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1);
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev);  // K6

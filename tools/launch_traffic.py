@@ -11,8 +11,8 @@ import json
 import sys
 from collections import defaultdict
 
-K4A = ("k_lookup_fast", "k_lookup_items", "k_lookup_batch")
-K4B = ("k_accumulate", "k_acc_persist")
+K4A = ("k_lookup_fast", "k_lookup_items")
+K4B = ("k_accumulate",)
 
 
 def short(name):
