@@ -512,9 +512,9 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   const AccDesc* dsc = descs + w;
   const int n = __ldg(&dsc->n);
   const int2* hl = hits + __ldg(&dsc->hoff);
-  // the item's hit list (<= 512 entries, contiguous) was written by K4a and may have left
-  // L2: one prefetch per 128 B line, all issued up front, instead of a DRAM round trip every
-  // few rounds
+  // the item's hit list (contiguous) was written by K4a and may have left L2: one prefetch
+  // per 128 B line for its first 512 entries, all issued up front, instead of a DRAM round
+  // trip every few rounds (covering longer lists too measured slower)
   if (16 * lane < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(hl + 16 * lane));
   double R[9], t[3];
 #pragma unroll

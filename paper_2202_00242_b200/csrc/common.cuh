@@ -18,7 +18,8 @@ namespace vg {
 constexpr int kKeyOffset = 1 << 20;   // preprocess.py:21-22
 constexpr int kWarpsPerBlock = 4;
 constexpr int kPartialStride = 32;    // doubles per work-item partial (29 used)
-constexpr int kMaxChunk = 512;        // points per work item => <= 16 points per lane
+constexpr int kMaxChunk = 1024;       // points per work item (whole factors at config 5:
+                                      // 512 measured 2.7% slower per step, 256 11%)
 
 // Voxel map on the device = open-addressing hash table (key -> reference row) + dense,
 // row-indexed, line-aligned voxel records.  Each record is one 128 B cache line, so a
