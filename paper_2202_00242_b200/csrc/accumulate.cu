@@ -238,27 +238,19 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     g[2] = v.z;
     g[3] = v.w;
   };
-  float4 a0 = __ldg(pa + min(begin + lane, last));
-  float4 a1 = __ldg(pa + min(begin + 32 + lane, last));
-  Q q0 = make_q(a0, begin + lane);
-  unsigned g0[4] = {0, 0, 0, 0};
-  if (q0.live) load_bucket(q0.bucket, g0);
-  for (int base = begin; base < end; base += 32) {
-    const int i = base + lane;
-    const Q q1 = make_q(a1, i + 32);
-    unsigned g1[4] = {0, 0, 0, 0};
-    if (q1.live) load_bucket(q1.bucket, g1);
-    a1 = __ldg(pa + min(i + 64, last));
+  // resolve the probe of one round (overflowing buckets continue into the next) and append
+  // its hits in point order
+  auto resolve = [&](const Q& q, unsigned (&g)[4], int i) {
     int slot = -1;
-    if (q0.live) {
-      unsigned bk = q0.bucket;
+    if (q.live) {
+      unsigned bk = q.bucket;
       for (;;) {
         int found = -1;
         bool empty = false;
 #pragma unroll
         for (int j = kBucket32 - 1; j >= 0; --j) {
-          if (g0[j] == q0.k32) found = j;
-          empty |= (g0[j] == kEmpty32);
+          if (g[j] == q.k32) found = j;
+          empty |= (g[j] == kEmpty32);
         }
         if (found >= 0) {
           slot = (int)(bk * kBucket32 + found);
@@ -266,16 +258,34 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
         }
         if (empty) break;
         bk = (bk + 1) & mask;
-        load_bucket(bk, g0);
+        load_bucket(bk, g);
       }
     }
     // misses contribute nothing (registration.py:150-156)
     const unsigned mb = __ballot_sync(0xffffffffu, slot >= 0);
     if (slot >= 0) out[cnt + __popc(mb & lt_mask)] = make_int2(i, slot);
     cnt += __popc(mb);
-    q0 = q1;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) g0[k] = g1[k];
+  };
+  // Two-deep pipeline, unrolled by two with ping-pong registers (A: even rounds, B: odd):
+  // the probe of the next round and the point of the round after are in flight while a
+  // round resolves, and no in-flight load result is ever copied (a copy would wait for it).
+  float4 pA = __ldg(pa + min(begin + lane, last));
+  float4 pB = __ldg(pa + min(begin + 32 + lane, last));
+  Q qA = make_q(pA, begin + lane);
+  unsigned gA[4] = {0, 0, 0, 0}, gB[4] = {0, 0, 0, 0};
+  if (qA.live) load_bucket(qA.bucket, gA);
+  pA = __ldg(pa + min(begin + 64 + lane, last));
+  for (int base = begin; base < end; base += 64) {
+    const int i = base + lane;
+    const Q qB = make_q(pB, i + 32);
+    if (qB.live) load_bucket(qB.bucket, gB);
+    pB = __ldg(pa + min(i + 96, last));
+    resolve(qA, gA, i);
+    if (base + 32 >= end) break;
+    qA = make_q(pA, i + 64);
+    if (qA.live) load_bucket(qA.bucket, gA);
+    pA = __ldg(pa + min(i + 128, last));
+    resolve(qB, gB, i + 32);
   }
   if (lane == 0) {
     counts[w] = cnt;
