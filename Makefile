@@ -3,7 +3,8 @@
 NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2202_00242_b200/csrc
-SRCS := $(CSRC)/capi.cu $(CSRC)/linearize.cu $(CSRC)/accumulate.cu $(CSRC)/map_build.cu $(CSRC)/knn_cov.cu
+SRCS := $(CSRC)/capi.cu $(CSRC)/linearize.cu $(CSRC)/accumulate.cu $(CSRC)/map_build.cu $(CSRC)/knn_cov.cu \
+        $(CSRC)/deskew.cu
 HDRS := $(CSRC)/common.cuh $(CSRC)/internal.h include/vgicp.h
 LIB := paper_2202_00242_b200/lib/libvgicp.so
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -I$(CSRC) \

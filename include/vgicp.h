@@ -79,6 +79,24 @@ int vg_ctx_launch_count(const vg_ctx* ctx, int64_t* count);
 /* replaces pack_voxel_keys (preprocess.py:21-22,68-70): floor(p/res)+2^20 packed 21 bits/axis */
 int vg_pack_voxel_keys(vg_ctx* ctx, const double* xyz, int64_t n, double resolution,
                        int64_t* keys_out);
+/* replaces voxel_downsample (preprocess.py:73-119): per packed voxel key (ascending), the
+ * mean position and mean stamp of its points; a voxel whose stamp spread exceeds split_tol
+ * (the reference passes scan.duration / 10) is split into a primary and an overflow cell by
+ * the running-mean rule, primary first.  Bit-identical to the reference (its summation
+ * orders included).  xyz_out (n x 3) and stamps_out (n) need room for n cells; *m_out
+ * receives the cell count.  VG_ERR_INVALID when resolution <= 0. */
+int vg_voxel_downsample(vg_ctx* ctx, const double* xyz, const double* stamps, int64_t n,
+                        double resolution, double split_tol, double* xyz_out,
+                        double* stamps_out, int64_t* m_out);
+
+/* replaces the per-point half of deskew (preprocess.py:218-231): each point's segment of the
+ * node trajectory (node_t ascending, K >= 2; searchsorted side="right", clipped), the slerped
+ * node quaternion (xyzw, _slerp_batch :167-178) and linearly interpolated translation at its
+ * stamp, and p' = p + 2w(u x p) + 2u x (u x p) + t.  The node trajectory is what the
+ * reference integrates on the host from the IMU (:199-216).  xyz_out: n x 3. */
+int vg_deskew_points(vg_ctx* ctx, const double* xyz, const double* stamps, int64_t n,
+                     const double* node_t, const double* quats, const double* trans, int64_t K,
+                     double* xyz_out);
 
 /* ---- clouds (Frame: preprocess.py:46-60) ----------------------------------------------- */
 /* xyz: n x 3; cov: n x 3 x 3 or NULL.  Points exactly representable in fp32 take the fast

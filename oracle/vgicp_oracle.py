@@ -215,6 +215,117 @@ def estimate_covariances(points: np.ndarray, neighbors: np.ndarray, plane_eps=1e
     return out, degenerate
 
 
+# ---- voxel downsampling (preprocess.py:73-119) ----------------------------------------------
+
+def pairwise_sum(a: np.ndarray) -> float:
+    """NumPy's 1-D float64 add.reduce (pairwise: 8 accumulators up to 128 elements, halves
+    rounded to a multiple of 8 above) — the summation order of `stamps[cell].mean()`."""
+    n = len(a)
+    if n < 8:
+        res = 0.0
+        for x in a:
+            res += float(x)
+        return res
+    if n <= 128:
+        r = [float(x) for x in a[:8]]
+        i = 8
+        while i < n - n % 8:
+            for j in range(8):
+                r[j] += float(a[i + j])
+            i += 8
+        res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+        for x in a[i:]:
+            res += float(x)
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return pairwise_sum(a[:n2]) + pairwise_sum(a[n2:])
+
+
+def _cell_mean(points, stamps, cell):
+    """`points[cell].mean(axis=0)` (sequential row sums from 0.0) and `stamps[cell].mean()`
+    (pairwise), each divided by the count."""
+    acc = np.zeros(3)
+    for i in cell:
+        acc = acc + points[i]
+    return acc / len(cell), (0.0 + pairwise_sum(stamps[cell])) / len(cell)
+
+
+def voxel_downsample(points: np.ndarray, stamps: np.ndarray, resolution: float,
+                     duration: float):
+    """preprocess.py:73-119 — points grouped by packed voxel key (ascending key, members in
+    scan order); a group whose stamp spread exceeds duration/10 is split by the running-mean
+    rule into a primary and an overflow cell.  Returns (points (m,3), stamps (m,))."""
+    if resolution <= 0.0:
+        raise ValueError("resolution must be positive")
+    pts = np.asarray(points, float).reshape(-1, 3)
+    ts = np.asarray(stamps, float).reshape(-1)
+    n = pts.shape[0]
+    if n == 0:
+        return pts, ts
+    tol = duration / 10.0
+    keys = pack_voxel_keys(pts, resolution)
+    order = np.argsort(keys, kind="stable")
+    starts = np.flatnonzero(np.r_[True, np.diff(keys[order]) != 0])
+    ends = np.r_[starts[1:], n]
+    out_p, out_t = [], []
+    for s, e in zip(starts, ends):
+        grp = order[s:e]
+        g = ts[grp]
+        if g.max() - g.min() <= tol:
+            cells = [grp]
+        else:
+            cells = [[], []]
+            sums = [0.0, 0.0]
+            for i in grp:
+                t = ts[i]
+                target = 0 if (not cells[0] or abs(t - sums[0] / len(cells[0])) <= tol) else 1
+                cells[target].append(i)
+                sums[target] += t
+            cells = [np.asarray(c, np.int64) for c in cells if c]
+        for c in cells:
+            mp, mt = _cell_mean(pts, ts, c)
+            out_p.append(mp)
+            out_t.append(mt)
+    return np.asarray(out_p).reshape(-1, 3), np.asarray(out_t)
+
+
+# ---- deskew, per-point half (preprocess.py:167-178, 218-231) -------------------------------
+
+def slerp(qa: np.ndarray, qb: np.ndarray, alpha: np.ndarray) -> np.ndarray:
+    """Shortest-arc slerp of xyzw rows (preprocess.py:167-178): near-parallel pairs
+    (dot > 1 - 1e-12) interpolate linearly; the result is renormalised."""
+    dot = np.sum(qa * qb, axis=1)
+    qb = np.where(dot[:, None] < 0.0, -qb, qb)
+    dot = np.abs(dot)
+    theta = np.arccos(np.clip(dot, -1.0, 1.0))
+    den = np.sin(theta)
+    den = np.where(den == 0.0, 1.0, den)
+    near = dot > 1.0 - 1e-12
+    w0 = np.where(near, 1.0 - alpha, np.sin((1.0 - alpha) * theta) / den)
+    w1 = np.where(near, alpha, np.sin(alpha * theta) / den)
+    q = w0[:, None] * qa + w1[:, None] * qb
+    return q / np.sqrt(np.sum(q * q, axis=1, keepdims=True))
+
+
+def deskew_points(points, stamps, node_t, quats, trans) -> np.ndarray:
+    """preprocess.py:218-231 — each point's trajectory segment (last node at or before its
+    stamp, clipped to the node range), slerped rotation and interpolated translation at its
+    stamp, then p' = p + w c1 + u x c1 + t with c1 = 2 u x p (q = (u, w))."""
+    p = np.asarray(points, float).reshape(-1, 3)
+    ts = np.asarray(stamps, float).reshape(-1)
+    node_t = np.asarray(node_t, float)
+    seg = np.clip(np.searchsorted(node_t, ts, side="right") - 1, 0, node_t.size - 2)
+    span = node_t[seg + 1] - node_t[seg]
+    alpha = np.where(span > 0, (ts - node_t[seg]) / np.where(span > 0, span, 1.0), 0.0)
+    alpha = np.clip(alpha, 0.0, 1.0)
+    q = slerp(quats[seg], quats[seg + 1], alpha)
+    t = (1.0 - alpha)[:, None] * trans[seg] + alpha[:, None] * trans[seg + 1]
+    u, w = q[:, :3], q[:, 3:4]
+    c1 = 2.0 * np.cross(u, p)
+    return p + w * c1 + np.cross(u, c1) + t
+
+
 # ---- poses (geometry.py:33-144, 231-237), vectorised over factors -------------------------
 
 def _qmul(a, b):

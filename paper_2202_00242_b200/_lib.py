@@ -18,7 +18,8 @@ import numpy as np
 
 from . import errors
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvgicp.so"
+LIB_PATH = Path(os.environ.get("VGICP_LIB") or
+                Path(__file__).resolve().parent / "lib" / "libvgicp.so")  # VGICP_LIB: A/B builds
 
 VG_OK = 0
 VG_ERR_INVALID = 1
@@ -58,6 +59,10 @@ _SIGNATURES = {
     "vg_ctx_synchronize": ([c_void_p], c_int),
     "vg_ctx_launch_count": ([c_void_p, _P_I64], c_int),
     "vg_pack_voxel_keys": ([c_void_p, _P_D, c_int64, c_double, _P_I64], c_int),
+    "vg_deskew_points": ([c_void_p, _P_D, _P_D, c_int64, _P_D, _P_D, _P_D, c_int64, _P_D],
+                         c_int),
+    "vg_voxel_downsample": ([c_void_p, _P_D, _P_D, c_int64, c_double, c_double, _P_D, _P_D,
+                             _P_I64], c_int),
     "vg_cloud_create": ([c_void_p, _P_D, _P_D, c_int64, _PP], c_int),
     "vg_cloud_info": ([c_void_p, _P_I64, POINTER(c_int32), POINTER(c_int32)], c_int),
     "vg_cloud_destroy": ([c_void_p], c_int),

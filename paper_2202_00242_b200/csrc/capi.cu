@@ -148,6 +148,32 @@ int vg_pack_voxel_keys(vg_ctx* ctx, const double* xyz, int64_t n, double res, in
   return rc;
 }
 
+int vg_voxel_downsample(vg_ctx* ctx, const double* xyz, const double* stamps, int64_t n,
+                        double res, double split_tol, double* xyz_out, double* stamps_out,
+                        int64_t* m_out) {
+  if (!ctx || !m_out || n < 0 || (n && (!xyz || !stamps || !xyz_out || !stamps_out)))
+    return fail(VG_ERR_INVALID, "null argument");
+  if (!(res > 0.0)) return fail(VG_ERR_INVALID, "resolution must be positive");
+  if (n >= (1LL << 31)) return fail(VG_ERR_INVALID, "scan too large");
+  VG_CUDA(cudaSetDevice(ctx->device));
+  long long m = 0;
+  VG_CHECK(launch_voxel_downsample(ctx, xyz, stamps, n, res, split_tol, xyz_out, stamps_out, &m));
+  *m_out = m;
+  return VG_OK;
+}
+
+int vg_deskew_points(vg_ctx* ctx, const double* xyz, const double* stamps, int64_t n,
+                     const double* node_t, const double* quats, const double* trans, int64_t K,
+                     double* xyz_out) {
+  if (!ctx || n < 0 || (n && (!xyz || !stamps || !xyz_out)) || !node_t || !quats || !trans)
+    return fail(VG_ERR_INVALID, "null argument");
+  if (K < 2 || K >= (1LL << 31)) return fail(VG_ERR_INVALID, "need at least two trajectory nodes");
+  for (int64_t i = 1; i < K; ++i)
+    if (!(node_t[i] >= node_t[i - 1])) return fail(VG_ERR_INVALID, "node stamps must ascend");
+  VG_CUDA(cudaSetDevice(ctx->device));
+  return launch_deskew(ctx, xyz, stamps, n, node_t, quats, trans, (int)K, xyz_out);
+}
+
 // ---- clouds -----------------------------------------------------------------------------
 int vg_cloud_create(vg_ctx* ctx, const double* xyz, const double* cov, int64_t n,
                     vg_cloud** out) {

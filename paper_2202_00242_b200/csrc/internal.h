@@ -214,6 +214,14 @@ int launch_pack_keys(vg_ctx* ctx, const double* xyz_dev, long long n, double res
                      long long* keys_dev);
 int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cloud);  // fp64 xyz/cov -> fp32 SoA
 int launch_map_build(vg_ctx* ctx, const vg_cloud* cloud, double res, vg_map* map);
+// per-point deskew (preprocess.py:218-231) from host arrays into host outputs
+int launch_deskew(vg_ctx* ctx, const double* xyz, const double* stamps, long long n,
+                  const double* node_t, const double* quats, const double* trans, int K,
+                  double* xyz_out);
+// voxel_downsample (preprocess.py:73-119) from host arrays into host outputs (capacity n)
+int launch_voxel_downsample(vg_ctx* ctx, const double* xyz, const double* stamps, long long n,
+                            double res, double tol, double* xyz_out, double* stamps_out,
+                            long long* m_out);
 int launch_map_finish(vg_ctx* ctx, vg_map* map);  // fp64 arrays -> slots + hash
 int launch_lookup(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                   const double* T_dev, long long* rows_dev, unsigned long long* hits_dev);

@@ -148,6 +148,128 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
   cnt_out[cidx] = cnt;
 }
 
+// ---- voxel downsampling (preprocess.py:73-119) -------------------------------------------
+// Grouping is the map build's: stable radix sort of (key, index) + run-length encode, so each
+// group lists its members in scan order (np.argsort(kind="stable") + np.split).  One thread
+// per group then reproduces the reference's arithmetic in its order: exact stamp min/max,
+// the running-mean split rule in scan order (:100-111), sequential fp64 position sums from
+// 0.0 (`points[cell].mean(axis=0)`) and NumPy's pairwise stamp sum (`stamps[cell].mean()`).
+
+// NumPy's float64 pairwise add.reduce over a contiguous array: < 8 elements sequentially,
+// <= 128 with 8 interleaved accumulators, above that split at a multiple of 8 and recurse
+// (evaluated here with explicit stacks: left subtree, right subtree, then their sum).
+__device__ double pairwise_leaf(const double* a, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res = add_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], a[i + j]);
+  double res = add_rn(add_rn(add_rn(r[0], r[1]), add_rn(r[2], r[3])),
+                      add_rn(add_rn(r[4], r[5]), add_rn(r[6], r[7])));
+  for (; i < n; ++i) res = add_rn(res, a[i]);
+  return res;
+}
+
+__device__ double pairwise_sum(const double* a, int n) {
+  if (n <= 128) return pairwise_leaf(a, n);
+  int2 ops[96];  // (offset, n); n < 0 marks "add the top two values"
+  double vals[48];
+  int no = 0, nv = 0;
+  ops[no++] = make_int2(0, n);
+  while (no > 0) {
+    const int2 op = ops[--no];
+    if (op.y < 0) {
+      const double r = vals[--nv];
+      vals[nv - 1] = add_rn(vals[nv - 1], r);
+    } else if (op.y <= 128) {
+      vals[nv++] = pairwise_leaf(a + op.x, op.y);
+    } else {
+      int n2 = op.y / 2;
+      n2 -= n2 % 8;
+      ops[no++] = make_int2(0, -1);
+      ops[no++] = make_int2(op.x + n2, op.y - n2);
+      ops[no++] = make_int2(op.x, n2);
+    }
+  }
+  return vals[0];
+}
+
+// per group: cell of every member (0 primary, 1 overflow) and the number of output cells
+__global__ void k_ds_assign(const int* __restrict__ offsets, const int* __restrict__ counts,
+                            const int* __restrict__ perm, const double* __restrict__ stamps,
+                            int m, double tol, unsigned char* __restrict__ cell,
+                            int* __restrict__ ncell) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= m) return;
+  const int off = offsets[g], cnt = counts[g];
+  double tmin = stamps[perm[off]], tmax = tmin;
+  for (int j = off + 1; j < off + cnt; ++j) {
+    const double t = stamps[perm[j]];
+    tmin = t < tmin ? t : tmin;
+    tmax = t > tmax ? t : tmax;
+  }
+  if (sub_rn(tmax, tmin) <= tol) {
+    for (int j = off; j < off + cnt; ++j) cell[j] = 0;
+    ncell[g] = 1;
+    return;
+  }
+  long long n0 = 0, n1 = 0;
+  double s0 = 0.0;
+  for (int j = off; j < off + cnt; ++j) {
+    const double t = stamps[perm[j]];
+    const bool primary = n0 == 0 || fabs(sub_rn(t, __ddiv_rn(s0, (double)n0))) <= tol;
+    cell[j] = primary ? 0 : 1;
+    if (primary) {
+      ++n0;
+      s0 = add_rn(s0, t);
+    } else {
+      ++n1;
+    }
+  }
+  ncell[g] = n1 > 0 ? 2 : 1;
+}
+
+// per group: the mean position and stamp of each of its cells, written at its output slot;
+// `scratch` (one double per point) holds each cell's stamps contiguously for the pairwise sum
+__global__ void k_ds_emit(const int* __restrict__ offsets, const int* __restrict__ counts,
+                          const int* __restrict__ perm, const double* __restrict__ xyz,
+                          const double* __restrict__ stamps, const unsigned char* __restrict__ cell,
+                          const int* __restrict__ ncell, const int* __restrict__ out_off, int m,
+                          double* __restrict__ scratch, double* __restrict__ xyz_out,
+                          double* __restrict__ stamps_out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= m) return;
+  const int off = offsets[g], cnt = counts[g];
+  int o = out_off[g];
+  int base = off;
+  for (int c = 0; c < ncell[g]; ++c) {
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    int k = 0;
+    for (int j = off; j < off + cnt; ++j) {
+      if (cell[j] != c) continue;
+      const int i = perm[j];
+      sx = add_rn(sx, xyz[3 * (size_t)i]);
+      sy = add_rn(sy, xyz[3 * (size_t)i + 1]);
+      sz = add_rn(sz, xyz[3 * (size_t)i + 2]);
+      scratch[base + k++] = stamps[i];
+    }
+    const double dk = (double)k;
+    xyz_out[3 * (size_t)o] = __ddiv_rn(sx, dk);
+    xyz_out[3 * (size_t)o + 1] = __ddiv_rn(sy, dk);
+    xyz_out[3 * (size_t)o + 2] = __ddiv_rn(sz, dk);
+    stamps_out[o] = __ddiv_rn(add_rn(0.0, pairwise_sum(scratch + base, k)), dk);
+    base += k;
+    ++o;
+  }
+}
+
 // one thread per cell: insert key into the bucketized hash (home bucket first, then the next
 // bucket; CAS on the key), then write the 128 B record (fp64 Gaussian + reference row) at the
 // slot (kmode 1) or at the row with a slot -> row entry (kmode 0).
@@ -315,6 +437,71 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
       map->pkeys32, map->recs);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_voxel_downsample(vg_ctx* ctx, const double* xyz, const double* stamps, long long n,
+                            double res, double tol, double* xyz_out, double* stamps_out,
+                            long long* m_out) {
+  *m_out = 0;
+  if (n == 0) return 0;
+  cudaStream_t st = ctx->stream;
+  long long *keys = nullptr, *keys_sorted = nullptr, *ukeys = nullptr;
+  int *idx = nullptr, *perm = nullptr, *counts = nullptr, *offsets = nullptr, *num_runs = nullptr;
+  int *ncell = nullptr, *out_off = nullptr;
+  unsigned char* cell = nullptr;
+  double *dx = nullptr, *dt = nullptr, *scratch = nullptr, *ox = nullptr, *ot = nullptr;
+  void* tmp = nullptr;
+  size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+  DeviceTemps temps(st);
+  VG_CUDA(temps.alloc(&dx, 3 * (size_t)n));
+  VG_CUDA(temps.alloc(&dt, (size_t)n));
+  VG_CUDA(temps.alloc(&keys, (size_t)n));
+  VG_CUDA(temps.alloc(&keys_sorted, (size_t)n));
+  VG_CUDA(temps.alloc(&ukeys, (size_t)n));
+  VG_CUDA(temps.alloc(&idx, (size_t)n));
+  VG_CUDA(temps.alloc(&perm, (size_t)n));
+  VG_CUDA(temps.alloc(&counts, (size_t)n));
+  VG_CUDA(temps.alloc(&offsets, (size_t)n));
+  VG_CUDA(temps.alloc(&ncell, (size_t)n));
+  VG_CUDA(temps.alloc(&out_off, (size_t)n));
+  VG_CUDA(temps.alloc(&cell, (size_t)n));
+  VG_CUDA(temps.alloc(&scratch, (size_t)n));
+  VG_CUDA(temps.alloc(&ox, 3 * (size_t)n));
+  VG_CUDA(temps.alloc(&ot, (size_t)n));
+  VG_CUDA(temps.alloc(&num_runs, 1));
+  VG_CUDA(cudaMemcpyAsync(dx, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+  VG_CUDA(cudaMemcpyAsync(dt, stamps, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  k_pack_keys<<<grid1(n, 256), 256, 0, st>>>(dx, n, res, keys, idx);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st);
+  cub::DeviceRunLengthEncode::Encode(nullptr, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t3, counts, offsets, (int)n, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, t4, ncell, out_off, (int)n, st);
+  VG_CUDA(temps.alloc((unsigned char**)&tmp, std::max(std::max(t1, t2), std::max(t3, t4))));
+  VG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st));
+  VG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st));
+  int m = 0;
+  VG_CUDA(cudaMemcpyAsync(&m, num_runs, sizeof(int), cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaStreamSynchronize(st));
+  VG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t3, counts, offsets, m, st));
+  k_ds_assign<<<(m + 127) / 128, 128, 0, st>>>(offsets, counts, perm, dt, m, tol, cell, ncell);
+  VG_CUDA(cudaGetLastError());
+  VG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t4, ncell, out_off, m, st));
+  k_ds_emit<<<(m + 127) / 128, 128, 0, st>>>(offsets, counts, perm, dx, dt, cell, ncell, out_off,
+                                             m, scratch, ox, ot);
+  VG_CUDA(cudaGetLastError());
+  ctx->launches += 9;  // pack, sort (>=2), rle, 2 scans, assign, emit (cub counted conservatively)
+  int total = 0, last = 0;
+  VG_CUDA(cudaMemcpyAsync(&total, out_off + m - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaMemcpyAsync(&last, ncell + m - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaStreamSynchronize(st));
+  total += last;
+  VG_CUDA(cudaMemcpyAsync(xyz_out, ox, sizeof(double) * 3 * total, cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaMemcpyAsync(stamps_out, ot, sizeof(double) * total, cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaStreamSynchronize(st));
+  *m_out = total;
   return 0;
 }
 

@@ -38,6 +38,7 @@ REPLACEMENTS = {
     },
     "preprocess": {
         "pack_voxel_keys": _pp.pack_voxel_keys,
+        "voxel_downsample": _pp.voxel_downsample,
         "knn_search": _pp.knn_search,
         "estimate_covariances": _pp.estimate_covariances,
     },
@@ -52,6 +53,7 @@ REPLACEMENTS = {
         "GaussianVoxelMap": _rg.GaussianVoxelMap,
         "build_voxelmap": _rg.build_voxelmap,
         "overlap_rate": _rg.overlap_rate,
+        "voxel_downsample": _pp.voxel_downsample,
         "knn_search": _pp.knn_search,
         "estimate_covariances": _pp.estimate_covariances,
     },
@@ -105,6 +107,17 @@ def patch(pkg="limapper"):
                 if name in vars(cls):
                     saved.append((cls, name, vars(cls)[name]))
                     setattr(cls, name, fn)
+
+    # deskew keeps the reference's host IMU integration (taken from its preprocess module) and
+    # moves the per-point work to the GPU (preprocess.py:181-232)
+    prep = _module(pkg, "preprocess") if not hasattr(pkg, "preprocess") else pkg.preprocess
+    if prep is not None and hasattr(prep, "deskew") and hasattr(prep, "integration_nodes"):
+        dk = _pp.make_deskew(prep)
+        for sub in ("preprocess", "odometry"):
+            mod = _module(pkg, sub) if not hasattr(pkg, sub) else getattr(pkg, sub)
+            if mod is not None and hasattr(mod, "deskew"):
+                saved.append((mod, "deskew", getattr(mod, "deskew")))
+                setattr(mod, "deskew", dk)
 
     def undo():
         for mod, name, obj in reversed(saved):

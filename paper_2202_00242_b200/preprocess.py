@@ -1,8 +1,9 @@
-"""Drop-in for the hot-path half of limapper/preprocess.py: voxel keys, exact kNN and
-plane-regularised covariances, computed by libvgicp on the GPU.
+"""Drop-in for the hot-path half of limapper/preprocess.py: voxel keys, voxel downsampling,
+exact kNN and plane-regularised covariances, computed by libvgicp on the GPU.
 
-``Frame`` mirrors preprocess.py:46-60 field for field; any object with ``points``,
-``covs`` and ``neighbors`` attributes (the reference Frame included) is accepted.
+``RawScan`` and ``Frame`` mirror preprocess.py:25-60 field for field; any object with the
+same attributes (the reference's own types included) is accepted, and voxel_downsample
+returns the caller's scan type.
 """
 
 from __future__ import annotations
@@ -16,6 +17,27 @@ from . import _lib
 from .errors import FrameTooSparse
 
 KEY_OFFSET = 1 << 20  # preprocess.py:21-22
+
+
+@dataclass(frozen=True)
+class RawScan:
+    """preprocess.py:25-43: points with absolute per-point stamps plus the scan time span."""
+
+    points: np.ndarray  # (n, 3)
+    stamps: np.ndarray  # (n,)
+    scan_start: float
+    scan_end: float
+
+    def __post_init__(self):
+        object.__setattr__(self, "points", np.asarray(self.points, dtype=float).reshape(-1, 3))
+        object.__setattr__(self, "stamps", np.asarray(self.stamps, dtype=float).reshape(-1))
+
+    @property
+    def duration(self) -> float:
+        return self.scan_end - self.scan_start
+
+    def __len__(self) -> int:
+        return self.points.shape[0]
 
 
 @dataclass(frozen=True)
@@ -72,6 +94,97 @@ def pack_voxel_keys(points: np.ndarray, resolution: float) -> np.ndarray:
                                           float(resolution), _lib.iptr(out)),
                "pack_voxel_keys")
     return out
+
+
+def voxel_downsample(scan, resolution: float):
+    """Average positions and stamps per voxel, splitting on stamp spread (preprocess.py:73-119).
+
+    Same grouping, split rule (a point whose stamp is more than a tenth of the scan duration
+    from its cell's running-mean stamp goes to one overflow cell of the same key), output
+    order and summation orders as the reference, so the result is bit-identical.  Returns an
+    object of the scan's own type (the reference RawScan included).
+    """
+    if resolution <= 0.0:
+        raise ValueError("resolution must be positive")
+    n = len(scan)
+    if n == 0:
+        return scan
+    pts = _lib.f64(scan.points).reshape(-1, 3)
+    ts = _lib.f64(scan.stamps).reshape(-1)
+    split_tol = scan.duration / 10.0
+    out_p = np.empty((n, 3))
+    out_t = np.empty(n)
+    m = np.zeros(1, dtype=np.int64)
+    ctx = _lib.context()
+    _lib.check(ctx.lib.vg_voxel_downsample(ctx.handle, _lib.dptr(pts), _lib.dptr(ts), n,
+                                           float(resolution), float(split_tol),
+                                           _lib.dptr(out_p), _lib.dptr(out_t), _lib.iptr(m)),
+               "voxel_downsample")
+    m = int(m[0])
+    return type(scan)(out_p[:m].copy(), out_t[:m].copy(), scan.scan_start, scan.scan_end)
+
+
+def deskew_points(points, stamps, node_t, quats, trans) -> np.ndarray:
+    """Per-point half of deskew (preprocess.py:218-231) on the GPU: every point moved into the
+    scan-start frame by the node trajectory (node_t ascending (K,), xyzw quats (K,4), trans
+    (K,3), relative to the scan-start pose) slerped/interpolated at its stamp."""
+    pts = _lib.f64(points).reshape(-1, 3)
+    ts = _lib.f64(stamps).reshape(-1)
+    nt = _lib.f64(node_t).reshape(-1)
+    q = _lib.f64(quats).reshape(-1, 4)
+    tr = _lib.f64(trans).reshape(-1, 3)
+    if not (len(nt) == len(q) == len(tr)) or len(ts) != len(pts):
+        raise ValueError("deskew_points: inconsistent array lengths")
+    out = np.empty_like(pts)
+    ctx = _lib.context()
+    _lib.check(ctx.lib.vg_deskew_points(ctx.handle, _lib.dptr(pts), _lib.dptr(ts), len(pts),
+                                        _lib.dptr(nt), _lib.dptr(q), _lib.dptr(tr), len(nt),
+                                        _lib.dptr(out)), "deskew")
+    return out
+
+
+def make_deskew(ns, points_fn=None):
+    """deskew(frame, imu_samples, state_at_scan_start, gravity, max_gap) (preprocess.py:181-232)
+    with the per-point work on the GPU.
+
+    The IMU integration across the scan stays on the host and is the reference's own:
+    `ns` is the namespace that provides integration_nodes, propagate_state,
+    samples_to_arrays, pose_inverse, ImuSample and GRAVITY (the reference's preprocess module
+    imports all of them, preprocess.py:17-19), so the node trajectory is computed exactly as
+    the reference computes it (:199-216) and only the per-point loop moves to libvgicp.
+    `points_fn` overrides the per-point step (tests only).
+    """
+    per_point = deskew_points if points_fn is None else points_fn
+
+    def deskew(frame, imu_samples, state_at_scan_start, gravity=ns.GRAVITY,
+               max_gap: float = 0.02):
+        if frame.deskewed:
+            raise ValueError("frame is already deskewed")
+        if len(frame) == 0:
+            return replace(frame, deskewed=True)
+        t0 = frame.stamp
+        t1 = max(float(frame.stamps.max()), frame.scan_end)
+        if t1 <= t0:
+            return replace(frame, deskewed=True)
+        arrays = (imu_samples if isinstance(imu_samples, tuple)
+                  else ns.samples_to_arrays(imu_samples))
+        node_t, node_a, node_g = ns.integration_nodes(arrays, t0, t1, max_gap)
+        ref_inv = ns.pose_inverse(state_at_scan_start.pose)
+        state = state_at_scan_start
+        quats = np.empty((node_t.size, 4))
+        trans = np.empty((node_t.size, 3))
+        quats[0] = (0.0, 0.0, 0.0, 1.0)
+        trans[0] = 0.0
+        for k in range(node_t.size - 1):
+            state = ns.propagate_state(state, ns.ImuSample(node_t[k], node_a[k], node_g[k]),
+                                       float(node_t[k + 1] - node_t[k]), gravity)
+            quats[k + 1] = (ref_inv.rotation * state.pose.rotation).quat
+            trans[k + 1] = ref_inv.rotation.apply(state.pose.translation) + ref_inv.translation
+        pts = per_point(frame.points, frame.stamps, node_t, quats, trans)
+        return replace(frame, points=pts, deskewed=True)
+
+    deskew.__doc__ = make_deskew.__doc__
+    return deskew
 
 
 def knn_search(frame, k: int) -> np.ndarray:

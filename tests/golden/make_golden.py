@@ -150,5 +150,90 @@ def main():
     print("wrote", sorted(p.name for p in OUT.glob("*.npz")))
 
 
+def downsample_cases():
+    """voxel_downsample (preprocess.py:73-119) on scans that exercise the split rule, groups
+    longer than NumPy's 128-element pairwise block, negative coordinates and exact faces."""
+    rng = np.random.default_rng(11)
+    cases = {}
+    # random order stamps over the whole scan: most multi-point voxels split
+    pts = rng.uniform(-2, 2, (3000, 3))
+    cases["rand"] = (pts, rng.uniform(0.0, 0.1, 3000), 0.5, 0.0, 0.1)
+    # one voxel holding 800 points with a stamp ramp: both cells > 128 members
+    pts = np.concatenate([rng.uniform(0.01, 0.49, (800, 3)), rng.uniform(-3, 3, (700, 3))])
+    ts = np.concatenate([np.linspace(0.0, 0.1, 800), rng.uniform(0.0, 0.1, 700)])
+    cases["big"] = (pts, ts, 0.5, 0.0, 0.1)
+    # a spinning scan: first and last azimuths share voxels
+    az = np.linspace(0.0, 2 * np.pi, 4096, endpoint=False)
+    r = 5.0 + rng.normal(0, 0.02, 4096)
+    pts = np.column_stack([r * np.cos(az), r * np.sin(az), rng.uniform(-0.5, 0.5, 4096)])
+    cases["spin"] = (pts.astype(np.float32).astype(float), 10.0 + az / (2 * np.pi) * 0.1, 0.3,
+                     10.0, 10.1)
+    # negative coordinates, exact faces, signed zeros, a non-power-of-two resolution
+    g = rng.integers(-8, 8, (400, 3)) * 0.25
+    g[:40] = -0.0
+    pts = np.concatenate([g, rng.uniform(-2, 2, (300, 3))])
+    cases["faces"] = (pts, rng.uniform(5.0, 5.05, 700), 0.25, 5.0, 5.05)
+    pts = rng.uniform(-2, 2, (500, 3))
+    cases["res04"] = (pts, np.sort(rng.uniform(0.0, 0.1, 500)), 0.4, 0.0, 0.1)
+    out = {}
+    for name, (p, t, res, t0, t1) in cases.items():
+        d = P.voxel_downsample(P.RawScan(p, t, t0, t1), res)
+        out[f"{name}_points"], out[f"{name}_stamps"] = p, t
+        out[f"{name}_meta"] = np.array([res, t0, t1])
+        out[f"{name}_out_points"], out[f"{name}_out_stamps"] = d.points, d.stamps
+    np.savez_compressed(OUT / "downsample.npz", **out)
+    print("wrote downsample.npz", {k: len(v) for k, v in out.items() if k.endswith("out_stamps")})
+
+
+def deskew_cases():
+    """deskew (preprocess.py:181-232) run by the reference; the node trajectory its host loop
+    builds is captured through this package's make_deskew glue (driven by the reference's own
+    integration_nodes / propagate_state) so the per-point kernel can be checked on the GPU box,
+    where the reference is absent."""
+    from limapper import imu as I
+    from paper_2202_00242_b200 import preprocess as PP
+
+    rng = np.random.default_rng(21)
+    out = {}
+
+    def run(name, n, gyro, accel, state, stamp_lo=0.0, jitter=0.0):
+        pts = rng.uniform(-20, 20, (n, 3))
+        ts = rng.uniform(stamp_lo, 0.1, n)
+        st = np.arange(-0.01, 0.125, 0.005) + rng.uniform(-jitter, jitter, 27)
+        samples = [I.ImuSample(float(t), -I.GRAVITY + np.asarray(accel(t)), np.asarray(gyro(t)))
+                   for t in np.sort(st)]
+        frame = P.Frame(points=pts, stamps=ts, stamp=0.0, scan_end=0.1)
+        ref = P.deskew(frame, samples, state)
+        cap = {}
+
+        def capture(p, t, node_t, quats, trans):
+            cap.update(node_t=node_t.copy(), quats=quats.copy(), trans=trans.copy())
+            return ref.points
+        PP.make_deskew(P, points_fn=capture)(frame, samples, state)
+        out[f"{name}_points"], out[f"{name}_stamps"] = pts, ts
+        for k, v in cap.items():
+            out[f"{name}_{k}"] = v
+        out[f"{name}_out"] = ref.points
+
+    zero = G.SensorState.zero()
+    run("stationary", 2000, lambda t: np.zeros(3), lambda t: np.zeros(3), zero)
+    run("yaw", 4096, lambda t: np.array([0.0, 0.0, 1.0]), lambda t: np.array([0.5, 0.0, 0.0]),
+        zero)
+    posed = G.SensorState(pose=G.Se3Pose(G.so3_exp([0.4, -0.1, 1.2]), np.array([10.0, -3.0, 2.0])),
+                          velocity=np.array([1.0, 0.5, -0.2]), bias_accel=np.zeros(3),
+                          bias_gyro=np.zeros(3), stamp=0.0)
+    run("tumble", 4096, lambda t: np.array([3.0 * np.sin(20 * t), -2.0, 4.0 * np.cos(9 * t)]),
+        lambda t: np.array([0.3, -0.2, 0.1]) * (1 + 5 * t), posed, stamp_lo=-0.02, jitter=0.002)
+    np.savez_compressed(OUT / "deskew.npz", **out)
+    print("wrote deskew.npz", {k: v.shape for k, v in out.items() if k.endswith("node_t")})
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["downsample"]:
+        downsample_cases()
+    elif sys.argv[1:] == ["deskew"]:
+        deskew_cases()
+    else:
+        main()
+        downsample_cases()
+        deskew_cases()

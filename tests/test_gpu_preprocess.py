@@ -140,3 +140,121 @@ def test_grid_knn_exact_on_hard_clouds(case):
     assert len(pts) >= 4096
     ours = P.knn_search(P.make_frame(pts), 10)
     assert np.array_equal(ours, _brute_knn(pts, 10))
+
+
+# ---- voxel_downsample (preprocess.py:73-119) ------------------------------------------------
+
+def _scan(points, stamps, start=0.0, end=0.1):
+    return P.RawScan(np.asarray(points, float), np.asarray(stamps, float), start, end)
+
+
+@pytest.mark.parametrize("case", ["rand", "big", "spin", "faces", "res04"])
+def test_voxel_downsample_matches_reference(golden, case):
+    """Bit-identical to the reference's own output (tests/golden/downsample.npz), order
+    included: split groups, 800-member cells (pairwise stamp sums), faces, signed zeros."""
+    g = golden("downsample")
+    res, t0, t1 = g[f"{case}_meta"]
+    out = P.voxel_downsample(_scan(g[f"{case}_points"], g[f"{case}_stamps"], t0, t1), res)
+    assert np.array_equal(out.points, g[f"{case}_out_points"])
+    assert np.array_equal(out.stamps, g[f"{case}_out_stamps"])
+    assert out.scan_start == t0 and out.scan_end == t1
+
+
+def test_voxel_downsample_reference_tests():
+    """test_preprocess.py:29-79 on the GPU path."""
+    out = P.voxel_downsample(_scan([[0.01, 0, 0], [0.02, 0, 0]], [0.000, 0.004]), 0.1)
+    assert len(out) == 1
+    assert np.allclose(out.points[0], [0.015, 0, 0]) and out.stamps[0] == pytest.approx(0.002)
+    assert len(P.voxel_downsample(_scan([[0.01, 0, 0], [0.02, 0, 0]], [0.0, 0.05]), 0.1)) == 2
+    out = P.voxel_downsample(_scan([[1.0, 2.0, 3.0]], [0.05]), 0.25)
+    assert len(out) == 1 and np.allclose(out.points[0], [1.0, 2.0, 3.0])
+    empty = _scan(np.zeros((0, 3)), np.zeros(0))
+    assert len(P.voxel_downsample(empty, 0.25)) == 0
+    pts = np.tile([[0.05, 0.05, 0.05]], (10, 1))
+    assert len(P.voxel_downsample(_scan(pts, np.linspace(0.0, 0.1, 10)), 1.0)) == 2
+    rng = np.random.default_rng(0)
+    pts = rng.uniform(-2, 2, (500, 3))
+    out = P.voxel_downsample(_scan(pts, rng.uniform(0.0, 0.1, 500)), 0.5)
+    uniq = {tuple(k) for k in np.floor(pts / 0.5).astype(int)}
+    assert len(uniq) <= len(out) <= 2 * len(uniq)
+    rng = np.random.default_rng(1)
+    pts = rng.uniform(-2, 2, (300, 3))
+    once = P.voxel_downsample(_scan(pts, np.full(300, 0.05)), 0.5)
+    twice = P.voxel_downsample(once, 0.5)
+    o1, o2 = np.lexsort(once.points.T), np.lexsort(twice.points.T)
+    assert len(once) == len(twice) and np.allclose(once.points[o1], twice.points[o2])
+    with pytest.raises(ValueError):
+        P.voxel_downsample(_scan([[0.0, 0, 0]], [0.0]), 0.0)
+
+
+@pytest.mark.parametrize("res", [0.1, 0.25, 0.4, 1.0])
+def test_voxel_downsample_spinning_scan_vs_oracle(res):
+    """A 65,536-point spinning scan (stamps by azimuth, so the seam voxels split) against the
+    oracle restatement, bit for bit."""
+    rng = np.random.default_rng(int(res * 100))
+    n = 65536
+    az = np.linspace(0.0, 2 * np.pi, n, endpoint=False)
+    el = rng.uniform(-0.4, 0.4, n)
+    r = rng.uniform(2.0, 30.0, n)
+    pts = np.column_stack([r * np.cos(el) * np.cos(az), r * np.cos(el) * np.sin(az),
+                           r * np.sin(el)]).astype(np.float32).astype(float)
+    ts = 100.0 + az / (2 * np.pi) * 0.1
+    out = P.voxel_downsample(_scan(pts, ts, 100.0, 100.1), res)
+    op, ot = O.voxel_downsample(pts, ts, res, out.scan_end - out.scan_start)
+    assert np.array_equal(out.points, op) and np.array_equal(out.stamps, ot)
+
+
+# ---- deskew, per-point half (preprocess.py:218-231) -----------------------------------------
+# tolerance: 1e-9 m absolute on coordinates up to ~35 m (CUDA's acos/sin are within 2 ulp of
+# NumPy's; the north_star allows 1e-6 abs for floating point)
+DESKEW_ATOL = 1e-9
+
+
+@pytest.mark.parametrize("case", ["stationary", "yaw", "tumble"])
+def test_deskew_points_matches_reference(golden, case):
+    g = golden("deskew")
+    out = P.deskew_points(g[f"{case}_points"], g[f"{case}_stamps"], g[f"{case}_node_t"],
+                          g[f"{case}_quats"], g[f"{case}_trans"])
+    np.testing.assert_allclose(out, g[f"{case}_out"], rtol=0, atol=DESKEW_ATOL)
+
+
+def _yaw_quat(a):
+    return np.column_stack([np.zeros_like(a), np.zeros_like(a), np.sin(a / 2), np.cos(a / 2)])
+
+
+def test_deskew_points_properties_and_edges():
+    rng = np.random.default_rng(3)
+    pts = rng.uniform(-10, 10, (1000, 3))
+    ts = rng.uniform(-0.02, 0.12, 1000)  # some stamps outside the node range: clipped
+    node_t = np.linspace(0.0, 0.1, 11)
+    # identity trajectory: points unchanged, bit for bit
+    out = P.deskew_points(pts, ts, node_t, _yaw_quat(np.zeros(11)), np.zeros((11, 3)))
+    assert np.array_equal(out, pts)
+    # constant yaw rate 1 rad/s: closed form rotation by the clipped stamp (slerp is exact)
+    out = P.deskew_points(pts, ts, node_t, _yaw_quat(node_t), np.zeros((11, 3)))
+    a = np.clip(ts, 0.0, 0.1)
+    exp = np.column_stack([np.cos(a) * pts[:, 0] - np.sin(a) * pts[:, 1],
+                           np.sin(a) * pts[:, 0] + np.cos(a) * pts[:, 1], pts[:, 2]])
+    np.testing.assert_allclose(out, exp, rtol=0, atol=1e-9)
+    # repeated node stamps (zero-length segments), two-node trajectories, antipodal quats
+    node_t = np.array([0.0, 0.05, 0.05, 0.1])
+    q = _yaw_quat(np.array([0.0, 0.3, 0.3, 0.9]))
+    q[2] *= -1.0
+    tr = rng.normal(size=(4, 3))
+    np.testing.assert_allclose(P.deskew_points(pts, ts, node_t, q, tr),
+                               O.deskew_points(pts, ts, node_t, q, tr), rtol=0, atol=DESKEW_ATOL)
+    np.testing.assert_allclose(P.deskew_points(pts, ts, node_t[[0, 3]], q[[0, 3]], tr[[0, 3]]),
+                               O.deskew_points(pts, ts, node_t[[0, 3]], q[[0, 3]], tr[[0, 3]]),
+                               rtol=0, atol=DESKEW_ATOL)
+    assert P.deskew_points(np.zeros((0, 3)), np.zeros(0), node_t, q, tr).shape == (0, 3)
+
+
+def test_deskew_points_large_scan_vs_oracle(golden):
+    """131,072 points against the oracle on the reference's tumbling trajectory."""
+    g = golden("deskew")
+    rng = np.random.default_rng(4)
+    pts = rng.uniform(-30, 30, (131072, 3))
+    ts = rng.uniform(-0.01, 0.1, 131072)
+    args = (g["tumble_node_t"], g["tumble_quats"], g["tumble_trans"])
+    np.testing.assert_allclose(P.deskew_points(pts, ts, *args), O.deskew_points(pts, ts, *args),
+                               rtol=0, atol=DESKEW_ATOL)

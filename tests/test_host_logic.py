@@ -6,6 +6,8 @@ exact); with the kernel's precision choices (fp64 covariances and inverse, fp32 
 Jacobian terms and lane sums) it must stay within the 1e-4 rel / 1e-6 abs parity bar.
 """
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -155,3 +157,49 @@ def test_normal_equations_flat_layout_and_dense():
     # 15-dof keys: blocks land top-left of each variable's slice
     h15, _ = ne.dense(offsets=[0, 15, 30, 45], dim=60)
     assert np.array_equal(h15[15:21, 45:51], off[1]) and not h15[21:30].any()
+
+
+@pytest.mark.skipif(not Path("/root/reference/pkg/src").exists(), reason="needs the reference")
+def test_make_deskew_glue_matches_reference_deskew():
+    """The drop-in deskew (reference host IMU integration + per-point step) equals the
+    reference's deskew on its own test scenarios (test_preprocess.py:162-231); the per-point
+    step is the oracle here (no GPU), the GPU kernel is checked against the same trajectories
+    in tests/test_gpu_preprocess.py."""
+    import importlib
+    import sys as _sys
+
+    _sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        P = importlib.import_module("limapper.preprocess")
+        G = importlib.import_module("limapper.geometry")
+        I = importlib.import_module("limapper.imu")
+        E = importlib.import_module("limapper.errors")
+    finally:
+        _sys.path.remove("/root/reference/pkg/src")
+    from oracle import vgicp_oracle as O
+    from paper_2202_00242_b200 import preprocess as PP
+
+    dk = PP.make_deskew(P, points_fn=O.deskew_points)
+    rng = np.random.default_rng(8)
+    pts = rng.uniform(-3, 3, (50, 3))
+    stamps = rng.uniform(0.0, 0.1, 50)
+    samples = [I.ImuSample(float(t), -I.GRAVITY + [0.3, -0.2, 0.1], [0.1, 0.2, -0.3])
+               for t in np.arange(-0.01, 0.12, 0.005)]
+    frame = P.Frame(points=pts, stamps=stamps, stamp=0.0, scan_end=0.1)
+    state = G.SensorState(pose=G.Se3Pose(G.so3_exp([0.4, -0.1, 1.2]), np.array([10.0, -3.0, 2.0])),
+                          velocity=np.array([1.0, 0.5, -0.2]), bias_accel=np.zeros(3),
+                          bias_gyro=np.zeros(3), stamp=0.0)
+    for st in (G.SensorState.zero(), state):
+        ref = P.deskew(frame, samples, st)
+        got = dk(frame, samples, st)
+        assert got.deskewed and type(got) is type(ref)
+        np.testing.assert_allclose(got.points, ref.points, rtol=0, atol=1e-12)
+    with pytest.raises(E.ImuCoverageGap):
+        dk(P.Frame(points=pts[:1], stamps=np.array([0.05]), stamp=0.0, scan_end=0.1),
+           [I.ImuSample(0.0, -I.GRAVITY, np.zeros(3)), I.ImuSample(0.1, -I.GRAVITY, np.zeros(3))],
+           G.SensorState.zero())
+    with pytest.raises(ValueError):
+        dk(P.Frame(points=np.zeros((1, 3)), stamps=np.zeros(1), stamp=0.0, scan_end=0.1,
+                   deskewed=True), samples, G.SensorState.zero())
+    empty = P.Frame(points=np.zeros((0, 3)), stamps=np.zeros(0), stamp=0.0, scan_end=0.1)
+    assert dk(empty, samples, G.SensorState.zero()).deskewed

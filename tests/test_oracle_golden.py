@@ -139,3 +139,50 @@ def test_config1_against_reference(golden):
     assert lin["inliers"] == int(g["inliers"])
     for k in ("h_ii", "h_ij", "h_jj", "b_i", "b_j", "cost"):
         close(lin[k], g[k], rel=1e-9, abs_=1e-6)
+
+
+DOWNSAMPLE_CASES = ("rand", "big", "spin", "faces", "res04")
+
+
+@pytest.mark.parametrize("case", DOWNSAMPLE_CASES)
+def test_voxel_downsample_bit_exact(golden, case):
+    """preprocess.py:73-119: the restated grouping, split rule and summation orders reproduce
+    the reference's output bit for bit (order included)."""
+    g = golden("downsample")
+    res, t0, t1 = g[f"{case}_meta"]
+    p, t = O.voxel_downsample(g[f"{case}_points"], g[f"{case}_stamps"], res, t1 - t0)
+    assert np.array_equal(p, g[f"{case}_out_points"])
+    assert np.array_equal(t, g[f"{case}_out_stamps"])
+
+
+def test_pairwise_sum_is_numpy_order():
+    rng = np.random.default_rng(5)
+    for n in (1, 7, 8, 9, 127, 128, 129, 255, 256, 1000, 4097):
+        a = rng.normal(size=n) * 10.0 ** rng.integers(-6, 6, n)
+        assert O.pairwise_sum(a) == np.add.reduce(a)
+
+
+def test_voxel_downsample_reference_cases():
+    """test_preprocess.py:29-79 restated on the oracle."""
+    p, t = O.voxel_downsample([[0.01, 0, 0], [0.02, 0, 0]], [0.0, 0.004], 0.1, 0.1)
+    assert len(p) == 1 and np.allclose(p[0], [0.015, 0, 0]) and t[0] == pytest.approx(0.002)
+    p, t = O.voxel_downsample([[0.01, 0, 0], [0.02, 0, 0]], [0.0, 0.05], 0.1, 0.1)
+    assert len(p) == 2
+    p, t = O.voxel_downsample(np.tile([[0.05, 0.05, 0.05]], (10, 1)), np.linspace(0, 0.1, 10),
+                              1.0, 0.1)
+    assert len(p) == 2
+    p, t = O.voxel_downsample(np.zeros((0, 3)), np.zeros(0), 0.25, 0.1)
+    assert len(p) == 0
+    with pytest.raises(ValueError):
+        O.voxel_downsample(np.zeros((1, 3)), np.zeros(1), 0.0, 0.1)
+
+
+@pytest.mark.parametrize("case", ["stationary", "yaw", "tumble"])
+def test_deskew_points_against_reference(golden, case):
+    """preprocess.py:218-231: the restated per-point step on the node trajectory the
+    reference's host loop built reproduces the reference's deskewed points (1e-12 m: NumPy's
+    own arccos/sin/einsum, same operation order)."""
+    g = golden("deskew")
+    out = O.deskew_points(g[f"{case}_points"], g[f"{case}_stamps"], g[f"{case}_node_t"],
+                          g[f"{case}_quats"], g[f"{case}_trans"])
+    np.testing.assert_allclose(out, g[f"{case}_out"], rtol=0, atol=1e-12)
