@@ -33,7 +33,10 @@ namespace vg {
 // (with 4-8 warp CTAs the slot waits for the CTA's slowest item; measured 12% slower for K4a,
 // 7% for K4b).  Residency is set through the min-CTAs launch bound: 32 (K4a fast path,
 // 64 registers), 24 (K4a generic), 12 (K4b, <= 170 registers).
-constexpr int kLookupWarps = 1;
+#ifndef VG_K4A_WARPS
+#define VG_K4A_WARPS 1
+#endif
+constexpr int kLookupWarps = VG_K4A_WARPS;
 
 // KM: 1 = every map of the batch uses 32-bit local keys, 0 = all int64, 2 = mixed (runtime)
 // P2: every map of the batch has a power-of-two resolution (x * (1/res) is exact)
@@ -318,6 +321,9 @@ __device__ __forceinline__ void cp_async_wait() {
 // per-warp stage: own point (1-2 x 16 B, fp32 or fp64 xyz), own source covariance (3 x 16 B),
 // and 32 voxel records gathered cooperatively (5 x 16 B each; the 80 B lane stride is 20
 // banks, so 8 lanes of a 16 B shared-memory read hit 8 distinct 4-bank groups: conflict free)
+#ifndef VG_K4A_MINB
+#define VG_K4A_MINB 32
+#endif
 constexpr int kRecUnits = 5;
 constexpr int kRecStride = 5;
 // PT: 16 B point units per lane — 2 (fp64 xyz possible) or 1 (every point fp32-exact)
@@ -604,7 +610,7 @@ static int launch_lookup_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int
   int* hc = b->hit_counts + off;
   AccDesc* dd = b->descs + off;
   if (b->key_mode == 1 && b->all_pow2 && b->all_f32)  // fast path
-    VG_CUDA(launch_pdl(k_lookup_fast<32>, dim3(lb), dim3(kLookupWarps * 32), 0, st,
+    VG_CUDA(launch_pdl(k_lookup_fast<VG_K4A_MINB>, dim3(lb), dim3(kLookupWarps * 32), 0, st,
                        (const ItemHdr*)(b->hdrs + off), cnt, b->hits, hc, p2, dd));
   else if (b->key_mode == 1 && b->all_pow2)
     k_lookup_items<1, 24, 1><<<lb, kLookupWarps * 32, 0, st>>>(it, cnt, b->factors, b->clouds,
