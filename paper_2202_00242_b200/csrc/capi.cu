@@ -667,15 +667,36 @@ static int run_to_host(vg_batch* b, int mode, double* out_host) {
     for (auto& e : ctx->events) VG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   const int kmode = kmode_of(mode);
+  // VGICP_STAGE_TRACE=1 (profiling): timed events at every stage boundary, printed to stderr
+  static const bool trace = getenv("VGICP_STAGE_TRACE") != nullptr;
+  cudaEvent_t tr[2 * 17 + 1] = {};
+  if (trace) {
+    for (auto& e : tr) VG_CUDA(cudaEventCreate(&e));
+    VG_CUDA(cudaEventRecord(tr[0], ctx->stream));
+  }
   for (int s = 0; s < b->stages; ++s) {
     const int f0 = b->stage_factors[s], f1 = b->stage_factors[s + 1];
     VG_CHECK(launch_accumulate_range(ctx, b, kmode, b->stage_items[s], b->stage_items[s + 1]));
     VG_CHECK(launch_finalize_range(ctx, b, mode, b->out, f0, f1));
     VG_CUDA(cudaEventRecord(ctx->events[s], ctx->stream));
+    if (trace) VG_CUDA(cudaEventRecord(tr[1 + 2 * s], ctx->stream));
     VG_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->events[s], 0));
     VG_CUDA(cudaMemcpyAsync(out_host + (size_t)f0 * rec, b->out + (size_t)f0 * rec,
                             sizeof(double) * rec * (size_t)(f1 - f0), cudaMemcpyDeviceToHost,
                             ctx->side_stream));
+    if (trace) VG_CUDA(cudaEventRecord(tr[2 + 2 * s], ctx->side_stream));
+  }
+  if (trace) {
+    VG_CUDA(cudaDeviceSynchronize());
+    fprintf(stderr, "stage_trace_ms compute/copy:");
+    for (int s = 0; s < b->stages; ++s) {
+      float c = 0.f, d = 0.f;
+      cudaEventElapsedTime(&c, tr[0], tr[1 + 2 * s]);
+      cudaEventElapsedTime(&d, tr[0], tr[2 + 2 * s]);
+      fprintf(stderr, " %.3f/%.3f", c, d);
+    }
+    fprintf(stderr, "\n");
+    for (auto& e : tr) cudaEventDestroy(e);
   }
   // the compute stream must not run ahead of the copies that still read b->out
   VG_CUDA(cudaEventRecord(ctx->events[b->stages], ctx->side_stream));
