@@ -677,6 +677,14 @@ int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi)
   return 0;
 }
 
+int launch_accumulate_range_ev(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi,
+                               cudaEvent_t after_lookup) {
+  if (hi > lo) VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
+  VG_CUDA(cudaEventRecord(after_lookup, ctx->stream));
+  if (hi > lo && kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
+  return 0;
+}
+
 // K4a + K4b over the whole batch (DESIGN.md §9 lists the alternatives that measured slower)
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   return launch_accumulate_range(ctx, b, kmode, 0, (int)b->num_items);

@@ -15,7 +15,8 @@ struct vg_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;  // where all work is enqueued
-  cudaStream_t side_stream = nullptr;  // K4a/K4b overlap (fork/join with events)
+  cudaStream_t side_stream = nullptr;  // host-output copies of the staged pipeline
+  cudaStream_t comp2 = nullptr;        // second compute stream (odd stages, overlapped)
   cudaEvent_t events[65] = {};
   long long launches = 0;         // kernels launched (bench evidence)
   // scratch (grown on demand, stream-ordered reuse)
@@ -235,6 +236,9 @@ int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1);
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev);  // K6
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi);  // K4a + K4b
+// the same, recording `after_lookup` on ctx->stream between K4a and K4b
+int launch_accumulate_range_ev(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi,
+                               cudaEvent_t after_lookup);
 int launch_knn(vg_ctx* ctx, const vg_cloud* cloud, int k, long long* nbrs_dev);
 int launch_cov(vg_ctx* ctx, const vg_cloud* cloud, const long long* nbrs_dev, int k,
                double eps, double* covs_dev, unsigned char* degen_dev);

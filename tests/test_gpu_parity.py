@@ -308,18 +308,20 @@ def test_factor_degenerate_and_empty():
         RG.linearize_matching_cost(empty, vm, G.Se3Pose.identity(), G.Se3Pose.identity())
 
 
-def test_staged_host_output_matches_single_launch(small_graph):
+@pytest.mark.parametrize("target", [9000, 33000])
+def test_staged_host_output_matches_single_launch(small_graph, target):
     """Batches of >= 8192 factors run K4/K5 in stages whose records are copied to the host
-    while the next stage computes; results must equal the one-launch device path bit for bit
-    (same items, same fixed-order sums), and the small batch of the test above to rounding."""
+    while the next stage computes (from 32,768 factors: 8 geometric stages over two compute
+    streams); results must equal the one-launch device path bit for bit (same items, same
+    fixed-order sums), and the small batch of the test above to rounding."""
     import torch
 
     poses, est, scans, covs, maps, srcs, pairs = small_graph
     clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
     dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
-    reps = 9000 // len(pairs) + 1
+    reps = target // len(pairs) + 1
     rng = np.random.default_rng(5)
-    sel = rng.permutation(np.tile(np.arange(len(pairs)), reps))   # F >= 8192 -> 4 stages
+    sel = rng.permutation(np.tile(np.arange(len(pairs)), reps))   # 4 or 8 stages
     P = pairs[sel]
     F = len(P)
     unary = [(int(s) % 7) == 3 for s in sel]
