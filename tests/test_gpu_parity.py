@@ -637,3 +637,44 @@ def test_hash_stress_every_cell_and_misses(wide):
     assert np.array_equal(rows, O.lookup(ref, pts)) and np.all(rows >= 0)
     q = rng.uniform(-1, 52, (200000, 3))
     assert np.array_equal(vm.lookup(q), O.lookup(ref, q))
+
+
+@pytest.mark.parametrize("name", ["odometry_window", "local_mapping"])
+def test_configs_3_and_4_full_size_sample_vs_oracle(name):
+    """BASELINE configs 3 (69 factors of 16,384-point frames at 0.5/1.0/2.0 m, 15 unary) and
+    4 (4,950 factors of 8,192-point frames at 0.5 m) at full size: the batch path's records
+    for a seeded sample of factors match the oracle (bit-exact inliers, blocks within
+    1e-4 rel / 1e-6 abs), and the host and device paths agree bit for bit."""
+    import torch
+
+    from paper_2202_00242_b200 import workloads
+
+    wl = getattr(workloads, name)()
+    batch = wl.batch()
+    table = wl.pose_table
+    F = len(wl.clouds)
+    host = batch.linearize_poses(table)
+    dev = torch.zeros((F, 92), dtype=torch.float64, device="cuda")
+    poses = torch.from_numpy(table).cuda()
+    torch.cuda.synchronize()
+    batch.linearize_poses_device(poses.data_ptr(), len(table), _lib.MODE_LINEARIZE, dev.data_ptr())
+    batch.ctx.synchronize()
+    assert np.array_equal(host, dev.cpu().numpy())
+    rng = np.random.default_rng(66)
+    gated_in = np.flatnonzero(host[:, 91] >= 10)
+    sample = np.unique(np.concatenate([rng.choice(gated_in, min(len(gated_in), 10), replace=False),
+                                       rng.choice(F, min(F, 4), replace=False)]))
+    R, t = O.relative_transforms(table, wl.var_source[sample], wl.var_target[sample])
+    checked = 0
+    for k, f in enumerate(sample):
+        pts, covs = wl.host_sources[f]
+        tp, tc, res = wl.host_targets[f]
+        vmap = O.build_voxelmap(tp, tc, res)
+        try:
+            ref = O.linearize(pts, covs, vmap, R[k], t[k], target_fixed=bool(wl.unary[f]))
+        except ValueError:
+            assert host[f][91] < 10
+            continue
+        assert_lin(RG.unpack_record(host[f], bool(wl.unary[f])), ref, bool(wl.unary[f]))
+        checked += 1
+    assert checked >= 7
