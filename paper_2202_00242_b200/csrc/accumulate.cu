@@ -33,6 +33,11 @@ namespace vg {
 // (with 4-8 warp CTAs the slot waits for the CTA's slowest item; measured 12% slower for K4a,
 // 7% for K4b).  Residency is set through the min-CTAs launch bound: 32 (K4a fast path,
 // 64 registers), 24 (K4a generic), 12 (K4b, <= 170 registers).
+// 1: K4a bucket probes with L1::no_allocate (measured 1.33x slower: consecutive points
+// share bucket lines, so the probes' L1 allocation pays)
+#ifndef VG_PROBE_NA
+#define VG_PROBE_NA 0
+#endif
 #ifndef VG_K4A_WARPS
 #define VG_K4A_WARPS 1
 #endif
@@ -235,7 +240,14 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     return q;
   };
   auto load_bucket = [&](unsigned bucket, unsigned (&g)[4]) {
+#if VG_PROBE_NA
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(keys32 + (size_t)bucket * kBucket32));
+#else
     const uint4 v = __ldg(reinterpret_cast<const uint4*>(keys32 + (size_t)bucket * kBucket32));
+#endif
     g[0] = v.x;
     g[1] = v.y;
     g[2] = v.z;
@@ -308,6 +320,22 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
 
+// bit 0: voxel-record gathers bypass L1 (cp.async.cg; K4 0.417 -> 0.411 ms, cost mode -10%:
+// records have no L1 reuse and their lines evicted the lane-own gathers' and hit entries');
+// bit 1: the lane-own gathers too (either bit alone measures the same, both slower: 0.437)
+#ifndef VG_CG_MASK
+#define VG_CG_MASK 1
+#endif
+// L2-only variant (no L1 allocation) for gathers without L1 reuse
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+template <int kBit>
+__device__ __forceinline__ void cp_async16_sel(void* smem, const void* gmem) {
+  if (VG_CG_MASK & kBit) cp_async16_cg(smem, gmem);
+  else cp_async16(smem, gmem);
+}
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
@@ -358,11 +386,11 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
       cp_async8(d + 1, p + 1);
       cp_async8(reinterpret_cast<double*>(&st.pt[PT - 1][lane]), p + 2);
     } else {
-      cp_async16(&st.pt[0][lane], cv.a + e.x);
+      cp_async16_sel<2>(&st.pt[0][lane], cv.a + e.x);
     }
-    cp_async16(&st.cov[0][lane], cv.c0 + e.x);
-    cp_async16(&st.cov[1][lane], cv.c1 + e.x);
-    cp_async16(&st.cov[2][lane], cv.c2 + e.x);
+    cp_async16_sel<2>(&st.cov[0][lane], cv.c0 + e.x);
+    cp_async16_sel<2>(&st.cov[1][lane], cv.c1 + e.x);
+    cp_async16_sel<2>(&st.cov[2][lane], cv.c2 + e.x);
   }
 #pragma unroll
   for (int c = 0; c < kRecUnits; ++c) {
@@ -370,7 +398,7 @@ __device__ __forceinline__ void issue_round(const CloudView& cv, const MapView& 
     const int q = u / kRecUnits, j = u - q * kRecUnits;
     const int row = __shfl_sync(0xffffffffu, e.y, q);
     if (q < nvalid)
-      cp_async16(&st.rec[q][j], reinterpret_cast<const char*>(mv.recs + row) + 16 * j);
+      cp_async16_sel<1>(&st.rec[q][j], reinterpret_cast<const char*>(mv.recs + row) + 16 * j);
   }
   cp_async_commit();
 }
