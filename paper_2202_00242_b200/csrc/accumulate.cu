@@ -160,6 +160,45 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
   if (descs && lane == 0) descs[w].n = cnt;
 }
 
+#ifndef VG_HITS_NA
+#define VG_HITS_NA 0
+#endif
+#ifndef VG_HITS_CS
+#define VG_HITS_CS 0
+#endif
+#ifndef VG_PTS_NA
+#define VG_PTS_NA 0
+#endif
+// cache-policy variants of the streaming accesses (read or written once), all measured on
+// config 5 and left off: hit-entry loads with L1::no_allocate / hit stores with .cs change
+// nothing (K4 0.4127 ms either way); K4a point loads with L1::no_allocate cost 1.2x (K4a)
+__device__ __forceinline__ int2 ld_hit(const int2* p) {
+#if VG_HITS_NA
+  int2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void st_hit(int2* p, int2 v) {
+#if VG_HITS_CS
+  asm volatile("st.global.cs.v2.s32 [%0], {%1, %2};" ::"l"(p), "r"(v.x), "r"(v.y));
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ float4 ld_pt(const float4* p) {
+#if VG_PTS_NA
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+
 // K4a fast path: every map uses 32-bit local keys and a power-of-two resolution, every
 // source point is fp32-exact.  The item header (T_ij + views, refreshed by K-compose) is read
 // in one dependent step instead of item -> factor -> cloud/map views.
@@ -278,28 +317,28 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     }
     // misses contribute nothing (registration.py:150-156)
     const unsigned mb = __ballot_sync(0xffffffffu, slot >= 0);
-    if (slot >= 0) out[cnt + __popc(mb & lt_mask)] = make_int2(i, slot);
+    if (slot >= 0) st_hit(out + cnt + __popc(mb & lt_mask), make_int2(i, slot));
     cnt += __popc(mb);
   };
   // Two-deep pipeline, unrolled by two with ping-pong registers (A: even rounds, B: odd):
   // the probe of the next round and the point of the round after are in flight while a
   // round resolves, and no in-flight load result is ever copied (a copy would wait for it).
-  float4 pA = __ldg(pa + min(begin + lane, last));
-  float4 pB = __ldg(pa + min(begin + 32 + lane, last));
+  float4 pA = ld_pt(pa + min(begin + lane, last));
+  float4 pB = ld_pt(pa + min(begin + 32 + lane, last));
   Q qA = make_q(pA, begin + lane);
   unsigned gA[4] = {0, 0, 0, 0}, gB[4] = {0, 0, 0, 0};
   if (qA.live) load_bucket(qA.bucket, gA);
-  pA = __ldg(pa + min(begin + 64 + lane, last));
+  pA = ld_pt(pa + min(begin + 64 + lane, last));
   for (int base = begin; base < end; base += 64) {
     const int i = base + lane;
     const Q qB = make_q(pB, i + 32);
     if (qB.live) load_bucket(qB.bucket, gB);
-    pB = __ldg(pa + min(i + 96, last));
+    pB = ld_pt(pa + min(i + 96, last));
     resolve(qA, gA, i);
     if (base + 32 >= end) break;
     qA = make_q(pA, i + 64);
     if (qA.live) load_bucket(qA.bucket, gA);
-    pA = __ldg(pa + min(i + 128, last));
+    pA = ld_pt(pa + min(i + 128, last));
     resolve(qB, gB, i + 32);
   }
   if (lane == 0) {
@@ -587,15 +626,15 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   if (n > 0) {
 #pragma unroll
     for (int r = 0; r < kAhead; ++r)
-      issue_round<kStages, PT>(cv, mv, sm, r, __ldg(hl + min(r * 32 + lane, klast)),
+      issue_round<kStages, PT>(cv, mv, sm, r, ld_hit(hl + min(r * 32 + lane, klast)),
                                gather ? n - r * 32 : 0, lane, own);
-    int2 nxt = __ldg(hl + min(kAhead * 32 + lane, klast));
-    int2 nxt2 = __ldg(hl + min((kAhead + 1) * 32 + lane, klast));
+    int2 nxt = ld_hit(hl + min(kAhead * 32 + lane, klast));
+    int2 nxt2 = ld_hit(hl + min((kAhead + 1) * 32 + lane, klast));
     for (int r = 0; r < rounds; ++r) {
       const int ri = r + kAhead;
       issue_round<kStages, PT>(cv, mv, sm, ri, nxt, gather ? n - ri * 32 : 0, lane, own);
       nxt = nxt2;
-      nxt2 = __ldg(hl + min((ri + 2) * 32 + lane, klast));
+      nxt2 = ld_hit(hl + min((ri + 2) * 32 + lane, klast));
       cp_async_wait<kAhead>();
       __syncwarp();
       if (math && r * 32 + lane < n)
