@@ -35,6 +35,18 @@ namespace vg {
 // 64 registers), 24 (K4a generic), 12 (K4b, <= 170 registers).
 // 1: K4a bucket probes with L1::no_allocate (measured 1.33x slower: consecutive points
 // share bucket lines, so the probes' L1 allocation pays)
+// K4b occupancy bound (one-warp CTAs): at 15 ptxas fits the per-hit math in 126 registers
+// without spills, so 16 warps are resident per SM instead of 12 at 160 registers (config 5:
+// K4 0.413 -> 0.394 ms; 13/14/16 measured 0.396/0.396/0.407, 18 spills)
+#ifndef VG_K4B_MINB
+#define VG_K4B_MINB 15
+#endif
+#ifndef VG_K4B_MINB_GEN
+#define VG_K4B_MINB_GEN 15
+#endif
+#ifndef VG_K4B_MINB_COST
+#define VG_K4B_MINB_COST 12
+#endif
 #ifndef VG_PROBE_NA
 #define VG_PROBE_NA 0
 #endif
@@ -720,21 +732,21 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
     double* p = b->partials + 2 * (size_t)off;
     if (b->all_f32)
       return b->all_plane
-                 ? launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1, 1>, s1, d, cnt, b->hits, p, st)
-                 : launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 1, 0>, s1, d, cnt, b->hits, p, st);
+                 ? launch_acc_kernel(ctx, k_accumulate<1, 2, VG_K4B_MINB_COST, 1, 1>, s1, d, cnt, b->hits, p, st)
+                 : launch_acc_kernel(ctx, k_accumulate<1, 2, VG_K4B_MINB_COST, 1, 0>, s1, d, cnt, b->hits, p, st);
     return b->all_plane
-               ? launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 2, 1>, s2, d, cnt, b->hits, p, st)
-               : launch_acc_kernel(ctx, k_accumulate<1, 2, 12, 2, 0>, s2, d, cnt, b->hits, p, st);
+               ? launch_acc_kernel(ctx, k_accumulate<1, 2, VG_K4B_MINB_COST, 2, 1>, s2, d, cnt, b->hits, p, st)
+               : launch_acc_kernel(ctx, k_accumulate<1, 2, VG_K4B_MINB_COST, 2, 0>, s2, d, cnt, b->hits, p, st);
   }
   double* p = b->partials + (size_t)off * kPartialStride;
   // PT = 1: every point fp32-exact, one 16 B point unit per lane (more L1 left)
   if (b->all_f32)
     return b->all_plane
-               ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 1>, s1, d, cnt, b->hits, p, st)
-               : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 1, 0>, s1, d, cnt, b->hits, p, st);
+               ? launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB, 1, 1>, s1, d, cnt, b->hits, p, st)
+               : launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB_GEN, 1, 0>, s1, d, cnt, b->hits, p, st);
   return b->all_plane
-             ? launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 2, 1>, s2, d, cnt, b->hits, p, st)
-             : launch_acc_kernel(ctx, k_accumulate<0, 2, 12, 2, 0>, s2, d, cnt, b->hits, p, st);
+             ? launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB_GEN, 2, 1>, s2, d, cnt, b->hits, p, st)
+             : launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB_GEN, 2, 0>, s2, d, cnt, b->hits, p, st);
 }
 
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi) {
