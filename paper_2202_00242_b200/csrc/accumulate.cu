@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
       q.live = qq.inside;
       q.k32 = qq.k32;
     }
-    q.bucket = (q.k32 * 0x9E3779B9u) >> shift;
+    q.bucket = bucket32(q.k32, shift);
     q.live = q.live && i < end && m > 0;
     return q;
   };

@@ -158,6 +158,22 @@ constexpr int kBucket = 8;    // kmode 0: int64 keys, 64 B buckets
 constexpr int kBucket32 = 4;  // kmode 1: 32-bit keys, 16 B buckets (one 128-bit load)
 constexpr unsigned kEmpty32 = 0xffffffffu;
 
+// kmode 1 home bucket of a cell-local key (lx | ly << 11 | lz << 22).  VG_BLOCK_HASH: the
+// 2x2x2 block of the cell picks a 128 B line (8 buckets), the cell's coordinate parities the
+// bucket inside it, so probes of neighbouring cells share lines (needs >= 16 buckets)
+#ifndef VG_BLOCK_HASH
+#define VG_BLOCK_HASH 0
+#endif
+__host__ __device__ __forceinline__ unsigned bucket32(unsigned k32, int shift) {
+#if VG_BLOCK_HASH
+  const unsigned sub = (k32 & 1u) | ((k32 >> 10) & 2u) | ((k32 >> 20) & 4u);
+  const unsigned blk = k32 & ~(1u | (1u << 11) | (1u << 22));
+  return (((blk * 0x9E3779B9u) >> (shift + 3)) << 3) | sub;
+#else
+  return (k32 * 0x9E3779B9u) >> shift;
+#endif
+}
+
 struct Query {
   long long key;   // packed reference key
   unsigned k32;    // local key (kmode 1)
@@ -190,7 +206,7 @@ __device__ __forceinline__ Query make_query(const MapView& mv, double fx, double
     q.inside = lx < (unsigned long long)mv.ex && ly < (unsigned long long)mv.ey &&
                lz < (unsigned long long)mv.ez;
     q.k32 = (unsigned)lx | ((unsigned)ly << 11) | ((unsigned)lz << 22);
-    q.bucket = (q.k32 * 0x9E3779B9u) >> mv.shift;
+    q.bucket = bucket32(q.k32, mv.shift);
   } else {
     q.inside = true;
     q.k32 = 0;
@@ -212,7 +228,7 @@ __device__ __forceinline__ Query make_query_local(const MapView& mv, double fx, 
     const unsigned lz = (unsigned)(__double2int_rz(fz) - mv.bz);
     q.inside = lx < (unsigned)mv.ex && ly < (unsigned)mv.ey && lz < (unsigned)mv.ez;
     q.k32 = lx | (ly << 11) | (lz << 22);
-    q.bucket = (q.k32 * 0x9E3779B9u) >> mv.shift;
+    q.bucket = bucket32(q.k32, mv.shift);
     return q;
   }
   return make_query(mv, fx, fy, fz, 1);

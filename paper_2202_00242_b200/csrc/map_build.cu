@@ -288,7 +288,7 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
     const unsigned k32 =
         (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
     bool placed = false;
-    for (unsigned b = (k32 * 0x9E3779B9u) >> mv.shift; !placed; b = (b + 1) & mv.mask)
+    for (unsigned b = bucket32(k32, mv.shift); !placed; b = (b + 1) & mv.mask)
       for (int j = 0; j < kBucket32 && !placed; ++j) {
         h = (size_t)b * kBucket32 + j;
         placed = atomicCAS(pkeys32 + h, kEmpty32, k32) == kEmpty32;
@@ -413,7 +413,7 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
   }
   map->empty_key = empty;
   // capacity: pow2 >= 4m slots (load <= 0.25) in 8-slot (kmode 0) / 4-slot (kmode 1) buckets
-  int l2 = 3;
+  int l2 = VG_BLOCK_HASH ? 6 : 3;  // the block hash needs >= 16 buckets of 4
   while ((1LL << l2) < 4 * map->m) ++l2;
   map->capacity = 1u << l2;
   map->log2cap = l2;
