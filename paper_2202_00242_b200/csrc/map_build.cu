@@ -109,7 +109,15 @@ __global__ void k_plane_fit(const double* __restrict__ cov, long long n, double2
   }
 }
 
-// one thread per cell: mean then scatter, both sequential in index order (np.add.at)
+// one thread per cell: mean then scatter, both sequential in index order (np.add.at).  The
+// member loads are issued kCellBatch at a time ahead of the in-order additions, so a cell of
+// thousands of points (coarse maps near the sensor) pays the dependent fp64 adds, not one
+// L2 round trip per member.
+constexpr int kCellBatch = 8;
+#ifndef VG_BIG_CELL
+#define VG_BIG_CELL 16
+#endif
+constexpr int kBigCell = VG_BIG_CELL;  // cells with at least this many points: one warp per cell
 __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restrict__ counts,
                              const int* __restrict__ perm, const double* __restrict__ xyz,
                              const double* __restrict__ cov, int m, double* __restrict__ means,
@@ -117,28 +125,60 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
   const int cidx = blockIdx.x * blockDim.x + threadIdx.x;
   if (cidx >= m) return;
   const int off = offsets[cidx], cnt = counts[cidx];
+  if (cnt >= kBigCell) return;  // k_cell_stats_big
   double sx = 0.0, sy = 0.0, sz = 0.0;
-  for (int j = off; j < off + cnt; ++j) {
-    const int i = perm[j];
-    sx = add_rn(sx, xyz[3 * i]);
-    sy = add_rn(sy, xyz[3 * i + 1]);
-    sz = add_rn(sz, xyz[3 * i + 2]);
+  for (int j0 = off; j0 < off + cnt; j0 += kCellBatch) {
+    const int nb = min(kCellBatch, off + cnt - j0);
+    double px[kCellBatch], py[kCellBatch], pz[kCellBatch];
+#pragma unroll
+    for (int u = 0; u < kCellBatch; ++u) {
+      if (u < nb) {
+        const int i = perm[j0 + u];
+        px[u] = xyz[3 * (size_t)i];
+        py[u] = xyz[3 * (size_t)i + 1];
+        pz[u] = xyz[3 * (size_t)i + 2];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kCellBatch; ++u) {
+      if (u < nb) {
+        sx = add_rn(sx, px[u]);
+        sy = add_rn(sy, py[u]);
+        sz = add_rn(sz, pz[u]);
+      }
+    }
   }
   const double dc = (double)cnt;
   const double mx = __ddiv_rn(sx, dc), my = __ddiv_rn(sy, dc), mz = __ddiv_rn(sz, dc);
   double acc[9];
 #pragma unroll
   for (int k = 0; k < 9; ++k) acc[k] = 0.0;
-  for (int j = off; j < off + cnt; ++j) {
-    const int i = perm[j];
-    const double c3[3] = {sub_rn(xyz[3 * i], mx), sub_rn(xyz[3 * i + 1], my),
-                          sub_rn(xyz[3 * i + 2], mz)};
+  constexpr int kB = kCellBatch / 2;
+  for (int j0 = off; j0 < off + cnt; j0 += kB) {
+    const int nb = min(kB, off + cnt - j0);
+    double c3[kB][3], cv[kB][9];
 #pragma unroll
-    for (int r = 0; r < 3; ++r)
+    for (int u = 0; u < kB; ++u) {
+      if (u < nb) {
+        const int i = perm[j0 + u];
+        c3[u][0] = sub_rn(xyz[3 * (size_t)i], mx);
+        c3[u][1] = sub_rn(xyz[3 * (size_t)i + 1], my);
+        c3[u][2] = sub_rn(xyz[3 * (size_t)i + 2], mz);
 #pragma unroll
-      for (int c = 0; c < 3; ++c)
-        acc[3 * r + c] = add_rn(acc[3 * r + c], add_rn(cov[9 * (size_t)i + 3 * r + c],
-                                                       mul_rn(c3[r], c3[c])));
+        for (int k = 0; k < 9; ++k) cv[u][k] = cov[9 * (size_t)i + k];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      if (u < nb) {
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            acc[3 * r + c] = add_rn(acc[3 * r + c],
+                                    add_rn(cv[u][3 * r + c], mul_rn(c3[u][r], c3[u][c])));
+      }
+    }
   }
   means[3 * cidx] = mx;
   means[3 * cidx + 1] = my;
@@ -146,6 +186,67 @@ __global__ void k_cell_stats(const int* __restrict__ offsets, const int* __restr
 #pragma unroll
   for (int k = 0; k < 9; ++k) covs[9 * (size_t)cidx + k] = __ddiv_rn(acc[k], dc);
   cnt_out[cidx] = cnt;
+}
+
+// one warp per big cell (>= kBigCell = 16 points; coarse maps near the sensor hold thousands;
+// thresholds 32/48/96 measured 5-17% slower for config 2's three maps).
+// The additions stay sequential in index order — lanes 0-2 carry the three position sums,
+// lanes 0-8 the nine covariance sums — while all 32 lanes load the next 32 members and form
+// their terms (C_k + (p_k - mu)(p_k - mu)^T, the same correctly rounded operations as the
+// per-thread kernel) into shared memory, so the result is bit-identical and a cell costs one
+// dependent fp64 add per member instead of a single thread's whole instruction stream.
+constexpr int kBigWarps = 4;
+__global__ void __launch_bounds__(kBigWarps * 32)
+    k_cell_stats_big(const int* __restrict__ offsets, const int* __restrict__ counts,
+                     const int* __restrict__ perm, const double* __restrict__ xyz,
+                     const double* __restrict__ cov, int m, double* __restrict__ means,
+                     double* __restrict__ covs, long long* __restrict__ cnt_out) {
+  __shared__ double term[kBigWarps][9][33];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int cidx = blockIdx.x * kBigWarps + wib;
+  if (cidx >= m) return;
+  const int off = offsets[cidx], cnt = counts[cidx];
+  if (cnt < kBigCell) return;
+  double (*t)[33] = term[wib];
+  double acc = 0.0;  // lane c < 3: position sum c; later lane k < 9: covariance sum k
+  for (int j0 = off; j0 < off + cnt; j0 += 32) {
+    const int nb = min(32, off + cnt - j0);
+    if (lane < nb) {
+      const int i = perm[j0 + lane];
+      t[0][lane] = xyz[3 * (size_t)i];
+      t[1][lane] = xyz[3 * (size_t)i + 1];
+      t[2][lane] = xyz[3 * (size_t)i + 2];
+    }
+    __syncwarp();
+    if (lane < 3)
+      for (int u = 0; u < nb; ++u) acc = add_rn(acc, t[lane][u]);
+    __syncwarp();
+  }
+  const double dc = (double)cnt;
+  const double mean_l = __ddiv_rn(acc, dc);
+  const double mx = __shfl_sync(0xffffffffu, mean_l, 0), my = __shfl_sync(0xffffffffu, mean_l, 1),
+               mz = __shfl_sync(0xffffffffu, mean_l, 2);
+  acc = 0.0;
+  for (int j0 = off; j0 < off + cnt; j0 += 32) {
+    const int nb = min(32, off + cnt - j0);
+    if (lane < nb) {
+      const int i = perm[j0 + lane];
+      const double c3[3] = {sub_rn(xyz[3 * (size_t)i], mx), sub_rn(xyz[3 * (size_t)i + 1], my),
+                            sub_rn(xyz[3 * (size_t)i + 2], mz)};
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+          t[3 * r + c][lane] = add_rn(cov[9 * (size_t)i + 3 * r + c], mul_rn(c3[r], c3[c]));
+    }
+    __syncwarp();
+    if (lane < 9)
+      for (int u = 0; u < nb; ++u) acc = add_rn(acc, t[lane][u]);
+    __syncwarp();
+  }
+  if (lane < 3) means[3 * cidx + lane] = lane == 0 ? mx : (lane == 1 ? my : mz);
+  if (lane < 9) covs[9 * (size_t)cidx + lane] = __ddiv_rn(acc, dc);
+  if (lane == 0) cnt_out[cidx] = cnt;
 }
 
 // ---- voxel downsampling (preprocess.py:73-119) -------------------------------------------
@@ -548,7 +649,9 @@ int launch_map_build(vg_ctx* ctx, const vg_cloud* cl, double res, vg_map* map) {
   VG_CUDA(cudaMemcpyAsync(map->keys, ukeys, sizeof(long long) * m, cudaMemcpyDeviceToDevice, st));
   k_cell_stats<<<(m + 127) / 128, 128, 0, st>>>(offsets, counts, perm, cl->xyz64, cl->cov64, m,
                                                 map->means, map->covs, map->counts);
-  ctx->launches++;
+  k_cell_stats_big<<<(m + kBigWarps - 1) / kBigWarps, kBigWarps * 32, 0, st>>>(
+      offsets, counts, perm, cl->xyz64, cl->cov64, m, map->means, map->covs, map->counts);
+  ctx->launches += 2;
   VG_CUDA(cudaGetLastError());
   return launch_map_finish(ctx, map);
 }

@@ -94,6 +94,25 @@ def test_build_voxelmap_bit_exact(golden, res):
     assert np.array_equal(vm.covs, g[f"map{tag}_covs"])
 
 
+@pytest.mark.parametrize("res", [0.5, 2.0, 8.0])
+def test_build_voxelmap_big_cells_bit_exact(res):
+    """A 131,072-point scan (config 2) with coarse cells of up to tens of thousands of
+    points: the warp-per-cell path for cells of >= 16 points keeps np.add.at's sequential
+    order, so keys/counts/means/covs equal the oracle's bit for bit."""
+    from paper_2202_00242_b200 import synthetic
+
+    pts = synthetic.scan(synthetic.yaw_pose(0.2, [1.0, -2.0, 0.0]), synthetic.ray_table(1024, 128),
+                         np.random.default_rng(2))
+    rng = np.random.default_rng(9)
+    a = rng.normal(size=(len(pts), 3, 3))
+    covs = a @ np.swapaxes(a, 1, 2) * 0.01
+    vm = RG.build_voxelmap(make_frame(pts, covs), res)
+    ref = O.build_voxelmap(pts, covs, res)
+    assert vm.counts.max() >= (96 if res >= 2.0 else 16)
+    assert np.array_equal(vm.keys, ref[1]) and np.array_equal(vm.counts, ref[4])
+    assert np.array_equal(vm.means, ref[2]) and np.array_equal(vm.covs, ref[3])
+
+
 def test_build_voxelmap_requires_covs_and_handles_empty():
     with pytest.raises(ValueError):
         RG.build_voxelmap(make_frame(np.zeros((3, 3))), 1.0)
