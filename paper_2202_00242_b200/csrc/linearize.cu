@@ -474,15 +474,44 @@ __device__ __forceinline__ void q_matrix(Quat q, double* R) {
 #undef A_
 #undef S_
 
-__global__ void k_compose(FactorDev* __restrict__ factors, int F, const double* __restrict__ poses,
-                          ItemHdr* __restrict__ hdrs) {
+// One thread composes one factor's T_ij; the 12 doubles are then stored warp-cooperatively
+// (staged in shared memory, 32 lanes writing contiguous 8 B words of ~3 records per store) so
+// the factor table and item headers take ~3x fewer L2 sectors per store than per-thread
+// 96 B writes (r02 ncu of the per-thread version: lg_throttle 24% + drain 30% of stalls).
+__device__ __forceinline__ void compose_T(const double* __restrict__ pi,
+                                          const double* __restrict__ pj, double* T);
+constexpr int kComposeThreads = 128;
+__global__ void __launch_bounds__(kComposeThreads)
+    k_compose(FactorDev* __restrict__ factors, int F, const double* __restrict__ poses,
+              ItemHdr* __restrict__ hdrs) {
+  __shared__ double sT[kComposeThreads][13];
   const int fi = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, wbase = fi - lane;
+  double* T = sT[threadIdx.x];
   pdl_release();
   pdl_wait();  // the previous step's K5 still reads T_ij
-  if (fi >= F) return;
-  FactorDev& f = factors[fi];
-  const double* pi = poses + 8 * (size_t)f.var_source;
-  const double* pj = poses + 8 * (size_t)f.var_target;
+  // (item_begin, item_count, var_source, var_target): one 16 B load
+  const int4 meta =
+      fi < F ? *reinterpret_cast<const int4*>(&factors[fi].item_begin) : make_int4(0, 0, 0, 0);
+  if (fi < F) compose_T(poses + 8 * (size_t)meta.z, poses + 8 * (size_t)meta.w, T);
+  __syncwarp();
+  const int nw = min(32, F - wbase);  // factors in this warp
+  for (int e = lane; e < 12 * 32; e += 32) {
+    const int j = e / 12, q = e - 12 * j;
+    const int ib = __shfl_sync(0xffffffffu, meta.x, j);
+    if (j < nw) {
+      const double v = sT[threadIdx.x - lane + j][q];
+      factors[wbase + j].T[q] = v;
+      hdrs[ib].T[q] = v;
+    }
+  }
+  if (fi < F)  // factors split into several items (> 1,024 source points): rare
+    for (int it = 1; it < meta.y; ++it)
+      for (int q = 0; q < 12; ++q) hdrs[meta.x + it].T[q] = T[q];
+}
+
+__device__ __forceinline__ void compose_T(const double* __restrict__ pi,
+                                          const double* __restrict__ pj, double* T) {
   // pose_inverse(t_j): rotation inverse (renormalised by the constructor), t = -R^-1 t_j
   Quat qj = q_normalize(Quat{-pj[0], -pj[1], -pj[2], pj[3]});
   double tj[3] = {pj[4], pj[5], pj[6]}, tinv[3];
@@ -495,12 +524,10 @@ __global__ void k_compose(FactorDev* __restrict__ factors, int F, const double* 
   Quat q = q_normalize(q_mul(qj, qi));
   double ti[3] = {pi[4], pi[5], pi[6]}, tt[3];
   q_apply(qj, ti, tt);
-  q_matrix(q, f.T);
-  f.T[9] = __dadd_rn(tt[0], tinv[0]);
-  f.T[10] = __dadd_rn(tt[1], tinv[1]);
-  f.T[11] = __dadd_rn(tt[2], tinv[2]);
-  for (int it = 0; it < f.item_count; ++it)
-    for (int q = 0; q < 12; ++q) hdrs[f.item_begin + it].T[q] = f.T[q];
+  q_matrix(q, T);
+  T[9] = __dadd_rn(tt[0], tinv[0]);
+  T[10] = __dadd_rn(tt[1], tinv[1]);
+  T[11] = __dadd_rn(tt[2], tinv[2]);
 }
 
 __global__ void k_spread_T(const FactorDev* __restrict__ factors, int F, ItemHdr* __restrict__ hdrs) {
@@ -629,7 +656,7 @@ int launch_terms(vg_ctx* ctx, const CloudView& cv, const MapView& mv, const doub
 
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev) {
   if (b->F == 0) return 0;
-  VG_CUDA(launch_pdl(k_compose, dim3(grid_for(b->F, 128, 1 << 30)), dim3(128), 0, ctx->stream,
+  VG_CUDA(launch_pdl(k_compose, dim3(grid_for(b->F, kComposeThreads, 1 << 30)), dim3(kComposeThreads), 0, ctx->stream,
                      b->factors, (int)b->F, poses_dev, b->hdrs));
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
