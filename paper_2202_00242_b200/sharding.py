@@ -80,3 +80,12 @@ def reduce_normal_equations(flat, dst: int = 0) -> None:
     import torch.distributed as dist
 
     dist.reduce(flat, dst, op=dist.ReduceOp.SUM)
+
+
+def allreduce_cost(cost_count) -> None:
+    """Cost-only pass (LM candidate steps, factor_graph.py:591; total_cost :472-474): every
+    rank's gated (cost, factor count) pair summed on all ranks (in place, 2 scalars).  With
+    a fixed rank count the sum order is fixed, so repeated passes are bit-identical."""
+    import torch.distributed as dist
+
+    dist.all_reduce(cost_count, op=dist.ReduceOp.SUM)

@@ -171,3 +171,56 @@ def test_global_pairs_layout():
     vt = np.array([1, 0, 0, 9, 2, 3])
     unary = np.array([False, False, False, False, False, True])
     assert sharding.global_pairs(vs, vt, unary, 4).tolist() == [[0, 1], [0, 2]]
+
+
+def _gated_cost(srcs, maps, pairs, table, ids):
+    """Per-factor cost with the inlier gate (factor_graph.py:271-275), summed in factor order."""
+    R, t = O.relative_transforms(table, pairs[ids, 0], pairs[ids, 1])
+    c = n = 0.0
+    for k, f in enumerate(ids):
+        i, j = pairs[f]
+        cost, inl = O.matching_cost(srcs[i][0], srcs[i][1], maps[j], R[k], t[k])
+        if inl >= O.MIN_INLIERS:
+            c += cost
+            n += 1
+    return c, n
+
+
+def _cost_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    srcs, maps, pairs, table = _graph()
+    shards = sharding.lpt_shards(np.array([len(srcs[i][0]) for i in pairs[:, 0]]), world)
+    poses = torch.from_numpy(table.copy()) if rank == 0 else torch.zeros(table.shape,
+                                                                         dtype=torch.float64)
+    sharding.broadcast_poses(poses, 0)
+    runs = []
+    for _ in range(2):  # repeated passes are bit-identical
+        cc = torch.tensor(_gated_cost(srcs, maps, pairs, poses.numpy(), shards[rank]),
+                          dtype=torch.float64)
+        sharding.allreduce_cost(cc)
+        runs.append(cc.numpy().copy())
+    ref = _gated_cost(srcs, maps, pairs, table, np.arange(len(pairs)))
+    q.put((rank, runs[0].tolist(), bool(np.array_equal(runs[0], runs[1])), list(ref)))
+    dist.destroy_process_group()
+
+
+def test_two_rank_cost_allreduce_matches_single_process():
+    """Cost-only LM passes: each rank's gated shard cost, all-reduced (2 scalars), equals the
+    single-process total on every rank (count exactly, cost to fp64 reassociation)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cost_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, (c, n), repeat_equal, (rc, rn) in got:
+        assert repeat_equal
+        assert n == rn and n > 0
+        assert abs(c - rc) <= 1e-12 * abs(rc)
+    assert got[0][1] == got[1][1]  # every rank holds the same total
