@@ -52,9 +52,9 @@ def parse():
 
 
 def traffic_record():
-    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01d_traffic.json,
-    written by tools/launch_traffic.py from profiles/r01d_launches.csv)."""
-    p = ROOT / "profiles" / "r01d_traffic.json"
+    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01e_traffic.json,
+    written by tools/launch_traffic.py from profiles/r01e_launches.csv)."""
+    p = ROOT / "profiles" / "r01e_traffic.json"
     try:
         return int(json.loads(p.read_text())["dram_bytes_per_launch"])
     except Exception:
