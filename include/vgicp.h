@@ -156,6 +156,15 @@ int vg_batch_linearize(vg_batch* batch, const double* T_host, int mode, double* 
 int vg_batch_linearize_poses(vg_batch* batch, const double* poses_host, int64_t num_poses,
                              int mode, double* out_host);
 
+/* correspondence rows of every factor at the pose table (GaussianVoxelMap.lookup of the moved
+ * source points, registration.py:47-55,149): rows_out holds sum(n_f) int64 in factor (spec)
+ * order, factor f's n_f points contiguous, the reference row of each hit or -1; inliers_out
+ * (F) the hit count per factor (MatchTerms.inliers, :157).  Runs K-compose and the very K4a
+ * launch the linearization runs, then scatters its compacted (point, record) hit lists: the
+ * correspondences K4b consumes, exported for bit-exact checking. */
+int vg_batch_lookup_rows(vg_batch* batch, const double* poses_host, int64_t num_poses,
+                         int64_t* rows_out, int64_t* inliers_out);
+
 /* device-resident variant: all pointers are device pointers on ctx's device; no host sync.
  * poses_dev may be NULL to reuse the poses of the previous call. */
 int vg_batch_linearize_poses_device(vg_batch* batch, const double* poses_dev,

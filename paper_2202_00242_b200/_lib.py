@@ -81,6 +81,7 @@ _SIGNATURES = {
     "vg_batch_linearize": ([c_void_p, _P_D, c_int, _P_D], c_int),
     "vg_batch_linearize_poses": ([c_void_p, _P_D, c_int64, c_int, _P_D], c_int),
     "vg_batch_linearize_poses_device": ([c_void_p, c_void_p, c_int64, c_int, c_void_p], c_int),
+    "vg_batch_lookup_rows": ([c_void_p, _P_D, c_int64, _P_I64, _P_I64], c_int),
     "vg_batch_compose_device": ([c_void_p, c_void_p, c_int64], c_int),
     "vg_batch_accumulate_device": ([c_void_p, c_int], c_int),
     "vg_batch_finalize_device": ([c_void_p, c_int, c_void_p], c_int),
@@ -325,6 +326,16 @@ class DeviceBatch:
                                                     int(mode), dptr(out)),
               "vg_batch_linearize_poses")
         return out
+
+    def lookup_rows(self, poses: np.ndarray):
+        """(rows, inliers): every factor's per-point reference row (-1 = miss), concatenated
+        in factor order, and its hit count — the correspondences K4a hands to K4b."""
+        poses = f64(poses).reshape(-1, 8)
+        rows = np.empty(self.num_points, dtype=np.int64)
+        inl = np.empty(self.num_factors, dtype=np.int64)
+        check(self.ctx.lib.vg_batch_lookup_rows(self.handle, dptr(poses), poses.shape[0],
+                                                iptr(rows), iptr(inl)), "vg_batch_lookup_rows")
+        return rows, inl
 
     def linearize_poses_device(self, poses_dev_ptr: int | None, num_poses: int, mode: int,
                                out_dev_ptr: int) -> None:

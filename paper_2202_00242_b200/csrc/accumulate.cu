@@ -776,3 +776,36 @@ int launch_accumulate_range_ev(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int 
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode) {
   return launch_accumulate_range(ctx, b, kmode, 0, (int)b->num_items);
 }
+
+namespace vg {
+// Correspondence export (vg_batch_lookup_rows): the (point, record) hit lists the last K4a
+// pass compacted — exactly what K4b consumes — scattered as the reference row of every hit
+// point (GaussianVoxelMap.lookup's result, registration.py:47-55,149) into the factor's slice
+// of `rows` (pre-filled with -1 = miss).  One warp per item.
+__global__ void k_export_rows(const ItemDev* __restrict__ items, int n_items,
+                              const AccDesc* __restrict__ descs, const int2* __restrict__ hits,
+                              const long long* __restrict__ pt_off,
+                              long long* __restrict__ rows) {
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= n_items) return;
+  const int n = descs[w].n;
+  const int hoff = items[w].hoff;
+  const VoxelRec* recs = descs[w].recs;
+  long long* dst = rows + pt_off[items[w].factor];
+  for (int k = lane; k < n; k += 32) {
+    const int2 h = hits[hoff + k];
+    dst[h.x] = recs[h.y].row;
+  }
+}
+}  // namespace vg
+
+int launch_export_rows(vg_ctx* ctx, vg_batch* b, const long long* pt_off_dev, long long* rows_dev) {
+  if (b->num_items == 0) return 0;
+  const int warps = 4;
+  k_export_rows<<<(int)((b->num_items + warps - 1) / warps), warps * 32, 0, ctx->stream>>>(
+      b->items, (int)b->num_items, b->descs, b->hits, pt_off_dev, rows_dev);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}

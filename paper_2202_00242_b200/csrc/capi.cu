@@ -541,7 +541,10 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     const long long n = specs[f].source->n;
     npts += n;
     fac[f].item_begin = (int)items.size();
-    long long nchunks = std::max<long long>(1, (n + chunk - 1) / chunk);
+    // an empty source gets no work item: its factor sums nothing (zero cost and inliers, as
+    // matching_cost / linearize_from_terms give for an empty frame, registration.py:160-165)
+    // and no kernel ever reads its (unallocated) point arrays
+    const long long nchunks = n == 0 ? 0 : (n + chunk - 1) / chunk;
     for (long long c = 0; c < nchunks; ++c) {
       ItemDev it;
       it.factor = (int)f;
@@ -566,6 +569,8 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   b->num_maps = (int)maps.size();
   b->max_var = (int)max_var;
   b->host_factors = fac;
+  b->pt_off.assign(F + 1, 0);
+  for (int64_t f = 0; f < F; ++f) b->pt_off[f + 1] = b->pt_off[f] + specs[f].source->n;
   b->all_covs = all_covs;
   b->stages = S;
   b->stage_factors = stage_factors;
@@ -796,6 +801,10 @@ int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_
 
 static int ensure_poses(vg_batch* b, int64_t V) {
   if (V > b->pose_cap) {
+    // the small-batch host graph has b->poses baked in: it must not outlive the buffer
+    if (b->hgraph) cudaGraphExecDestroy(b->hgraph);
+    b->hgraph = nullptr;
+    b->hgraph_V = -1;
     dfree(b->ctx, b->poses);
     VG_CHECK(dalloc(b->ctx, &b->poses, 8 * (size_t)V));
     b->pose_cap = V;
@@ -879,6 +888,34 @@ int vg_batch_linearize_poses_device(vg_batch* b, const double* poses_dev, int64_
     VG_CHECK(launch_compose(b->ctx, b, poses_dev));
   }
   return run_device(b, mode, out_dev);
+}
+
+int vg_batch_lookup_rows(vg_batch* b, const double* poses_host, int64_t V, int64_t* rows_out,
+                         int64_t* inliers_out) {
+  if (!b || (b->F && (!poses_host || !rows_out || !inliers_out)))
+    return fail(VG_ERR_INVALID, "null argument");
+  if (b->F == 0) return VG_OK;
+  if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  vg_ctx* ctx = b->ctx;
+  const long long npts = b->pt_off[b->F];
+  DeviceTemps temps(ctx->stream);
+  long long *d_off = nullptr, *d_rows = nullptr;
+  VG_CUDA(temps.alloc(&d_off, (size_t)b->F + 1));
+  VG_CUDA(temps.alloc(&d_rows, (size_t)std::max(npts, 1LL)));
+  VG_CHECK(h2d(ctx, d_off, b->pt_off.data(), sizeof(long long) * (b->F + 1)));
+  VG_CUDA(cudaMemsetAsync(d_rows, 0xff, sizeof(long long) * (size_t)npts, ctx->stream));
+  VG_CHECK(ensure_poses(b, V));
+  VG_CHECK(h2d(ctx, b->poses, poses_host, sizeof(double) * 8 * V));
+  VG_CHECK(launch_compose(ctx, b, b->poses));
+  // the same K4a launch the linearization runs (VG_MODE_INLIERS stops after it), then K5
+  VG_CHECK(launch_accumulate(ctx, b, kmode_of(VG_MODE_INLIERS)));
+  VG_CHECK(launch_export_rows(ctx, b, d_off, d_rows));
+  VG_CHECK(launch_finalize(ctx, b, VG_MODE_INLIERS, b->out));
+  std::vector<double> rec(2 * (size_t)b->F);
+  if (npts) VG_CUDA(cudaMemcpyAsync(rows_out, d_rows, sizeof(long long) * npts, cudaMemcpyDeviceToHost, ctx->stream));
+  VG_CHECK(d2h_sync(ctx, rec.data(), b->out, sizeof(double) * rec.size()));
+  for (int64_t f = 0; f < b->F; ++f) inliers_out[f] = (int64_t)rec[2 * f + 1];
+  return VG_OK;
 }
 
 int vg_batch_compose_device(vg_batch* b, const double* poses_dev, int64_t V) {

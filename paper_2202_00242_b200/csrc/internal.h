@@ -137,6 +137,8 @@ struct vg_batch {
   double* h_poses = nullptr;
   double* h_out = nullptr;
   std::vector<vg::FactorDev> host_factors;
+  std::vector<long long> pt_off;      // F + 1: first point of each factor in spec order
+                                      // (vg_batch_lookup_rows output layout)
   // normal-equation assembly (vg_batch_assemble_*): CSR of contributions per output unit
   long long asm_vars = -1;            // variables (pose-table rows < asm_vars); -1: not set up
   long long asm_pairs_n = 0;
@@ -236,6 +238,8 @@ int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
 int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1);
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev);  // K6
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi);  // K4a + K4b
+// scatter the last K4a pass's hit lists as reference rows (vg_batch_lookup_rows)
+int launch_export_rows(vg_ctx* ctx, vg_batch* b, const long long* pt_off_dev, long long* rows_dev);
 // the same, recording `after_lookup` on ctx->stream between K4a and K4b
 int launch_accumulate_range_ev(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi,
                                cudaEvent_t after_lookup);

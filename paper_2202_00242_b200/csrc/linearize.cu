@@ -499,10 +499,11 @@ __global__ void __launch_bounds__(kComposeThreads)
   for (int e = lane; e < 12 * 32; e += 32) {
     const int j = e / 12, q = e - 12 * j;
     const int ib = __shfl_sync(0xffffffffu, meta.x, j);
+    const int ic = __shfl_sync(0xffffffffu, meta.y, j);
     if (j < nw) {
       const double v = sT[threadIdx.x - lane + j][q];
       factors[wbase + j].T[q] = v;
-      hdrs[ib].T[q] = v;
+      if (ic > 0) hdrs[ib].T[q] = v;  // empty sources have no item
     }
   }
   if (fi < F)  // factors split into several items (> 1,024 source points): rare

@@ -157,22 +157,33 @@ def d2d_error(point: Gaussian3, voxel: Gaussian3, t_ij):
     """Single-pair distribution-to-distribution error (registration.py:101-110).
 
     Evaluated on the GPU as a one-point factor so it exercises the same arithmetic as the
-    batched kernel.  Returns (error, residual, weight).
+    batched kernel.  Returns (error, residual, weight) for any input, like the reference.
+
+    The voxel is placed in every cell of the 3x3x3 block around the host-transformed point,
+    so the device transform (a different FMA order, so possibly one ulp away across a cell
+    face) lands in a cell carrying it; the resolution is a power of two large enough that the
+    21-bit packed key never wraps (|moved| < 2^18 res).
     """
     frame = Frame(points=np.asarray(point.mean, float).reshape(1, 3), stamps=np.zeros(1),
                   stamp=0.0, covs=np.asarray(point.cov, float).reshape(1, 3, 3), deskewed=True)
     rmat = t_ij.rotation.matrix()
     moved = rmat @ np.asarray(point.mean, float) + t_ij.translation
-    res = 1.0
-    # a single-cell map placed around the transformed point
-    idx = np.floor(moved / res).astype(np.int64) + (1 << 20)
-    key = np.array([(idx[0] << 42) | (idx[1] << 21) | idx[2]], dtype=np.int64)
-    vmap = GaussianVoxelMap(res, key, np.asarray(voxel.mean, float).reshape(1, 3),
-                            np.asarray(voxel.cov, float).reshape(1, 3, 3),
-                            np.ones(1, dtype=np.int64))
+    big = float(np.max(np.abs(moved)))
+    if not np.isfinite(big):
+        raise ValueError("d2d_error: non-finite transformed point")
+    res = 1.0 if big < 2.0 ** 18 else 2.0 ** int(np.ceil(np.log2(big / 2.0 ** 18)))
+    base = np.floor(moved / res).astype(np.int64)
+    off = np.stack(np.meshgrid([-1, 0, 1], [-1, 0, 1], [-1, 0, 1], indexing="ij"),
+                   axis=-1).reshape(27, 3)
+    idx = base + off + (1 << 20)
+    keys = np.sort((idx[:, 0] << 42) | (idx[:, 1] << 21) | idx[:, 2])
+    vmap = GaussianVoxelMap(res, keys,
+                            np.broadcast_to(np.asarray(voxel.mean, float), (27, 3)).copy(),
+                            np.broadcast_to(np.asarray(voxel.cov, float), (27, 3, 3)).copy(),
+                            np.ones(27, dtype=np.int64))
     terms = match_terms(frame, vmap, t_ij)
-    if terms.inliers != 1:
-        raise ValueError("d2d_error: point did not land in its own voxel")
+    if terms.inliers != 1:  # cannot happen: the block covers every rounding of the transform
+        raise RuntimeError("d2d_error: transformed point left its voxel block")
     return float(terms.cost), terms.d[0], terms.weight[0]
 
 

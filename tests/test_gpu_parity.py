@@ -697,3 +697,169 @@ def test_configs_3_and_4_full_size_sample_vs_oracle(name):
         assert_lin(RG.unpack_record(host[f], bool(wl.unary[f])), ref, bool(wl.unary[f]))
         checked += 1
     assert checked >= 7
+
+
+# ---- round 2: ADVICE regressions ------------------------------------------------------------
+
+def test_empty_source_inside_a_batch(small_graph):
+    """A factor whose source cloud has no points gets no work item (its point arrays are never
+    read): zero record, and its neighbours in the batch are unaffected — also when the empty
+    factor is the last one (K-compose must not write a header past the item table)."""
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    empty = _lib.DeviceCloud(np.zeros((0, 3)), np.zeros((0, 3, 3)))
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs[:3]]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans[:3], covs[:3])]
+    table = np.array([G.pose_row(p) for p in est[:3]])
+    solo = _lib.DeviceBatch([clouds[0], clouds[1]], [dmaps[1], dmaps[0]], [False] * 2, [10] * 2,
+                            [0, 1], [1, 0]).linearize_poses(table)
+    for order in ([empty, clouds[0], clouds[1]], [clouds[0], clouds[1], empty]):
+        maps_ = [dmaps[2] if c is empty else (dmaps[1] if c is clouds[0] else dmaps[0])
+                 for c in order]
+        vs = [2 if c is empty else (0 if c is clouds[0] else 1) for c in order]
+        vt = [0 if c is empty else (1 if c is clouds[0] else 0) for c in order]
+        b = _lib.DeviceBatch(order, maps_, [False] * 3, [10] * 3, vs, vt)
+        for mode in (_lib.MODE_LINEARIZE, _lib.MODE_COST, _lib.MODE_INLIERS):
+            out = b.linearize_poses(table, mode)
+            k = [i for i, c in enumerate(order) if c is empty][0]
+            assert np.all(out[k] == 0.0)
+            if mode == _lib.MODE_LINEARIZE:
+                rest = [i for i in range(3) if i != k]
+                assert np.array_equal(out[rest], solo)
+        rows, inl = b.lookup_rows(table)
+        assert inl[[i for i, c in enumerate(order) if c is empty][0]] == 0
+
+
+def test_small_host_graph_survives_pose_table_growth(small_graph):
+    """The small-batch host path replays a graph with the batch's pose buffer baked in; a call
+    with a larger pose table reallocates that buffer and must retire the graph."""
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs[:2]]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans[:2], covs[:2])]
+    b = _lib.DeviceBatch(clouds, [dmaps[1], dmaps[0]], [False] * 2, [10] * 2, [0, 1], [1, 0])
+    small = np.array([G.pose_row(p) for p in est[:2]])
+    first = b.linearize_poses(small)            # captures the host graph at V = 2
+    big = np.vstack([small, np.array([G.pose_row(p) for p in est[2:12]])])
+    rows_big, _ = b.lookup_rows(big)             # V = 12: reallocates the pose buffer
+    junk = torch_junk_allocations()
+    again = b.linearize_poses(small)             # must not replay against the freed buffer
+    assert np.array_equal(first, again)
+    del junk
+
+
+def torch_junk_allocations():
+    """Device allocations that would land in a freed pool block (makes a stale-pointer replay
+    read garbage instead of stale-but-equal data)."""
+    import torch
+
+    return [torch.full((4096,), float("nan"), dtype=torch.float64, device="cuda")
+            for _ in range(8)]
+
+
+def test_d2d_error_matches_reference_formula_anywhere():
+    """d2d_error (registration.py:101-110) returns (error, d, W) for any input — points on a
+    voxel face, far-away points (|x| >= 2^20 m would wrap a 1 m key) — matching the reference's
+    np.linalg.inv formula within the parity bar."""
+    rng = np.random.default_rng(5)
+    cases = [np.array([0.0, 0.0, 0.0]), np.array([1.0, -2.0, 3.0]), np.array([0.5, 0.25, -7.0]),
+             np.array([2.0 ** 21 + 0.5, 3.0, -1.0]), rng.normal(size=3) * 100]
+    for mean in cases:
+        cov_p = np.diag(rng.uniform(0.01, 0.1, 3))
+        cov_v = np.diag(rng.uniform(0.01, 0.1, 3))
+        for tij in (G.Se3Pose.identity(), G.Se3Pose(G.so3_exp([0.1, -0.2, 0.3]), [0.25, 0.5, 0.0])):
+            p = G.Gaussian3(mean, cov_p)
+            v = G.Gaussian3(tij.rotation.matrix() @ mean + tij.translation + [0.01, -0.02, 0.03],
+                            cov_v)
+            err, d, w = RG.d2d_error(p, v, tij)
+            R = tij.rotation.matrix()
+            d_ref = v.mean - (R @ mean + tij.translation)
+            w_ref = np.linalg.inv(cov_v + R @ cov_p @ R.T)
+            assert_tol(d, d_ref, "d")
+            assert_tol(w, w_ref, "W")
+            assert_tol(err, d_ref @ w_ref @ d_ref, "error")
+
+
+# ---- round 2: the headline workload's correspondences, every factor -------------------------
+
+def _oracle_rows_by_target(wl, R, t):
+    """Vectorised oracle lookup (registration.py:47-55,149: searchsorted over the sorted packed
+    keys of np.unique) for every factor of the workload, grouped by target submap; returns
+    the concatenated rows in factor order and the count of points whose transformed
+    coordinate lies within 1e-12 (relative, in cells) of a voxel face."""
+    F = len(wl.pairs)
+    n = np.array([len(wl.source_index[i]) for i in wl.pairs[:, 0]])
+    off = np.concatenate([[0], np.cumsum(n)])
+    rows = np.empty(off[-1], np.int64)
+    near = 0
+    res = wl.resolution
+    by_target = np.argsort(wl.pairs[:, 1], kind="stable")
+    bounds = np.flatnonzero(np.r_[True, np.diff(wl.pairs[by_target, 1]) != 0, True])
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        fids = by_target[a:b]
+        j = wl.pairs[fids[0], 1]
+        keys = np.unique(O.pack_voxel_keys(wl.scans[j], res))
+        pts = [wl.scans[i][wl.source_index[i]] for i in wl.pairs[fids, 0]]
+        owner = np.repeat(np.arange(len(fids)), [len(p) for p in pts])
+        P = np.concatenate(pts)
+        moved = np.einsum("nij,nj->ni", R[fids][owner], P) + t[fids][owner]
+        q = moved / res
+        frac = q - np.floor(q)
+        near += int(np.sum((frac < 1e-12 * np.maximum(1.0, np.abs(q))) |
+                           (1.0 - frac < 1e-12 * np.maximum(1.0, np.abs(q)))))
+        qk = O.pack_voxel_keys(moved, res)
+        pos = np.minimum(np.searchsorted(keys, qk), len(keys) - 1)
+        r = np.where(keys[pos] == qk, pos, -1)
+        start = 0
+        for f, p in zip(fids, pts):
+            rows[off[f]:off[f + 1]] = r[start:start + len(p)]
+            start += len(p)
+        assert start == len(P)
+    return rows, off, near
+
+
+def test_config5_every_factor_rows_and_inliers_bit_exact(config5):
+    """north_star: correspondence indices and inlier counts bit-exact at the size the headline
+    is quoted on — all 50,000 factors, 19.9M correspondences, straight from the K4a hit lists
+    K4b consumes (vg_batch_lookup_rows) — plus the linearization records' inlier counts."""
+    wl = config5
+    batch = wl.batch()
+    table = wl.pose_table
+    rows, inl = batch.lookup_rows(table)
+    R, t = O.relative_transforms(table, wl.pairs[:, 0], wl.pairs[:, 1])
+    ref_rows, off, near = _oracle_rows_by_target(wl, R, t)
+    print(f"config 5: {len(ref_rows)} correspondences, {int((ref_rows >= 0).sum())} hits, "
+          f"{near} near a voxel face")
+    assert near == 0
+    assert len(rows) == len(ref_rows) == wl.num_points
+    assert np.array_equal(rows, ref_rows)
+    ref_inl = np.add.reduceat((ref_rows >= 0).astype(np.int64), off[:-1])
+    assert np.array_equal(inl, ref_inl)
+    rec = batch.linearize_poses(table)
+    assert np.array_equal(rec[:, 91].astype(np.int64), ref_inl)
+    cost = batch.linearize_poses(table, _lib.MODE_COST)
+    assert np.array_equal(cost[:, 1].astype(np.int64), ref_inl)
+
+
+def test_config5_blocks_of_600_factors_vs_oracle(config5):
+    """H/b/cost of every factor of 12 seeded target submaps (~600 factors of the headline
+    workload) within 1e-4 rel / 1e-6 abs of the fp64 oracle; gated factors gate in both."""
+    wl = config5
+    batch = wl.batch()
+    table = wl.pose_table
+    host = batch.linearize_poses(table)
+    rng = np.random.default_rng(56)
+    targets = rng.choice(wl.n_submaps, 12, replace=False)
+    fids = np.flatnonzero(np.isin(wl.pairs[:, 1], targets))
+    R, t = O.relative_transforms(table, wl.pairs[fids, 0], wl.pairs[fids, 1])
+    maps = {int(j): O.build_voxelmap(wl.scans[j], wl.scan_covs[j], wl.resolution) for j in targets}
+    gated = 0
+    for k, f in enumerate(fids):
+        i, j = wl.pairs[f]
+        sel = wl.source_index[i]
+        try:
+            ref = O.linearize(wl.scans[i][sel], wl.scan_covs[i][sel], maps[int(j)], R[k], t[k])
+        except ValueError:
+            assert host[f][91] < 10 and np.all(host[f][:90] == 0)
+            gated += 1
+            continue
+        assert_lin(RG.unpack_record(host[f], False), ref, False)
+    assert len(fids) >= 500 and gated < len(fids) // 4
