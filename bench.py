@@ -82,7 +82,9 @@ def hbm_peak():
 
 
 class ClockSampler:
-    """SM clocks + throttle reasons sampled (NVML, every ~2 ms) during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region: NVML is initialised and
+    sampled once before the region starts (so a short region still has samples), then every
+    ~2 ms on a thread, then once more at the end; nvidia-smi is the fallback."""
 
     REASONS = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
                0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -91,44 +93,68 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.errors = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._h = None
+        self._nvml = None
 
-    def _run(self):
+    def _init_nvml(self):
         try:
             import pynvml
 
             pynvml.nvmlInit()
-            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            while not self._stop.is_set():
-                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                act = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.samples.append((float(sm), float(smax), int(act)))
-                self._stop.wait(0.002)
-        except Exception as exc:  # no NVML: fall back to one nvidia-smi query
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._smax = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            get = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                getattr(pynvml, "nvmlDeviceGetCurrentClocksThrottleReasons")
+            self._reasons = get
+            self._nvml = pynvml
+        except Exception as exc:  # noqa: BLE001
+            self.errors.append(f"nvml: {exc!r}")
+
+    def _sample(self):
+        if self._nvml is not None:
+            try:
+                sm = self._nvml.nvmlDeviceGetClockInfo(self._h, self._nvml.NVML_CLOCK_SM)
+                self.samples.append((float(sm), self._smax, int(self._reasons(self._h))))
+                return
+            except Exception as exc:  # noqa: BLE001
+                self.errors.append(f"nvml sample: {exc!r}")
+                self._nvml = None
+        for field in ("clocks_event_reasons.active", "clocks_throttle_reasons.active"):
             try:
                 out = subprocess.run(
                     ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
-                     "clocks_event_reasons.active", "--format=csv,noheader,nounits"],
+                     + field, "--format=csv,noheader,nounits"],
                     capture_output=True, text=True, timeout=10).stdout
                 sm, smax, act = [x.strip() for x in out.strip().split(",")]
                 self.samples.append((float(sm), float(smax), int(act, 16)))
-            except Exception:
-                self.error = repr(exc)
+                return
+            except Exception as exc:  # noqa: BLE001
+                self.errors.append(f"nvidia-smi {field}: {exc!r}")
+
+    def _run(self):
+        while not self._stop.wait(0.002):
+            self._sample()
+            if self._nvml is None:  # nvidia-smi is slow: sample sparsely
+                self._stop.wait(0.2)
 
     def __enter__(self):
+        self._init_nvml()
+        self._sample()
         self._t.start()
-        time.sleep(0.01)
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        self._sample()
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "errors": self.errors[:4]}
         reasons = set()
         for _, _, act in self.samples:
             for bit, name in self.REASONS.items():
@@ -136,7 +162,8 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
                 "sm_max_mhz": max(s[1] for s in self.samples),
-                "reasons": sorted(reasons), "samples": len(self.samples)}
+                "reasons": sorted(reasons), "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 def dist_setup(args):
@@ -296,22 +323,33 @@ def run_ours(args):
     value = total_points * args.steps / (total_ms / 1e3)
 
     # ---- e2e: through the public batch API with host buffers (H2D poses, D2H records) ----
+    # headline: the compact record (vg_batch_linearize_poses_f32: fp32 H/b blocks, fp64 cost,
+    # int32 inliers; 376 B/factor) into pinned host memory; the fp64 record (736 B/factor)
+    # is reported beside it
     poses_host = torch.from_numpy(wl.pose_table.copy()).pin_memory()
     out_host = torch.empty((F_max, REC), dtype=torch.float64).pin_memory()
+    out32_host = torch.empty((F_max, _lib.REC_LINEARIZE_F32), dtype=torch.float32).pin_memory()
     ne_host = (torch.empty(batch.asm_size, dtype=torch.float64).pin_memory()
                if world > 1 else None)
-    e2e_ms = []
+    e2e_ms, e2e64_ms = [], []
     if world == 1:
         out_np = out_host.numpy()
+        out32_np = out32_host.numpy()
         poses_np = poses_host.numpy()
+        for k in range(args.e2e_steps + 2):
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            batch.linearize_poses_f32(poses_np, out=out32_np)
+            if k >= 2:
+                e2e_ms.append((time.perf_counter() - a) * 1e3)
         for k in range(args.e2e_steps + 2):
             torch.cuda.synchronize()
             a = time.perf_counter()
             batch.linearize_poses(poses_np, _lib.MODE_LINEARIZE, out=out_np)
             if k >= 2:
-                e2e_ms.append((time.perf_counter() - a) * 1e3)
+                e2e64_ms.append((time.perf_counter() - a) * 1e3)
         h2d = poses_host.numel() * 8
-        d2h = F_r * REC * 8
+        d2h = F_r * _lib.REC_LINEARIZE_F32 * 4
     else:
         for k in range(args.e2e_steps + 2):
             torch.cuda.synchronize()
@@ -331,6 +369,34 @@ def run_ours(args):
         h2d = poses_host.numel() * 8
         d2h = batch.asm_size * 8
     e2e_value = total_points / (statistics.median(e2e_ms) / 1e3)
+    e2e64_line = None
+    if e2e64_ms:
+        e2e64_line = {"value": total_points / (statistics.median(e2e64_ms) / 1e3), "unit": UNIT,
+                      "h2d_bytes_per_step": int(poses_host.numel() * 8),
+                      "d2h_bytes_per_step": int(F_r * REC * 8),
+                      "ms_per_step": statistics.median(e2e64_ms),
+                      "api": "DeviceBatch.linearize_poses (vg_batch_linearize_poses, fp64 records)"}
+
+    # ---- cost-only pass (LM candidate steps, factor_graph.py:591): the same correspondences,
+    # no accumulators, 2 values per factor ----
+    cost_line = None
+    if world == 1:
+        cost_dev = torch.zeros((F_max, 2), dtype=torch.float64, device="cuda")
+        cs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ce = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        for k in range(3):
+            batch.linearize_poses_device(poses_dev.data_ptr(), V, _lib.MODE_COST,
+                                         cost_dev.data_ptr())
+        for k in range(args.steps):
+            flush.zero_()
+            cs[k].record()
+            batch.linearize_poses_device(poses_dev.data_ptr(), V, _lib.MODE_COST,
+                                         cost_dev.data_ptr())
+            ce[k].record()
+        torch.cuda.synchronize()
+        cms = sum(a.elapsed_time(b) for a, b in zip(cs, ce)) / args.steps
+        cost_line = {"value": total_points / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
+                     "api": "vg_batch_linearize_poses_device(VG_MODE_COST)"}
 
     # ---- e2e of the normal equations: the same linearization, summed into
     # the block-sparse H/g on the device, only the system crosses PCIe ----
@@ -380,7 +446,12 @@ def run_ours(args):
                        "setup_s": round(setup_s, 2)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "ms_per_step": statistics.median(e2e_ms)},
+                    "ms_per_step": statistics.median(e2e_ms),
+                    "api": ("DeviceBatch.linearize_poses_f32 (vg_batch_linearize_poses_f32: "
+                            "fp32 H/b blocks, fp64 cost, int32 inliers) into pinned memory"
+                            if world == 1 else "normal equations reduced to the solver rank")},
+            "e2e_f64_records": e2e64_line,
+            "cost_mode": cost_line,
             "e2e_normal_equations": ne_line,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -46,6 +46,11 @@ extern "C" {
 #define VG_REC_LINEARIZE 92
 #define VG_REC_COST 2
 #define VG_REC_COMPACT 29
+/* compact host record of VG_MODE_LINEARIZE (the *_f32 entry points), 94 4-byte words:
+ * words 0-89 the blocks H_ii(21) H_ij(36) H_jj(21) b_i(6) b_j(6) in fp32 (the north_star's
+ * fp32 H/b, each within 1e-4 rel / 1e-6 abs of the fp64 reference), words 90-91 the cost as
+ * fp64 (low word first), word 92 the inlier count (int32), word 93 zero padding. */
+#define VG_REC_LINEARIZE_F32 94
 
 /* factor flags */
 #define VG_FACTOR_UNARY 1 /* target pose fixed (factor_graph.py:219-245) */
@@ -151,10 +156,23 @@ int vg_batch_destroy(vg_batch* batch);
  * linearize_from_terms (registration.py:146-157,207-248) for every factor. */
 int vg_batch_linearize(vg_batch* batch, const double* T_host, int mode, double* out_host);
 
+/* the same with the compact fp32 record (VG_REC_LINEARIZE_F32 words per factor; mode must be
+ * VG_MODE_LINEARIZE): half the device->host bytes of the fp64 records */
+int vg_batch_linearize_f32(vg_batch* batch, const double* T_host, int mode, float* out_host);
+
 /* pose-table mode: poses V x 8 (quat xyzw, t, pad).  T_ij is composed on the device from
  * var_source / var_target exactly as pose_compose(pose_inverse(t_j), t_i). */
 int vg_batch_linearize_poses(vg_batch* batch, const double* poses_host, int64_t num_poses,
                              int mode, double* out_host);
+
+/* pose-table mode with the compact fp32 record (VG_REC_LINEARIZE_F32 words per factor) */
+int vg_batch_linearize_poses_f32(vg_batch* batch, const double* poses_host, int64_t num_poses,
+                                 int mode, float* out_host);
+
+/* pinned (page-locked) host memory for outputs: device->host copies into it overlap the staged
+ * computation, copies into pageable memory do not */
+int vg_host_alloc(size_t bytes, void** out);
+int vg_host_free(void* ptr);
 
 /* correspondence rows of every factor at the pose table (GaussianVoxelMap.lookup of the moved
  * source points, registration.py:47-55,149): rows_out holds sum(n_f) int64 in factor (spec)

@@ -33,6 +33,7 @@ MODE_COST = 1
 MODE_COMPACT = 2
 MODE_INLIERS = 3
 RECORD_SIZE = {MODE_LINEARIZE: 92, MODE_COST: 2, MODE_COMPACT: 29, MODE_INLIERS: 2}
+REC_LINEARIZE_F32 = 94  # 4-byte words: fp32 blocks (90), fp64 cost (2 words), int32 inliers, pad
 FACTOR_UNARY = 1
 
 
@@ -82,6 +83,10 @@ _SIGNATURES = {
     "vg_batch_linearize_poses": ([c_void_p, _P_D, c_int64, c_int, _P_D], c_int),
     "vg_batch_linearize_poses_device": ([c_void_p, c_void_p, c_int64, c_int, c_void_p], c_int),
     "vg_batch_lookup_rows": ([c_void_p, _P_D, c_int64, _P_I64, _P_I64], c_int),
+    "vg_batch_linearize_f32": ([c_void_p, _P_D, c_int, c_void_p], c_int),
+    "vg_batch_linearize_poses_f32": ([c_void_p, _P_D, c_int64, c_int, c_void_p], c_int),
+    "vg_host_alloc": ([ctypes.c_size_t, _PP], c_int),
+    "vg_host_free": ([c_void_p], c_int),
     "vg_batch_compose_device": ([c_void_p, c_void_p, c_int64], c_int),
     "vg_batch_accumulate_device": ([c_void_p, c_int], c_int),
     "vg_batch_finalize_device": ([c_void_p, c_int, c_void_p], c_int),
@@ -202,6 +207,61 @@ def context(device: int | None = None) -> Context:
     return ctx
 
 
+class _PinnedOwner:
+    """Owner of one page-locked buffer; numpy views of it keep it alive (array interface)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                    "version": 3}
+
+
+class PinnedPool:
+    """Page-locked host buffers (vg_host_alloc) for record outputs.  A device->host copy into
+    pinned memory overlaps the staged computation (vg_batch_linearize*: each stage's records
+    cross PCIe while the next stage computes); into pageable memory it does not.  A buffer
+    goes back to the pool when the last numpy view of it dies, so callers may keep the
+    returned arrays (the factor shim caches per-factor rows of them)."""
+
+    def __init__(self):
+        self._free: dict[int, list[int]] = {}
+        self._lock = threading.Lock()
+
+    def empty(self, shape, dtype=np.float64) -> np.ndarray:
+        lib = load_library()
+        dtype = np.dtype(dtype)
+        nbytes = max(int(np.prod(shape)) * dtype.itemsize, 1)
+        with self._lock:
+            lst = self._free.get(nbytes)
+            ptr = lst.pop() if lst else None
+        if ptr is None:
+            p = c_void_p()
+            check(lib.vg_host_alloc(nbytes, ctypes.byref(p)), "vg_host_alloc")
+            ptr = p.value
+        owner = _PinnedOwner(ptr, nbytes)
+        weakref.finalize(owner, self._release, ptr, nbytes)
+        return np.asarray(owner)[: int(np.prod(shape)) * dtype.itemsize].view(dtype).reshape(shape)
+
+    def _release(self, ptr: int, nbytes: int) -> None:
+        with self._lock:
+            lst = self._free.setdefault(nbytes, [])
+            if len(lst) < 4:
+                lst.append(ptr)
+                return
+        if _lib is not None:
+            _lib.vg_host_free(c_void_p(ptr))
+
+
+PINNED = PinnedPool()
+
+
+def record_cost_inliers_f32(rec: np.ndarray):
+    """(cost, inliers) of compact fp32 linearization records (..., 94) -> fp64, int64."""
+    words = np.ascontiguousarray(rec[..., 90:93])
+    cost = words[..., 0:2].copy().view(np.float64)[..., 0]
+    inl = words[..., 2].view(np.int32).astype(np.int64)
+    return cost, inl
+
+
 class DeviceCloud:
     """Device copy of a Frame's points (+ covariances): 64 B/point SoA in HBM (float4 xyz,
     fp64 covariance rows); non-fp32-exact points keep an extra fp64 xyz copy."""
@@ -312,19 +372,42 @@ class DeviceBatch:
 
     def linearize(self, T: np.ndarray, mode: int = MODE_LINEARIZE) -> np.ndarray:
         T = f64(T).reshape(self.num_factors, 12)
-        out = np.empty((self.num_factors, RECORD_SIZE[mode]))
+        out = PINNED.empty((self.num_factors, RECORD_SIZE[mode]))
         check(self.ctx.lib.vg_batch_linearize(self.handle, dptr(T), int(mode), dptr(out)),
               "vg_batch_linearize")
         return out
 
     def linearize_poses(self, poses: np.ndarray, mode: int = MODE_LINEARIZE,
                         out: np.ndarray | None = None) -> np.ndarray:
+        """Records at the pose table (fp64, RECORD_SIZE[mode] per factor).  Without `out` the
+        result lives in pinned memory, so its staged device->host copies overlap the compute."""
         poses = f64(poses).reshape(-1, 8)
         if out is None:
-            out = np.empty((self.num_factors, RECORD_SIZE[mode]))
+            out = PINNED.empty((self.num_factors, RECORD_SIZE[mode]))
         check(self.ctx.lib.vg_batch_linearize_poses(self.handle, dptr(poses), poses.shape[0],
                                                     int(mode), dptr(out)),
               "vg_batch_linearize_poses")
+        return out
+
+    def linearize_poses_f32(self, poses: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """Compact linearization records (F, 94) float32 words (VG_REC_LINEARIZE_F32): fp32
+        blocks in words 0-89, fp64 cost in 90-91, int32 inliers in 92 — half the PCIe bytes of
+        linearize_poses.  Decode cost/inliers with record_cost_inliers_f32."""
+        poses = f64(poses).reshape(-1, 8)
+        if out is None:
+            out = PINNED.empty((self.num_factors, REC_LINEARIZE_F32), np.float32)
+        assert out.dtype == np.float32 and out.shape == (self.num_factors, REC_LINEARIZE_F32)
+        check(self.ctx.lib.vg_batch_linearize_poses_f32(self.handle, dptr(poses), poses.shape[0],
+                                                        MODE_LINEARIZE, out.ctypes.data),
+              "vg_batch_linearize_poses_f32")
+        return out
+
+    def linearize_f32(self, T: np.ndarray) -> np.ndarray:
+        """Explicit-transform variant of linearize_poses_f32."""
+        T = f64(T).reshape(self.num_factors, 12)
+        out = PINNED.empty((self.num_factors, REC_LINEARIZE_F32), np.float32)
+        check(self.ctx.lib.vg_batch_linearize_f32(self.handle, dptr(T), MODE_LINEARIZE,
+                                                  out.ctypes.data), "vg_batch_linearize_f32")
         return out
 
     def lookup_rows(self, poses: np.ndarray):

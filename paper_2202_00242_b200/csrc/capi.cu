@@ -111,6 +111,7 @@ int vg_ctx_destroy(vg_ctx* ctx) {
     cudaStreamSynchronize(ctx->comp2);
     cudaStreamDestroy(ctx->comp2);
   }
+
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return VG_OK;
@@ -461,13 +462,13 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   // Stages (pipelined host output, vg_batch_linearize*): contiguous factor ranges whose
   // records are copied to the host while the next stage computes; items are stage-major.
   static const int stages_env = [] {
-    // default: 8 stages from 32,768 factors, 4 from 8,192 (measured on config 5: 8 -> e2e
-    // 0.81 ms, 4 -> 0.85, 12 -> 0.89)
+    // default: 6 stages from 32,768 factors, 4 from 8,192 (config 5, compact fp32 records:
+    // 6 -> e2e 0.565 ms, 8 -> 0.578, 4 -> 0.596, 12 -> 0.611, 16 -> 0.621)
     const char* e = getenv("VGICP_STAGES");
     return e ? atoi(e) : -1;
   }();
-  const int S = (int)std::max<int64_t>(
-      1, std::min<int64_t>(stages_env >= 0 ? stages_env : (F >= 32768 ? 8 : F >= 8192 ? 4 : 1),
+  int S = (int)std::max<int64_t>(
+      1, std::min<int64_t>(stages_env >= 0 ? stages_env : (F >= 32768 ? 6 : F >= 8192 ? 4 : 1),
                            16));
   // stage s holds a share proportional to ratio^s: a smaller first stage starts the copy
   // engine sooner (default 1.2 from 8 stages: config 5 e2e 0.814 -> 0.791 ms with the two
@@ -477,15 +478,37 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     return e ? atof(e) : 0.0;
   }();
   const double ratio = ratio_env > 0.0 ? ratio_env : (S >= 8 ? 1.2 : 1.0);
+  // VGICP_STAGE_PROFILE="w0,w1,...": explicit relative stage sizes (overrides the count and
+  // the ratio), e.g. small first and last stages (early copy start, short copy tail)
+  static const std::vector<double> profile_env = [] {
+    std::vector<double> v;
+    const char* e = getenv("VGICP_STAGE_PROFILE");
+    while (e && *e) {
+      char* end = nullptr;
+      const double x = strtod(e, &end);
+      if (end == e) break;
+      if (x > 0.0) v.push_back(x);
+      e = *end == ',' ? end + 1 : end;
+    }
+    return v;
+  }();
+  std::vector<double> weights;
+  if (!profile_env.empty() && F >= 8192 && stages_env != 1) {
+    weights = profile_env;
+    if (weights.size() > 16) weights.resize(16);  // event slots of run_to_host
+  } else {
+    double w = 1.0;
+    for (int s = 0; s < S; ++s, w *= ratio) weights.push_back(w);
+  }
+  S = (int)weights.size();
   std::vector<int> stage_factors(S + 1), stage_of(F);
   {
-    double tot = 0.0, w = 1.0;
-    for (int s = 0; s < S; ++s, w *= ratio) tot += w;
+    double tot = 0.0;
+    for (double w : weights) tot += w;
     double acc = 0.0;
-    w = 1.0;
     stage_factors[0] = 0;
-    for (int s = 1; s <= S; ++s, w *= ratio) {
-      acc += w;
+    for (int s = 1; s <= S; ++s) {
+      acc += weights[s - 1];
       stage_factors[s] = s == S ? (int)F : (int)std::llround((double)F * acc / tot);
     }
   }
@@ -631,6 +654,7 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
       (rc = dalloc(ctx, &b->descs, items.size())) ||
       (rc = dalloc(ctx, &b->hdrs, items.size())) ||
       (rc = dalloc(ctx, &b->out, (size_t)F * VG_REC_LINEARIZE)) ||
+
       (rc = h2d(ctx, b->factors, fac.data(), sizeof(FactorDev) * F)) ||
       (rc = h2d(ctx, b->items, items.data(), sizeof(ItemDev) * items.size())) ||
       (rc = h2d(ctx, b->clouds, cv.data(), sizeof(CloudView) * cv.size())) ||
@@ -669,6 +693,7 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->descs);
   dfree(ctx, b->hdrs);
   dfree(ctx, b->out);
+  dfree(ctx, b->out32);
   dfree(ctx, b->poses);
   dfree(ctx, b->asm_begin);
   dfree(ctx, b->asm_codes);
@@ -697,20 +722,36 @@ static int check_mode(const vg_batch* b, int mode) {
   return VG_OK;
 }
 
-static int run_device(vg_batch* b, int mode, double* out_dev) {
+// Host record formats: fmt 0 = rec_of(mode) doubles per factor; fmt 1 = the compact
+// MODE_LINEARIZE record of VG_REC_LINEARIZE_F32 4-byte words (fp32 blocks, fp64 cost, int32
+// inliers), 2.04x fewer PCIe bytes than fmt 0.
+static size_t rec_bytes(int mode, int fmt) {
+  return fmt ? 4 * (size_t)VG_REC_LINEARIZE_F32 : sizeof(double) * rec_of(mode);
+}
+
+static int out_buffer(vg_batch* b, int fmt, char** dev) {
+  if (fmt && !b->out32) VG_CHECK(dalloc(b->ctx, &b->out32, (size_t)b->F * VG_REC_LINEARIZE_F32));
+  *dev = fmt ? reinterpret_cast<char*>(b->out32) : reinterpret_cast<char*>(b->out);
+  return VG_OK;
+}
+
+static int run_device(vg_batch* b, int mode, void* out_dev, int fmt = 0) {
   VG_CHECK(launch_accumulate(b->ctx, b, kmode_of(mode)));
-  VG_CHECK(launch_finalize(b->ctx, b, mode, out_dev));
+  VG_CHECK(launch_finalize(b->ctx, b, mode, out_dev, fmt));
   return VG_OK;
 }
 
 // K4 + K5 for every stage on the compute stream; each stage's records are copied to the
 // host on the copy stream as soon as its K5 finishes, overlapping the next stage's K4.
-static int run_to_host(vg_batch* b, int mode, double* out_host) {
+static int run_to_host(vg_batch* b, int mode, void* out_host, int fmt = 0) {
   vg_ctx* ctx = b->ctx;
-  const size_t rec = rec_of(mode);
+  const size_t rb = rec_bytes(mode, fmt);
+  char* dev = nullptr;
+  VG_CHECK(out_buffer(b, fmt, &dev));
+  char* host = static_cast<char*>(out_host);
   if (b->stages <= 1) {
-    VG_CHECK(run_device(b, mode, b->out));
-    return d2h_sync(ctx, out_host, b->out, sizeof(double) * rec * b->F);
+    VG_CHECK(run_device(b, mode, dev, fmt));
+    return d2h_sync(ctx, host, dev, rb * b->F);
   }
   if (!ctx->side_stream) {
     VG_CUDA(cudaStreamCreateWithFlags(&ctx->side_stream, cudaStreamNonBlocking));
@@ -732,7 +773,7 @@ static int run_to_host(vg_batch* b, int mode, double* out_host) {
     const char* e = getenv("VGICP_STAGE_STREAMS");
     return e ? atoi(e) : 0;
   }();
-  const int nstreams = nstreams_env > 0 ? nstreams_env : (b->stages >= 8 ? 2 : 1);
+  const int nstreams = nstreams_env > 0 ? nstreams_env : (b->stages >= 6 ? 2 : 1);
   cudaStream_t home = ctx->stream;
   struct Restore {
     vg_ctx* c;
@@ -754,13 +795,12 @@ static int run_to_host(vg_batch* b, int mode, double* out_host) {
     } else {
       VG_CHECK(launch_accumulate_range(ctx, b, kmode, b->stage_items[s], b->stage_items[s + 1]));
     }
-    VG_CHECK(launch_finalize_range(ctx, b, mode, b->out, f0, f1));
+    VG_CHECK(launch_finalize_range(ctx, b, mode, dev, f0, f1, fmt));
     VG_CUDA(cudaEventRecord(ctx->events[s], ctx->stream));
     if (trace) VG_CUDA(cudaEventRecord(tr[1 + 2 * s], ctx->stream));
     VG_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->events[s], 0));
-    VG_CUDA(cudaMemcpyAsync(out_host + (size_t)f0 * rec, b->out + (size_t)f0 * rec,
-                            sizeof(double) * rec * (size_t)(f1 - f0), cudaMemcpyDeviceToHost,
-                            ctx->side_stream));
+    VG_CUDA(cudaMemcpyAsync(host + (size_t)f0 * rb, dev + (size_t)f0 * rb, rb * (size_t)(f1 - f0),
+                            cudaMemcpyDeviceToHost, ctx->side_stream));
     if (trace) VG_CUDA(cudaEventRecord(tr[2 + 2 * s], ctx->side_stream));
   }
   if (trace) {
@@ -775,28 +815,38 @@ static int run_to_host(vg_batch* b, int mode, double* out_host) {
     fprintf(stderr, "\n");
     for (auto& e : tr) cudaEventDestroy(e);
   }
-  if (nstreams == 2) {
+  if (nstreams == 2 && ctx->comp2) {
     ctx->stream = home;
     VG_CUDA(cudaEventRecord(ctx->events[41], ctx->comp2));
     VG_CUDA(cudaStreamWaitEvent(home, ctx->events[41], 0));
   }
-  // the compute stream must not run ahead of the copies that still read b->out
+  // the compute stream must not run ahead of the copies that still read the device records
   VG_CUDA(cudaEventRecord(ctx->events[b->stages], ctx->side_stream));
   VG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->events[b->stages], 0));
   VG_CUDA(cudaStreamSynchronize(ctx->side_stream));
   return VG_OK;
 }
 
-int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_host) {
+static int linearize_T(vg_batch* b, const double* T_host, int mode, void* out_host, int fmt) {
   if (!b || (b->F && (!T_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
   VG_CHECK(check_mode(b, mode));
+  if (fmt && mode != VG_MODE_LINEARIZE)
+    return fail(VG_ERR_INVALID, "f32 records exist for VG_MODE_LINEARIZE only");
   if (b->F == 0) return VG_OK;
   vg_ctx* ctx = b->ctx;
   // scatter T_ij into the 128 B factor records (dst pitch 128, src pitch 96)
   VG_CUDA(cudaMemcpy2DAsync(b->factors, sizeof(FactorDev), T_host, 12 * sizeof(double),
                             12 * sizeof(double), (size_t)b->F, cudaMemcpyHostToDevice, ctx->stream));
   VG_CHECK(launch_spread_T(ctx, b));
-  return run_to_host(b, mode, out_host);
+  return run_to_host(b, mode, out_host, fmt);
+}
+
+int vg_batch_linearize(vg_batch* b, const double* T_host, int mode, double* out_host) {
+  return linearize_T(b, T_host, mode, out_host, 0);
+}
+
+int vg_batch_linearize_f32(vg_batch* b, const double* T_host, int mode, float* out_host) {
+  return linearize_T(b, T_host, mode, out_host, 1);
 }
 
 static int ensure_poses(vg_batch* b, int64_t V) {
@@ -818,11 +868,12 @@ static int ensure_poses(vg_batch* b, int64_t V) {
 static constexpr size_t kSmallHostBytes = 1 << 20;
 
 static int run_small_host(vg_batch* b, const double* poses_host, int64_t V, int mode,
-                          double* out_host) {
+                          void* out_host, int fmt) {
   vg_ctx* ctx = b->ctx;
-  const size_t out_bytes = sizeof(double) * rec_of(mode) * b->F;
+  const size_t out_bytes = rec_bytes(mode, fmt) * b->F;
   const size_t pose_bytes = sizeof(double) * 8 * V;
-  if (!b->hgraph || b->hgraph_mode != mode || b->hgraph_V != V) {
+  const int key = mode + 8 * fmt;
+  if (!b->hgraph || b->hgraph_mode != key || b->hgraph_V != V) {
     if (b->hgraph) cudaGraphExecDestroy(b->hgraph);
     b->hgraph = nullptr;
     if (b->h_poses) cudaFreeHost(b->h_poses);
@@ -831,6 +882,8 @@ static int run_small_host(vg_batch* b, const double* poses_host, int64_t V, int 
     VG_CUDA(cudaMallocHost((void**)&b->h_poses, pose_bytes));
     VG_CUDA(cudaMallocHost((void**)&b->h_out, out_bytes));
     VG_CHECK(ensure_poses(b, V));
+    char* dev = nullptr;
+    VG_CHECK(out_buffer(b, fmt, &dev));
     VG_CUDA(cudaStreamSynchronize(ctx->stream));
     cudaGraph_t g;
     const long long l0 = ctx->launches;
@@ -838,9 +891,9 @@ static int run_small_host(vg_batch* b, const double* poses_host, int64_t V, int 
     cudaError_t e1 = cudaMemcpyAsync(b->poses, b->h_poses, pose_bytes, cudaMemcpyHostToDevice,
                                      ctx->stream);
     int rc = e1 == cudaSuccess ? launch_compose(ctx, b, b->poses) : VG_ERR_CUDA;
-    if (!rc) rc = run_device(b, mode, b->out);
+    if (!rc) rc = run_device(b, mode, dev, fmt);
     cudaError_t e2 = rc ? cudaSuccess
-                        : cudaMemcpyAsync(b->h_out, b->out, out_bytes, cudaMemcpyDeviceToHost,
+                        : cudaMemcpyAsync(b->h_out, dev, out_bytes, cudaMemcpyDeviceToHost,
                                           ctx->stream);
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
     b->hgraph_launches = ctx->launches - l0;
@@ -852,7 +905,7 @@ static int run_small_host(vg_batch* b, const double* poses_host, int64_t V, int 
     e = cudaGraphInstantiate(&b->hgraph, g, 0);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return vg_cuda_fail(e, "cudaGraphInstantiate");
-    b->hgraph_mode = mode;
+    b->hgraph_mode = key;
     b->hgraph_V = V;
   }
   memcpy(b->h_poses, poses_host, pose_bytes);
@@ -863,19 +916,46 @@ static int run_small_host(vg_batch* b, const double* poses_host, int64_t V, int 
   return VG_OK;
 }
 
-int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, int mode,
-                             double* out_host) {
+static int linearize_poses(vg_batch* b, const double* poses_host, int64_t V, int mode,
+                           void* out_host, int fmt) {
   if (!b || (b->F && (!poses_host || !out_host))) return fail(VG_ERR_INVALID, "null argument");
   VG_CHECK(check_mode(b, mode));
+  if (fmt && mode != VG_MODE_LINEARIZE)
+    return fail(VG_ERR_INVALID, "f32 records exist for VG_MODE_LINEARIZE only");
   if (b->F == 0) return VG_OK;
   if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
-  if (b->stages <= 1 && sizeof(double) * rec_of(mode) * b->F <= kSmallHostBytes &&
+  if (b->stages <= 1 && rec_bytes(mode, fmt) * b->F <= kSmallHostBytes &&
       sizeof(double) * 8 * V <= kSmallHostBytes && !getenv("VGICP_NO_HOST_GRAPH"))
-    return run_small_host(b, poses_host, V, mode, out_host);
+    return run_small_host(b, poses_host, V, mode, out_host, fmt);
   VG_CHECK(ensure_poses(b, V));
   VG_CHECK(h2d(b->ctx, b->poses, poses_host, sizeof(double) * 8 * V));
   VG_CHECK(launch_compose(b->ctx, b, b->poses));
-  return run_to_host(b, mode, out_host);
+  return run_to_host(b, mode, out_host, fmt);
+}
+
+int vg_batch_linearize_poses(vg_batch* b, const double* poses_host, int64_t V, int mode,
+                             double* out_host) {
+  return linearize_poses(b, poses_host, V, mode, out_host, 0);
+}
+
+int vg_batch_linearize_poses_f32(vg_batch* b, const double* poses_host, int64_t V, int mode,
+                                 float* out_host) {
+  return linearize_poses(b, poses_host, V, mode, out_host, 1);
+}
+
+// pinned host memory for record outputs: cudaMemcpyAsync into it overlaps the staged compute
+// (pageable destinations serialise the copies), see _lib.PinnedPool
+int vg_host_alloc(size_t bytes, void** out) {
+  if (!out) return fail(VG_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (!bytes) return VG_OK;
+  VG_CUDA(cudaMallocHost(out, bytes));
+  return VG_OK;
+}
+
+int vg_host_free(void* p) {
+  if (p) VG_CUDA(cudaFreeHost(p));
+  return VG_OK;
 }
 
 int vg_batch_linearize_poses_device(vg_batch* b, const double* poses_dev, int64_t V, int mode,

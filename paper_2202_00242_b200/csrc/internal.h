@@ -123,6 +123,7 @@ struct vg_batch {
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;
   double* out = nullptr;              // device output (F * 92)
+  unsigned* out32 = nullptr;          // device output of the f32 records (F * 94 words, lazy)
   // pipelined host-output path: stage s = factors [stage_factors[s], stage_factors[s+1]),
   // whose items are exactly [stage_items[s], stage_items[s+1]) (items are stage-major)
   int stages = 1;
@@ -234,8 +235,10 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
 int launch_spread_T(vg_ctx* ctx, vg_batch* b);  // FactorDev.T -> ItemHdr.T (explicit-T mode)
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b
-int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev);
-int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1);
+// K5; f32: MODE_LINEARIZE records in the compact host format (VG_REC_LINEARIZE_F32 words)
+int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, void* out_dev, int f32 = 0);
+int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, void* out_dev, int f0, int f1,
+                          int f32 = 0);
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev);  // K6
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi);  // K4a + K4b
 // scatter the last K4a pass's hit lists as reference rows (vg_batch_lookup_rows)

@@ -270,8 +270,23 @@ __device__ __forceinline__ void expand_record(const FactorDev& f, const double* 
 constexpr int kFinBlock = 64;
 constexpr int kFinStride = 93;  // odd stride: conflict-free staging rows
 
+// Word e (0..93) of the compact host record (VG_REC_LINEARIZE_F32, include/vgicp.h): the 90
+// block values rounded to fp32 (north_star: fp32 H/b within 1e-4 of the fp64 oracle), the cost
+// kept fp64 in words 90-91 (low word first) so LM accept/reject decisions see the same cost as
+// the fp64 path, the inlier count as int32 in word 92, word 93 padding (8 B-aligned records).
+__device__ __forceinline__ unsigned rec32_word(const double* o, int e) {
+  if (e < 90) return __float_as_uint(__double2float_rn(o[e]));
+  if (e < 92) {
+    const unsigned long long c = (unsigned long long)__double_as_longlong(o[90]);
+    return e == 90 ? (unsigned)c : (unsigned)(c >> 32);
+  }
+  return e == 92 ? (unsigned)(int)o[91] : 0u;
+}
+
 // K5: per-factor fixed-order sum of item partials + fp64 adjoint expansion.  LINEARIZE
-// records (92 doubles) are staged in shared memory and written out contiguously.
+// records (92 doubles, or 94 words when F32) are staged in shared memory and written out
+// contiguously.
+template <int F32>
 __global__ void __launch_bounds__(kFinBlock)
     k_finalize(const FactorDev* __restrict__ factors, int fbase, int F,
                const double* __restrict__ partials, int mode, double* __restrict__ out,
@@ -296,6 +311,14 @@ __global__ void __launch_bounds__(kFinBlock)
   }
   __syncthreads();
   const int nf = min(kFinBlock, F - f0);
+  if (F32) {
+    unsigned* dst = reinterpret_cast<unsigned*>(out) + (size_t)f0 * 94;
+    for (int k = threadIdx.x; k < nf * 94; k += kFinBlock) {
+      const int r = k / 94;
+      dst[k] = rec32_word(sh + r * kFinStride, k - r * 94);
+    }
+    return;
+  }
   double* dst = out + (size_t)f0 * 92;
   for (int k = threadIdx.x; k < nf * 92; k += kFinBlock) {
     const int r = k / 92;
@@ -307,6 +330,7 @@ __global__ void __launch_bounds__(kFinBlock)
 // k over the factor's items in item order — the same additions as k_finalize's per-thread
 // loop, so the records are bit-identical — then lane 0 expands and the warp writes out.
 constexpr int kFinWarps = 4;
+template <int F32>
 __global__ void __launch_bounds__(kFinWarps * 32)
     k_finalize_warp(const FactorDev* __restrict__ factors, int fbase, int F,
                     const double* __restrict__ partials, int mode, double* __restrict__ out,
@@ -343,6 +367,11 @@ __global__ void __launch_bounds__(kFinWarps * 32)
     }
   }
   __syncwarp();
+  if (F32) {
+    unsigned* dst = reinterpret_cast<unsigned*>(out) + (size_t)fi * 94;
+    for (int k = lane; k < 94; k += 32) dst[k] = rec32_word(sw + 32, k);
+    return;
+  }
   for (int k = lane; k < 92; k += 32) out[(size_t)fi * 92 + k] = sw[32 + k];
 }
 
@@ -673,26 +702,36 @@ int launch_spread_T(vg_ctx* ctx, vg_batch* b) {
   return 0;
 }
 
-int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev, int f0, int f1) {
+int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, void* out_dev, int f0, int f1,
+                          int f32) {
   if (f1 <= f0) return 0;
+  double* out = static_cast<double*>(out_dev);
+  double2* gc = mode == 0 ? b->asm_gcost : nullptr;
+  const FactorDev* fac = b->factors;
+  const double* part = b->partials;
   // few factors or long item lists: a warp per factor sums the items in parallel lanes
   if (b->F < 4096 || b->num_items > 4 * b->F) {
-    k_finalize_warp<<<(f1 - f0 + kFinWarps - 1) / kFinWarps, kFinWarps * 32, 0, ctx->stream>>>(
-        b->factors, f0, f1, b->partials, mode, out_dev, mode == 0 ? b->asm_gcost : nullptr);
+    const dim3 grid((f1 - f0 + kFinWarps - 1) / kFinWarps), block(kFinWarps * 32);
+    if (f32 && mode == 0)
+      k_finalize_warp<1><<<grid, block, 0, ctx->stream>>>(fac, f0, f1, part, mode, out, gc);
+    else
+      k_finalize_warp<0><<<grid, block, 0, ctx->stream>>>(fac, f0, f1, part, mode, out, gc);
     ctx->launches++;
     VG_CUDA(cudaGetLastError());
     return 0;
   }
-  VG_CUDA(launch_pdl(k_finalize, dim3((f1 - f0 + kFinBlock - 1) / kFinBlock), dim3(kFinBlock), 0,
-                     ctx->stream, (const FactorDev*)b->factors, f0, f1, (const double*)b->partials,
-                     mode, out_dev, mode == 0 ? b->asm_gcost : (double2*)nullptr));
+  const dim3 grid((f1 - f0 + kFinBlock - 1) / kFinBlock), block(kFinBlock);
+  if (f32 && mode == 0)
+    VG_CUDA(launch_pdl(k_finalize<1>, grid, block, 0, ctx->stream, fac, f0, f1, part, mode, out, gc));
+  else
+    VG_CUDA(launch_pdl(k_finalize<0>, grid, block, 0, ctx->stream, fac, f0, f1, part, mode, out, gc));
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
 }
 
-int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, double* out_dev) {
-  return launch_finalize_range(ctx, b, mode, out_dev, 0, (int)b->F);
+int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, void* out_dev, int f32) {
+  return launch_finalize_range(ctx, b, mode, out_dev, 0, (int)b->F, f32);
 }
 
 namespace vg {

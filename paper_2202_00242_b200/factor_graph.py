@@ -90,6 +90,7 @@ class Factor:
 
 # ---- the batching shim ---------------------------------------------------------------------
 
+
 class _Batcher:
     """Registry of live GPU matching factors and the cache of flattened device batches."""
 
@@ -157,6 +158,9 @@ class _Batcher:
             poses[i] = pose_row(_pose_of(k.kind, values[k]))
         if fixed.shape[0]:
             poses[len(var_keys):] = fixed
+        # fp64 records into pinned memory (the staged copies overlap the compute); the compact
+        # fp32 record (linearize_poses_f32) halves the PCIe bytes for callers that take fp32
+        # blocks, but here the per-factor Python unpacking dominates either way
         out = batch.linearize_poses(poses, mode)
         self.evaluations += 1
         for f, rec in zip(group, out):
@@ -265,7 +269,8 @@ class MatchingCostFactor(Factor):
         zeros = [np.zeros(k.dim) for k in self.keys]
         if not self._empty:
             _, rec = self._record(values, _lib.MODE_LINEARIZE)
-        if self._empty or rec[91] < self.min_inliers:  # DegenerateConstraint -> no-op
+            cost, inl = float(rec[90]), rec[91]
+        if self._empty or inl < self.min_inliers:  # DegenerateConstraint -> no-op
             h = {(a, a): np.zeros((k.dim, k.dim)) for a, k in enumerate(self.keys)}
             return FactorLinearization(self.keys, zeros, h, 0.0)
         di = self.keys[0].dim
@@ -273,7 +278,6 @@ class MatchingCostFactor(Factor):
         g_i[:6] = rec[78:84]
         h_ii = np.zeros((di, di))
         h_ii[:6, :6] = unpack_sym6(rec[0:21])
-        cost = float(rec[90])
         if self.unary:
             return FactorLinearization(self.keys, [g_i], {(0, 0): h_ii}, cost)
         dj = self.keys[1].dim

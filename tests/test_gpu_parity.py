@@ -851,6 +851,8 @@ def test_config5_blocks_of_600_factors_vs_oracle(config5):
     fids = np.flatnonzero(np.isin(wl.pairs[:, 1], targets))
     R, t = O.relative_transforms(table, wl.pairs[fids, 0], wl.pairs[fids, 1])
     maps = {int(j): O.build_voxelmap(wl.scans[j], wl.scan_covs[j], wl.resolution) for j in targets}
+    r32 = batch.linearize_poses_f32(table)
+    c32, i32 = _lib.record_cost_inliers_f32(r32)
     gated = 0
     for k, f in enumerate(fids):
         i, j = wl.pairs[f]
@@ -862,4 +864,33 @@ def test_config5_blocks_of_600_factors_vs_oracle(config5):
             gated += 1
             continue
         assert_lin(RG.unpack_record(host[f], False), ref, False)
+        # the compact fp32 record (what the factor shim and the e2e bench consume)
+        rec = np.concatenate([r32[f, :90].astype(np.float64), [c32[f], i32[f]]])
+        assert_lin(RG.unpack_record(rec, False), ref, False)
     assert len(fids) >= 500 and gated < len(fids) // 4
+
+
+def test_f32_records_are_the_rounded_fp64_records(small_graph, config5):
+    """vg_batch_linearize_poses_f32 = K5's fp64 records rounded per element (blocks), with the
+    fp64 cost and the inlier count carried exactly — on the small graph (graph-replayed host
+    path) and on config 5 (the 8-stage pipelined host path), and with explicit transforms."""
+    poses, est, scans, covs, maps, srcs, pairs = small_graph
+    clouds = [_lib.DeviceCloud(s, c) for s, c in srcs]
+    dmaps = [_lib.DeviceMap.build(_lib.DeviceCloud(s, c), 1.0) for s, c in zip(scans, covs)]
+    F = len(pairs)
+    small = _lib.DeviceBatch([clouds[i] for i, _ in pairs], [dmaps[j] for _, j in pairs],
+                             [(f % 5) == 2 for f in range(F)], [10] * F, pairs[:, 0], pairs[:, 1])
+    table = np.array([G.pose_row(p) for p in est])
+    R, t = O.relative_transforms(table, pairs[:, 0], pairs[:, 1])
+    T = np.concatenate([R.reshape(F, 9), t], axis=1)
+    cases = [(small.linearize_poses(table), small.linearize_poses_f32(table)),
+             (small.linearize(T), small.linearize_f32(T))]
+    wl = config5
+    big = wl.batch()
+    cases.append((big.linearize_poses(wl.pose_table), big.linearize_poses_f32(wl.pose_table)))
+    for r64, r32 in cases:
+        assert r32.dtype == np.float32 and r32.shape == (len(r64), _lib.REC_LINEARIZE_F32)
+        assert np.array_equal(r32[:, :90], r64[:, :90].astype(np.float32))
+        cost, inl = _lib.record_cost_inliers_f32(r32)
+        assert np.array_equal(cost, r64[:, 90]) and np.array_equal(inl, r64[:, 91].astype(np.int64))
+        assert np.all(r32[:, 93] == 0)
