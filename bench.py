@@ -5,10 +5,18 @@ global-mapping workload (config 5: 1000 submaps, 50 nearest-neighbour binary fac
 
 One step = one linearization of every factor of the graph: compose T_ij from the pose table
 (K-compose), fused transform/lookup/fused-covariance/accumulate (K4), fixed-order finalize
-into the per-factor H_ii/H_ij/H_jj/b_i/b_j/cost records (K5).  Under torchrun the factors are
-LPT-sharded by point count across ranks (strong scaling of the fixed graph); each step
-broadcasts the pose table from the solver rank, and every rank sums its shard into the
-global block-sparse normal equations (K6), which one NCCL reduction puts on the solver rank.
+into the per-factor H_ii/H_ij/H_jj/b_i/b_j/cost records (K5).
+
+N > 1 (one process per GPU; `--gpus N` spawns them through torch.distributed.run when
+WORLD_SIZE is unset): the fixed 50,000-factor graph is sharded pair-disjointly across the ranks
+(strong scaling; sharding.pair_shards), the solver rank broadcasts the pose table, every rank
+linearizes its shard and assembles its compact normal equations (K6: diagonal blocks +
+gradient for every variable, the off-diagonal blocks of its own pairs), and one all-gather
+puts them on the solver rank, which combines them into the global block-sparse system
+(sharding.PairExchange) — so the N > 1 step does strictly more than the N = 1 step (K6, the
+exchange and the combine on top), and the driver's scaling ratio is conservative.
+`--backend gloo` runs the same multi-rank path with CPU collectives, ranks sharing GPUs
+(a functional check on a one-GPU box, not a timing).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -48,6 +56,9 @@ def parse():
                     help="target maps in the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--cpu-full-pass", action="store_true",
+                    help="reference arm: also time one pass over the whole workload")
     return ap.parse_args()
 
 
@@ -173,7 +184,25 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_reference(wl, args, steps, warmup):
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a launcher: start N ranks with torch.distributed.run (one process
+    per GPU, rendezvous on 127.0.0.1) and pass their output through."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # rank/channel setup evidence, on stderr
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
+def cpu_reference(wl, args, steps, warmup, one_process=False):
     from oracle import cpu_baseline
 
     sample = cpu_baseline.build_sample(wl, args.cpu_targets)
@@ -181,7 +210,13 @@ def cpu_reference(wl, args, steps, warmup):
     desc = (f"{len(sample['pairs'])} factors (every factor whose target is one of submaps "
             f"0..{args.cpu_targets - 1}), {sample['points']} correspondences per pass, "
             f"oracle linearization, {procs}-process fork pool, {steps} passes")
-    return rate, sec, procs, desc
+    extra = {"cpu_model": cpu_baseline.cpu_model(), "cpu_count": os.cpu_count()}
+    if one_process:
+        r1, s1, _ = cpu_baseline.time_sample(sample, 1, 0, processes=1)
+        extra["one_process"] = {"value": r1, "unit": UNIT, "seconds_per_pass": s1,
+                                "sample": "the same sample, 1 process (the reference's "
+                                          "single-threaded NumPy path)"}
+    return rate, sec, procs, desc, extra
 
 
 def run_reference(args):
@@ -192,15 +227,26 @@ def run_reference(args):
 
     wl = workloads.global_mapping(args.submaps, args.neighbors, device_objects=False)
     steps = max(1, args.steps)
-    rate, sec, procs, desc = cpu_reference(wl, args, steps, max(1, min(args.warmup, 3)))
+    rate, sec, procs, desc, extra = cpu_reference(wl, args, steps, max(1, min(args.warmup, 3)),
+                                                  one_process=True)
+    if args.cpu_full_pass:
+        from oracle import cpu_baseline
+
+        t0 = time.perf_counter()
+        full = cpu_baseline.build_sample(wl, wl.n_submaps)
+        prep = time.perf_counter() - t0
+        r, s_, p_ = cpu_baseline.time_sample(full, 1, 0)
+        extra["full_pass"] = {"value": r, "unit": UNIT, "seconds": s_, "processes": p_,
+                              "factors": len(full["pairs"]), "corr": full["points"],
+                              "input_prep_s": round(prep, 1)}
     line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": "global-mapping (BASELINE config 5): bounded CPU sample",
                        "submaps": args.submaps, "neighbors": args.neighbors},
-            "cpu_baseline": {"value": rate, "unit": UNIT, "cores": procs, "kind": "port",
-                             "sample": desc},
+            "cpu_baseline": dict({"value": rate, "unit": UNIT, "cores": procs, "kind": "port",
+                                  "sample": desc}, **extra),
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -212,13 +258,19 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = dist_setup(args)
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev = local % max(ndev, 1)   # gloo check runs may put several ranks on one GPU
+    torch.cuda.set_device(dev)
+    gloo = args.backend == "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2202_00242_b200 import _lib, workloads
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    from paper_2202_00242_b200 import _lib, sharding, workloads
 
-    _lib.set_device(local)
-    ctx = _lib.context(local)
+    _lib.set_device(dev)
+    ctx = _lib.context(dev)
     # a real (non-legacy) stream shared by torch events, NCCL and the library's launches
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -227,40 +279,59 @@ def run_ours(args):
     t0 = time.perf_counter()
     wl = workloads.global_mapping(args.submaps, args.neighbors)
     weights = np.array([len(wl.source_index[i]) for i in wl.pairs[:, 0]])
-    shards = workloads.lpt_shards(weights, world) if world > 1 else [np.arange(len(wl.pairs))]
+    F = len(wl.pairs)
+    V = wl.pose_table.shape[0]
+    if world > 1:
+        shards = sharding.pair_shards(wl.pairs[:, 0], wl.pairs[:, 1], weights, world)
+        ex = sharding.PairExchange(wl.pairs[:, 0], wl.pairs[:, 1], np.zeros(F, bool), V, shards)
+    else:
+        shards, ex = [np.arange(F)], None
     mine = shards[rank]
     batch = wl.batch(mine, ctx=ctx)
     ctx.set_stream(stream.cuda_stream)
     setup_s = time.perf_counter() - t0
     F_r = len(mine)
-    F_max = max(len(s) for s in shards)
     total_points = wl.num_points
     my_points = int(weights[mine].sum())
-    V = wl.pose_table.shape[0]
     REC = _lib.RECORD_SIZE[_lib.MODE_LINEARIZE]
 
     poses_dev = torch.from_numpy(wl.pose_table).to("cuda")
-    out_dev = torch.zeros((F_max, REC), dtype=torch.float64, device="cuda")
+    out_dev = torch.zeros((max(F_r, 1), REC), dtype=torch.float64, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+
+    ne_local = gathered = ne_global = None
+    if world > 1:
+        # this rank's compact normal equations: diagonal blocks + gradient of every variable,
+        # off-diagonal blocks of its own pairs (pair-disjoint shards)
+        batch.assemble_setup(V, ex.rank_pairs[rank])
+        assert batch.asm_size == ex.local_size(rank)
+        ne_local = torch.zeros(ex.L, dtype=torch.float64, device="cuda")
+        gathered = torch.zeros(world * ex.L, dtype=torch.float64,
+                               device="cpu" if gloo else "cuda")
+        ne_global = torch.zeros(ex.size, dtype=torch.float64, device="cuda")
+
+    def exchange():
+        if gloo:  # CPU collectives (functional check)
+            host = ne_local.cpu()
+            sharding.exchange_normal_equations(host, ex, rank, gathered)
+            if rank == 0:
+                ne_global.copy_(ex.combine(gathered))
+        else:
+            sharding.exchange_normal_equations(ne_local, ex, rank, gathered, ne_global)
+
+    def bcast_poses():
+        if gloo:
+            h = poses_dev.cpu()
+            sharding.broadcast_poses(h, 0)
+            poses_dev.copy_(h)
+        else:
+            sharding.broadcast_poses(poses_dev, 0)
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
 
-    from paper_2202_00242_b200 import sharding
-
-    ne_dev = None
-    if world > 1:
-        # the exchange (north_star): every rank sums its shard's blocks into the
-        # global normal-equation layout (K6) and one NCCL reduction puts the per-pose-pair
-        # H/b blocks on the solver rank -- 8.2 MB instead of gathering 36.8 MB of records.
-        # N > 1 does strictly more device work per factor than N = 1 (K6).
-        gp = sharding.global_pairs(wl.pairs[:, 0], wl.pairs[:, 1],
-                                   np.zeros(len(wl.pairs), bool), V)
-        batch.assemble_setup(V, gp)
-        ne_dev = torch.empty(batch.asm_size, dtype=torch.float64, device="cuda")
-
     def step(e=None):
         if world > 1:
-            sharding.broadcast_poses(poses_dev, 0)
+            bcast_poses()
         if e:
             e[0].record()
         batch.compose_device(poses_dev.data_ptr(), V)
@@ -271,19 +342,21 @@ def run_ours(args):
             e[2].record()
         batch.finalize_device(_lib.MODE_LINEARIZE, out_dev.data_ptr())
         if world > 1:
-            batch.assemble_records_device(out_dev.data_ptr(), ne_dev.data_ptr())
-            sharding.reduce_normal_equations(ne_dev, 0)
+            batch.assemble_records_device(out_dev.data_ptr(), ne_local.data_ptr())
+            if e:
+                e[3].record()
+            exchange()
 
     def step_fast():
         # the same step as one library call (K-compose, K4a, K4b, K5 chained with programmatic
         # dependent launch; no host events between the kernels)
         if world > 1:
-            sharding.broadcast_poses(poses_dev, 0)
+            bcast_poses()
         batch.linearize_poses_device(poses_dev.data_ptr(), V, _lib.MODE_LINEARIZE,
                                      out_dev.data_ptr())
         if world > 1:
-            batch.assemble_records_device(out_dev.data_ptr(), ne_dev.data_ptr())
-            sharding.reduce_normal_equations(ne_dev, 0)
+            batch.assemble_records_device(out_dev.data_ptr(), ne_local.data_ptr())
+            exchange()
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -295,8 +368,8 @@ def run_ours(args):
     launches0 = ctx.launch_count()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        # timed region 1 (the metric): K steps, each one library call
+    with ClockSampler(dev) as clk:
+        # timed region 1 (the metric): K steps, each one library call (+ K6 and the exchange)
         for k in range(args.steps):
             flush.zero_()  # evict L2 between timed steps (outside the timed events)
             starts[k].record()
@@ -315,27 +388,29 @@ def run_ours(args):
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     k4_ms = [e[1].elapsed_time(e[2]) for e in ev]
     total_ms = float(sum(step_ms))
+    rank_ms = None
     if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        t = torch.tensor([total_ms], dtype=torch.float64,
+                         device="cpu" if gloo else "cuda")
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        rank_ms = [float(x.item()) / args.steps for x in allt]
+        total_ms = max(float(x.item()) for x in allt)
     ms_per_step = total_ms / args.steps
     value = total_points * args.steps / (total_ms / 1e3)
 
     # ---- e2e: through the public batch API with host buffers (H2D poses, D2H records) ----
-    # headline: the compact record (vg_batch_linearize_poses_f32: fp32 H/b blocks, fp64 cost,
-    # int32 inliers; 376 B/factor) into pinned host memory; the fp64 record (736 B/factor)
-    # is reported beside it
+    # N = 1 headline: the compact record (vg_batch_linearize_poses_f32: fp32 H/b blocks, fp64
+    # cost, int32 inliers; 376 B/factor) into pinned host memory; the fp64 record (736 B) is
+    # reported beside it.  N > 1: host pose table in on the solver rank, the combined normal
+    # equations out of it.
     poses_host = torch.from_numpy(wl.pose_table.copy()).pin_memory()
-    out_host = torch.empty((F_max, REC), dtype=torch.float64).pin_memory()
-    out32_host = torch.empty((F_max, _lib.REC_LINEARIZE_F32), dtype=torch.float32).pin_memory()
-    ne_host = (torch.empty(batch.asm_size, dtype=torch.float64).pin_memory()
-               if world > 1 else None)
     e2e_ms, e2e64_ms = [], []
+    e2e64_line = cost_line = None
     if world == 1:
-        out_np = out_host.numpy()
-        out32_np = out32_host.numpy()
-        poses_np = poses_host.numpy()
+        out_host = torch.empty((F_r, REC), dtype=torch.float64).pin_memory()
+        out32_host = torch.empty((F_r, _lib.REC_LINEARIZE_F32), dtype=torch.float32).pin_memory()
+        out_np, out32_np, poses_np = out_host.numpy(), out32_host.numpy(), poses_host.numpy()
         for k in range(args.e2e_steps + 2):
             torch.cuda.synchronize()
             a = time.perf_counter()
@@ -350,38 +425,13 @@ def run_ours(args):
                 e2e64_ms.append((time.perf_counter() - a) * 1e3)
         h2d = poses_host.numel() * 8
         d2h = F_r * _lib.REC_LINEARIZE_F32 * 4
-    else:
-        for k in range(args.e2e_steps + 2):
-            torch.cuda.synchronize()
-            dist.barrier()
-            a = time.perf_counter()
-            if rank == 0:
-                poses_dev.copy_(poses_host, non_blocking=True)
-            step()
-            if rank == 0:
-                ne_host.copy_(ne_dev, non_blocking=False)
-            torch.cuda.synchronize()
-            dt = torch.tensor([(time.perf_counter() - a) * 1e3], dtype=torch.float64,
-                              device="cuda")
-            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-            if k >= 2:
-                e2e_ms.append(float(dt.item()))
-        h2d = poses_host.numel() * 8
-        d2h = batch.asm_size * 8
-    e2e_value = total_points / (statistics.median(e2e_ms) / 1e3)
-    e2e64_line = None
-    if e2e64_ms:
         e2e64_line = {"value": total_points / (statistics.median(e2e64_ms) / 1e3), "unit": UNIT,
-                      "h2d_bytes_per_step": int(poses_host.numel() * 8),
-                      "d2h_bytes_per_step": int(F_r * REC * 8),
+                      "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(F_r * REC * 8),
                       "ms_per_step": statistics.median(e2e64_ms),
                       "api": "DeviceBatch.linearize_poses (vg_batch_linearize_poses, fp64 records)"}
-
-    # ---- cost-only pass (LM candidate steps, factor_graph.py:591): the same correspondences,
-    # no accumulators, 2 values per factor ----
-    cost_line = None
-    if world == 1:
-        cost_dev = torch.zeros((F_max, 2), dtype=torch.float64, device="cuda")
+        # cost-only pass (LM candidate steps, factor_graph.py:591): the same correspondences,
+        # no accumulators, 2 values per factor
+        cost_dev = torch.zeros((F_r, 2), dtype=torch.float64, device="cuda")
         cs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ce = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         for k in range(3):
@@ -397,6 +447,26 @@ def run_ours(args):
         cms = sum(a.elapsed_time(b) for a, b in zip(cs, ce)) / args.steps
         cost_line = {"value": total_points / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
                      "api": "vg_batch_linearize_poses_device(VG_MODE_COST)"}
+    else:
+        ne_host = torch.empty(ex.size, dtype=torch.float64).pin_memory()
+        for k in range(args.e2e_steps + 2):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a = time.perf_counter()
+            if rank == 0:
+                poses_dev.copy_(poses_host, non_blocking=True)
+            step_fast()
+            if rank == 0:
+                ne_host.copy_(ne_global, non_blocking=False)
+            torch.cuda.synchronize()
+            dt = torch.tensor([(time.perf_counter() - a) * 1e3], dtype=torch.float64,
+                              device="cpu" if gloo else "cuda")
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            if k >= 2:
+                e2e_ms.append(float(dt.item()))
+        h2d = poses_host.numel() * 8
+        d2h = ex.size * 8
+    e2e_value = total_points / (statistics.median(e2e_ms) / 1e3)
 
     # ---- e2e of the normal equations: the same linearization, summed into
     # the block-sparse H/g on the device, only the system crosses PCIe ----
@@ -423,13 +493,22 @@ def run_ours(args):
     k4_avg_s = statistics.mean(k4_ms) / 1e3
     achieved = BYTES_PER_CORR * my_points / k4_avg_s / 1e9
 
-    line = None
     if rank == 0:
         clocks = clk.summary()
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rate, sec, procs, desc = cpu_reference(wl, args, steps=3, warmup=1)
-            cpu = {"value": rate, "unit": UNIT, "cores": procs, "kind": "port", "sample": desc}
+            rate, sec, procs, desc, extra = cpu_reference(wl, args, steps=3, warmup=1)
+            cpu = dict({"value": rate, "unit": UNIT, "cores": procs, "kind": "port",
+                        "sample": desc}, **extra)
+        multi = None
+        if world > 1:
+            multi = {"backend": args.backend, "sharding": "pair-disjoint LPT on point count",
+                     "rank_ms_per_step": rank_ms,
+                     "rank_factors": [int(len(s)) for s in shards],
+                     "rank_points": [int(weights[s].sum()) for s in shards],
+                     "exchange": "all-gather of compact normal equations + solver-rank combine",
+                     "exchange_bytes_per_rank": int(ex.L * 8), "global_pairs": int(len(ex.pairs)),
+                     "global_system_bytes": int(ex.size * 8)}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -437,22 +516,25 @@ def run_ours(args):
             "dtype": "f32+f64", "data": "synthetic",
             "config": {"workload": "global-mapping (BASELINE config 5)",
                        "submaps": args.submaps, "neighbors": args.neighbors,
-                       "factors": int(len(wl.pairs)), "corr_per_step": total_points,
+                       "factors": int(F), "corr_per_step": total_points,
                        "voxel_resolution_m": wl.resolution, "scan_points": 16384,
                        "source_points": "U[200,600]", "parallelism": f"factor-shard x{world}",
                        "l2": "flushed between timed steps (256 MB write)",
-                       "timing": "steps as one library call (PDL-chained kernels); K4 timed "
-                                 "in a second pass of the same steps with events around it",
+                       "timing": ("steps as one library call (PDL-chained kernels); K4 timed "
+                                  "in a second pass of the same steps with events around it"
+                                  + ("; N > 1 steps add K6 + all-gather + combine" if world > 1
+                                     else "")),
                        "setup_s": round(setup_s, 2)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "ms_per_step": statistics.median(e2e_ms),
                     "api": ("DeviceBatch.linearize_poses_f32 (vg_batch_linearize_poses_f32: "
                             "fp32 H/b blocks, fp64 cost, int32 inliers) into pinned memory"
-                            if world == 1 else "normal equations reduced to the solver rank")},
+                            if world == 1 else "normal equations combined on the solver rank")},
             "e2e_f64_records": e2e64_line,
-            "cost_mode": cost_line,
             "e2e_normal_equations": ne_line,
+            "cost_mode": cost_line,
+            "multi_gpu": multi,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic_record(),
@@ -472,6 +554,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -37,22 +37,57 @@ def knn_query(full: np.ndarray, queries_idx: np.ndarray, k: int) -> np.ndarray:
     return np.take_along_axis(cand, order, axis=1)
 
 
-def build_sample(wl, n_targets: int = 16, knn: int = 10):
+_WL = None  # the workload, shared with fork()ed preparation workers
+
+
+def _prep_map(j):
+    s = _WL.scans[j]
+    covs, _ = O.estimate_covariances(s, O.knn_search(s, _KNN))
+    return int(j), O.build_voxelmap(s, covs, _WL.resolution)
+
+
+def _prep_source(i):
+    s, sel = _WL.scans[i], _WL.source_index[i]
+    covs, _ = O.estimate_covariances(s, knn_query(s, sel, _KNN))
+    return int(i), (s[sel], covs)
+
+
+_KNN = 10
+
+
+def build_sample(wl, n_targets: int = 16, knn: int = 10, processes: int | None = None):
+    """Oracle inputs of every factor whose target is one of the first n_targets submaps
+    (n_targets >= wl.n_submaps: the whole workload), prepared on all host cores."""
+    global _WL, _KNN
     targets = np.arange(min(n_targets, wl.n_submaps))
     fids = np.flatnonzero(np.isin(wl.pairs[:, 1], targets))
-    maps = {}
-    for j in targets:
-        s = wl.scans[j]
-        covs, _ = O.estimate_covariances(s, O.knn_search(s, knn))
-        maps[int(j)] = O.build_voxelmap(s, covs, wl.resolution)
-    sources = {}
-    for i in np.unique(wl.pairs[fids, 0]):
-        s, sel = wl.scans[i], wl.source_index[i]
-        covs, _ = O.estimate_covariances(s, knn_query(s, sel, knn))
-        sources[int(i)] = (s[sel], covs)
+    sources_needed = np.unique(wl.pairs[fids, 0])
+    _WL, _KNN = wl, knn
+    procs = processes or os.cpu_count() or 1
+    if procs > 1:
+        with mp.get_context("fork").Pool(procs) as pool:
+            maps = dict(pool.map(_prep_map, targets, chunksize=4))
+            sources = dict(pool.map(_prep_source, sources_needed, chunksize=8))
+    else:
+        maps = dict(map(_prep_map, targets))
+        sources = dict(map(_prep_source, sources_needed))
+    _WL = None
     R, t = O.relative_transforms(wl.pose_table, wl.pairs[fids, 0], wl.pairs[fids, 1])
     return {"fids": fids, "pairs": wl.pairs[fids], "maps": maps, "sources": sources, "R": R,
             "t": t, "points": int(sum(len(sources[int(i)][0]) for i in wl.pairs[fids, 0]))}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def _work(chunk):

@@ -5,10 +5,19 @@ are partitioned across ranks with longest-processing-time-first balancing on poi
 (the per-factor cost).  Per linearization the solver rank broadcasts the pose table
 (V x 8 doubles), every rank linearizes its shard, and the result goes back to the solver
 rank — the one real exchange step of this path (the LM solve stays on the solver rank's host,
-as in the reference: factor_graph.py:546-612).  Two forms: the per-factor records gathered
-and reassembled in factor order (the drop-in's per-factor API), or each rank's block-sparse
-normal equations in the global pair layout, sum-reduced onto the solver rank (what the LM
-consumes: per-pose-pair H/b blocks, 4.5x fewer bytes at config 5).
+as in the reference: factor_graph.py:546-612).  Forms of the exchange:
+
+* per-factor records gathered and reassembled in factor order (the drop-in's per-factor API);
+* normal equations (what the LM consumes, factor_graph.py:522-536), the default of bench.py:
+  factors are sharded PAIR-DISJOINTLY (both factors of an unordered variable pair on one
+  rank, ``pair_shards``), so every rank assembles (K6) a compact system — its diagonal blocks
+  and gradient for all variables plus the off-diagonal blocks of ITS pairs only — and one
+  all-gather brings the per-rank systems to the solver rank, which sums the diagonal parts in
+  rank order and places the pair blocks (``PairExchange``): per-rank K6 work and exchange
+  bytes shrink with the rank count instead of every rank assembling the full 27,825-pair
+  layout;
+* the full global pair layout on every rank, sum-reduced (``global_pairs`` +
+  ``reduce_normal_equations``; any sharding).
 
 The helpers are backend-agnostic torch.distributed calls: NCCL over NVLink on the B200 box,
 gloo in the CPU tests (tests/test_distributed_gloo.py).
@@ -30,6 +39,85 @@ def lpt_shards(weights, n_shards: int) -> list:
         members[r].append(int(f))
         loads[r] += w[f]
     return [np.sort(np.array(m, dtype=np.int64)) for m in members]
+
+
+def pair_shards(var_source, var_target, weights, n_shards: int) -> list:
+    """Pair-disjoint LPT shards: factors grouped by unordered variable pair (i -> j and
+    j -> i together), groups balanced on their summed weight; each shard sorted ascending
+    (the batch keeps the caller's target-major factor order)."""
+    vs = np.asarray(var_source, np.int64)
+    vt = np.asarray(var_target, np.int64)
+    w = np.asarray(weights, np.float64)
+    n = int(max(vs.max(initial=0), vt.max(initial=0))) + 1
+    key = np.minimum(vs, vt) * n + np.maximum(vs, vt)
+    _, group = np.unique(key, return_inverse=True)
+    gw = np.bincount(group, weights=w)
+    rank_of_group = np.empty(len(gw), np.int64)
+    for r, members in enumerate(lpt_shards(gw, n_shards)):
+        rank_of_group[members] = r
+    rank = rank_of_group[group]
+    return [np.flatnonzero(rank == r).astype(np.int64) for r in range(n_shards)]
+
+
+class PairExchange:
+    """Layout of the pair-disjoint normal-equation exchange (see the module docstring).
+
+    Rank r's compact system is the K6 flat layout over its own sorted pair list
+    ``rank_pairs[r]``: [cost, count, diag V x 21, grad V x 6, pairs P_r x 36], padded to a
+    common length ``L`` for the all-gather.  ``combine`` turns the gathered (N, L) block into
+    the global system over ``pairs`` (the sorted union): cost, count, diagonal blocks and
+    gradient summed over ranks in rank order, pair blocks copied from their owning rank
+    (each pair's contributions were already summed on that rank in factor order, exactly as
+    the single-GPU assembly sums them)."""
+
+    def __init__(self, var_source, var_target, unary, num_vars: int, shards):
+        vs = np.asarray(var_source, np.int64)
+        vt = np.asarray(var_target, np.int64)
+        un = np.asarray(unary, bool)
+        self.V = int(num_vars)
+        self.rank_pairs = [global_pairs(vs[s], vt[s], un[s], self.V) for s in shards]
+        self.pairs = global_pairs(vs, vt, un, self.V)
+        index = {(int(a), int(b)): k for k, (a, b) in enumerate(self.pairs)}
+        self.gidx = [np.array([index[(int(a), int(b))] for a, b in rp], np.int64)
+                     for rp in self.rank_pairs]
+        cat = np.concatenate(self.gidx) if self.gidx else np.zeros(0, np.int64)
+        if len(cat) != len(self.pairs) or len(np.unique(cat)) != len(cat):
+            raise ValueError("shards are not pair-disjoint")
+        self.head = 2 + 27 * self.V
+        self.pmax = max((len(p) for p in self.rank_pairs), default=0)
+        self.L = self.head + 36 * self.pmax
+        self.size = self.head + 36 * len(self.pairs)   # the global system (K6 flat layout)
+
+    def local_size(self, rank: int) -> int:
+        return self.head + 36 * len(self.rank_pairs[rank])
+
+    def combine(self, gathered, out=None):
+        """(N, L) gathered per-rank systems -> the global flat system (torch, on the device
+        the tensors live on)."""
+        import torch
+
+        g = gathered.reshape(len(self.rank_pairs), self.L)
+        if out is None:
+            out = torch.empty(self.size, dtype=g.dtype, device=g.device)
+        out[: self.head] = g[:, : self.head].sum(0)
+        blocks = out[self.head:].view(-1, 36)
+        if not hasattr(self, "_gidx_t") or self._gidx_t[0].device != g.device:
+            self._gidx_t = [torch.as_tensor(i, device=g.device) for i in self.gidx]
+        for r, gi in enumerate(self._gidx_t):
+            if len(gi):
+                blocks.index_copy_(0, gi, g[r, self.head: self.head + 36 * len(gi)].view(-1, 36))
+        return out
+
+
+def exchange_normal_equations(local, ex: PairExchange, rank: int, gathered, out=None):
+    """All-gather every rank's compact system (length ex.L, zero-padded) and combine it on
+    the solver rank (rank 0).  `gathered` is an (N * L) buffer on the same device."""
+    import torch.distributed as dist
+
+    dist.all_gather_into_tensor(gathered, local)
+    if rank == 0:
+        return ex.combine(gathered, out)
+    return None
 
 
 def shard_loads(weights, shards) -> np.ndarray:

@@ -224,3 +224,76 @@ def test_two_rank_cost_allreduce_matches_single_process():
         assert n == rn and n > 0
         assert abs(c - rc) <= 1e-12 * abs(rc)
     assert got[0][1] == got[1][1]  # every rank holds the same total
+
+
+def _pair_ex_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(8)
+    V, F = 12, 90
+    vs = rng.integers(0, V, F)
+    vt = (vs + rng.integers(1, V, F)) % V
+    unary = np.zeros(F, bool)
+    rec = rng.normal(size=(F, 92))
+    rec[:, 91] = rng.integers(0, 40, F)
+    shards = sharding.pair_shards(vs, vt, rng.integers(200, 600, F), world)
+    ex = sharding.PairExchange(vs, vt, unary, V, shards)
+    mine = shards[rank]
+    local = np.zeros(ex.L)
+    part = assemble_np(rec[mine], vs[mine], vt[mine], unary[mine], V, ex.rank_pairs[rank])
+    assert len(part) == ex.local_size(rank)
+    local[: len(part)] = part
+    gathered = torch.zeros(world * ex.L, dtype=torch.float64)
+    out = sharding.exchange_normal_equations(torch.from_numpy(local), ex, rank, gathered)
+    if rank == 0:
+        ref = assemble_np(rec, vs, vt, unary, V, ex.pairs)
+        got = out.numpy()
+        head = ex.head
+        q.put((bool(np.array_equal(got[head:], ref[head:])),
+               float(np.max(np.abs(got[:head] - ref[:head]) / np.maximum(np.abs(ref[:head]), 1.0))),
+               [len(p) for p in ex.rank_pairs], len(ex.pairs)))
+    dist.destroy_process_group()
+
+
+def test_pair_disjoint_exchange_matches_single_process():
+    """Pair-disjoint shards (both factors of a variable pair on one rank): every rank's compact
+    system (all diagonal blocks, its own pair blocks), all-gathered and combined on the
+    solver rank, equals the single-process assembly — pair blocks bit for bit (each pair is
+    summed on one rank in factor order), diagonal blocks / gradient / cost to fp64
+    reassociation (rank-order sum)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pair_ex_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    pairs_exact, head_err, rank_pairs, total_pairs = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert pairs_exact
+    assert head_err < 1e-12
+    assert sum(rank_pairs) == total_pairs and min(rank_pairs) > 0
+
+
+def test_pair_shards_are_pair_disjoint_and_balanced():
+    rng = np.random.default_rng(1)
+    poses = synthetic.random_submap_poses(rng, 300)
+    pairs = synthetic.nearest_pairs(poses, 20)
+    w = rng.integers(200, 601, 300)[pairs[:, 0]]
+    for n in (2, 4, 8):
+        shards = sharding.pair_shards(pairs[:, 0], pairs[:, 1], w, n)
+        assert sorted(np.concatenate(shards).tolist()) == list(range(len(pairs)))
+        owner = np.empty(len(pairs), int)
+        for r, s in enumerate(shards):
+            owner[s] = r
+        key = {}
+        for f, (a, b) in enumerate(pairs):
+            k = (min(a, b), max(a, b))
+            assert key.setdefault(k, owner[f]) == owner[f]
+        loads = sharding.shard_loads(w, shards)
+        assert loads.max() / loads.min() < 1.02
+        ex = sharding.PairExchange(pairs[:, 0], pairs[:, 1], np.zeros(len(pairs), bool), 300,
+                                   shards)
+        assert ex.pmax <= 1.1 * len(ex.pairs) / n + 1
