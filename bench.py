@@ -8,13 +8,13 @@ One step = one linearization of every factor of the graph: compose T_ij from the
 into the per-factor H_ii/H_ij/H_jj/b_i/b_j/cost records (K5).
 
 N > 1 (one process per GPU; `--gpus N` spawns them through torch.distributed.run when
-WORLD_SIZE is unset): the fixed 50,000-factor graph is sharded pair-disjointly across the ranks
-(strong scaling; sharding.pair_shards), the solver rank broadcasts the pose table, every rank
-linearizes its shard and assembles its compact normal equations (K6: diagonal blocks +
-gradient for every variable, the off-diagonal blocks of its own pairs), and one all-gather
-puts them on the solver rank, which combines them into the global block-sparse system
-(sharding.PairExchange) — so the N > 1 step does strictly more than the N = 1 step (K6, the
-exchange and the combine on top), and the driver's scaling ratio is conservative.
+WORLD_SIZE is unset): the fixed 50,000-factor graph is sharded by target map across the ranks
+(strong scaling; sharding.target_shards: each rank reads ~1/N of the voxel maps), the solver
+rank broadcasts the pose table, every rank linearizes its shard and assembles its blocks of
+the normal equations straight into the global block-sparse layout (K6: diagonal blocks +
+gradient of every variable, its pairs' blocks at their global slots), and one NCCL
+sum-reduction puts the system on the solver rank — so the N > 1 step does strictly more than
+the N = 1 step (K6 and the reduction on top), and the driver's scaling ratio is conservative.
 `--backend gloo` runs the same multi-rank path with CPU collectives, ranks sharing GPUs
 (a functional check on a one-GPU box, not a timing).
 
@@ -57,6 +57,12 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--sharding", choices=["target", "pair"], default="target",
+                    help="N > 1: target-local shards along a Morton curve (default) or "
+                         "pair-disjoint LPT shards")
+    ap.add_argument("--exchange", choices=["reduce", "gather"], default="reduce",
+                    help="N > 1: sum-reduce the global layout (default) or all-gather "
+                         "compact per-rank systems and combine on the solver rank")
     ap.add_argument("--cpu-full-pass", action="store_true",
                     help="reference arm: also time one pass over the whole workload")
     return ap.parse_args()
@@ -282,7 +288,10 @@ def run_ours(args):
     F = len(wl.pairs)
     V = wl.pose_table.shape[0]
     if world > 1:
-        shards = sharding.pair_shards(wl.pairs[:, 0], wl.pairs[:, 1], weights, world)
+        if args.sharding == "target":
+            shards = sharding.target_shards(wl.pairs[:, 1], weights, world, wl.pose_table[:, 4:7])
+        else:
+            shards = sharding.pair_shards(wl.pairs[:, 0], wl.pairs[:, 1], weights, world)
         ex = sharding.PairExchange(wl.pairs[:, 0], wl.pairs[:, 1], np.zeros(F, bool), V, shards)
     else:
         shards, ex = [np.arange(F)], None
@@ -301,23 +310,47 @@ def run_ours(args):
 
     ne_local = gathered = ne_global = None
     if world > 1:
-        # this rank's compact normal equations: diagonal blocks + gradient of every variable,
-        # off-diagonal blocks of its own pairs (pair-disjoint shards)
-        batch.assemble_setup(V, ex.rank_pairs[rank])
-        assert batch.asm_size == ex.local_size(rank)
-        ne_local = torch.zeros(ex.L, dtype=torch.float64, device="cuda")
-        gathered = torch.zeros(world * ex.L, dtype=torch.float64,
-                               device="cpu" if gloo else "cuda")
-        ne_global = torch.zeros(ex.size, dtype=torch.float64, device="cuda")
+        if args.exchange == "reduce":
+            # K6 writes this rank's blocks straight into the global layout (diagonal blocks +
+            # gradient of every variable, its own pair blocks at their global slots; other
+            # slots stay zero) and one sum-reduction to the solver rank yields the system
+            batch.assemble_setup_mapped(V, ex.rank_pairs[rank], ex.gidx[rank], len(ex.pairs))
+            assert batch.asm_size == ex.size
+            ne_local = torch.zeros(ex.size, dtype=torch.float64, device="cuda")
+            ne_global = ne_local
+        else:
+            # compact per-rank layout, all-gather, solver-rank combine (sharding.PairExchange)
+            batch.assemble_setup(V, ex.rank_pairs[rank])
+            assert batch.asm_size == ex.local_size(rank)
+            ne_local = torch.zeros(ex.L, dtype=torch.float64, device="cuda")
+            gathered = torch.zeros(world * ex.L, dtype=torch.float64,
+                                   device="cpu" if gloo else "cuda")
+            ne_global = torch.zeros(ex.size, dtype=torch.float64, device="cuda")
 
     def exchange():
-        if gloo:  # CPU collectives (functional check)
+        if args.exchange == "reduce":
+            if gloo:  # CPU collectives (functional check)
+                host = ne_local.cpu()
+                sharding.reduce_normal_equations(host, 0)
+                if rank == 0:
+                    ne_local.copy_(host)
+            else:
+                sharding.reduce_normal_equations(ne_local, 0)
+            return
+        if gloo:
             host = ne_local.cpu()
             sharding.exchange_normal_equations(host, ex, rank, gathered)
             if rank == 0:
                 ne_global.copy_(ex.combine(gathered))
         else:
             sharding.exchange_normal_equations(ne_local, ex, rank, gathered, ne_global)
+
+    def assemble():
+        # the solver rank's buffer holds the last reduction: its other ranks' pair slots must be
+        # zero again before this rank's K6 writes its own blocks
+        if args.exchange == "reduce" and rank == 0:
+            ne_local.zero_()
+        batch.assemble_records_device(out_dev.data_ptr(), ne_local.data_ptr())
 
     def bcast_poses():
         if gloo:
@@ -342,7 +375,7 @@ def run_ours(args):
             e[2].record()
         batch.finalize_device(_lib.MODE_LINEARIZE, out_dev.data_ptr())
         if world > 1:
-            batch.assemble_records_device(out_dev.data_ptr(), ne_local.data_ptr())
+            assemble()
             if e:
                 e[3].record()
             exchange()
@@ -355,7 +388,7 @@ def run_ours(args):
         batch.linearize_poses_device(poses_dev.data_ptr(), V, _lib.MODE_LINEARIZE,
                                      out_dev.data_ptr())
         if world > 1:
-            batch.assemble_records_device(out_dev.data_ptr(), ne_local.data_ptr())
+            assemble()
             exchange()
 
     for _ in range(max(3, args.warmup)):
@@ -502,12 +535,20 @@ def run_ours(args):
                         "sample": desc}, **extra)
         multi = None
         if world > 1:
-            multi = {"backend": args.backend, "sharding": "pair-disjoint LPT on point count",
+            multi = {"backend": args.backend,
+                     "sharding": ("target-local (Morton order of the submap positions), balanced "
+                                  "on point count" if args.sharding == "target"
+                                  else "pair-disjoint LPT on point count"),
                      "rank_ms_per_step": rank_ms,
                      "rank_factors": [int(len(s)) for s in shards],
                      "rank_points": [int(weights[s].sum()) for s in shards],
-                     "exchange": "all-gather of compact normal equations + solver-rank combine",
-                     "exchange_bytes_per_rank": int(ex.L * 8), "global_pairs": int(len(ex.pairs)),
+                     "exchange": ("sum-reduction of the global layout to the solver rank "
+                                  "(each rank's K6 writes only its own pair blocks)"
+                                  if args.exchange == "reduce" else
+                                  "all-gather of compact normal equations + solver-rank combine"),
+                     "exchange_bytes_per_rank": int((ex.size if args.exchange == "reduce"
+                                                     else ex.L) * 8),
+                     "global_pairs": int(len(ex.pairs)),
                      "global_system_bytes": int(ex.size * 8)}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,

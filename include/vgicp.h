@@ -217,6 +217,13 @@ int vg_batch_assemble_setup(vg_batch* batch, int64_t num_vars, int64_t* num_pair
  * combines them.  Pairs of this batch missing from the list: VG_ERR_INVALID. */
 int vg_batch_assemble_setup_pairs(vg_batch* batch, int64_t num_vars, const int32_t* pairs,
                                   int64_t num_pairs, int64_t* out_doubles);
+/* the batch's own pair list, each block written at out_index[p] of an output layout with
+ * out_pairs pair slots (increasing): a rank of a pair-disjoint shard writes its blocks
+ * straight into the global layout (slots of other ranks' pairs stay untouched, i.e. zero in a
+ * zeroed buffer), so one sum-reduction yields the global system */
+int vg_batch_assemble_setup_mapped(vg_batch* batch, int64_t num_vars, const int32_t* pairs,
+                                   int64_t num_pairs, const int32_t* out_index,
+                                   int64_t out_pairs, int64_t* out_doubles);
 int vg_batch_assemble_pairs(const vg_batch* batch, int32_t* pairs_out /* P x 2 */);
 int vg_batch_assemble_poses(vg_batch* batch, const double* poses_host, int64_t num_poses,
                             double* out_host);

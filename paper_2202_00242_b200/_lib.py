@@ -95,6 +95,8 @@ _SIGNATURES = {
     "vg_batch_assemble_setup": ([c_void_p, c_int64, _P_I64, _P_I64], c_int),
     "vg_batch_assemble_setup_pairs": ([c_void_p, c_int64, POINTER(c_int32), c_int64, _P_I64],
                                       c_int),
+    "vg_batch_assemble_setup_mapped": ([c_void_p, c_int64, POINTER(c_int32), c_int64,
+                                        POINTER(c_int32), c_int64, _P_I64], c_int),
     "vg_batch_assemble_pairs": ([c_void_p, POINTER(c_int32)], c_int),
     "vg_batch_assemble_poses": ([c_void_p, _P_D, c_int64, _P_D], c_int),
     "vg_batch_assemble_poses_device": ([c_void_p, c_void_p, c_int64, c_void_p], c_int),
@@ -469,6 +471,22 @@ class DeviceBatch:
         self.asm_pairs = pairs
         self.asm_size = int(total.value)
         return pairs
+
+    def assemble_setup_mapped(self, num_vars: int, pairs: np.ndarray, out_index: np.ndarray,
+                              out_pairs: int) -> int:
+        """Assembly over this batch's `pairs` (sorted), pair p's block written at slot
+        out_index[p] of a layout with out_pairs slots; returns that layout's size (doubles)."""
+        pairs = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        idx = np.ascontiguousarray(out_index, dtype=np.int32)
+        total = c_int64()
+        check(self.ctx.lib.vg_batch_assemble_setup_mapped(
+            self.handle, int(num_vars), pairs.ctypes.data_as(POINTER(c_int32)), len(pairs),
+            idx.ctypes.data_as(POINTER(c_int32)), int(out_pairs), ctypes.byref(total)),
+            "vg_batch_assemble_setup_mapped")
+        self.asm_vars = int(num_vars)
+        self.asm_pairs = pairs
+        self.asm_size = int(total.value)
+        return self.asm_size
 
     def assemble_poses(self, poses: np.ndarray, out: np.ndarray | None = None,
                        unpack: bool = True):

@@ -560,6 +560,11 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
   const long long want = (long long)sms * 32;
   long long chunk = ((total_pts + want - 1) / want + 31) / 32 * 32;
   chunk = std::max<long long>(64, std::min<long long>(kMaxChunk, chunk));
+  static const long long chunk_env = [] {
+    const char* e = getenv("VGICP_CHUNK");  // ablation: fixed points per work item
+    return e ? atoll(e) : 0LL;
+  }();
+  if (chunk_env > 0) chunk = std::max<long long>(32, std::min<long long>(kMaxChunk, chunk_env));
   for (int64_t f : order) {
     const long long n = specs[f].source->n;
     npts += n;
@@ -697,6 +702,7 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->poses);
   dfree(ctx, b->asm_begin);
   dfree(ctx, b->asm_codes);
+  dfree(ctx, b->asm_pidx);
   dfree(ctx, b->asm_out);
   dfree(ctx, b->asm_partial);
   dfree(ctx, b->asm_done);
@@ -1016,7 +1022,8 @@ int vg_batch_finalize_device(vg_batch* b, int mode, double* out_dev) {
 }
 
 static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, int64_t given_P,
-                          int64_t* num_pairs, int64_t* out_doubles);
+                          int64_t* num_pairs, int64_t* out_doubles,
+                          const int32_t* out_index = nullptr, int64_t out_pairs = -1);
 
 int vg_batch_assemble_setup(vg_batch* b, int64_t num_vars, int64_t* num_pairs,
                             int64_t* out_doubles) {
@@ -1029,8 +1036,21 @@ int vg_batch_assemble_setup_pairs(vg_batch* b, int64_t num_vars, const int32_t* 
   return assemble_setup(b, num_vars, pairs, num_pairs, nullptr, out_doubles);
 }
 
+int vg_batch_assemble_setup_mapped(vg_batch* b, int64_t num_vars, const int32_t* pairs,
+                                   int64_t num_pairs, const int32_t* out_index,
+                                   int64_t out_pairs, int64_t* out_doubles) {
+  if (num_pairs < 0 || (num_pairs && (!pairs || !out_index)) || out_pairs < num_pairs)
+    return fail(VG_ERR_INVALID, "invalid pair list");
+  for (int64_t p = 0; p < num_pairs; ++p)
+    if (out_index[p] < 0 || out_index[p] >= out_pairs || (p && out_index[p] <= out_index[p - 1]))
+      return fail(VG_ERR_INVALID, "output pair slots must be increasing and < out_pairs");
+  return assemble_setup(b, num_vars, pairs, num_pairs, nullptr, out_doubles, out_index,
+                        out_pairs);
+}
+
 static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, int64_t given_P,
-                          int64_t* num_pairs, int64_t* out_doubles) {
+                          int64_t* num_pairs, int64_t* out_doubles, const int32_t* out_index,
+                          int64_t out_pairs) {
   if (!b || num_vars <= 0 || num_vars >= (1LL << 28))
     return fail(VG_ERR_INVALID, "invalid assembly arguments");
   vg_ctx* ctx = b->ctx;
@@ -1098,9 +1118,15 @@ static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, i
   }
   begin.push_back((int)codes.size());
   const long long P = (long long)pairs.size() / 2;
-  const long long total = 2 + V * 27 + P * 36;
+  const long long P_out = out_index ? out_pairs : P;
+  const long long total = 2 + V * 27 + P_out * 36;
   dfree(ctx, b->asm_begin);
   dfree(ctx, b->asm_codes);
+  dfree(ctx, b->asm_pidx);
+  if (out_index && P) {
+    VG_CHECK(dalloc(ctx, &b->asm_pidx, (size_t)P));
+    VG_CHECK(h2d(ctx, b->asm_pidx, out_index, sizeof(int) * P));
+  }
   dfree(ctx, b->asm_out);
   b->asm_begin = nullptr;
   b->asm_codes = nullptr;
@@ -1118,6 +1144,7 @@ static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, i
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
   b->asm_vars = V;
   b->asm_pairs_n = P;
+  b->asm_out_pairs = P_out;
   b->asm_pairs = pairs;
   if (num_pairs) *num_pairs = P;
   if (out_doubles) *out_doubles = total;
@@ -1163,7 +1190,7 @@ int vg_batch_assemble_poses(vg_batch* b, const double* poses_host, int64_t V, do
   VG_CHECK(ensure_poses(b, V));
   VG_CHECK(h2d(b->ctx, b->poses, poses_host, sizeof(double) * 8 * V));
   VG_CHECK(run_assemble(b, b->poses, V, b->asm_out));
-  const size_t total = 2 + (size_t)b->asm_vars * 27 + (size_t)b->asm_pairs_n * 36;
+  const size_t total = 2 + (size_t)b->asm_vars * 27 + (size_t)b->asm_out_pairs * 36;
   return d2h_sync(b->ctx, out_host, b->asm_out, sizeof(double) * total);
 }
 

@@ -146,6 +146,8 @@ struct vg_batch {
   std::vector<int> asm_pairs;         // P x 2 (a < b)
   int* asm_begin = nullptr;           // units + 1
   int* asm_codes = nullptr;           // factor * 8 + role
+  int* asm_pidx = nullptr;            // P: output slot of each pair block (mapped setup) or null
+  long long asm_out_pairs = 0;        // pair blocks in the output layout (>= asm_pairs_n)
   double* asm_out = nullptr;          // device output (host-buffer entry point)
   double* asm_partial = nullptr;      // per-CTA cost partials of k_assemble_cost
   unsigned* asm_done = nullptr;       // its arrival counter (reset by the last CTA)

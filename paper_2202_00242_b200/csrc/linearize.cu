@@ -407,9 +407,11 @@ constexpr int kAsmWarps = 1;  // one-warp CTAs: the long diagonal units do not h
 __global__ void __launch_bounds__(kAsmWarps * 32)
     k_assemble(const double* __restrict__ rec, const FactorDev* __restrict__ factors, int F,
                const int* __restrict__ begin, const int* __restrict__ codes, int V, int P,
-               double* __restrict__ out) {
+               const int* __restrict__ pidx, double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * kAsmWarps + (threadIdx.x >> 5);
+  pdl_release();
+  pdl_wait();  // records written by K5
   if (u >= V + P) return;
   const int k0 = __ldg(begin + u), k1 = __ldg(begin + u + 1);
   const bool diag = u < V;
@@ -446,7 +448,9 @@ __global__ void __launch_bounds__(kAsmWarps * 32)
     if (lane < 21) out[2 + (size_t)u * 21 + lane] = acc0;
     else if (lane < 27) out[2 + (size_t)V * 21 + (size_t)u * 6 + (lane - 21)] = acc0;
   } else {
-    double* o = out + 2 + (size_t)V * 27 + (size_t)(u - V) * 36;
+    // pair block slot: the unit's own index, or its slot in a larger (e.g. global) layout
+    const int slot = pidx ? __ldg(pidx + (u - V)) : u - V;
+    double* o = out + 2 + (size_t)V * 27 + (size_t)slot * 36;
     o[lane] = acc0;
     if (has1) o[lane + 32] = acc1;
   }
@@ -747,6 +751,8 @@ __global__ void __launch_bounds__(kCostThreads)
   __shared__ double sc[kCostThreads], sn[kCostThreads];
   __shared__ bool last;
   const int t = threadIdx.x;
+  pdl_release();
+  pdl_wait();  // per-factor gated costs written by K5
   const int per = (F + kCostBlocks - 1) / kCostBlocks;
   const int f0 = blockIdx.x * per, f1 = min(F, f0 + per);
   double c = 0.0, n = 0.0;
@@ -789,11 +795,13 @@ __global__ void __launch_bounds__(kCostThreads)
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev) {
   const int units = (int)(b->asm_vars + b->asm_pairs_n);
   if (units > 0)
-    k_assemble<<<(units + kAsmWarps - 1) / kAsmWarps, kAsmWarps * 32, 0, ctx->stream>>>(rec, b->factors, (int)b->F, b->asm_begin,
-                                                       b->asm_codes, (int)b->asm_vars,
-                                                       (int)b->asm_pairs_n, out_dev);
-  k_assemble_cost<<<kCostBlocks, kCostThreads, 0, ctx->stream>>>(
-      b->asm_gcost, (int)b->F, b->asm_partial, b->asm_done, out_dev);
+    VG_CUDA(launch_pdl(k_assemble, dim3((units + kAsmWarps - 1) / kAsmWarps), dim3(kAsmWarps * 32),
+                       0, ctx->stream, rec, (const FactorDev*)b->factors, (int)b->F,
+                       (const int*)b->asm_begin, (const int*)b->asm_codes, (int)b->asm_vars,
+                       (int)b->asm_pairs_n, (const int*)b->asm_pidx, out_dev));
+  VG_CUDA(launch_pdl(k_assemble_cost, dim3(kCostBlocks), dim3(kCostThreads), 0, ctx->stream,
+                     (const double2*)b->asm_gcost, (int)b->F, b->asm_partial, b->asm_done,
+                     out_dev));
   ctx->launches += 2;
   VG_CUDA(cudaGetLastError());
   return 0;

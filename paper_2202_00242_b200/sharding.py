@@ -59,6 +59,41 @@ def pair_shards(var_source, var_target, weights, n_shards: int) -> list:
     return [np.flatnonzero(rank == r).astype(np.int64) for r in range(n_shards)]
 
 
+def target_shards(var_target, weights, n_shards: int, positions=None) -> list:
+    """Target-local shards: all factors of a target map on one rank, targets ordered along a
+    Morton (Z-order) curve of their positions (`positions`: (V, 3), e.g. the pose table's
+    translations; target index order when absent) and cut into n contiguous runs of equal
+    summed weight.  A rank then reads ~1/n of the voxel maps — and mostly the source clouds of
+    nearby submaps, the ones its targets are paired with — instead of nearly all of them, so
+    its DRAM traffic shrinks with n (pair-disjoint shards scatter every map over all ranks).
+    A variable pair's two factors can land on two ranks: their pair block is then summed by
+    the exchange's reduction (global layout) or combine."""
+    vt = np.asarray(var_target, np.int64)
+    w = np.asarray(weights, np.float64)
+    nv = int(vt.max(initial=0)) + 1
+    tw = np.bincount(vt, weights=w, minlength=nv)
+    if positions is not None:
+        p = np.asarray(positions, np.float64)[:nv, :3]
+        lo, hi = p.min(0), p.max(0)
+        q = np.clip(((p - lo) / np.maximum(hi - lo, 1e-12) * 1023).astype(np.int64), 0, 1023)
+        code = np.zeros(nv, np.int64)
+        for bit in range(10):
+            for ax in range(3):
+                code |= ((q[:, ax] >> bit) & 1) << (3 * bit + ax)
+        order = np.argsort(code, kind="stable")
+    else:
+        order = np.arange(nv)
+    cum = np.cumsum(tw[order])
+    total = cum[-1] if len(cum) else 0.0
+    # target k of the order goes to the rank whose weight interval holds its midpoint
+    mid = cum - tw[order] / 2
+    rank_sorted = np.minimum((mid / max(total, 1e-30) * n_shards).astype(np.int64), n_shards - 1)
+    rank_of_target = np.empty(nv, np.int64)
+    rank_of_target[order] = rank_sorted
+    rank = rank_of_target[vt]
+    return [np.flatnonzero(rank == r).astype(np.int64) for r in range(n_shards)]
+
+
 class PairExchange:
     """Layout of the pair-disjoint normal-equation exchange (see the module docstring).
 
@@ -66,9 +101,9 @@ class PairExchange:
     ``rank_pairs[r]``: [cost, count, diag V x 21, grad V x 6, pairs P_r x 36], padded to a
     common length ``L`` for the all-gather.  ``combine`` turns the gathered (N, L) block into
     the global system over ``pairs`` (the sorted union): cost, count, diagonal blocks and
-    gradient summed over ranks in rank order, pair blocks copied from their owning rank
-    (each pair's contributions were already summed on that rank in factor order, exactly as
-    the single-GPU assembly sums them)."""
+    gradient summed over ranks in rank order, pair blocks placed from their rank (with
+    pair-disjoint shards each pair's contributions were summed on one rank in factor order,
+    exactly as the single-GPU assembly sums them; a pair shared by two ranks is summed)."""
 
     def __init__(self, var_source, var_target, unary, num_vars: int, shards):
         vs = np.asarray(var_source, np.int64)
@@ -81,8 +116,9 @@ class PairExchange:
         self.gidx = [np.array([index[(int(a), int(b))] for a, b in rp], np.int64)
                      for rp in self.rank_pairs]
         cat = np.concatenate(self.gidx) if self.gidx else np.zeros(0, np.int64)
-        if len(cat) != len(self.pairs) or len(np.unique(cat)) != len(cat):
-            raise ValueError("shards are not pair-disjoint")
+        if len(np.unique(cat)) != len(self.pairs):
+            raise ValueError("the shards do not cover the graph's pairs")
+        self.pair_disjoint = len(cat) == len(self.pairs)
         self.head = 2 + 27 * self.V
         self.pmax = max((len(p) for p in self.rank_pairs), default=0)
         self.L = self.head + 36 * self.pmax
@@ -103,9 +139,10 @@ class PairExchange:
         blocks = out[self.head:].view(-1, 36)
         if not hasattr(self, "_gidx_t") or self._gidx_t[0].device != g.device:
             self._gidx_t = [torch.as_tensor(i, device=g.device) for i in self.gidx]
-        for r, gi in enumerate(self._gidx_t):
+        blocks.zero_()
+        for r, gi in enumerate(self._gidx_t):   # rank order: a shared pair sums in rank order
             if len(gi):
-                blocks.index_copy_(0, gi, g[r, self.head: self.head + 36 * len(gi)].view(-1, 36))
+                blocks.index_add_(0, gi, g[r, self.head: self.head + 36 * len(gi)].view(-1, 36))
         return out
 
 

@@ -31,12 +31,21 @@ def _torchrun(n, script, *args, env=None):
     return [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
 
 
-@pytest.mark.parametrize("n", [2, 3])
-def test_sharded_normal_equations_equal_one_rank(n):
-    (res,) = _torchrun(n, ROOT / "tests" / "multirank_worker.py")
-    assert res["world"] == n and min(res["rank_factors"]) > 0
-    assert res["pair_blocks_bit_exact"] and res["count_equal"]
+@pytest.mark.parametrize("n,exchange,shard", [(2, "reduce", "target"), (3, "reduce", "target"),
+                                               (2, "gather", "target"), (2, "reduce", "pair"),
+                                               (3, "gather", "pair")])
+def test_sharded_normal_equations_equal_one_rank(n, exchange, shard):
+    """Rank systems reduced / gathered onto the solver rank equal the one-rank assembly: pair
+    blocks bit for bit when the shards are pair-disjoint, else (a pair's two factors on two
+    ranks, summed by the exchange) to fp64 reassociation, like the diagonal blocks."""
+    (res,) = _torchrun(n, ROOT / "tests" / "multirank_worker.py",
+                       env={"MR_EXCHANGE": exchange, "MR_SHARDING": shard})
+    assert res["world"] == n and res["exchange"] == exchange and min(res["rank_factors"]) > 0
+    assert res["count_equal"]
     assert res["head_max_rel"] < 1e-12
+    if res["pair_disjoint"]:
+        assert res["pair_blocks_bit_exact"]
+    assert res["pair_max_rel"] < 1e-12
 
 
 def test_bench_two_ranks_gloo_runs_the_multi_gpu_path():
