@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--exchange", choices=["reduce", "gather"], default="reduce",
                     help="N > 1: sum-reduce the global layout (default) or all-gather "
                          "compact per-rank systems and combine on the solver rank")
+    ap.add_argument("--no-lm", action="store_true",
+                    help="skip the one-iteration reference LM measurement (N = 1)")
     ap.add_argument("--cpu-full-pass", action="store_true",
                     help="reference arm: also time one pass over the whole workload")
     return ap.parse_args()
@@ -257,6 +259,66 @@ def run_reference(args):
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def lm_iteration(wl):
+    """One config-5 LM iteration through the REFERENCE's own FactorGraph.optimize_lm
+    (factor_graph.py:546-612, installed unmodified in baseline/_ref) with the drop-in patched
+    in (integrate.patch): 1,000 submap-pose variables, a gauge prior on submap 0, the 50,000
+    MatchingCostFactors of the workload.  Wall-clock seconds of the iteration and of its
+    parts; the sparse solve stays the reference's host splu (north_star)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "limapper").is_dir():
+        return {"unavailable": "reference not installed in baseline/_ref "
+                               "(tools/install_reference.sh)"}
+    if str(ref) not in sys.path:
+        sys.path.append(str(ref))
+    import limapper.factor_graph as fg
+    import limapper.geometry as rgeo
+    from limapper.preprocess import Frame
+
+    from paper_2202_00242_b200 import integrate
+    from paper_2202_00242_b200.registration import GaussianVoxelMap
+
+    integrate.patch("limapper")
+    t0 = time.perf_counter()
+    g = fg.FactorGraph()
+    for i in range(wl.n_submaps):
+        row = wl.pose_table[i]
+        g.add_variable(fg.submap_key(i), rgeo.Se3Pose(rgeo.Rotation(row[:4]), row[4:7].copy()))
+    g.add_factor(fg.PriorFactor(fg.submap_key(0), g.values[fg.submap_key(0)], np.full(6, 1e6)))
+    frames = [Frame(points=wl.scans[i][sel], stamps=np.zeros(len(sel)), stamp=0.0,
+                    covs=wl.scan_covs[i][sel], deskewed=True)
+              for i, sel in enumerate(wl.source_index)]
+    maps = [GaussianVoxelMap._from_device(wl.resolution, m) for m in wl.maps]
+    for i, j in wl.pairs:
+        g.add_factor(fg.MatchingCostFactor(fg.submap_key(int(i)), frames[i], maps[j],
+                                           key_target=fg.submap_key(int(j))))
+    build_s = time.perf_counter() - t0
+    slices, dim = g._slices()
+    t0 = time.perf_counter()
+    g.total_cost()                      # first call: device batch + assembly setup
+    g._assemble_dense(g.values, slices, dim)
+    setup_s = time.perf_counter() - t0
+    parts = {}
+    for name, fn in (("total_cost_s", lambda: g.total_cost()),
+                     ("assemble_dense_s", lambda: g._assemble_dense(g.values, slices, dim))):
+        ts = []
+        for _ in range(3):
+            a = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - a)
+        parts[name] = statistics.median(ts)
+    a = time.perf_counter()
+    res = g.optimize_lm(fg.LmSettings(max_iterations=1))
+    it_s = time.perf_counter() - a
+    return {"seconds": it_s, "iterations": res.iterations, "final_cost": res.final_cost,
+            "variables": wl.n_submaps, "factors": int(len(wl.pairs)), "tangent_dim": dim,
+            "graph_build_s": round(build_s, 2), "first_call_setup_s": round(setup_s, 2),
+            **parts,
+            "api": "limapper FactorGraph.optimize_lm(LmSettings(max_iterations=1)), reference "
+                   "LM + host sparse solve, drop-in total_cost / _assemble_dense / "
+                   "MatchingCostFactor"}
 
 
 def run_ours(args):
@@ -526,6 +588,12 @@ def run_ours(args):
     k4_avg_s = statistics.mean(k4_ms) / 1e3
     achieved = BYTES_PER_CORR * my_points / k4_avg_s / 1e9
 
+    lm_line = None
+    if world == 1 and not args.no_lm:
+        try:
+            lm_line = lm_iteration(wl)
+        except Exception as exc:  # report, never sink the bench line
+            lm_line = {"error": repr(exc)[:300]}
     if rank == 0:
         clocks = clk.summary()
         cpu = None
@@ -575,6 +643,7 @@ def run_ours(args):
             "e2e_f64_records": e2e64_line,
             "e2e_normal_equations": ne_line,
             "cost_mode": cost_line,
+            "lm_iteration": lm_line,
             "multi_gpu": multi,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -142,6 +142,15 @@ int vg_match_terms(vg_ctx* ctx, const vg_cloud* cloud, const vg_map* map, const 
                    int64_t* rows, double* moved, double* d, double* weight, double* wd,
                    double* cost, int64_t* inliers);
 
+/* replaces linearize_from_terms (registration.py:207-248) for a MatchTerms that carries the
+ * per-point terms but not the voxel map (e.g. one built by the reference's own match_terms):
+ * points = the hit source points (n x 3), weight (n x 3 x 3), wd (n x 3), T = T_ij; cost and
+ * inliers as in the terms.  out: one VG_MODE_LINEARIZE record (92 doubles).  Returns
+ * VG_ERR_DEGENERATE when inliers < min_inliers. */
+int vg_linearize_terms(vg_ctx* ctx, const double T[12], const double* points,
+                       const double* weight, const double* wd, int64_t n, double cost,
+                       int64_t inliers, int32_t flags, int32_t min_inliers, double* out);
+
 /* ---- batched linearization (the hot path) ---------------------------------------------- */
 /* A batch is the set of MatchingCostFactors of one graph (factor_graph.py:209-308); it is
  * flattened once into (factor, chunk) work items resident in HBM. */

@@ -76,6 +76,8 @@ _SIGNATURES = {
     "vg_cloud_lookup": ([c_void_p, c_void_p, c_void_p, _P_D, _P_I64, _P_I64], c_int),
     "vg_match_terms": ([c_void_p, c_void_p, c_void_p, _P_D, _P_I64, _P_D, _P_D, _P_D, _P_D,
                         _P_D, _P_I64], c_int),
+    "vg_linearize_terms": ([c_void_p, _P_D, _P_D, _P_D, _P_D, c_int64, c_double, c_int64,
+                            c_int32, c_int32, _P_D], c_int),
     "vg_batch_create": ([c_void_p, POINTER(vg_factor_spec), c_int64, _PP], c_int),
     "vg_batch_info": ([c_void_p, _P_I64, _P_I64, _P_I64], c_int),
     "vg_batch_destroy": ([c_void_p], c_int),

@@ -410,6 +410,33 @@ int vg_match_terms(vg_ctx* ctx, const vg_cloud* cloud, const vg_map* map, const 
   return VG_OK;
 }
 
+int vg_linearize_terms(vg_ctx* ctx, const double T[12], const double* points, const double* weight,
+                       const double* wd, int64_t n, double cost, int64_t inliers, int32_t flags,
+                       int32_t min_inliers, double* out) {
+  if (!ctx || !T || !out || n < 0 || (n && (!points || !weight || !wd)))
+    return fail(VG_ERR_INVALID, "null argument");
+  if (inliers < min_inliers)  // registration.py:213-215
+    return fail(VG_ERR_DEGENERATE, std::to_string(inliers) + " inliers (minimum " +
+                                       std::to_string(min_inliers) + ")");
+  VG_CUDA(cudaSetDevice(ctx->device));
+  FactorDev f;
+  memset(&f, 0, sizeof(f));
+  for (int k = 0; k < 12; ++k) f.T[k] = T[k];
+  f.flags = flags;
+  f.min_inliers = min_inliers;
+  DeviceTemps temps(ctx->stream);
+  double *dp = nullptr, *dw = nullptr, *dwd = nullptr, *dout = nullptr;
+  VG_CUDA(temps.alloc(&dp, 3 * (size_t)n));
+  VG_CUDA(temps.alloc(&dw, 9 * (size_t)n));
+  VG_CUDA(temps.alloc(&dwd, 3 * (size_t)n));
+  VG_CUDA(temps.alloc(&dout, 92));
+  VG_CHECK(h2d(ctx, dp, points, sizeof(double) * 3 * n));
+  VG_CHECK(h2d(ctx, dw, weight, sizeof(double) * 9 * n));
+  VG_CHECK(h2d(ctx, dwd, wd, sizeof(double) * 3 * n));
+  VG_CHECK(launch_terms_linearize(ctx, dp, dw, dwd, n, f, cost, (double)inliers, dout));
+  return d2h_sync(ctx, out, dout, sizeof(double) * 92);
+}
+
 // ---- batches ----------------------------------------------------------------------------
 int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batch** out) {
   if (!ctx || !out || F < 0 || (F && !specs)) return fail(VG_ERR_INVALID, "invalid batch arguments");

@@ -235,6 +235,10 @@ int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                  const double* T_dev, long long* rows, double* moved, double* d, double* w,
                  double* wd, double* partial_cost, long long* partial_inl, int nblocks);
 int launch_compose(vg_ctx* ctx, vg_batch* b, const double* poses_dev);
+// linearize_from_terms over explicit per-point terms (vg_linearize_terms)
+int launch_terms_linearize(vg_ctx* ctx, const double* mu_dev, const double* W_dev,
+                           const double* wd_dev, long long n, const vg::FactorDev& f,
+                           double cost, double inliers, double* out_dev);
 int launch_spread_T(vg_ctx* ctx, vg_batch* b);  // FactorDev.T -> ItemHdr.T (explicit-T mode)
 int launch_accumulate(vg_ctx* ctx, vg_batch* b, int kmode);  // K4a + K4b
 // K5; f32: MODE_LINEARIZE records in the compact host format (VG_REC_LINEARIZE_F32 words)

@@ -375,6 +375,92 @@ __global__ void __launch_bounds__(kFinWarps * 32)
   for (int k = lane; k < 92; k += 32) out[(size_t)fi * 92 + k] = sw[32 + k];
 }
 
+
+// ---- K3f: Gauss-Newton blocks from explicit per-point terms (linearize_from_terms with a
+// MatchTerms that carries no voxel map, e.g. one made by the reference's own match_terms,
+// registration.py:207-248).  The weights W and W d come from the caller; per point the kernel
+// forms the target-frame terms about the source origin (lever arm x' = R mu, as K4b) and
+// one block reduces them in a fixed order; thread 0 then expands the 29 sums like K5.
+constexpr int kTermThreads = 256;
+__global__ void __launch_bounds__(kTermThreads)
+    k_terms_linearize(const double* __restrict__ mu, const double* __restrict__ W,
+                      const double* __restrict__ wd, long long n, FactorDev f, double cost,
+                      double inliers, double* __restrict__ out) {
+  __shared__ double red[kTermThreads / 32][29];
+  __shared__ double sums[32];
+  __shared__ double rec[92];
+  double acc[27];
+#pragma unroll
+  for (int k = 0; k < 27; ++k) acc[k] = 0.0;
+  const double* R = f.T;
+  for (long long i = threadIdx.x; i < n; i += kTermThreads) {
+    const double px = mu[3 * i], py = mu[3 * i + 1], pz = mu[3 * i + 2];
+    const double vx = fma(R[0], px, fma(R[1], py, R[2] * pz));
+    const double vy = fma(R[3], px, fma(R[4], py, R[5] * pz));
+    const double vz = fma(R[6], px, fma(R[7], py, R[8] * pz));
+    const double* w = W + 9 * i;
+    const double i00 = w[0], i01 = w[1], i02 = w[2], i11 = w[4], i12 = w[5], i22 = w[8];
+    const double wd0 = wd[3 * i], wd1 = wd[3 * i + 1], wd2 = wd[3 * i + 2];
+    // N = hat(x') W, P = N hat(x')^T, b' = [x' x Wd ; Wd] (J' = [-hat(x') | I]), as K4b
+    const double N00 = fma(-vz, i01, vy * i02), N01 = fma(-vz, i11, vy * i12),
+                 N02 = fma(-vz, i12, vy * i22);
+    const double N10 = fma(vz, i00, -vx * i02), N11 = fma(vz, i01, -vx * i12),
+                 N12 = fma(vz, i02, -vx * i22);
+    const double N20 = fma(-vy, i00, vx * i01), N21 = fma(-vy, i01, vx * i11),
+                 N22 = fma(-vy, i02, vx * i12);
+    acc[0] += fma(-vz, N01, vy * N02);
+    acc[1] += fma(vz, N00, -vx * N02);
+    acc[2] += fma(-vy, N00, vx * N01);
+    acc[3] += fma(vz, N10, -vx * N12);
+    acc[4] += fma(-vy, N10, vx * N11);
+    acc[5] += fma(-vy, N20, vx * N21);
+    acc[6] += N00;
+    acc[7] += N01;
+    acc[8] += N02;
+    acc[9] += N10;
+    acc[10] += N11;
+    acc[11] += N12;
+    acc[12] += N20;
+    acc[13] += N21;
+    acc[14] += N22;
+    acc[15] += i00;
+    acc[16] += i01;
+    acc[17] += i02;
+    acc[18] += i11;
+    acc[19] += i12;
+    acc[20] += i22;
+    acc[21] += fma(vy, wd2, -vz * wd1);
+    acc[22] += fma(vz, wd0, -vx * wd2);
+    acc[23] += fma(vx, wd1, -vy * wd0);
+    acc[24] += wd0;
+    acc[25] += wd1;
+    acc[26] += wd2;
+  }
+  // fixed-order reduction: butterfly inside each warp, warps in index order
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 27; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+    if (lane == 0) red[wid][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 27) {
+    double v = 0.0;
+    for (int q = 0; q < kTermThreads / 32; ++q) v += red[q][threadIdx.x];
+    sums[threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    sums[27] = cost;
+    sums[28] = inliers;
+    expand_record(f, sums, rec);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 92; k += kTermThreads) out[k] = rec[k];
+}
+
 // ---- K6: block-sparse normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536)
 // One warp per output unit: unit u < V is variable u's diagonal block (21, upper) + gradient
 // (6); V <= u < V + P is the H block of variable pair u - V (36).  The cost is k_assemble_cost.
@@ -683,6 +769,16 @@ int launch_terms(vg_ctx* ctx, const CloudView& cv, const MapView& mv, const doub
   if (cv.n == 0) return 0;
   k_terms<<<nblocks, 256, 0, ctx->stream>>>(cv, mv, T_dev, rows, moved, d, w, wd, partial_cost,
                                             partial_inl);
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_terms_linearize(vg_ctx* ctx, const double* mu_dev, const double* W_dev,
+                           const double* wd_dev, long long n, const FactorDev& f, double cost,
+                           double inliers, double* out_dev) {
+  k_terms_linearize<<<1, kTermThreads, 0, ctx->stream>>>(mu_dev, W_dev, wd_dev, n, f, cost,
+                                                         inliers, out_dev);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;

@@ -10,9 +10,12 @@ each factor then serves its own record from an identity-keyed cache, exactly as 
 reference's ``_terms_cache`` does for one factor (:253-269).  Values are immutable, so
 identity of (v_i, v_j) is a safe key.
 
-``FactorGraph`` / ``PriorFactor`` restate the reference's host LM (:425-612) so the drop-in
-can be exercised end to end where the reference package is absent (the GPU box); the LM
-solve stays on the host as in the reference.
+The LM stays the reference's own (factor_graph.py:445-612): ``integrate.patch(limapper)``
+swaps in this MatchingCostFactor and replaces two FactorGraph methods whose per-factor loops
+dominate at global-mapping scale — ``total_cost`` (:472-474: one batched cost launch for all
+of the graph's matching factors) and ``_assemble_dense`` (:522-536: the normal equations
+summed on the device, K6, and scattered into the reference's dense H/g); see
+``graph_total_cost`` / ``graph_assemble_dense``.
 """
 
 from __future__ import annotations
@@ -23,17 +26,9 @@ from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
-import scipy.linalg
-import scipy.sparse
-import scipy.sparse.linalg
 
 from . import _lib
-from .geometry import (
-    pose_local,
-    pose_retract,
-    pose_row,
-    so3_right_jacobian_inv,
-)
+from .geometry import pose_row
 from .preprocess import device_cloud
 from .registration import _as_device_map, unpack_sym6
 
@@ -167,6 +162,20 @@ class _Batcher:
             f._store(values, mode, rec)
 
 
+    def gated_costs(self, group, values) -> np.ndarray:
+        """Per-factor gated cost of `group` at `values` (MatchingCostFactor.cost, factor order)
+        from ONE cost-mode launch over exactly these factors."""
+        batch, var_keys, fixed, _ = self._batch_for(group)
+        poses = np.empty((len(var_keys) + fixed.shape[0], 8))
+        for i, k in enumerate(var_keys):
+            poses[i] = pose_row(_pose_of(k.kind, values[k]))
+        if fixed.shape[0]:
+            poses[len(var_keys):] = fixed
+        rec = batch.linearize_poses(poses, _lib.MODE_COST)
+        self.evaluations += 1
+        mins = np.fromiter((f.min_inliers for f in group), np.float64, len(group))
+        return np.where(rec[:, 1] >= mins, rec[:, 0], 0.0)
+
     def assemble(self, group, values, var_keys) -> "_lib.NormalEquations":
         """Device-assembled normal equations of `group` over the graph variables `var_keys`
         (FactorGraph._assemble_dense, factor_graph.py:522-536)."""
@@ -291,178 +300,60 @@ class MatchingCostFactor(Factor):
                                    {(0, 0): h_ii, (0, 1): h_ij, (1, 1): h_jj}, cost)
 
 
-# ---- host-side graph (restated so the drop-in runs where limapper is absent) ---------------
+# ---- FactorGraph methods replaced by integrate.patch (factor_graph.py:472-474, 522-536) ------
 
-class PriorFactor(Factor):
-    """Quadratic prior on a submap pose's tangent offset (factor_graph.py:129-167)."""
-
-    grounding = True
-    kind = "prior"
-
-    def __init__(self, key: Key, prior_value, information):
-        if key.kind != "submap-pose":
-            raise ValueError("this restatement supports submap-pose priors only")
-        self.keys = (key,)
-        self.prior = prior_value
-        info = np.asarray(information, dtype=float)
-        self.information = np.diag(info) if info.ndim == 1 else info
-
-    def cost(self, values) -> float:
-        r = pose_local(values[self.keys[0]], self.prior)
-        return float(r @ self.information @ r)
-
-    def linearize(self, values) -> FactorLinearization:
-        cur = values[self.keys[0]]
-        r = pose_local(cur, self.prior)
-        jac = np.eye(6)
-        jac[0:3, 0:3] = so3_right_jacobian_inv(r[:3])
-        jac[3:6, 3:6] = self.prior.rotation.matrix().T @ cur.rotation.matrix()
-        jtw = 2.0 * jac.T @ self.information
-        return FactorLinearization(self.keys, [jtw @ r], {(0, 0): jtw @ jac},
-                                   float(r @ self.information @ r))
+def _split_factors(graph):
+    """(GPU matching factors, the rest) of a graph, cached while its factor list is unchanged."""
+    facs = graph.factors
+    sig = (id(facs), len(facs), id(facs[-1]) if facs else 0)
+    cached = graph.__dict__.get("_vgicp_split")
+    if cached is not None and cached[0] == sig:
+        return cached[1], cached[2]
+    gpu, rest = [], []
+    for f in facs:
+        (gpu if isinstance(f, MatchingCostFactor) and not f._empty else rest).append(f)
+    graph.__dict__["_vgicp_split"] = (sig, gpu, rest)
+    return gpu, rest
 
 
-@dataclass
-class LmSettings:
-    max_iterations: int = 64
-    rel_cost_tol: float = 1e-9
-    update_tol: float = 1e-9
-    lambda_init: float = 1e-6
-    lambda_down: float = 0.5
-    lambda_up: float = 4.0
-    lambda_max: float = 1e12
-    dense_threshold: int = 600
+def graph_total_cost(self, values=None) -> float:
+    """FactorGraph.total_cost (factor_graph.py:472-474): the graph's matching factors in one
+    batched cost launch (their gated costs summed in factor order), the others per factor."""
+    values = self.values if values is None else values
+    gpu, rest = _split_factors(self)
+    total = 0.0
+    if gpu:
+        for c in _BATCHER.gated_costs(gpu, values):
+            total += float(c)
+    for f in rest:
+        total += f.cost(values)
+    return float(total)
 
 
-@dataclass
-class OptimizeResult:
-    estimates: dict
-    final_cost: float
-    iterations: int
-    converged: bool = True
-
-
-class NotConverged(RuntimeError):
-    def __init__(self, message, estimates=None, cost=None):
-        super().__init__(message)
-        self.estimates = estimates
-        self.cost = cost
-
-
-class FactorGraph:
-    """Variables + factors with the reference's damped Gauss-Newton (factor_graph.py:445-612)."""
-
-    def __init__(self):
-        self.values: dict = {}
-        self.factors: list = []
-
-    def add_variable(self, key: Key, initial_value) -> None:
-        if key in self.values:
-            raise ValueError(f"{key} already in graph")
-        self.values[key] = initial_value
-
-    def add_factor(self, factor: Factor) -> None:
-        for k in factor.keys:
-            if k not in self.values:
-                raise KeyError(f"factor references missing {k}")
-        self.factors.append(factor)
-
-    def total_cost(self, values=None) -> float:
-        values = self.values if values is None else values
-        return float(sum(f.cost(values) for f in self.factors))
-
-    def _slices(self):
-        out, off = {}, 0
-        for k in self.values:
-            out[k] = slice(off, off + k.dim)
-            off += k.dim
-        return out, off
-
-    #: sum the matching factors' blocks on the device (vg_batch_assemble_*) instead of per
-    #: factor on the host; results agree to fp64 rounding (block sums in factor order)
-    device_assembly = True
-
-    def _assemble_dense(self, values, slices, dim):
-        h = np.zeros((dim, dim))
-        g = np.zeros(dim)
-        cost = 0.0
-        factors = self.factors
-        if self.device_assembly:
-            gpu = [f for f in factors if isinstance(f, MatchingCostFactor) and not f._empty]
-            if gpu:
-                keys = list(self.values)
-                ne = _BATCHER.assemble(gpu, values, keys)
-                hd, gd = ne.dense([slices[k].start for k in keys], dim)
-                h += hd
-                g += gd
-                cost += ne.cost
-                factors = [f for f in factors
-                           if not (isinstance(f, MatchingCostFactor) and not f._empty)]
-        for f in factors:
-            lin = f.linearize(values)
-            cost += lin.cost
-            sls = [slices[k] for k in lin.keys]
-            for a, ga in enumerate(lin.g):
-                g[sls[a]] += ga
-            for (a, b), blk in lin.h.items():
-                h[sls[a], sls[b]] += blk
-                if a != b:
-                    h[sls[b], sls[a]] += blk.T
-        return h, g, cost
-
-    def _retract_all(self, values, slices, delta):
-        return {k: pose_retract(v, delta[slices[k]]) for k, v in values.items()}
-
-    def _solve(self, h, g, lam, diag, dense):
-        a = h + np.diag(lam * diag)
-        if dense:
-            return scipy.linalg.cho_solve(scipy.linalg.cho_factor(a, lower=True), -g)
-        return scipy.sparse.linalg.splu(scipy.sparse.csc_matrix(a)).solve(-g)
-
-    def optimize_lm(self, settings: LmSettings | None = None) -> OptimizeResult:
-        s = settings or LmSettings()
-        slices, dim = self._slices()
-        values = dict(self.values)
-        cost = self.total_cost(values)
-        lam = s.lambda_init
-        iterations = 0
-        dense = dim <= s.dense_threshold
-        for _ in range(s.max_iterations):
-            h, g, cost = self._assemble_dense(values, slices, dim)
-            iterations += 1
-            diag = np.diag(h).copy()
-            accepted = converged = False
-            while True:
-                try:
-                    delta = self._solve(h, g, lam, diag, dense)
-                    if not np.all(np.isfinite(delta)):
-                        raise np.linalg.LinAlgError("non-finite update")
-                except (np.linalg.LinAlgError, RuntimeError, ValueError):
-                    lam *= s.lambda_up
-                    if lam > s.lambda_max:
-                        self.values = values
-                        raise NotConverged("damping exhausted", estimates=values, cost=cost)
-                    continue
-                if np.max(np.abs(delta)) < s.update_tol:
-                    converged = True
-                    break
-                candidate = self._retract_all(values, slices, delta)
-                new_cost = self.total_cost(candidate)
-                if np.isfinite(new_cost) and new_cost < cost:
-                    values = candidate
-                    accepted = True
-                    lam = max(lam * s.lambda_down, 1e-12)
-                    break
-                lam *= s.lambda_up
-                if lam > s.lambda_max:
-                    self.values = values
-                    raise NotConverged("no cost-reducing step", estimates=values, cost=cost)
-            if converged:
-                break
-            if accepted and (cost - new_cost) <= s.rel_cost_tol * max(cost, 1e-30):
-                cost = new_cost
-                break
-            cost = new_cost
-        self.values = values
-        _, _, final = self._assemble_dense(values, slices, dim)
-        return OptimizeResult(values, final, iterations)
+def graph_assemble_dense(self, values, slices, dim):
+    """FactorGraph._assemble_dense (factor_graph.py:522-536): the matching factors' blocks
+    summed into the block-sparse normal equations on the device (K6, factor order per block)
+    and scattered into the dense H/g the reference's solver takes (6-dof blocks top-left of
+    15-dof frame-state slices, :292-308); the other factors per factor as the reference does."""
+    h = np.zeros((dim, dim))
+    g = np.zeros(dim)
+    cost = 0.0
+    gpu, rest = _split_factors(self)
+    if gpu:
+        keys = list(self.values)
+        ne = _BATCHER.assemble(gpu, values, keys)
+        hd, gd = ne.dense([slices[k].start for k in keys], dim)
+        h += hd
+        g += gd
+        cost += ne.cost
+    for f in rest:
+        lin = f.linearize(values)
+        cost += lin.cost
+        sls = [slices[k] for k in lin.keys]
+        for a, ga in enumerate(lin.g):
+            g[sls[a]] += ga
+        for (a, b), blk in lin.h.items():
+            h[sls[a], sls[b]] += blk
+            if a != b:
+                h[sls[b], sls[a]] += blk.T
+    return h, g, cost

@@ -7,11 +7,13 @@
 
 Every replaced name keeps the reference's signature, argument meaning and exceptions
 (registration.py:29-269, preprocess.py:68-164, factor_graph.py:209-308); the keyframe overlap
-matrix of OdometryEstimator (odometry.py:396-403) becomes one batched lookup launch.  Modules that
+matrix of OdometryEstimator (odometry.py:396-403) becomes one batched lookup launch, and
+FactorGraph.total_cost / _assemble_dense (factor_graph.py:472-474, 522-536) batch the graph's
+matching factors (one cost launch; device-assembled normal equations).  Modules that
 imported a name with ``from .registration import ...`` (factor_graph.py:49-55,
-odometry.py:21-46) get their module-level binding replaced too; the reference's
-FactorGraph, LM solver, IMU factors and odometry logic are untouched and call the drop-in
-through the unchanged per-factor Factor protocol.
+odometry.py:21-46) get their module-level binding replaced too; the reference's LM solver
+(optimize_lm), IMU factors and odometry logic are untouched and call the drop-in through the
+unchanged Factor protocol.  patch() is idempotent (a second call changes nothing).
 """
 
 from __future__ import annotations
@@ -67,10 +69,18 @@ def _overlap_matrix(self):
                               [kf.pose() for kf in kfs])
 
 
-# methods of reference classes whose per-pair loops become one batched GPU call
+# methods of reference classes whose per-factor / per-pair loops become batched GPU calls
 METHOD_REPLACEMENTS = {
     "odometry": {"OdometryEstimator": {"_overlap_matrix": _overlap_matrix}},
+    # FactorGraph.total_cost (factor_graph.py:472-474): one batched cost launch for the
+    # graph's matching factors; _assemble_dense (:522-536): their normal equations summed on
+    # the device (K6) and scattered into the dense H/g the reference's LM solves
+    "factor_graph": {"FactorGraph": {"total_cost": _fg.graph_total_cost,
+                                     "_assemble_dense": _fg.graph_assemble_dense}},
 }
+
+#: (class, method name) -> the reference's own function, for callers that compare against it
+ORIGINALS: dict = {}
 
 
 def _module(pkg, sub):
@@ -94,7 +104,7 @@ def patch(pkg="limapper"):
         if mod is None:
             continue
         for name, obj in names.items():
-            if hasattr(mod, name):
+            if hasattr(mod, name) and getattr(mod, name) is not obj:
                 saved.append((mod, name, getattr(mod, name)))
                 setattr(mod, name, obj)
     for sub, classes in METHOD_REPLACEMENTS.items():
@@ -104,8 +114,9 @@ def patch(pkg="limapper"):
             if cls is None:
                 continue
             for name, fn in methods.items():
-                if name in vars(cls):
+                if name in vars(cls) and vars(cls)[name] is not fn:
                     saved.append((cls, name, vars(cls)[name]))
+                    ORIGINALS.setdefault((cls, name), vars(cls)[name])
                     setattr(cls, name, fn)
 
     # deskew keeps the reference's host IMU integration (taken from its preprocess module) and

@@ -394,16 +394,29 @@ def linearize_from_terms(frame_i, terms: MatchTerms, t_ij, target_fixed: bool = 
                          source_hats: np.ndarray | None = None) -> MatchingCostLinearization:
     """Gauss-Newton blocks from a MatchTerms (registration.py:207-248).
 
-    The correspondences of ``terms`` are a deterministic function of (frame, map, t_ij), so
-    the fused kernel recomputes them in registers instead of reading them back.
+    A MatchTerms from this package's match_terms carries its voxel map, so the fused kernel
+    recomputes the correspondences in registers instead of reading them back.  Any other
+    MatchTerms (e.g. the reference's own, which has no map) is linearized on the GPU from its
+    explicit per-point weights (vg_linearize_terms).
     """
     if terms.inliers < min_inliers:
         raise DegenerateConstraint(f"{terms.inliers} inliers (minimum {min_inliers})")
     vmap = getattr(terms, "_map", None)
-    if vmap is None:
-        raise TypeError("linearize_from_terms needs MatchTerms produced by this package's "
-                        "match_terms (it carries the voxel map the kernel re-reads)")
-    return _linearize_tij(frame_i, vmap, t_ij, target_fixed, min_inliers)
+    if vmap is not None:
+        return _linearize_tij(frame_i, vmap, t_ij, target_fixed, min_inliers)
+    hit = np.asarray(terms.hit, bool)
+    pts = _lib.f64(np.asarray(frame_i.points, float)[hit])
+    W = _lib.f64(terms.weight).reshape(-1, 9)
+    wd = _lib.f64(terms.wd).reshape(-1, 3)
+    if not (len(pts) == len(W) == len(wd)):
+        raise ValueError("MatchTerms arrays disagree with the frame's hit mask")
+    rec = np.empty(92)
+    ctx = _lib.context()
+    _lib.check(ctx.lib.vg_linearize_terms(
+        ctx.handle, _lib.dptr(transform12(t_ij)), _lib.dptr(pts), _lib.dptr(W), _lib.dptr(wd),
+        len(pts), float(terms.cost), int(terms.inliers), _lib.FACTOR_UNARY if target_fixed else 0,
+        int(min_inliers), _lib.dptr(rec)), "linearize_from_terms")
+    return unpack_record(rec, target_fixed)
 
 
 def linearize_matching_cost(frame_i, map_j, t_i, t_j, target_fixed: bool = False,

@@ -894,3 +894,46 @@ def test_f32_records_are_the_rounded_fp64_records(small_graph, config5):
         cost, inl = _lib.record_cost_inliers_f32(r32)
         assert np.array_equal(cost, r64[:, 90]) and np.array_equal(inl, r64[:, 91].astype(np.int64))
         assert np.all(r32[:, 93] == 0)
+
+
+def test_linearize_from_terms_accepts_foreign_match_terms(golden):
+    """linearize_from_terms with a MatchTerms that carries no voxel map (the reference's own
+    match_terms makes those: registration.py:133-157) linearizes the explicit per-point
+    weights on the GPU (vg_linearize_terms) — the same blocks as the map-carrying path and the
+    oracle, within the parity bar; binary and unary."""
+    from dataclasses import dataclass
+
+    @dataclass
+    class ForeignTerms:  # the reference MatchTerms' fields, nothing else
+        hit: np.ndarray
+        moved: np.ndarray
+        d: np.ndarray
+        weight: np.ndarray
+        wd: np.ndarray
+        cost: float
+        inliers: int
+
+    g = golden("registration")
+    src = make_frame(g["src_points"], g["src_covs"])
+    _, k, mu, c, n = golden_map(g)
+    vm = RG.GaussianVoxelMap(0.5, k, mu, c, n)
+    for case in range(6):
+        R, t = g[f"case{case}_R"], g[f"case{case}_t"]
+        unary = bool(g[f"case{case}_unary"])
+        terms = RG.match_terms(src, vm, _TPose(R, t))
+        if terms.inliers < 10:
+            continue
+        foreign = ForeignTerms(terms.hit, terms.moved, terms.d, terms.weight, terms.wd,
+                               terms.cost, terms.inliers)
+        ref = {k: (g[f"case{case}_{k}"] if f"case{case}_{k}" in g.files else None)
+               for k in NAMES + ("cost", "inliers")}
+        ref["inliers"] = int(ref["inliers"])
+        lin = RG.linearize_from_terms(src, foreign, _TPose(R, t), target_fixed=unary)
+        assert_lin(lin, ref, unary)
+        mine = RG.linearize_from_terms(src, terms, _TPose(R, t), target_fixed=unary)
+        for name in NAMES:
+            if getattr(mine, name) is not None:
+                assert_tol(getattr(lin, name), getattr(mine, name), name)
+    with pytest.raises(DegenerateConstraint):
+        RG.linearize_from_terms(src, ForeignTerms(terms.hit, terms.moved, terms.d, terms.weight,
+                                                  terms.wd, terms.cost, 3), _TPose(R, t))

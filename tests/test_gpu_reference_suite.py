@@ -1,0 +1,84 @@
+"""The reference's own test suite through the drop-in boundary (VERDICT r1 "missing" 2-4).
+
+Runs the unmodified limapper tests (installed with the reference by tools/install_reference.sh
+into baseline/_ref, git-ignored; skipped where that install is absent) in a subprocess whose
+pytest plugin applies ``integrate.patch(limapper)`` first — so registration (build_voxelmap,
+match_terms, matching_cost, overlap_rate, linearize_*), preprocess (pack_voxel_keys,
+voxel_downsample, knn_search, estimate_covariances, deskew), MatchingCostFactor (driven by the
+reference's own FactorGraph / optimize_lm) and the odometry overlap matrix run on libvgicp.
+Among them: the reference's quadratic-expansion oracle and finite-difference Jacobian check
+(test_registration.py:254-370), the kNN/covariance tests (test_preprocess.py:84-160) and the
+two-pose registration + determinism tests (test_factor_graph.py:120-191)."""
+
+import os
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parents[1]
+REF = ROOT / "baseline" / "_ref"
+SUITE = REF / "limapper_tests"
+
+
+def _run(files, unpatched=False, timeout=1500):
+    env = dict(os.environ)
+    env["PYTHONPATH"] = os.pathsep.join([str(REF), str(ROOT), str(ROOT / "tests"),
+                                         env.get("PYTHONPATH", "")])
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    if unpatched:
+        env["VGICP_REF_SUITE_UNPATCHED"] = "1"
+    cmd = [sys.executable, "-m", "pytest", "-p", "ref_suite_plugin", "-p", "no:cacheprovider",
+           "-q", "-rA", "--rootdir", str(SUITE), "-c", os.devnull,
+           *[str(SUITE / f) for f in files]]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env,
+                       cwd=str(SUITE))
+    passed = re.findall(r"^PASSED (\S+)", r.stdout, re.M)
+    failed = re.findall(r"^(?:FAILED|ERROR) (\S+)", r.stdout, re.M)
+    return r, passed, failed
+
+
+needs_ref = pytest.mark.skipif(not SUITE.is_dir(),
+                               reason="reference install absent (tools/install_reference.sh)")
+
+
+@needs_ref
+@pytest.mark.parametrize("module", ["test_registration.py", "test_preprocess.py",
+                                    "test_factor_graph.py", "*"])
+def test_reference_suite_module_through_the_drop_in(module):
+    files = sorted(p.name for p in SUITE.glob("test_*.py")) if module == "*" else [module]
+    r, passed, failed = _run(files)
+    print(r.stdout[-4000:])
+    m = re.search(r"paper_2202_00242_b200 drop-in .*kernel launches: (\d+)", r.stdout)
+    assert m, r.stdout[-3000:]
+    assert not failed, f"{module}: {failed}\n{r.stdout[-6000:]}\n{r.stderr[-3000:]}"
+    assert r.returncode == 0 and len(passed) > 0
+    assert int(m.group(1)) > 0  # the suite's VGICP calls ran on libvgicp
+
+
+@needs_ref
+def test_drop_in_is_what_the_reference_suite_called():
+    """The patched suite really ran libvgicp: a reference test module sees the drop-in's
+    classes and the library's kernel launch counter moved."""
+    code = ("import sys; sys.path[:0] = [%r, %r]\n"
+            "from paper_2202_00242_b200 import integrate, _lib\n"
+            "integrate.patch('limapper')\n"
+            "import limapper.registration as R, limapper.factor_graph as F\n"
+            "import numpy as np\n"
+            "assert R.build_voxelmap.__module__.startswith('paper_2202_00242_b200')\n"
+            "assert F.MatchingCostFactor.__module__.startswith('paper_2202_00242_b200')\n"
+            "from limapper.preprocess import Frame\n"
+            "p = np.random.default_rng(0).uniform(-2, 2, (500, 3))\n"
+            "f = Frame(points=p, stamps=np.zeros(500), stamp=0.0,\n"
+            "          covs=np.tile(np.eye(3) * 0.01, (500, 1, 1)), deskewed=True)\n"
+            "from limapper.geometry import Se3Pose\n"
+            "vm = R.build_voxelmap(f, 0.5)\n"
+            "c, n = R.matching_cost(f, vm, Se3Pose.identity())\n"
+            "print('launches', _lib.context().launch_count(), n)\n") % (str(REF), str(ROOT))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    launches, n = map(int, r.stdout.split()[1:3])
+    assert launches > 0 and n == 500
