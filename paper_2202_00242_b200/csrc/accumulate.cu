@@ -310,7 +310,8 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     int slot = -1;
     if (q.live) {
       unsigned bk = q.bucket;
-      for (;;) {
+      for (unsigned probes = 0;; ++probes) {
+        VG_DEVICE_CHECK(probes <= mask, "K4a: every bucket visited");
         int found = -1;
         bool empty = false;
 #pragma unroll
@@ -329,6 +330,9 @@ __global__ void __launch_bounds__(kLookupWarps * 32, kMinBlocks)
     }
     // misses contribute nothing (registration.py:150-156)
     const unsigned mb = __ballot_sync(0xffffffffu, slot >= 0);
+    VG_DEVICE_CHECK(cnt + __popc(mb) <= end - begin, "K4a: hits overflow the item region");
+    VG_DEVICE_CHECK(slot < 0 || (i >= begin && i < end), "K4a: hit outside the item");
+    VG_DEVICE_CHECK(slot < (int)((mask + 1) * kBucket32), "K4a: slot out of the table");
     if (slot >= 0) st_hit(out + cnt + __popc(mb & lt_mask), make_int2(i, slot));
     cnt += __popc(mb);
   };
@@ -613,6 +617,8 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
   AccSmem<kStages, PT>& sm = reinterpret_cast<AccSmem<kStages, PT>*>(smem_raw)[wib];
   const AccDesc* dsc = descs + w;
   const int n = __ldg(&dsc->n);
+  VG_DEVICE_CHECK(n >= 0 && n <= isz, "K4b: hit count exceeds the item");
+  VG_DEVICE_CHECK(__ldg(&dsc->hoff) == hoff, "K4b: descriptor / item hit-list offsets differ");
   const int2* hl = hits + hoff;
   // the item's hit list (contiguous) was written by K4a and may have left L2: one prefetch
   // per 128 B line for its first 512 entries, all issued up front, instead of a DRAM round
@@ -795,6 +801,7 @@ __global__ void k_export_rows(const ItemDev* __restrict__ items, int n_items,
   long long* dst = rows + pt_off[items[w].factor];
   for (int k = lane; k < n; k += 32) {
     const int2 h = hits[hoff + k];
+    VG_DEVICE_CHECK(h.x >= items[w].begin && h.x < items[w].end, "export: point outside item");
     dst[h.x] = recs[h.y].row;
   }
 }

@@ -9,11 +9,35 @@
 //            use int64 keys (64 B buckets) + a row array and row-indexed records.
 //   work   : (factor, chunk) items, one warp per item; fp64 partials, fixed-order reduce.
 #pragma once
+#include <cstdio>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace vg {
+
+// Device-side bounds / invariant checks, compiled in by the checked build
+// (tools/build_variant.sh checked "-DVG_CHECKS=1"): the memory-safety net used in place of
+// compute-sanitizer, which is closed on this GPU pool.  A failed check prints and traps (the
+// launch fails with cudaErrorLaunchFailure / illegal instruction; the library returns
+// VG_ERR_CUDA), so a test run against the checked library fails loudly on a violation.
+#ifndef VG_CHECKS
+#define VG_CHECKS 0
+#endif
+#if VG_CHECKS
+#define VG_DEVICE_CHECK(cond, what)                                                       \
+  do {                                                                                     \
+    if (!(cond)) {                                                                         \
+      printf("VG_DEVICE_CHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__,   \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define VG_DEVICE_CHECK(cond, what) \
+  do {                              \
+  } while (0)
+#endif
 
 constexpr int kKeyOffset = 1 << 20;   // preprocess.py:21-22
 constexpr int kWarpsPerBlock = 4;
@@ -292,7 +316,8 @@ __device__ __forceinline__ int slot_row(const MapView& mv, int slot, int kmode) 
 __device__ __forceinline__ int probe_query(const MapView& mv, const Query& q) {
   if (mv.m == 0 || !q.inside) return -1;
   unsigned b = q.bucket;
-  for (;;) {
+  for (unsigned probes = 0;; ++probes) {
+    VG_DEVICE_CHECK(probes <= mv.mask, "probe_query: every bucket visited");
     const ProbeGroup g = probe_load(mv, b, mv.kmode);
     int slot = -1;
     const int r = probe_scan(mv, g, b, q, slot, mv.kmode);

@@ -514,6 +514,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32)
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int code = __shfl_sync(0xffffffffu, my_code, (j + q) & 31);
+        VG_DEVICE_CHECK(j + q >= nk || (code >> 3) < F, "K6: contribution of no factor");
         v0[q] = 0.0;
         v1[q] = 0.0;
         if (j + q < nk) {

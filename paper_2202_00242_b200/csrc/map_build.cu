@@ -389,14 +389,19 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
     const unsigned k32 =
         (unsigned)(dx - mv.bx) | ((unsigned)(dy - mv.by) << 11) | ((unsigned)(dz - mv.bz) << 22);
     bool placed = false;
-    for (unsigned b = bucket32(k32, mv.shift); !placed; b = (b + 1) & mv.mask)
+    unsigned probes = 0;
+    for (unsigned b = bucket32(k32, mv.shift); !placed; b = (b + 1) & mv.mask, ++probes) {
+      VG_DEVICE_CHECK(probes <= mv.mask, "k_hash_insert: table full (32-bit keys)");
       for (int j = 0; j < kBucket32 && !placed; ++j) {
         h = (size_t)b * kBucket32 + j;
         placed = atomicCAS(pkeys32 + h, kEmpty32, k32) == kEmpty32;
       }
+    }
   } else {
     bool placed = false;
-    for (unsigned b = slot_of(key, mv.shift); !placed; b = (b + 1) & mv.mask)
+    unsigned probes = 0;
+    for (unsigned b = slot_of(key, mv.shift); !placed; b = (b + 1) & mv.mask, ++probes) {
+      VG_DEVICE_CHECK(probes <= mv.mask, "k_hash_insert: table full (int64 keys)");
       for (int j = 0; j < kBucket && !placed; ++j) {
         h = (size_t)b * kBucket + j;
         const unsigned long long prev =
@@ -404,6 +409,7 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
                       (unsigned long long)mv.empty_key, (unsigned long long)key);
         placed = prev == (unsigned long long)mv.empty_key;
       }
+    }
     prows[h] = r;
   }
   VoxelRec v;
@@ -420,6 +426,8 @@ __global__ void k_hash_insert(const long long* __restrict__ keys, const double* 
   v.row = r;
 #pragma unroll
   for (int k = 0; k < 6; ++k) v.pad[k] = 0.0;
+  VG_DEVICE_CHECK(h < (size_t)(mv.mask + 1) * (mv.kmode ? kBucket32 : kBucket),
+                  "k_hash_insert: slot out of the table");
   recs[mv.kmode ? h : (size_t)r] = v;
 }
 
