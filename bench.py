@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--exchange", choices=["reduce", "gather"], default="reduce",
                     help="N > 1: sum-reduce the global layout (default) or all-gather "
                          "compact per-rank systems and combine on the solver rank")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the single-GPU BASELINE configs 1-4 (N = 1 extra keys)")
     ap.add_argument("--no-lm", action="store_true",
                     help="skip the one-iteration reference LM measurement (N = 1)")
     ap.add_argument("--cpu-full-pass", action="store_true",
@@ -588,6 +590,23 @@ def run_ours(args):
     k4_avg_s = statistics.mean(k4_ms) / 1e3
     achieved = BYTES_PER_CORR * my_points / k4_avg_s / 1e9
 
+    configs = None
+    if world == 1 and not args.no_configs:
+        # BASELINE configs 1-4 (the single-GPU workloads north_star names) as extra keys: the
+        # same fields as this line (tools/bench_configs.py), with hit counts next to the
+        # correspondence counts
+        sys.path.insert(0, str(ROOT / "tools"))
+        import bench_configs
+
+        cargs = argparse.Namespace(steps=20, no_cpu=args.no_cpu_baseline, no_graph=False)
+        configs = {}
+        for c in (1, 2, 3, 4):
+            try:
+                configs[str(c)] = (bench_configs.run_preprocess(cargs) if c == 2
+                                   else bench_configs.run(c, cargs, ctx, stream))
+            except Exception as exc:
+                configs[str(c)] = {"error": repr(exc)[:300]}
+        ctx.set_stream(stream.cuda_stream)
     lm_line = None
     if world == 1 and not args.no_lm:
         try:
@@ -644,6 +663,7 @@ def run_ours(args):
             "e2e_normal_equations": ne_line,
             "cost_mode": cost_line,
             "lm_iteration": lm_line,
+            "configs": configs,
             "multi_gpu": multi,
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

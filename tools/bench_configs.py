@@ -130,8 +130,10 @@ def run(cfg, args, ctx, stream):
                "sample": f"first {nf} factors, {sample['points']} correspondences per pass, "
                          f"oracle linearization (unary factors evaluated as binary), "
                          f"{procs}-process fork pool, 2 passes"}
+    hits = int(out_h[:, 91].sum())  # inlier correspondences (hits) of the e2e records
     cfgd = dict(wl.config)
-    cfgd.update({"workload": wl.name, "corr_per_step": wl.num_points,
+    cfgd.update({"workload": wl.name, "corr_per_step": wl.num_points, "hits_per_step": hits,
+                 "hit_fraction": round(hits / max(wl.num_points, 1), 4),
                  "l2": "flushed between timed steps (256 MB write)",
                  "step": "one CUDA graph (compose + K4a + K4b + K5)" if not args.no_graph
                  else "stream launches"})
