@@ -690,6 +690,168 @@ __global__ void __launch_bounds__(kAccWarps * 32, kMinBlocks)
 }
 
 
+
+// ---- K4b with TMA record gathers (VG_TMA_REC) ---------------------------------------------
+// The fast-path K4b (fp32-exact points, plane-form covariances) with the 80 B voxel records
+// fetched by the tensor-memory accelerator instead of cooperative cp.async: per round, lanes
+// 0..7 each issue one cp.async.bulk.tensor.2d...tile::gather4 (4 record rows of the map's
+// record tensor -> 320 B of shared memory), completing on the stage's mbarrier; no LSU / L1
+// wavefronts for the record gathers.  Lane-own point / covariance gathers stay cp.async.
+// Record rows of a group land 80 B apart in a 128 B-aligned 384 B slot.
+struct alignas(128) AccStageTma {
+  float4 pt[32];
+  float4 cov[3][32];
+  float4 rec[8][24];  // group g = records 4g..4g+3 at rec[g][5 * (q % 4) + unit]
+};
+struct alignas(128) AccSmemTma {
+  AccStageTma stage[2];
+  unsigned long long bar[2];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred P1;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE_%=;\nbra WAIT_%=;\nDONE_%=:\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void* dst, const void* tmap, int r0, int r1, int r2,
+                                            int r3, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void issue_round_tma(const CloudView& cv, const void* tmap,
+                                                AccSmemTma& sm, int round, int2 e, int nvalid,
+                                                int lane) {
+  AccStageTma& st = sm.stage[round & 1];
+  if (lane < nvalid) {
+    cp_async16_sel<2>(&st.pt[lane], cv.a + e.x);
+    cp_async16_sel<2>(&st.cov[0][lane], cv.c0 + e.x);
+    cp_async16_sel<2>(&st.cov[1][lane], cv.c1 + e.x);
+    cp_async16_sel<2>(&st.cov[2][lane], cv.c2 + e.x);
+  }
+  cp_async_commit();
+  // record rows of group (lane & 7); rows past the round's hits replay a valid one
+  const int g = lane & 7;
+  int rr[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) rr[k] = __shfl_sync(0xffffffffu, e.y, 4 * g + k);
+  const int ngroups = nvalid <= 0 ? 0 : min(8, (nvalid + 3) >> 2);
+#pragma unroll
+  for (int k = 1; k < 4; ++k)
+    if (4 * g + k >= nvalid) rr[k] = rr[0];
+  if (lane == 0) mbar_expect_tx(&sm.bar[round & 1], 320u * (unsigned)ngroups);
+  if (lane < ngroups) tma_gather4(&st.rec[g][0], tmap, rr[0], rr[1], rr[2], rr[3], &sm.bar[round & 1]);
+}
+
+template <int MODE, int kMinBlocks>
+__global__ void __launch_bounds__(32, kMinBlocks)
+    k_accumulate_tma(const AccDesc* __restrict__ descs, const ItemDev* __restrict__ items,
+                     const void* const* __restrict__ item_tmap, int n_items,
+                     const int2* __restrict__ hits, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  AccSmemTma& sm = *reinterpret_cast<AccSmemTma*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x;
+  pdl_release();
+  const int w_ = min(w, n_items - 1);
+  const int hoff = __ldg(&items[w_].hoff);
+  const int isz = __ldg(&items[w_].end) - __ldg(&items[w_].begin);
+  const void* tmap = item_tmap[w_];
+  if (lane == 0) {
+    mbar_init(&sm.bar[0], 1);
+    mbar_init(&sm.bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  pdl_wait();  // descriptors and hit lists written by K4a
+  if (w >= n_items) return;
+  const AccDesc* dsc = descs + w;
+  const int n = __ldg(&dsc->n);
+  VG_DEVICE_CHECK(n >= 0 && n <= isz, "K4b-tma: hit count exceeds the item");
+  const int2* hl = hits + hoff;
+  if (16 * lane < isz) asm volatile("prefetch.global.L2 [%0];" ::"l"(hl + 16 * lane));
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(dsc->T + k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = __ldg(dsc->T + 9 + k);
+  CloudView cv;
+  cv.a = (const float4*)__ldg((const unsigned long long*)&dsc->a);
+  cv.xyz64 = nullptr;
+  cv.c0 = (const double2*)__ldg((const unsigned long long*)&dsc->c0);
+  cv.c1 = (const double2*)__ldg((const unsigned long long*)&dsc->c1);
+  cv.c2 = (const double2*)__ldg((const unsigned long long*)&dsc->c2);
+  cv.n = 0;
+  double acc[28];
+#pragma unroll
+  for (int k = 0; k < 28; ++k) acc[k] = 0.0;
+  const int rounds = (n + 31) / 32;
+  const int klast = isz > 0 ? isz - 1 : 0;
+  if (n > 0) {
+    issue_round_tma(cv, tmap, sm, 0, ld_hit(hl + min(lane, klast)), n, lane);
+    int2 nxt = ld_hit(hl + min(32 + lane, klast));
+    int2 nxt2 = ld_hit(hl + min(64 + lane, klast));
+    for (int r = 0; r < rounds; ++r) {
+      const int ri = r + 1;
+      issue_round_tma(cv, tmap, sm, ri, nxt, n - ri * 32, lane);
+      nxt = nxt2;
+      nxt2 = ld_hit(hl + min((ri + 2) * 32 + lane, klast));
+      cp_async_wait<1>();
+      mbar_wait(&sm.bar[r & 1], (unsigned)((r >> 1) & 1));
+      __syncwarp();
+      if (r * 32 + lane < n) {
+        const AccStageTma& st = sm.stage[r & 1];
+        const float4 a = st.pt[lane];
+        const double2 s0 = *reinterpret_cast<const double2*>(&st.cov[0][lane]);
+        const double2 s1 = *reinterpret_cast<const double2*>(&st.cov[1][lane]);
+        const double2 s2 = *reinterpret_cast<const double2*>(&st.cov[2][lane]);
+        hit_core<MODE, 1>(a.x, a.y, a.z, s0, s1, s2, &st.rec[lane >> 2][5 * (lane & 3)], R, t,
+                          1.0, acc);
+      }
+      __syncwarp();  // stage r & 1 is refilled by round r + 2
+    }
+    cp_async_wait<0>();
+    // the last issued round (rounds) may still be in flight on its mbarrier: drain it so no
+    // async-proxy write lands in shared memory after the CTA exits
+    mbar_wait(&sm.bar[rounds & 1], (unsigned)((rounds >> 1) & 1));
+  }
+  if (MODE == 1) {
+    double c = acc[27];
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+    if (lane == 0) {
+      partials[2 * (size_t)w] = c;
+      partials[2 * (size_t)w + 1] = (double)n;
+    }
+    return;
+  }
+  double v[32];
+#pragma unroll
+  for (int k = 0; k < 28; ++k) v[k] = acc[k];
+  v[28] = lane == 0 ? (double)n : 0.0;
+  v[29] = 0.0;
+  v[30] = 0.0;
+  v[31] = 0.0;
+  partials[(size_t)w * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
+}
+
 }  // namespace vg
 
 using namespace vg;
@@ -738,9 +900,40 @@ static int launch_acc_kernel(vg_ctx* ctx, K kern, size_t smem, const AccDesc* d,
   return 0;
 }
 
+#ifndef VG_TMA_REC
+#define VG_TMA_REC 0
+#endif
+#ifndef VG_K4B_MINB_TMA
+#define VG_K4B_MINB_TMA 15
+#endif
+
 static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cnt,
                             cudaStream_t st) {
   const AccDesc* d = b->descs + off;
+  static const int tma_env = [] {
+    const char* e = getenv("VGICP_TMA_REC");  // 0/1 overrides the build default
+    return e ? atoi(e) : VG_TMA_REC;
+  }();
+  if (tma_env && b->item_tmap && b->all_f32 && b->all_plane && kmode != 2) {
+    const size_t smem = sizeof(AccSmemTma);
+    const void* const* tm = b->item_tmap + off;
+    if (kmode == 1) {
+      VG_CUDA(cudaFuncSetAttribute(k_accumulate_tma<1, VG_K4B_MINB_COST>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      VG_CUDA(launch_pdl(k_accumulate_tma<1, VG_K4B_MINB_COST>, dim3(cnt), dim3(32), smem, st, d,
+                         (const ItemDev*)(b->items + off), tm, cnt, (const int2*)b->hits,
+                         b->partials + 2 * (size_t)off));
+    } else {
+      VG_CUDA(cudaFuncSetAttribute(k_accumulate_tma<0, VG_K4B_MINB_TMA>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      VG_CUDA(launch_pdl(k_accumulate_tma<0, VG_K4B_MINB_TMA>, dim3(cnt), dim3(32), smem, st, d,
+                         (const ItemDev*)(b->items + off), tm, cnt, (const int2*)b->hits,
+                         b->partials + (size_t)off * kPartialStride));
+    }
+    ctx->launches++;
+    VG_CUDA(cudaGetLastError());
+    return 0;
+  }
   const size_t s2 = sizeof(AccSmem<2>) * kAccWarps, s1 = sizeof(AccSmem<2, 1>) * kAccWarps;
   if (kmode == 1) {  // cost only (LM candidate steps, factor_graph.py:591)
     double* p = b->partials + 2 * (size_t)off;

@@ -312,6 +312,7 @@ int vg_map_destroy(vg_map* m) {
   dfree(ctx, m->prows);
   dfree(ctx, m->pkeys32);
   dfree(ctx, m->recs);
+  if (m->tmap) cudaFree(m->tmap);
   dfree(ctx, m->keys);
   dfree(ctx, m->means);
   dfree(ctx, m->covs);
@@ -677,7 +678,19 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     h.end = items[i].end;
     h.hoff = items[i].hoff;
   }
+  // per-item record tensor map of the target (K4b's TMA gathers); none if any map lacks one
+  std::vector<const void*> item_tmap(items.size());
+  bool all_tmap = !items.empty();
+  for (size_t i = 0; i < items.size(); ++i) {
+    item_tmap[i] = maps[fac[items[i].factor].map]->tmap;
+    all_tmap &= item_tmap[i] != nullptr;
+  }
   int rc = VG_OK;
+  if (all_tmap && ((rc = dalloc(ctx, &b->item_tmap, items.size())) ||
+                   (rc = h2d(ctx, b->item_tmap, item_tmap.data(), sizeof(void*) * items.size())))) {
+    vg_batch_destroy(b);
+    return rc;
+  }
   if ((rc = dalloc(ctx, &b->factors, F)) || (rc = dalloc(ctx, &b->items, items.size())) ||
       (rc = dalloc(ctx, &b->clouds, cv.size())) || (rc = dalloc(ctx, &b->maps, mv.size())) ||
       (rc = dalloc(ctx, &b->partials, items.size() * kPartialStride)) ||
@@ -724,6 +737,7 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->hit_counts);
   dfree(ctx, b->descs);
   dfree(ctx, b->hdrs);
+  dfree(ctx, b->item_tmap);
   dfree(ctx, b->out);
   dfree(ctx, b->out32);
   dfree(ctx, b->poses);

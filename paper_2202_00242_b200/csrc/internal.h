@@ -63,6 +63,8 @@ struct vg_map {
   int* prows = nullptr;           // kmode 0 row per slot (capacity)
   unsigned* pkeys32 = nullptr;    // kmode 1 keys (capacity)
   vg::VoxelRec* recs = nullptr;   // kmode 1: capacity, slot-indexed; kmode 0: m, row-indexed
+  void* tmap = nullptr;           // device CUtensorMap of recs (rows x 16 fp64, box 10 x 1) for
+                                  // K4b's TMA gather4 record fetches, or null
   long long empty_key = 0;
   int kmode = 0;
   int bx = 0, by = 0, bz = 0, ex = 0, ey = 0, ez = 0;
@@ -119,6 +121,7 @@ struct vg_batch {
   int* hit_counts = nullptr;          // num_items
   vg::AccDesc* descs = nullptr;       // num_items (K4a -> K4b)
   vg::ItemHdr* hdrs = nullptr;        // num_items (K4a fast-path headers; T refreshed per step)
+  const void** item_tmap = nullptr;   // num_items: the target map's record tensor map (TMA)
   long long hit_capacity = 0;
   double* poses = nullptr;            // pose table (device), capacity pose_cap
   long long pose_cap = 0;

@@ -17,6 +17,8 @@
 #include <cub/device/device_run_length_encode.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -486,6 +488,42 @@ int launch_cloud_pack(vg_ctx* ctx, vg_cloud* cl) {
   return 0;
 }
 
+// Record tensor map of a voxel map for K4b's TMA gathers: a 2D fp64 tensor of `rows` records x
+// 16 doubles (128 B rows), box 10 x 1 (the 80 B of mean, covariance and row that K4b reads),
+// no swizzle.  Encoded on the host (driver entry point resolved through the runtime) and kept
+// in device memory; null when the driver refuses (K4b then gathers with cp.async).
+static void make_record_tmap(vg_map* map, unsigned long long rows) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return (EncodeFn) nullptr;
+    return (EncodeFn)p;
+  }();
+  if (!encode || !map->recs || rows == 0 || rows >= (1ull << 31)) return;
+  CUtensorMap tm;
+  const cuuint64_t dims[2] = {16, rows};
+  const cuuint64_t strides[1] = {sizeof(VoxelRec)};
+  const cuuint32_t box[2] = {10, 1};
+  const cuuint32_t estr[2] = {1, 1};
+  if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, map->recs, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  void* d = nullptr;
+  if (cudaMalloc(&d, sizeof(tm)) != cudaSuccess) return;
+  if (cudaMemcpy(d, &tm, sizeof(tm), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return;
+  }
+  map->tmap = d;
+}
+
 int launch_map_finish(vg_ctx* ctx, vg_map* map) {
   long long empty = (long long)0x8000000000000000ull;
   map->kmode = 0;
@@ -546,6 +584,7 @@ int launch_map_finish(vg_ctx* ctx, vg_map* map) {
       map->pkeys32, map->recs);
   ctx->launches++;
   VG_CUDA(cudaGetLastError());
+  make_record_tmap(map, map->kmode ? map->capacity : (unsigned long long)map->m);
   return 0;
 }
 
