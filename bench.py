@@ -73,9 +73,9 @@ def parse():
 
 
 def traffic_record():
-    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r01e_traffic.json,
-    written by tools/launch_traffic.py from profiles/r01e_launches.csv)."""
-    p = ROOT / "profiles" / "r01e_traffic.json"
+    """DRAM bytes per K4 launch from the committed ncu capture (profiles/r02_traffic.json,
+    written by tools/launch_traffic.py from profiles/r02_launches.csv)."""
+    p = ROOT / "profiles" / "r02_traffic.json"
     try:
         return int(json.loads(p.read_text())["dram_bytes_per_launch"])
     except Exception:
@@ -83,9 +83,9 @@ def traffic_record():
 
 
 def ncu_metrics():
-    """Per-kernel ncu digest of K4a/K4b from the committed capture (profiles/r01d_ncu_metrics.json,
+    """Per-kernel ncu digest of K4a/K4b from the committed capture (profiles/r02_ncu_metrics.json,
     tools/ncu_summary.py): L2/L1 hit rates and pipe use beside the roofline."""
-    p = ROOT / "profiles" / "r01d_ncu_metrics.json"
+    p = ROOT / "profiles" / "r02_ncu_metrics.json"
     try:
         return json.loads(p.read_text())
     except Exception:
