@@ -606,6 +606,16 @@ def run_ours(args):
                                    else bench_configs.run(c, cargs, ctx, stream))
             except Exception as exc:
                 configs[str(c)] = {"error": repr(exc)[:300]}
+        if not args.no_lm and isinstance(configs.get("4"), dict):
+            # config 4 at the LM level: the reference's FactorGraph with its IMU and prior
+            # factors on the host and the 4,950 matching factors on the GPU (one iteration)
+            try:
+                import lm_workloads
+
+                configs["4"]["lm_iteration"] = lm_workloads.time_lm_iteration(
+                    *lm_workloads.local_mapping_lm())
+            except Exception as exc:
+                configs["4"]["lm_iteration"] = {"error": repr(exc)[:300]}
         ctx.set_stream(stream.cuda_stream)
     lm_line = None
     if world == 1 and not args.no_lm:

@@ -163,3 +163,31 @@ def test_device_assembly_matches_per_factor_assembly():
     b = g2.optimize_lm()
     for k in a.estimates:
         assert np.linalg.norm(G.pose_local(a.estimates[k], b.estimates[k])) < 1e-6
+
+
+def test_local_mapping_with_imu_and_prior_factors_through_the_reference_lm():
+    """A config-4-shaped local-mapping graph on the reference's own FactorGraph: frame-state
+    variables, ImuFactors preintegrated by the reference, prior factors, and all-to-all
+    matching factors on the GPU (tools/lm_workloads.py, 15 frames here).  The reference LM
+    with the drop-in's batched total_cost / _assemble_dense brings the perturbed frames back
+    to the trajectory."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import lm_workloads
+
+    try:
+        g, fg, info = lm_workloads.local_mapping_lm(frames=15)
+    except RuntimeError as exc:  # the reference is not installed here
+        pytest.skip(str(exc))
+    c0 = g.total_cost()
+    res = g.optimize_lm(fg.LmSettings(max_iterations=20))
+    assert res.final_cost < 0.05 * c0
+    import limapper.synthetic as syn
+
+    traj = syn.PathTrajectory(syn.CirclePath(15 * 0.4 / (2 * np.pi), laps=1.0), 4.0, settle=0.0,
+                              ramp_time=0.0)
+    for k in range(15):
+        est = res.estimates[fg.frame_key(k)].pose
+        assert np.linalg.norm(est.translation - traj.pose(k * 0.1).translation) < 0.02
