@@ -112,6 +112,7 @@ int vg_ctx_destroy(vg_ctx* ctx) {
     cudaStreamDestroy(ctx->comp2);
   }
 
+
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return VG_OK;
@@ -807,6 +808,8 @@ static int run_to_host(vg_batch* b, int mode, void* out_host, int fmt = 0) {
   const int kmode = kmode_of(mode);
   // VGICP_STAGE_TRACE=1 (profiling): timed events at every stage boundary, printed to stderr
   static const bool trace = getenv("VGICP_STAGE_TRACE") != nullptr;
+  // VGICP_STAGE_NOCOPY=1 (profiling only, results not delivered): the staged compute alone
+  static const bool nocopy = getenv("VGICP_STAGE_NOCOPY") != nullptr;
   cudaEvent_t tr[2 * 17 + 1] = {};
   if (trace) {
     for (auto& e : tr) VG_CUDA(cudaEventCreate(&e));
@@ -846,8 +849,9 @@ static int run_to_host(vg_batch* b, int mode, void* out_host, int fmt = 0) {
     VG_CUDA(cudaEventRecord(ctx->events[s], ctx->stream));
     if (trace) VG_CUDA(cudaEventRecord(tr[1 + 2 * s], ctx->stream));
     VG_CUDA(cudaStreamWaitEvent(ctx->side_stream, ctx->events[s], 0));
-    VG_CUDA(cudaMemcpyAsync(host + (size_t)f0 * rb, dev + (size_t)f0 * rb, rb * (size_t)(f1 - f0),
-                            cudaMemcpyDeviceToHost, ctx->side_stream));
+    if (!nocopy)
+      VG_CUDA(cudaMemcpyAsync(host + (size_t)f0 * rb, dev + (size_t)f0 * rb,
+                              rb * (size_t)(f1 - f0), cudaMemcpyDeviceToHost, ctx->side_stream));
     if (trace) VG_CUDA(cudaEventRecord(tr[2 + 2 * s], ctx->side_stream));
   }
   if (trace) {
