@@ -132,10 +132,13 @@ class _Batcher:
         return entry
 
     def evaluate(self, values, mode: int, requester: "MatchingCostFactor") -> None:
+        # factors added to a FactorGraph (graph_add_factor) batch with their own graph only:
+        # another graph reusing the same keys neither joins the batch nor can fail it
+        owner = requester._graph
         group = []
         for serial in sorted(self._live.keys()):
             f = self._live.get(serial)
-            if f is None or f._empty:
+            if f is None or f._empty or f._graph is not owner:
                 continue
             if any(k not in values for k in f.keys):
                 continue
@@ -230,7 +233,12 @@ class MatchingCostFactor(Factor):
         self._empty = (len(source) == 0 or len(target_map) == 0
                        or getattr(source, "covs", None) is None)
         self._cache = None  # (v_i, v_j, mode, record)
+        self._graph_ref = None  # the FactorGraph it was added to (graph_add_factor), weak
         _BATCHER.register(self)
+
+    @property
+    def _graph(self):
+        return self._graph_ref() if self._graph_ref is not None else None
 
     @property
     def unary(self) -> bool:
@@ -314,6 +322,18 @@ def _split_factors(graph):
         (gpu if isinstance(f, MatchingCostFactor) and not f._empty else rest).append(f)
     graph.__dict__["_vgicp_split"] = (sig, gpu, rest)
     return gpu, rest
+
+
+def graph_add_factor(self, factor) -> None:
+    """FactorGraph.add_factor (factor_graph.py:460-467) that also tags a MatchingCostFactor with
+    its graph, so the per-factor batching shim groups a graph's own factors only."""
+    _ORIGINAL_ADD_FACTOR[type(self)](self, factor)
+    if isinstance(factor, MatchingCostFactor):
+        factor._graph_ref = weakref.ref(self)
+
+
+#: the reference's add_factor per patched class (integrate.patch fills it)
+_ORIGINAL_ADD_FACTOR: dict = {}
 
 
 def graph_total_cost(self, values=None) -> float:

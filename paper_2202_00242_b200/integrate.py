@@ -76,7 +76,8 @@ METHOD_REPLACEMENTS = {
     # graph's matching factors; _assemble_dense (:522-536): their normal equations summed on
     # the device (K6) and scattered into the dense H/g the reference's LM solves
     "factor_graph": {"FactorGraph": {"total_cost": _fg.graph_total_cost,
-                                     "_assemble_dense": _fg.graph_assemble_dense}},
+                                     "_assemble_dense": _fg.graph_assemble_dense,
+                                     "add_factor": _fg.graph_add_factor}},
 }
 
 #: (class, method name) -> the reference's own function, for callers that compare against it
@@ -117,6 +118,8 @@ def patch(pkg="limapper"):
                 if name in vars(cls) and vars(cls)[name] is not fn:
                     saved.append((cls, name, vars(cls)[name]))
                     ORIGINALS.setdefault((cls, name), vars(cls)[name])
+                    if fn is _fg.graph_add_factor:
+                        _fg._ORIGINAL_ADD_FACTOR[cls] = vars(cls)[name]
                     setattr(cls, name, fn)
 
     # deskew keeps the reference's host IMU integration (taken from its preprocess module) and

@@ -6,6 +6,7 @@ reference's own FactorGraph (integrate.patch); see graph_api() below.
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -17,6 +18,7 @@ from paper_2202_00242_b200.factor_graph import (
     Factor,
     FactorLinearization,
     Key,
+    MatchingCostFactor,
     graph_assemble_dense,
     graph_total_cost,
     submap_key,
@@ -125,6 +127,8 @@ class FactorGraph:
             if k not in self.values:
                 raise KeyError(f"factor references missing {k}")
         self.factors.append(factor)
+        if isinstance(factor, MatchingCostFactor):  # as graph_add_factor does when patched
+            factor._graph_ref = weakref.ref(self)
 
     def _slices(self):
         out, off = {}, 0

@@ -191,3 +191,28 @@ def test_local_mapping_with_imu_and_prior_factors_through_the_reference_lm():
     for k in range(15):
         est = res.estimates[fg.frame_key(k)].pose
         assert np.linalg.norm(est.translation - traj.pose(k * 0.1).translation) < 0.02
+
+
+def test_shim_batches_per_graph():
+    """Two graphs reusing the same keys: evaluating one graph's factor batches that graph's
+    factors only (the batch no longer sweeps in other graphs' factors)."""
+    rng = np.random.default_rng(21)
+    pts, covs = plane_cloud(rng)
+    vmap = RG.build_voxelmap(make_frame(pts, covs), 0.5)
+    graphs, facs = [], []
+    for _ in range(2):
+        g = FactorGraph()
+        g.add_variable(submap_key(0), G.Se3Pose.identity())
+        fs = []
+        for i in range(1, 4):
+            rel = G.Se3Pose(G.so3_exp(rng.uniform(-0.05, 0.05, 3)), rng.uniform(-0.1, 0.1, 3))
+            g.add_variable(submap_key(i), rel)
+            f = MatchingCostFactor(submap_key(i), make_frame(G.pose_apply(G.pose_inverse(rel), pts),
+                                                             covs), vmap, key_target=submap_key(0))
+            g.add_factor(f)
+            fs.append(f)
+        graphs.append(g)
+        facs.append(fs)
+    facs[0][0].cost(graphs[0].values)
+    assert all(f._cache is not None for f in facs[0])       # its graph: one batch
+    assert all(f._cache is None for f in facs[1])           # the other graph: untouched

@@ -203,3 +203,19 @@ def test_make_deskew_glue_matches_reference_deskew():
                    deskewed=True), samples, G.SensorState.zero())
     empty = P.Frame(points=np.zeros((0, 3)), stamps=np.zeros(0), stamp=0.0, scan_end=0.1)
     assert dk(empty, samples, G.SensorState.zero()).deskewed
+
+
+def test_f32_record_decoding():
+    """record_cost_inliers_f32 reads the compact record's fp64 cost (words 90-91, low word
+    first) and int32 inlier count (word 92) — the layout K5's rec32_word writes."""
+    from paper_2202_00242_b200 import _lib
+
+    rec = np.zeros((3, _lib.REC_LINEARIZE_F32), np.float32)
+    costs = np.array([1.5e5 + 1e-9, 0.0, -3.25], np.float64)
+    inl = np.array([13004, 0, 7], np.int32)
+    rec[:, 90:92] = costs.view(np.float32).reshape(3, 2)
+    rec[:, 92] = inl.view(np.float32)
+    rec[:, :90] = np.arange(90, dtype=np.float32)
+    c, n = _lib.record_cost_inliers_f32(rec)
+    assert np.array_equal(c, costs) and np.array_equal(n, inl.astype(np.int64))
+    assert c.dtype == np.float64 and n.dtype == np.int64
