@@ -538,7 +538,9 @@ int vg_batch_create(vg_ctx* ctx, const vg_factor_spec* specs, int64_t F, vg_batc
     stage_factors[0] = 0;
     for (int s = 1; s <= S; ++s) {
       acc += weights[s - 1];
-      stage_factors[s] = s == S ? (int)F : (int)std::llround((double)F * acc / tot);
+      // interior boundaries on 64-factor windows: K5's per-window cost partials (k_finalize)
+      // must not straddle two stages' launches
+      stage_factors[s] = s == S ? (int)F : (int)(std::llround((double)F * acc / tot) / 64 * 64);
     }
   }
   for (int s = 0; s < S; ++s)
@@ -746,8 +748,6 @@ int vg_batch_destroy(vg_batch* b) {
   dfree(ctx, b->asm_codes);
   dfree(ctx, b->asm_pidx);
   dfree(ctx, b->asm_out);
-  dfree(ctx, b->asm_partial);
-  dfree(ctx, b->asm_done);
   dfree(ctx, b->asm_gcost);
   cudaStreamSynchronize(ctx->stream);
   delete b;
@@ -1180,10 +1180,9 @@ static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, i
   VG_CHECK(dalloc(ctx, &b->asm_begin, begin.size()));
   VG_CHECK(dalloc(ctx, &b->asm_codes, std::max<size_t>(codes.size(), 1)));
   VG_CHECK(dalloc(ctx, &b->asm_out, (size_t)total));
-  if (!b->asm_partial) VG_CHECK(dalloc(ctx, &b->asm_partial, 2 * 128));
-  if (!b->asm_done) VG_CHECK(dalloc(ctx, &b->asm_done, 1));
   if (!b->asm_gcost && F) VG_CHECK(dalloc(ctx, &b->asm_gcost, (size_t)F));
-  VG_CUDA(cudaMemsetAsync(b->asm_done, 0, sizeof(unsigned), ctx->stream));
+  // K5's cost partials: per factor for the warp-per-factor K5 (linearize.cu), else per window
+  b->asm_gparts = (F < 4096 || b->num_items > 4 * F) ? F : (F + 63) / 64;
   VG_CHECK(h2d(ctx, b->asm_begin, begin.data(), sizeof(int) * begin.size()));
   if (!codes.empty()) VG_CHECK(h2d(ctx, b->asm_codes, codes.data(), sizeof(int) * codes.size()));
   VG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -152,9 +152,9 @@ struct vg_batch {
   int* asm_pidx = nullptr;            // P: output slot of each pair block (mapped setup) or null
   long long asm_out_pairs = 0;        // pair blocks in the output layout (>= asm_pairs_n)
   double* asm_out = nullptr;          // device output (host-buffer entry point)
-  double* asm_partial = nullptr;      // per-CTA cost partials of k_assemble_cost
-  unsigned* asm_done = nullptr;       // its arrival counter (reset by the last CTA)
-  double2* asm_gcost = nullptr;       // per-factor (gated cost, 1 if gated in), written by K5
+  double2* asm_gcost = nullptr;       // gated (cost, count) partials written by K5: one per
+                                      // 64-factor window (k_finalize) or per factor (warp K5)
+  long long asm_gparts = 0;           // how many (K6's cost unit sums them)
 };
 
 // Programmatic dependent launch: the kernel may be scheduled while its stream predecessor

@@ -300,14 +300,28 @@ __global__ void __launch_bounds__(kFinBlock)
     if (fi < F) finalize_one(factors[fi], fi, partials, mode, out, nullptr);
     return;
   }
+  double gc = 0.0, gn = 0.0;
   if (fi < F) {
     const double* o = sh + threadIdx.x * kFinStride;
     finalize_one(factors[fi], fi, partials, mode, out, sh + threadIdx.x * kFinStride);
-    // gated cost + count per factor for the normal-equation assembly (factor_graph.py:271-275)
-    if (gcost) {
-      const bool in = o[91] >= (double)factors[fi].min_inliers;
-      gcost[fi] = make_double2(in ? o[90] : 0.0, in ? 1.0 : 0.0);
+    const bool in = o[91] >= (double)factors[fi].min_inliers;
+    gc = in ? o[90] : 0.0;
+    gn = in ? 1.0 : 0.0;
+  }
+  if (gcost) {
+    // gated cost + count of this CTA's 64 factors for the normal-equation assembly
+    // (factor_graph.py:271-275): a fixed butterfly per warp, warp 0 then warp 1; one partial
+    // per 64-factor window (stage boundaries are multiples of 64), summed by K6's cost unit
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+      gc += __shfl_xor_sync(0xffffffffu, gc, sft);
+      gn += __shfl_xor_sync(0xffffffffu, gn, sft);
     }
+    __shared__ double2 wsum[kFinBlock / 32];
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = make_double2(gc, gn);
+    __syncthreads();
+    if (threadIdx.x == 0)
+      gcost[f0 / kFinBlock] = make_double2(wsum[0].x + wsum[1].x, wsum[0].y + wsum[1].y);
   }
   __syncthreads();
   const int nf = min(kFinBlock, F - f0);
@@ -463,7 +477,8 @@ __global__ void __launch_bounds__(kTermThreads)
 
 // ---- K6: block-sparse normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536)
 // One warp per output unit: unit u < V is variable u's diagonal block (21, upper) + gradient
-// (6); V <= u < V + P is the H block of variable pair u - V (36).  The cost is k_assemble_cost.
+// (6); V <= u < V + P is the H block of variable pair u - V (36); unit -1 (the first block)
+// sums the gated cost and count.
 // A unit's contributions are listed in factor order (CSR, code = factor * 8 + role), and each
 // lane sums its element in that order from 0.0, so the result is the reference's sequential
 // per-block sum.  Roles: 0 source block (H_ii, b_i), 1 target block (H_jj, b_j), 2 H_ij as is,
@@ -490,29 +505,61 @@ __device__ __forceinline__ double asm_value(const double* __restrict__ r, int ro
 }
 
 constexpr int kAsmWarps = 1;  // one-warp CTAs: the long diagonal units do not hold CTA slots
+#ifndef VG_K6_MLP
+#define VG_K6_MLP 8
+#endif
 __global__ void __launch_bounds__(kAsmWarps * 32)
     k_assemble(const double* __restrict__ rec, const FactorDev* __restrict__ factors, int F,
                const int* __restrict__ begin, const int* __restrict__ codes, int V, int P,
-               const int* __restrict__ pidx, double* __restrict__ out) {
+               const int* __restrict__ pidx, const double2* __restrict__ gcost, int n_parts,
+               double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int u = blockIdx.x * kAsmWarps + (threadIdx.x >> 5);
+  const int u = blockIdx.x * kAsmWarps + (threadIdx.x >> 5) - 1;  // unit -1: the cost
   pdl_release();
-  pdl_wait();  // records written by K5
+  pdl_wait();  // records and gated costs written by K5
   if (u >= V + P) return;
+  if (u < 0) {
+    // cost and count of the factors that pass their inlier gate (factor_graph.py:271-275),
+    // from K5's per-window partials (64 factors, or 1 for the warp-per-factor K5): lane L sums
+    // partials L, L + 32, ... in four interleaved chains, chains and lanes combined in a fixed
+    // order (deterministic); this is the first block, so it starts first
+    double c[4] = {0.0, 0.0, 0.0, 0.0}, n[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int f = lane; f < n_parts; f += 128) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+        if (f + 32 * a < n_parts) {
+          const double2 v = __ldg(gcost + f + 32 * a);
+          c[a] += v.x;
+          n[a] += v.y;
+        }
+    }
+    double cs = (c[0] + c[1]) + (c[2] + c[3]), ns = (n[0] + n[1]) + (n[2] + n[3]);
+#pragma unroll
+    for (int sft = 16; sft >= 1; sft >>= 1) {
+      cs += __shfl_xor_sync(0xffffffffu, cs, sft);
+      ns += __shfl_xor_sync(0xffffffffu, ns, sft);
+    }
+    if (lane == 0) {
+      out[0] = cs;
+      out[1] = ns;
+    }
+    return;
+  }
   const int k0 = __ldg(begin + u), k1 = __ldg(begin + u + 1);
   const bool diag = u < V;
   const int nel = diag ? 27 : 36;
   double acc0 = 0.0, acc1 = 0.0;  // elements lane and lane + 32
   const bool has0 = lane < nel, has1 = lane + 32 < nel;
-  // 32 codes per coalesced load, eight contributions' values in flight per step; the
+  // 32 codes per coalesced load and VG_K6_MLP contributions' values in flight per step (the
+  // long diagonal units — ~100 contributions at config 5 — are chains of L2 round trips); the
   // additions stay in contribution order
   for (int kb = k0; kb < k1; kb += 32) {
     const int my_code = kb + lane < k1 ? __ldg(codes + kb + lane) : 0;
     const int nk = min(32, k1 - kb);
-    for (int j = 0; j < nk; j += 8) {
-      double v0[8], v1[8];
+    for (int j = 0; j < nk; j += VG_K6_MLP) {
+      double v0[VG_K6_MLP], v1[VG_K6_MLP];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
+      for (int q = 0; q < VG_K6_MLP; ++q) {
         const int code = __shfl_sync(0xffffffffu, my_code, (j + q) & 31);
         VG_DEVICE_CHECK(j + q >= nk || (code >> 3) < F, "K6: contribution of no factor");
         v0[q] = 0.0;
@@ -524,7 +571,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32)
         }
       }
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
+      for (int q = 0; q < VG_K6_MLP; ++q)
         if (j + q < nk) {
           acc0 += v0[q];
           acc1 += v1[q];
@@ -822,6 +869,7 @@ int launch_finalize_range(vg_ctx* ctx, vg_batch* b, int mode, void* out_dev, int
     return 0;
   }
   const dim3 grid((f1 - f0 + kFinBlock - 1) / kFinBlock), block(kFinBlock);
+  if (gc && f0 % kFinBlock) return vg_cuda_fail(cudaErrorInvalidValue, "K5 window alignment");
   if (f32 && mode == 0)
     VG_CUDA(launch_pdl(k_finalize<1>, grid, block, 0, ctx->stream, fac, f0, f1, part, mode, out, gc));
   else
@@ -835,71 +883,14 @@ int launch_finalize(vg_ctx* ctx, vg_batch* b, int mode, void* out_dev, int f32) 
   return launch_finalize_range(ctx, b, mode, out_dev, 0, (int)b->F, f32);
 }
 
-namespace vg {
-// cost and count of the factors that pass their inlier gate (K5 writes them per factor to
-// asm_gcost, coalesced): kCostBlocks CTAs each sum a
-// fixed contiguous factor range (strided per thread, fixed tree), the last CTA to finish adds
-// the partials in block order (deterministic)
-constexpr int kCostThreads = 256;
-constexpr int kCostBlocks = 128;
-__global__ void __launch_bounds__(kCostThreads)
-    k_assemble_cost(const double2* __restrict__ gcost, int F, double* __restrict__ partial,
-                    unsigned* __restrict__ done, double* __restrict__ out) {
-  __shared__ double sc[kCostThreads], sn[kCostThreads];
-  __shared__ bool last;
-  const int t = threadIdx.x;
-  pdl_release();
-  pdl_wait();  // per-factor gated costs written by K5
-  const int per = (F + kCostBlocks - 1) / kCostBlocks;
-  const int f0 = blockIdx.x * per, f1 = min(F, f0 + per);
-  double c = 0.0, n = 0.0;
-  for (int f = f0 + t; f < f1; f += kCostThreads) {
-    const double2 v = __ldg(gcost + f);
-    c += v.x;
-    n += v.y;
-  }
-  sc[t] = c;
-  sn[t] = n;
-  __syncthreads();
-  for (int s = kCostThreads / 2; s >= 1; s >>= 1) {
-    if (t < s) {
-      sc[t] += sc[t + s];
-      sn[t] += sn[t + s];
-    }
-    __syncthreads();
-  }
-  if (t == 0) {
-    partial[2 * blockIdx.x] = sc[0];
-    partial[2 * blockIdx.x + 1] = sn[0];
-    __threadfence();
-    last = atomicAdd(done, 1u) == kCostBlocks - 1;
-  }
-  __syncthreads();
-  if (last && t == 0) {
-    __threadfence();
-    double cc = 0.0, nn = 0.0;
-    for (int b = 0; b < kCostBlocks; ++b) {
-      cc += __ldcg(partial + 2 * b);
-      nn += __ldcg(partial + 2 * b + 1);
-    }
-    out[0] = cc;
-    out[1] = nn;
-    *done = 0u;  // ready for the next launch
-  }
-}
-}  // namespace vg
-
 int launch_assemble(vg_ctx* ctx, vg_batch* b, const double* rec, double* out_dev) {
-  const int units = (int)(b->asm_vars + b->asm_pairs_n);
-  if (units > 0)
-    VG_CUDA(launch_pdl(k_assemble, dim3((units + kAsmWarps - 1) / kAsmWarps), dim3(kAsmWarps * 32),
-                       0, ctx->stream, rec, (const FactorDev*)b->factors, (int)b->F,
-                       (const int*)b->asm_begin, (const int*)b->asm_codes, (int)b->asm_vars,
-                       (int)b->asm_pairs_n, (const int*)b->asm_pidx, out_dev));
-  VG_CUDA(launch_pdl(k_assemble_cost, dim3(kCostBlocks), dim3(kCostThreads), 0, ctx->stream,
-                     (const double2*)b->asm_gcost, (int)b->F, b->asm_partial, b->asm_done,
-                     out_dev));
-  ctx->launches += 2;
+  const int units = (int)(b->asm_vars + b->asm_pairs_n) + 1;  // + the cost unit
+  VG_CUDA(launch_pdl(k_assemble, dim3((units + kAsmWarps - 1) / kAsmWarps), dim3(kAsmWarps * 32),
+                     0, ctx->stream, rec, (const FactorDev*)b->factors, (int)b->F,
+                     (const int*)b->asm_begin, (const int*)b->asm_codes, (int)b->asm_vars,
+                     (int)b->asm_pairs_n, (const int*)b->asm_pidx,
+                     (const double2*)b->asm_gcost, (int)b->asm_gparts, out_dev));
+  ctx->launches++;
   VG_CUDA(cudaGetLastError());
   return 0;
 }

@@ -67,6 +67,14 @@ def main():
             return statistics.median(ts)
 
         lin = timeit(lambda: b.linearize_poses_device(poses.data_ptr(), V, 0, rec.data_ptr()))
+        parts = {
+            "compose_us": timeit(lambda: b.compose_device(poses.data_ptr(), V)),
+            "k4a_us": timeit(lambda: b.accumulate_device(_lib.MODE_INLIERS)),
+            "k4_us": timeit(lambda: b.accumulate_device(_lib.MODE_LINEARIZE)),
+            "k5_us": timeit(lambda: b.finalize_device(_lib.MODE_LINEARIZE, rec.data_ptr())),
+            "k6_us": timeit(lambda: b.assemble_records_device(rec.data_ptr(), ne.data_ptr())),
+            "zero_us": timeit(lambda: ne.zero_()),
+        }
         full = timeit(lambda: (ne.zero_(),
                                b.linearize_poses_device(poses.data_ptr(), V, 0, rec.data_ptr()),
                                b.assemble_records_device(rec.data_ptr(), ne.data_ptr())))
@@ -79,7 +87,7 @@ def main():
             "ranks": n, "sharding": a.sharding, "slowest_rank_factors": len(shards[r]),
             "slowest_rank_points": int(w[shards[r]].sum()), "items": b.num_items,
             "linearize_us": round(lin, 1), "zero_linearize_k6_us": round(full, 1),
-            "reduce_bytes": xbytes,
+            "reduce_bytes": xbytes, **{k: round(v, 1) for k, v in parts.items()},
             "exchange_model_us": round(xus, 1), "step_model_us": round(step_us, 1),
             "speedup_vs_1": round(base / step_us, 2)}), flush=True)
 
