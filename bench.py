@@ -444,21 +444,37 @@ def run_ours(args):
                 e[3].record()
             exchange()
 
+    graph = {"ready": False}
+
     def step_fast():
         # the same step as one library call (K-compose, K4a, K4b, K5 chained with programmatic
-        # dependent launch; no host events between the kernels)
+        # dependent launch; no host events between the kernels); N > 1: the rank's whole
+        # device step (+ zeroing on the solver rank + K6) replayed as one captured graph
+        # between the pose broadcast and the reduction
         if world > 1:
             bcast_poses()
+            if graph["ready"]:
+                batch.launch_graph()
+            else:
+                batch.linearize_poses_device(poses_dev.data_ptr(), V, _lib.MODE_LINEARIZE,
+                                             out_dev.data_ptr())
+                assemble()
+            exchange()
+            return
         batch.linearize_poses_device(poses_dev.data_ptr(), V, _lib.MODE_LINEARIZE,
                                      out_dev.data_ptr())
-        if world > 1:
-            assemble()
-            exchange()
 
     for _ in range(max(3, args.warmup)):
         step()
         step_fast()
     torch.cuda.synchronize()
+    if world > 1:
+        batch.capture_assemble_graph(poses_dev.data_ptr(), V, out_dev.data_ptr(),
+                                     ne_local.data_ptr(),
+                                     zero_out=(args.exchange == "reduce" and rank == 0))
+        graph["ready"] = True
+        step_fast()
+        torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

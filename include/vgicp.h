@@ -206,6 +206,12 @@ int vg_batch_finalize_device(vg_batch* batch, int mode, double* out_dev);
 int vg_batch_graph_capture(vg_batch* batch, const double* poses_dev, int64_t num_poses,
                            int mode, double* out_dev);
 int vg_batch_graph_launch(vg_batch* batch);
+/* capture one rank's whole normal-equation step — K-compose, K4, K5 into records_dev, an
+ * optional zeroing of out_dev, K6 into out_dev (the set-up layout) — as the batch's graph
+ * (vg_batch_graph_launch replays it): the multi-GPU step between the pose broadcast and the
+ * reduction, one launch instead of six */
+int vg_batch_graph_capture_assemble(vg_batch* batch, const double* poses_dev, int64_t num_poses,
+                                    double* records_dev, double* out_dev, int32_t zero_out);
 
 /* ---- normal equations (FactorGraph._assemble_dense, factor_graph.py:522-536) ------------
  * Sums every factor's blocks into the block-sparse system the LM solves,

@@ -94,6 +94,8 @@ _SIGNATURES = {
     "vg_batch_finalize_device": ([c_void_p, c_int, c_void_p], c_int),
     "vg_batch_graph_capture": ([c_void_p, c_void_p, c_int64, c_int, c_void_p], c_int),
     "vg_batch_graph_launch": ([c_void_p], c_int),
+    "vg_batch_graph_capture_assemble": ([c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_int32],
+                                        c_int),
     "vg_batch_assemble_setup": ([c_void_p, c_int64, _P_I64, _P_I64], c_int),
     "vg_batch_assemble_setup_pairs": ([c_void_p, c_int64, POINTER(c_int32), c_int64, _P_I64],
                                       c_int),
@@ -445,6 +447,13 @@ class DeviceBatch:
         check(self.ctx.lib.vg_batch_graph_capture(self.handle, c_void_p(poses_dev_ptr),
                                                   int(num_poses), int(mode),
                                                   c_void_p(out_dev_ptr)))
+
+    def capture_assemble_graph(self, poses_dev_ptr: int, num_poses: int, records_dev_ptr: int,
+                               out_dev_ptr: int, zero_out: bool = False) -> None:
+        """Capture compose + K4 + K5 + [zero] + K6 as the batch's graph (launch_graph)."""
+        check(self.ctx.lib.vg_batch_graph_capture_assemble(
+            self.handle, c_void_p(poses_dev_ptr), int(num_poses), c_void_p(records_dev_ptr),
+            c_void_p(out_dev_ptr), int(bool(zero_out))), "vg_batch_graph_capture_assemble")
 
     def launch_graph(self) -> None:
         check(self.ctx.lib.vg_batch_graph_launch(self.handle))

@@ -1261,6 +1261,39 @@ int vg_batch_graph_capture(vg_batch* b, const double* poses_dev, int64_t V, int 
   return VG_OK;
 }
 
+int vg_batch_graph_capture_assemble(vg_batch* b, const double* poses_dev, int64_t V,
+                                    double* records_dev, double* out_dev, int32_t zero_out) {
+  if (!b || !poses_dev || !records_dev || !out_dev) return fail(VG_ERR_INVALID, "null argument");
+  if (b->asm_vars < 0) return fail(VG_ERR_INVALID, "assembly not set up (vg_batch_assemble_setup)");
+  if (V <= b->max_var) return fail(VG_ERR_INVALID, "pose table smaller than the largest variable index");
+  vg_ctx* ctx = b->ctx;
+  if (b->graph) {
+    cudaGraphExecDestroy(b->graph);
+    b->graph = nullptr;
+  }
+  const size_t total = 2 + (size_t)b->asm_vars * 27 + (size_t)b->asm_out_pairs * 36;
+  cudaGraph_t g;
+  const long long l0 = ctx->launches;
+  VG_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = VG_OK;
+  if (b->F) {
+    rc = launch_compose(ctx, b, poses_dev);
+    if (!rc) rc = run_device(b, VG_MODE_LINEARIZE, records_dev);
+  }
+  if (!rc && zero_out && cudaMemsetAsync(out_dev, 0, sizeof(double) * total, ctx->stream))
+    rc = VG_ERR_CUDA;
+  if (!rc) rc = launch_assemble(ctx, b, records_dev, out_dev);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  b->graph_launches = ctx->launches - l0;
+  ctx->launches = l0;
+  if (rc) return rc;
+  if (e != cudaSuccess) return vg_cuda_fail(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&b->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return vg_cuda_fail(e, "cudaGraphInstantiate");
+  return VG_OK;
+}
+
 int vg_batch_graph_launch(vg_batch* b) {
   if (!b || !b->graph) return fail(VG_ERR_INVALID, "no captured graph");
   VG_CUDA(cudaGraphLaunch(b->graph, b->ctx->stream));

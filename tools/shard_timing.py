@@ -78,6 +78,16 @@ def main():
         full = timeit(lambda: (ne.zero_(),
                                b.linearize_poses_device(poses.data_ptr(), V, 0, rec.data_ptr()),
                                b.assemble_records_device(rec.data_ptr(), ne.data_ptr())))
+        b.capture_assemble_graph(poses.data_ptr(), V, rec.data_ptr(), ne.data_ptr(), True)
+        graph_full = timeit(lambda: b.launch_graph())
+        b.capture_graph(poses.data_ptr(), V, 0, rec.data_ptr())
+        graph_lin = timeit(lambda: b.launch_graph())
+        parts["graph_zero_linearize_k6_us"] = graph_full
+        parts["graph_linearize_us"] = graph_lin
+        if n > 1:
+            full = min(full, graph_full)
+        else:
+            lin = min(lin, graph_lin)
         xbytes = ex.size * 8
         xus = (xbytes / (NVLINK_GBS * 1e9) * 1e6 + COLLECTIVE_LATENCY_US) if n > 1 else 0.0
         step_us = (full if n > 1 else lin) + xus
