@@ -4,7 +4,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 CSRC := paper_2202_00242_b200/csrc
 SRCS := $(CSRC)/capi.cu $(CSRC)/linearize.cu $(CSRC)/accumulate.cu $(CSRC)/map_build.cu $(CSRC)/knn_cov.cu \
-        $(CSRC)/deskew.cu
+        $(CSRC)/deskew.cu $(CSRC)/solve.cu
 HDRS := $(CSRC)/common.cuh $(CSRC)/internal.h include/vgicp.h
 OBJDIR := build/obj
 OBJS := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(SRCS))
@@ -20,7 +20,7 @@ $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $(LIB))
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcusolver
 	@cat $(OBJS:.o=.o.ptxas.log) > build_ptxas.log
 
 clean:

@@ -264,63 +264,24 @@ def run_reference(args):
 
 
 def lm_iteration(wl):
-    """One config-5 LM iteration through the REFERENCE's own FactorGraph.optimize_lm
-    (factor_graph.py:546-612, installed unmodified in baseline/_ref) with the drop-in patched
-    in (integrate.patch): 1,000 submap-pose variables, a gauge prior on submap 0, the 50,000
-    MatchingCostFactors of the workload.  Wall-clock seconds of the iteration and of its
-    parts; the sparse solve stays the reference's host splu (north_star)."""
-    ref = ROOT / "baseline" / "_ref"
-    if not (ref / "limapper").is_dir():
+    """One config-5 LM iteration through the REFERENCE's own FactorGraph (factor_graph.py:
+    546-612, installed unmodified in baseline/_ref) with the drop-in patched in
+    (integrate.patch): 1,000 submap-pose variables, a gauge prior on submap 0, the 50,000
+    MatchingCostFactors of the workload (tools/lm_workloads.global_mapping_lm).  Wall-clock
+    seconds of the iteration with the device solve and, from the same
+    values, of the reference's optimize_lm with its host splu solve."""
+    if not (ROOT / "baseline" / "_ref" / "limapper").is_dir():
         return {"unavailable": "reference not installed in baseline/_ref "
                                "(tools/install_reference.sh)"}
-    if str(ref) not in sys.path:
-        sys.path.append(str(ref))
-    import limapper.factor_graph as fg
-    import limapper.geometry as rgeo
-    from limapper.preprocess import Frame
+    sys.path.insert(0, str(ROOT / "tools"))
+    import lm_workloads
 
-    from paper_2202_00242_b200 import integrate
-    from paper_2202_00242_b200.registration import GaussianVoxelMap
-
-    integrate.patch("limapper")
     t0 = time.perf_counter()
-    g = fg.FactorGraph()
-    for i in range(wl.n_submaps):
-        row = wl.pose_table[i]
-        g.add_variable(fg.submap_key(i), rgeo.Se3Pose(rgeo.Rotation(row[:4]), row[4:7].copy()))
-    g.add_factor(fg.PriorFactor(fg.submap_key(0), g.values[fg.submap_key(0)], np.full(6, 1e6)))
-    frames = [Frame(points=wl.scans[i][sel], stamps=np.zeros(len(sel)), stamp=0.0,
-                    covs=wl.scan_covs[i][sel], deskewed=True)
-              for i, sel in enumerate(wl.source_index)]
-    maps = [GaussianVoxelMap._from_device(wl.resolution, m) for m in wl.maps]
-    for i, j in wl.pairs:
-        g.add_factor(fg.MatchingCostFactor(fg.submap_key(int(i)), frames[i], maps[j],
-                                           key_target=fg.submap_key(int(j))))
+    g, fg, info = lm_workloads.global_mapping_lm(wl)
     build_s = time.perf_counter() - t0
-    slices, dim = g._slices()
-    t0 = time.perf_counter()
-    g.total_cost()                      # first call: device batch + assembly setup
-    g._assemble_dense(g.values, slices, dim)
-    setup_s = time.perf_counter() - t0
-    parts = {}
-    for name, fn in (("total_cost_s", lambda: g.total_cost()),
-                     ("assemble_dense_s", lambda: g._assemble_dense(g.values, slices, dim))):
-        ts = []
-        for _ in range(3):
-            a = time.perf_counter()
-            fn()
-            ts.append(time.perf_counter() - a)
-        parts[name] = statistics.median(ts)
-    a = time.perf_counter()
-    res = g.optimize_lm(fg.LmSettings(max_iterations=1))
-    it_s = time.perf_counter() - a
-    return {"seconds": it_s, "iterations": res.iterations, "final_cost": res.final_cost,
-            "variables": wl.n_submaps, "factors": int(len(wl.pairs)), "tangent_dim": dim,
-            "graph_build_s": round(build_s, 2), "first_call_setup_s": round(setup_s, 2),
-            **parts,
-            "api": "limapper FactorGraph.optimize_lm(LmSettings(max_iterations=1)), reference "
-                   "LM + host sparse solve, drop-in total_cost / _assemble_dense / "
-                   "MatchingCostFactor"}
+    out = lm_workloads.time_lm_iteration(g, fg, info)
+    out["graph_build_s"] = round(build_s, 2)
+    return out
 
 
 def run_ours(args):

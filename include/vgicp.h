@@ -249,6 +249,43 @@ int vg_batch_assemble_poses_device(vg_batch* batch, const double* poses_dev,
 int vg_batch_assemble_records_device(vg_batch* batch, const double* records_dev,
                                      double* out_dev);
 
+/* ---- damped normal-equation solve ------------------------------------
+ * Replaces the LM's linear solve, factor_graph.py:565-576 — `cho_factor(h + diag(lam *
+ * diag(h)))` for dim <= dense_threshold, `splu(csc(h + diag(lam * diag(h))))` above — and the
+ * factorizations of marginal_covariance (:707-722).  H (dim x dim, dense fp64) and g stay on
+ * the device: the batch's block-sparse normal equations (K6) are scattered into H there, the
+ * host adds only the few non-matching factors' blocks (priors, IMU), and each damping attempt
+ * copies 8 * dim bytes of solution back instead of 8 * dim^2 bytes of H. */
+typedef struct vg_solver vg_solver;
+#define VG_SOLVE_CHOLESKY 0    /* cho_factor semantics: not positive definite -> info > 0 */
+#define VG_SOLVE_CHOLESKY_LU 1 /* splu semantics: Cholesky, else partial-pivot LU; info > 0
+                                  only when the damped matrix is exactly singular */
+int vg_solver_create(vg_ctx* ctx, int64_t dim, vg_solver** out);
+int vg_solver_destroy(vg_solver* solver);
+/* H := 0, g := 0, cost := 0 */
+int vg_solver_reset(vg_solver* solver);
+/* add the batch's normal equations at the pose table (K-compose .. K6, vg_batch_assemble_setup
+ * first): variable v's 6x6 block at tangent offset offsets[v] (factor_graph.py:292-308 puts
+ * the pose block top-left of a 15-dof frame state); *cost_out = the batch's gated cost sum */
+int vg_solver_add_batch(vg_solver* solver, vg_batch* batch, const double* poses_host,
+                        int64_t num_poses, const int64_t* offsets, double* cost_out);
+/* add host blocks (the reference's per-factor scatter of other factors, :529-535): block k is
+ * desc[4k .. 4k+3] = (row0, col0, rows, cols), its values row-major at consecutive positions
+ * of `values`; blocks must not overlap each other.  g_host (dim) is added when non-null. */
+int vg_solver_add_blocks(vg_solver* solver, int64_t num_blocks, const int64_t* desc,
+                         const double* values, const double* g_host);
+/* factor A = H + lam * diag(H) + jitter * I (method VG_SOLVE_*); *info = 0 on success, else
+ * the failing minor (Cholesky) / pivot (LU) — the reference's LinAlgError / RuntimeError */
+int vg_solver_factor(vg_solver* solver, double lam, double jitter, int32_t method,
+                     int64_t* info);
+/* solve A X = B with the last factorization: B = rhs_host (dim x nrhs, column-major), or -g
+ * when rhs_host is NULL (nrhs 1); X to x_host (dim x nrhs, column-major) */
+int vg_solver_solve(vg_solver* solver, const double* rhs_host, int64_t nrhs, double* x_host);
+/* copy H (dim x dim, symmetric), g (dim) and the accumulated cost to the host; any may be NULL */
+int vg_solver_export(vg_solver* solver, double* h_host, double* g_host, double* cost_out);
+/* diag(H) (dim) to the host: the jitter scale of marginal_covariance (:716-717) */
+int vg_solver_diagonal(vg_solver* solver, double* diag_host);
+
 /* ---- preprocessing (preprocess.py:122-164) --------------------------------------------- */
 /* replaces knn_search (preprocess.py:122-139): exact k nearest (self included), ordered by
  * (squared distance, index).  Returns VG_ERR_TOO_SPARSE when n < k. */

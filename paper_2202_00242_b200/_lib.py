@@ -105,6 +105,15 @@ _SIGNATURES = {
     "vg_batch_assemble_poses": ([c_void_p, _P_D, c_int64, _P_D], c_int),
     "vg_batch_assemble_poses_device": ([c_void_p, c_void_p, c_int64, c_void_p], c_int),
     "vg_batch_assemble_records_device": ([c_void_p, c_void_p, c_void_p], c_int),
+    "vg_solver_create": ([c_void_p, c_int64, _PP], c_int),
+    "vg_solver_destroy": ([c_void_p], c_int),
+    "vg_solver_reset": ([c_void_p], c_int),
+    "vg_solver_add_batch": ([c_void_p, c_void_p, _P_D, c_int64, _P_I64, _P_D], c_int),
+    "vg_solver_add_blocks": ([c_void_p, c_int64, _P_I64, _P_D, _P_D], c_int),
+    "vg_solver_factor": ([c_void_p, c_double, c_double, c_int32, _P_I64], c_int),
+    "vg_solver_solve": ([c_void_p, _P_D, c_int64, _P_D], c_int),
+    "vg_solver_export": ([c_void_p, _P_D, _P_D, _P_D], c_int),
+    "vg_solver_diagonal": ([c_void_p, _P_D], c_int),
     "vg_knn": ([c_void_p, c_void_p, c_int32, _P_I64], c_int),
     "vg_covariances": ([c_void_p, c_void_p, _P_I64, c_int32, c_double, _P_D, _P_U8], c_int),
     "vg_cloud_estimate_covariances": ([c_void_p, c_void_p, c_int32, c_double, _P_I64, _P_D,
@@ -520,6 +529,89 @@ class DeviceBatch:
         check(self.ctx.lib.vg_batch_assemble_poses_device(
             self.handle, c_void_p(poses_dev_ptr), int(num_poses), c_void_p(out_dev_ptr)),
             "vg_batch_assemble_poses_device")
+
+
+SOLVE_CHOLESKY, SOLVE_CHOLESKY_LU = 0, 1
+
+
+class DeviceSolver:
+    """Dense normal equations of a graph on the device and their damped solve (vg_solver_*,
+    SURVEY §8f row 3): the replacement of optimize_lm's per-attempt host factorization
+    (factor_graph.py:565-576) and marginal_covariance's (:707-722)."""
+
+    def __init__(self, dim: int, ctx: "Context | None" = None):
+        self.ctx = ctx or context()
+        self.dim = int(dim)
+        h = c_void_p()
+        check(self.ctx.lib.vg_solver_create(self.ctx.handle, self.dim, ctypes.byref(h)),
+              "vg_solver_create")
+        self.handle = h
+        self._fin = weakref.finalize(self, self.ctx.lib.vg_solver_destroy, h)
+
+    def reset(self) -> None:
+        check(self.ctx.lib.vg_solver_reset(self.handle), "vg_solver_reset")
+
+    def add_batch(self, batch: "DeviceBatch", poses: np.ndarray, offsets) -> float:
+        """Scatter the batch's device-assembled normal equations (assemble_setup first) at the
+        pose table; variable v's 6x6 block at tangent offset offsets[v].  Returns its cost."""
+        poses = f64(poses).reshape(-1, 8)
+        offs = np.ascontiguousarray(offsets, dtype=np.int64)
+        if len(offs) != batch.asm_vars:
+            raise ValueError("one tangent offset per assembled variable")
+        cost = c_double()
+        check(self.ctx.lib.vg_solver_add_batch(self.handle, batch.handle, dptr(poses),
+                                               poses.shape[0], iptr(offs), ctypes.byref(cost)),
+              "vg_solver_add_batch")
+        return float(cost.value)
+
+    def add_blocks(self, blocks, g: np.ndarray | None = None) -> None:
+        """Add host blocks [(row0, col0, array)] (non-overlapping) and a gradient vector."""
+        if blocks:
+            desc = np.array([(r, c, a.shape[0], a.shape[1]) for r, c, a in blocks],
+                            dtype=np.int64)
+            vals = np.concatenate([f64(a).ravel() for _, _, a in blocks])
+        else:
+            desc, vals = None, None
+        gg = None if g is None else f64(g)
+        check(self.ctx.lib.vg_solver_add_blocks(self.handle, 0 if desc is None else len(desc),
+                                                iptr(desc), dptr(vals), dptr(gg)),
+              "vg_solver_add_blocks")
+
+    def factor(self, lam: float = 0.0, jitter: float = 0.0,
+               method: int = SOLVE_CHOLESKY) -> int:
+        """Factor H + lam diag(H) + jitter I; 0 on success, else the failing minor / pivot."""
+        info = c_int64()
+        check(self.ctx.lib.vg_solver_factor(self.handle, float(lam), float(jitter), int(method),
+                                            ctypes.byref(info)), "vg_solver_factor")
+        return int(info.value)
+
+    def solve(self, rhs: np.ndarray | None = None) -> np.ndarray:
+        """X with A X = rhs (dim or dim x k); rhs None solves A x = -g."""
+        if rhs is None:
+            x = np.empty(self.dim)
+            check(self.ctx.lib.vg_solver_solve(self.handle, None, 1, dptr(x)), "vg_solver_solve")
+            return x
+        rhs = np.asarray(rhs, dtype=np.float64)
+        k = 1 if rhs.ndim == 1 else rhs.shape[1]
+        b = np.asfortranarray(rhs.reshape(self.dim, k))
+        x = np.empty((self.dim, k), order="F")
+        check(self.ctx.lib.vg_solver_solve(self.handle, b.ctypes.data_as(_P_D), k,
+                                           x.ctypes.data_as(_P_D)), "vg_solver_solve")
+        return x.reshape(rhs.shape)
+
+    def diagonal(self) -> np.ndarray:
+        d = np.empty(self.dim)
+        check(self.ctx.lib.vg_solver_diagonal(self.handle, dptr(d)), "vg_solver_diagonal")
+        return d
+
+    def export(self, h: bool = True):
+        """(H or None, g, accumulated batch cost)."""
+        hh = np.empty((self.dim, self.dim)) if h else None
+        g = np.empty(self.dim)
+        cost = c_double()
+        check(self.ctx.lib.vg_solver_export(self.handle, dptr(hh), dptr(g), ctypes.byref(cost)),
+              "vg_solver_export")
+        return hh, g, float(cost.value)
 
 
 _UPPER6 = np.triu_indices(6)

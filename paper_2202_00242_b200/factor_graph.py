@@ -10,17 +10,19 @@ each factor then serves its own record from an identity-keyed cache, exactly as 
 reference's ``_terms_cache`` does for one factor (:253-269).  Values are immutable, so
 identity of (v_i, v_j) is a safe key.
 
-The LM stays the reference's own (factor_graph.py:445-612): ``integrate.patch(limapper)``
-swaps in this MatchingCostFactor and replaces two FactorGraph methods whose per-factor loops
-dominate at global-mapping scale — ``total_cost`` (:472-474: one batched cost launch for all
-of the graph's matching factors) and ``_assemble_dense`` (:522-536: the normal equations
-summed on the device, K6, and scattered into the reference's dense H/g); see
-``graph_total_cost`` / ``graph_assemble_dense``.
+``integrate.patch(limapper)`` swaps in this MatchingCostFactor and replaces the FactorGraph
+methods whose host work dominates at global-mapping scale — ``total_cost`` (:472-474: one
+batched cost launch for all of the graph's matching factors), ``_assemble_dense`` (:522-536:
+the normal equations summed on the device, K6, and scattered into the reference's dense H/g),
+and, above the reference's dense threshold, ``optimize_lm`` / ``marginal_covariance``
+(:546-612, :703-722: H kept on the device, each damped solve a device factorization; the
+reference's control flow, and its own method below the threshold).
 """
 
 from __future__ import annotations
 
 import itertools
+import sys
 import weakref
 from collections import OrderedDict
 from dataclasses import dataclass
@@ -182,6 +184,12 @@ class _Batcher:
     def assemble(self, group, values, var_keys) -> "_lib.NormalEquations":
         """Device-assembled normal equations of `group` over the graph variables `var_keys`
         (FactorGraph._assemble_dense, factor_graph.py:522-536)."""
+        batch, poses = self.assembly_batch(group, values, var_keys)
+        return batch.assemble_poses(poses)
+
+    def assembly_batch(self, group, values, var_keys):
+        """(device batch set up to assemble `group` over `var_keys`, its pose table at
+        `values`) — one evaluation of the normal equations follows."""
         sig = ("asm", tuple(f._serial for f in group), tuple(var_keys))
         hit = self._batches.get(sig)
         if hit is None:
@@ -211,7 +219,7 @@ class _Batcher:
         if fixed.shape[0]:
             poses[len(var_keys):] = fixed
         self.evaluations += 1
-        return batch.assemble_poses(poses)
+        return batch, poses
 
 
 _BATCHER = _Batcher()
@@ -324,16 +332,24 @@ def _split_factors(graph):
     return gpu, rest
 
 
+#: (patched reference class, method name) -> the reference's own function (integrate.patch)
+_ORIGINALS: dict = {}
+
+
+def _original(graph, name):
+    for cls in type(graph).__mro__:
+        fn = _ORIGINALS.get((cls, name))
+        if fn is not None:
+            return fn
+    raise TypeError(f"{type(graph).__name__}.{name} was not patched by integrate.patch")
+
+
 def graph_add_factor(self, factor) -> None:
     """FactorGraph.add_factor (factor_graph.py:460-467) that also tags a MatchingCostFactor with
     its graph, so the per-factor batching shim groups a graph's own factors only."""
-    _ORIGINAL_ADD_FACTOR[type(self)](self, factor)
+    _original(self, "add_factor")(self, factor)
     if isinstance(factor, MatchingCostFactor):
         factor._graph_ref = weakref.ref(self)
-
-
-#: the reference's add_factor per patched class (integrate.patch fills it)
-_ORIGINAL_ADD_FACTOR: dict = {}
 
 
 def graph_total_cost(self, values=None) -> float:
@@ -377,3 +393,158 @@ def graph_assemble_dense(self, values, slices, dim):
             if a != b:
                 h[sls[b], sls[a]] += blk.T
     return h, g, cost
+
+
+# ---- the LM's linear solve on the device ----------------------------------
+#
+# For graphs above the reference's dense_threshold its LM factors a CSC copy of the dense
+# damped H with splu on every damping attempt (factor_graph.py:565-576); at global-mapping
+# size that is a 6,000 x 6,000 system assembled and factored on the host.  Here H and g never
+# leave the device: the matching factors' normal equations go from K6 straight into the dense
+# device H (vg_solver_add_batch), the other factors' host blocks are added by one upload, and
+# each damping attempt is a device Cholesky (LU when not positive definite: splu's semantics)
+# returning only the dim-sized step.  The LM control flow is the reference's (:546-612); the
+# small dense branch (dim <= dense_threshold) stays the reference's own code.
+
+
+def _ref_module(graph):
+    """The module defining the reference FactorGraph (LmSettings, OptimizeResult, errors)."""
+    for cls in type(graph).__mro__:
+        mod = sys.modules.get(cls.__module__)
+        if mod is not None and hasattr(mod, "LmSettings") and hasattr(mod, "OptimizeResult"):
+            return mod
+    raise TypeError(f"{type(graph).__name__} is not a reference FactorGraph")
+
+
+class DeviceNormalEquations:
+    """A graph's H, g on the device at given values (the device side of _assemble_dense,
+    factor_graph.py:522-536) and the damped solves of its LM."""
+
+    def __init__(self, graph, slices, dim):
+        self.graph, self.slices, self.dim = graph, slices, dim
+        self.solver = _lib.DeviceSolver(dim)
+
+    @classmethod
+    def of(cls, graph, slices, dim) -> "DeviceNormalEquations":
+        """The graph's solver (kept on the graph while its dimension is unchanged)."""
+        ne = graph.__dict__.get("_vgicp_normal")
+        if ne is None or ne.dim != dim:
+            graph.__dict__.pop("_vgicp_normal", None)
+            ne = cls(graph, slices, dim)
+            graph.__dict__["_vgicp_normal"] = ne
+        ne.slices = slices
+        return ne
+
+    def assemble(self, values) -> float:
+        """H, g := the normal equations at `values`; returns the total cost (:522-536)."""
+        s = self.solver
+        s.reset()
+        gpu, rest = _split_factors(self.graph)
+        cost = 0.0
+        if gpu:
+            keys = list(self.graph.values)
+            batch, poses = _BATCHER.assembly_batch(gpu, values, keys)
+            cost += s.add_batch(batch, poses, [self.slices[k].start for k in keys])
+        if rest:
+            blocks: dict = {}
+            g = np.zeros(self.dim)
+            for f in rest:
+                lin = f.linearize(values)
+                cost += lin.cost
+                sls = [self.slices[k] for k in lin.keys]
+                for a, ga in enumerate(lin.g):
+                    g[sls[a]] += ga
+                for (a, b), blk in lin.h.items():
+                    _add_block(blocks, sls[a].start, sls[b].start, blk)
+                    if a != b:
+                        _add_block(blocks, sls[b].start, sls[a].start, blk.T)
+            s.add_blocks([(r, c, blk) for (r, c), blk in blocks.items()], g)
+        return float(cost)
+
+    def damped_step(self, lam: float):
+        """delta solving (H + lam diag(H)) delta = -g, or None where the reference's solve
+        raises (singular system, non-finite update: :574-578)."""
+        if self.solver.factor(lam, 0.0, _lib.SOLVE_CHOLESKY_LU):
+            return None
+        delta = self.solver.solve()
+        return delta if np.all(np.isfinite(delta)) else None
+
+
+def _add_block(blocks, r, c, blk):
+    cur = blocks.get((r, c))
+    blocks[(r, c)] = np.array(blk, dtype=np.float64) if cur is None else cur + blk
+
+
+def graph_optimize_lm(self, settings=None):
+    """FactorGraph.optimize_lm (factor_graph.py:546-612) with the damped solve on the device
+    above the dense threshold; the reference's own method at or below it."""
+    ref = _ref_module(self)
+    settings = settings or ref.LmSettings()
+    slices, dim = self._slices()
+    if dim <= settings.dense_threshold:
+        return _original(self, "optimize_lm")(self, settings)
+    self.check_structure()
+    values = dict(self.values)
+    cost = self.total_cost(values)
+    lam = settings.lambda_init
+    ne = DeviceNormalEquations.of(self, slices, dim)
+    iterations = 0
+
+    def give_up(message):
+        self.values = values
+        self._cached_normal = None
+        raise ref.NotConverged(message, estimates=values, cost=cost)
+
+    for _ in range(settings.max_iterations):
+        cost = ne.assemble(values)
+        iterations += 1
+        converged = False
+        while True:  # damping attempts (:568-600)
+            delta = ne.damped_step(lam)
+            if delta is None:
+                lam *= settings.lambda_up
+                if lam > settings.lambda_max:
+                    give_up("damping exhausted on singular system")
+                continue
+            if np.max(np.abs(delta)) < settings.update_tol:
+                converged = True
+                break
+            candidate = self._retract_all(values, slices, delta)
+            new_cost = self.total_cost(candidate)
+            if np.isfinite(new_cost) and new_cost < cost:
+                break
+            lam *= settings.lambda_up
+            if lam > settings.lambda_max:
+                give_up("no cost-reducing step found")
+        if converged:
+            break
+        values = candidate  # accepted (:590-594)
+        lam = max(lam * settings.lambda_down, 1e-12)
+        small = (cost - new_cost) <= settings.rel_cost_tol * max(cost, 1e-30)
+        cost = new_cost
+        if small:
+            break
+    self.values = values
+    final = ne.assemble(values)
+    # H is not copied back: marginal_covariance re-assembles it on the device (:705-709)
+    self._cached_normal = None
+    return ref.OptimizeResult(values, final, iterations)
+
+
+def graph_marginal_covariance(self, key):
+    """FactorGraph.marginal_covariance (factor_graph.py:703-722) with the factorization on the
+    device above the dense threshold (same jitter retry); the reference's method below it."""
+    ref = _ref_module(self)
+    slices, dim = self._slices()
+    if dim <= ref.LmSettings().dense_threshold:
+        return _original(self, "marginal_covariance")(self, key)
+    ne = DeviceNormalEquations.of(self, slices, dim)
+    ne.assemble(self.values)
+    sl = slices[key]
+    rhs = np.zeros((dim, key.dim))
+    rhs[sl] = np.eye(key.dim)
+    if ne.solver.factor(0.0, 0.0, _lib.SOLVE_CHOLESKY):
+        jitter = 1e-9 * max(1.0, float(np.max(np.abs(ne.solver.diagonal()))))
+        if ne.solver.factor(0.0, jitter, _lib.SOLVE_CHOLESKY):
+            raise np.linalg.LinAlgError("marginal covariance: H + jitter I is not positive definite")
+    return ne.solver.solve(rhs)[sl]

@@ -11,9 +11,10 @@ matrix of OdometryEstimator (odometry.py:396-403) becomes one batched lookup lau
 FactorGraph.total_cost / _assemble_dense (factor_graph.py:472-474, 522-536) batch the graph's
 matching factors (one cost launch; device-assembled normal equations).  Modules that
 imported a name with ``from .registration import ...`` (factor_graph.py:49-55,
-odometry.py:21-46) get their module-level binding replaced too; the reference's LM solver
-(optimize_lm), IMU factors and odometry logic are untouched and call the drop-in through the
-unchanged Factor protocol.  patch() is idempotent (a second call changes nothing).
+odometry.py:21-46) get their module-level binding replaced too.  Above the reference's dense
+threshold (600 tangent dims) optimize_lm and marginal_covariance keep H on the device and
+factor it there (factor_graph.py:546-612, 703-722; the reference's control flow); IMU factors
+and odometry logic are untouched and call the drop-in through the unchanged Factor protocol.  patch() is idempotent (a second call changes nothing).
 """
 
 from __future__ import annotations
@@ -75,9 +76,13 @@ METHOD_REPLACEMENTS = {
     # FactorGraph.total_cost (factor_graph.py:472-474): one batched cost launch for the
     # graph's matching factors; _assemble_dense (:522-536): their normal equations summed on
     # the device (K6) and scattered into the dense H/g the reference's LM solves
+    # optimize_lm / marginal_covariance (:546-612, :703-722): above the dense threshold the
+    # damped solves run on the device against a device-resident H
     "factor_graph": {"FactorGraph": {"total_cost": _fg.graph_total_cost,
                                      "_assemble_dense": _fg.graph_assemble_dense,
-                                     "add_factor": _fg.graph_add_factor}},
+                                     "add_factor": _fg.graph_add_factor,
+                                     "optimize_lm": _fg.graph_optimize_lm,
+                                     "marginal_covariance": _fg.graph_marginal_covariance}},
 }
 
 #: (class, method name) -> the reference's own function, for callers that compare against it
@@ -118,8 +123,7 @@ def patch(pkg="limapper"):
                 if name in vars(cls) and vars(cls)[name] is not fn:
                     saved.append((cls, name, vars(cls)[name]))
                     ORIGINALS.setdefault((cls, name), vars(cls)[name])
-                    if fn is _fg.graph_add_factor:
-                        _fg._ORIGINAL_ADD_FACTOR[cls] = vars(cls)[name]
+                    _fg._ORIGINALS.setdefault((cls, name), vars(cls)[name])
                     setattr(cls, name, fn)
 
     # deskew keeps the reference's host IMU integration (taken from its preprocess module) and
