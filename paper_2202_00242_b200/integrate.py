@@ -81,6 +81,7 @@ METHOD_REPLACEMENTS = {
     "factor_graph": {"FactorGraph": {"total_cost": _fg.graph_total_cost,
                                      "_assemble_dense": _fg.graph_assemble_dense,
                                      "add_factor": _fg.graph_add_factor,
+                                     "check_structure": _fg.graph_check_structure,
                                      "optimize_lm": _fg.graph_optimize_lm,
                                      "marginal_covariance": _fg.graph_marginal_covariance}},
 }

@@ -103,3 +103,35 @@ def test_singular_system_exhausts_damping_like_the_reference(lm):
     b = _run(lambda: original(singular_graph(lw, fg), settings))
     assert a[0] == "NotConverged" and "singular" in str(a[1])
     _same(a, b)
+
+
+class _Edge:
+    """A structural stand-in factor: keys and the grounding flag are all check_structure
+    reads (factor_graph.py:478-510)."""
+
+    def __init__(self, keys, grounding=False):
+        self.keys = tuple(keys)
+        self.grounding = grounding
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_check_structure_matches_reference(lm, seed):
+    """graph_check_structure (connected components over integer indices) raises exactly what
+    the reference's union-find raises, message included, or passes where it passes."""
+    lw, fg, _ = lm
+    from paper_2202_00242_b200 import integrate
+
+    original = integrate.ORIGINALS[(fg.FactorGraph, "check_structure")]
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(3, 40))
+    g = fg.FactorGraph()
+    for i in range(n):
+        g.add_variable(fg.submap_key(i), None)
+    for _ in range(int(rng.integers(0, 2 * n))):
+        k = int(rng.integers(1, 4))
+        ids = rng.choice(n, size=k, replace=False)
+        g.factors.append(_Edge([fg.submap_key(int(i)) for i in ids], rng.random() < 0.15))
+    a = _run(lambda: g.check_structure())
+    g.__dict__.pop("_vgicp_checked", None)
+    b = _run(lambda: original(g))
+    assert a[0] == b[0] and (a[0] == "ok" or str(a[1]) == str(b[1]))
