@@ -852,6 +852,203 @@ __global__ void __launch_bounds__(32, kMinBlocks)
   partials[(size_t)w * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
 }
 
+// ---- K4c: cost mode, lookup and cost fused ----------------------------------------------------
+// The LM's candidate evaluations need only each factor's cost and inlier count
+// (factor_graph.py:589-591 -> MatchingCostFactor.cost -> matching_cost, registration.py:160-165).
+// Without the 28 accumulators the per-hit math is ~70 fp64 ops, so the K4a -> K4b split (hit
+// list written and re-read, a second launch with its own per-item prologue) costs more than
+// compaction saves: here one warp per item probes a round of 32 points exactly as K4a does,
+// gathers that round's hit records (cooperatively, 5 lanes per 80 B record) and plane-form
+// covariances into a 2-stage shared-memory ring, and computes the previous round's costs while
+// those gathers fly; lanes whose point missed sit out the math.  Fast path only (32-bit local
+// keys, power-of-two resolutions, fp32-exact points, plane-form covariances).  Per-hit cost:
+// hit_core's, term for term; summed per lane in round order, then a fixed butterfly.
+// OWN_REG: the point and plane covariance of a hit ride in registers to the next round (lane-own,
+// nearly coalesced loads) and only the records are staged: 5 KB of shared memory per warp
+// instead of 9 KB, which leaves the L1 to the point / bucket loads.
+struct CostSmem {
+  float4 rec[2][32][kRecStride];
+};
+template <int kMinBlocks, int OWN_REG>
+__global__ void __launch_bounds__(32, kMinBlocks)
+    k_cost_fused(const ItemHdr* __restrict__ hdrs, int n_items, double* __restrict__ partials) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  AccSmem<2, 1>& sm = *reinterpret_cast<AccSmem<2, 1>*>(smem_raw);
+  CostSmem& smr = *reinterpret_cast<CostSmem*>(smem_raw);
+  const int lane = threadIdx.x & 31;
+  const int w = blockIdx.x;
+  pdl_release();
+  pdl_wait();  // item headers carry T_ij written by K-compose
+  if (w >= n_items) return;
+  const ItemHdr* h = hdrs + w;
+  double R[9], t[3];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[k] = __ldg(h->T + k);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) t[k] = __ldg(h->T + 9 + k);
+  const float4* pa = (const float4*)__ldg((const unsigned long long*)&h->a);
+  const double2* c0 = (const double2*)__ldg((const unsigned long long*)&h->c0);
+  const double2* c1 = (const double2*)__ldg((const unsigned long long*)&h->c1);
+  const double2* c2 = (const double2*)__ldg((const unsigned long long*)&h->c2);
+  const VoxelRec* recs = (const VoxelRec*)__ldg((const unsigned long long*)&h->mv.recs);
+  const unsigned* keys32 = (const unsigned*)__ldg((const unsigned long long*)&h->mv.keys32);
+  const double inv_res = __ldg(&h->mv.inv_res);
+  const int shift = __ldg(&h->mv.shift);
+  const unsigned mask = __ldg(&h->mv.mask);
+  const int m = __ldg(&h->mv.m);
+  const int bx = __ldg(&h->mv.bx), by = __ldg(&h->mv.by), bz = __ldg(&h->mv.bz);
+  const int ex = __ldg(&h->mv.ex), ey = __ldg(&h->mv.ey), ez = __ldg(&h->mv.ez);
+  const int begin = __ldg(&h->begin), end = __ldg(&h->end);
+  const int last = end - 1;
+  struct Q {
+    unsigned k32, bucket;
+    bool live;
+  };
+  auto make_q = [&](float4 a, int i) {  // k_lookup_fast's query, step for step
+    const double px = a.x, py = a.y, pz = a.z;
+    const double x = fma(R[0], px, fma(R[1], py, R[2] * pz)) + t[0];
+    const double y = fma(R[3], px, fma(R[4], py, R[5] * pz)) + t[1];
+    const double z = fma(R[6], px, fma(R[7], py, R[8] * pz)) + t[2];
+    const double qx = x * inv_res, qy = y * inv_res, qz = z * inv_res;
+    const int ix = __double2int_rd(qx), iy = __double2int_rd(qy), iz = __double2int_rd(qz);
+    Q q;
+    q.live = false;
+    q.k32 = 0;
+    if ((unsigned)(ix + 1048575) < 2097151u && (unsigned)(iy + 1048575) < 2097151u &&
+        (unsigned)(iz + 1048575) < 2097151u) {
+      const unsigned lx = (unsigned)(ix - bx), ly = (unsigned)(iy - by), lz = (unsigned)(iz - bz);
+      q.live = lx < (unsigned)ex && ly < (unsigned)ey && lz < (unsigned)ez;
+      q.k32 = lx | (ly << 11) | (lz << 22);
+    } else {
+      MapView mv;
+      mv.bx = bx; mv.by = by; mv.bz = bz; mv.ex = ex; mv.ey = ey; mv.ez = ez; mv.shift = shift;
+      const Query qq = make_query(mv, floor(qx), floor(qy), floor(qz), 1);
+      q.live = qq.inside;
+      q.k32 = qq.k32;
+    }
+    q.bucket = bucket32(q.k32, shift);
+    q.live = q.live && i < end && m > 0;
+    return q;
+  };
+  auto load_bucket = [&](unsigned bucket, unsigned (&g)[4]) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(keys32 + (size_t)bucket * kBucket32));
+    g[0] = v.x;
+    g[1] = v.y;
+    g[2] = v.z;
+    g[3] = v.w;
+  };
+  auto resolve = [&](const Q& q, unsigned (&g)[4]) {
+    int slot = -1;
+    if (q.live) {
+      unsigned bk = q.bucket;
+      for (unsigned probes = 0;; ++probes) {
+        VG_DEVICE_CHECK(probes <= mask, "K4c: every bucket visited");
+        int found = -1;
+        bool empty = false;
+#pragma unroll
+        for (int j = kBucket32 - 1; j >= 0; --j) {
+          if (g[j] == q.k32) found = j;
+          empty |= (g[j] == kEmpty32);
+        }
+        if (found >= 0) {
+          slot = (int)(bk * kBucket32 + found);
+          break;
+        }
+        if (empty) break;
+        bk = (bk + 1) & mask;
+        load_bucket(bk, g);
+      }
+    }
+    return slot;
+  };
+  double acc[28];
+  acc[27] = 0.0;
+  int cnt = 0;
+  bool prev_hit = false;
+  float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);  // OWN_REG: previous round's point, covariance
+  double2 s0p = make_double2(0.0, 0.0), s1p = s0p, s2p = s0p;
+  float4 p0 = ld_pt(pa + min(begin + lane, last));
+  float4 p1 = ld_pt(pa + min(begin + 32 + lane, last));
+  unsigned g0[4] = {0, 0, 0, 0}, g1[4] = {0, 0, 0, 0};
+  Q q0 = make_q(p0, begin + lane);
+  if (q0.live) load_bucket(q0.bucket, g0);
+  int r = 0;
+  for (int base = begin; base < end; base += 32, ++r) {
+    const int i = base + lane;
+    // the next round's probe and the point after it are in flight while this round resolves
+    const Q q1 = make_q(p1, i + 32);
+    if (q1.live) load_bucket(q1.bucket, g1);
+    const float4 p2 = ld_pt(pa + min(i + 64, last));
+    const int slot = resolve(q0, g0);
+    cnt += __popc(__ballot_sync(0xffffffffu, slot >= 0));
+    // this round's gathers into stage r & 1 (misses contribute nothing, registration.py:150-156)
+    AccStageT<1>& st = sm.stage[r & 1];
+    double2 s0n = make_double2(0.0, 0.0), s1n = s0n, s2n = s0n;
+    if (slot >= 0) {
+      if (OWN_REG) {
+        s0n = __ldg(c0 + i);
+        s1n = __ldg(c1 + i);
+        s2n = __ldg(c2 + i);
+      } else {
+        st.pt[0][lane] = p0;
+        cp_async16_sel<2>(&st.cov[0][lane], c0 + i);
+        cp_async16_sel<2>(&st.cov[1][lane], c1 + i);
+        cp_async16_sel<2>(&st.cov[2][lane], c2 + i);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kRecUnits; ++c) {
+      const int u = c * 32 + lane;
+      const int q = u / kRecUnits, j = u - q * kRecUnits;
+      const int row = __shfl_sync(0xffffffffu, slot, q);
+      if (row >= 0)
+        cp_async16_sel<1>(OWN_REG ? &smr.rec[r & 1][q][j] : &st.rec[q][j],
+                          reinterpret_cast<const char*>(recs + row) + 16 * j);
+    }
+    cp_async_commit();
+    // the previous round's costs
+    if (r > 0) {
+      cp_async_wait<1>();
+      __syncwarp();
+      if (prev_hit) {
+        if (OWN_REG)
+          hit_core<1, 1>(pp.x, pp.y, pp.z, s0p, s1p, s2p, smr.rec[(r - 1) & 1][lane], R, t, 1.0,
+                         acc);
+        else
+          hit_math<1, 1, 1>(sm.stage[(r - 1) & 1], lane, false, R, t, 1.0, acc);
+      }
+      __syncwarp();  // stage (r - 1) & 1 is refilled by round r + 1
+    }
+    prev_hit = slot >= 0;
+    if (OWN_REG) {
+      pp = p0;
+      s0p = s0n;
+      s1p = s1n;
+      s2p = s2n;
+    }
+    p0 = p1;
+    p1 = p2;
+    q0 = q1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) g0[k] = g1[k];
+  }
+  cp_async_wait<0>();
+  __syncwarp();
+  if (r > 0 && prev_hit) {
+    if (OWN_REG)
+      hit_core<1, 1>(pp.x, pp.y, pp.z, s0p, s1p, s2p, smr.rec[(r - 1) & 1][lane], R, t, 1.0, acc);
+    else
+      hit_math<1, 1, 1>(sm.stage[(r - 1) & 1], lane, false, R, t, 1.0, acc);
+  }
+  double c = acc[27];
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+  if (lane == 0) {
+    partials[2 * (size_t)w] = c;
+    partials[2 * (size_t)w + 1] = (double)cnt;
+  }
+}
+
 }  // namespace vg
 
 using namespace vg;
@@ -956,8 +1153,36 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
              : launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB_GEN, 2, 0>, s2, d, b->items + off, cnt, b->hits, p, st);
 }
 
+#ifndef VG_COST_MINB
+#define VG_COST_MINB 24
+#endif
+#ifndef VG_COST_OWN_REG
+#define VG_COST_OWN_REG 1
+#endif
+
+// cost mode on the fast path: K4c (lookup + cost fused) instead of K4a + K4b
+static bool cost_fused(const vg_batch* b, int kmode) {
+  static const int env = [] {
+    const char* e = getenv("VGICP_COST_FUSED");  // 0: K4a + K4b (ablation)
+    return e ? atoi(e) : 1;
+  }();
+  return env && kmode == 1 && b->key_mode == 1 && b->all_pow2 && b->all_f32 && b->all_plane;
+}
+
+static int launch_cost_fused(vg_ctx* ctx, vg_batch* b, int off, int cnt, cudaStream_t st) {
+  const size_t smem = VG_COST_OWN_REG ? sizeof(CostSmem) : sizeof(AccSmem<2, 1>);
+  auto kern = k_cost_fused<VG_COST_MINB, VG_COST_OWN_REG>;
+  VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  VG_CUDA(launch_pdl(kern, dim3(cnt), dim3(32), smem, st,
+                     (const ItemHdr*)(b->hdrs + off), cnt, b->partials + 2 * (size_t)off));
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi) {
   if (hi <= lo) return 0;
+  if (cost_fused(b, kmode)) return launch_cost_fused(ctx, b, lo, hi - lo, ctx->stream);
   VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
   if (kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
   return 0;
@@ -965,6 +1190,11 @@ int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi)
 
 int launch_accumulate_range_ev(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi,
                                cudaEvent_t after_lookup) {
+  if (cost_fused(b, kmode)) {  // one kernel: the event marks its end
+    if (hi > lo) VG_CHECK(launch_cost_fused(ctx, b, lo, hi - lo, ctx->stream));
+    VG_CUDA(cudaEventRecord(after_lookup, ctx->stream));
+    return 0;
+  }
   if (hi > lo) VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
   VG_CUDA(cudaEventRecord(after_lookup, ctx->stream));
   if (hi > lo && kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream));

@@ -837,6 +837,10 @@ def test_config5_every_factor_rows_and_inliers_bit_exact(config5):
     assert np.array_equal(rec[:, 91].astype(np.int64), ref_inl)
     cost = batch.linearize_poses(table, _lib.MODE_COST)
     assert np.array_equal(cost[:, 1].astype(np.int64), ref_inl)
+    # cost mode (K4c: lookup + cost fused, no hit compaction) against the linearization's
+    # cost (K4a + K4b): the same per-hit terms, summed in another order
+    live = ref_inl >= 10
+    assert np.allclose(cost[live, 0], rec[live, 90], rtol=1e-12, atol=0.0)
 
 
 def test_config5_blocks_of_600_factors_vs_oracle(config5):
