@@ -150,31 +150,41 @@ def time_lm_iteration(g, fg, info: dict) -> dict:
         parts[name] = float(np.median(ts))
     start = dict(g.values)
     c0 = g.total_cost()
-    a = time.perf_counter()
-    res = g.optimize_lm(fg.LmSettings(max_iterations=1))
-    it = time.perf_counter() - a
-    out = dict(info, seconds=it, iterations=res.iterations, initial_cost=c0,
-               final_cost=res.final_cost, tangent_dim=dim, first_call_setup_s=round(setup, 2),
-               **parts)
-    if dim > fg.LmSettings().dense_threshold:
-        dev_values = g.values
+    one = fg.LmSettings(max_iterations=1)
+
+    def run(fn):  # one LM iteration from the same starting values
         g.values = dict(start)
         g._cached_normal = None
-        host = integrate.ORIGINALS[(fg.FactorGraph, "optimize_lm")]
         a = time.perf_counter()
-        res_h = host(g, fg.LmSettings(max_iterations=1))
-        out["seconds_host_solve"] = time.perf_counter() - a
+        res = fn()
+        return time.perf_counter() - a, res
+
+    first, res = run(lambda: g.optimize_lm(one))
+    reps = [run(lambda: g.optimize_lm(one)) for _ in range(3)]
+    it, res = sorted(reps, key=lambda r: r[0])[1]
+    out = dict(info, seconds=it, seconds_first_call=first, iterations=res.iterations,
+               initial_cost=c0, final_cost=res.final_cost, tangent_dim=dim,
+               first_call_setup_s=round(setup, 2), **parts)
+    if dim > fg.LmSettings().dense_threshold:
+        dev_values = res.estimates
+        host = integrate.ORIGINALS[(fg.FactorGraph, "optimize_lm")]
+        reps_h = [run(lambda: host(g, one)) for _ in range(3)]
+        t_h, res_h = sorted(reps_h, key=lambda r: r[0])[1]
+        out["seconds_host_solve"] = t_h
         out["final_cost_host_solve"] = res_h.final_cost
+
         def trans(v):
             return v.translation if hasattr(v, "translation") else v.pose.translation
 
         out["max_translation_difference_m"] = float(max(
-            np.max(np.abs(trans(dev_values[k]) - trans(g.values[k]))) for k in g.values))
+            np.max(np.abs(trans(dev_values[k]) - trans(res_h.estimates[k]))) for k in dev_values))
         out["api"] = ("limapper FactorGraph.optimize_lm(LmSettings(max_iterations=1)) with the "
                       "drop-in: device-resident H, device damped solve (vg_solver_*: cuSOLVER "
-                      "Cholesky, LU fallback), reference LM control flow; seconds_host_solve = "
-                      "the reference's own optimize_lm (host splu) with only total_cost / "
-                      "_assemble_dense / MatchingCostFactor replaced, from the same values")
+                      "Cholesky, LU fallback), reference LM control flow; seconds = median of 3 "
+                      "iterations from the same values (seconds_first_call: the first, with "
+                      "check_structure and the solver's first factorization); seconds_host_solve "
+                      "= the reference's own optimize_lm (host splu) with only total_cost / "
+                      "_assemble_dense / check_structure / MatchingCostFactor replaced, median of 3")
     else:
         out["api"] = ("limapper FactorGraph.optimize_lm(LmSettings(max_iterations=1)): reference "
                       "LM and host dense solve (dim <= dense_threshold); drop-in total_cost / "
