@@ -1,6 +1,7 @@
 // capi.cu — the extern "C" boundary (include/vgicp.h): handle lifetime, host<->device
 // staging, batch flattening, and status-code error reporting.  No exception crosses the ABI.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -1187,6 +1188,8 @@ static int assemble_setup(vg_batch* b, int64_t num_vars, const int32_t* given, i
   if (!codes.empty()) VG_CHECK(h2d(ctx, b->asm_codes, codes.data(), sizeof(int) * codes.size()));
   VG_CUDA(cudaStreamSynchronize(ctx->stream));
   b->asm_vars = V;
+  static std::atomic<long long> setups{0};
+  b->asm_gen = ++setups;  // unique across batches: a reused batch address is a new setup
   b->asm_pairs_n = P;
   b->asm_out_pairs = P_out;
   b->asm_pairs = pairs;

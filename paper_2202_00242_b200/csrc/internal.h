@@ -145,6 +145,7 @@ struct vg_batch {
                                       // (vg_batch_lookup_rows output layout)
   // normal-equation assembly (vg_batch_assemble_*): CSR of contributions per output unit
   long long asm_vars = -1;            // variables (pose-table rows < asm_vars); -1: not set up
+  long long asm_gen = 0;              // unique id of the current assembly setup (consumers' caches)
   long long asm_pairs_n = 0;
   std::vector<int> asm_pairs;         // P x 2 (a < b)
   int* asm_begin = nullptr;           // units + 1

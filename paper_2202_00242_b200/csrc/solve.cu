@@ -41,8 +41,8 @@ struct vg_solver {
   long long offs_cap = 0;
   int* pairs = nullptr;       // pair list (device) of the batch last scattered
   long long pairs_cap = 0;
-  const vg_batch* pairs_of = nullptr;
-  long long pairs_sig = -1;
+  const vg_batch* pairs_of = nullptr;  // the pair list on the device is this batch's ...
+  long long pairs_gen = -1;            // ... as of this assembly setup
   long long* blk = nullptr;   // host block descriptors (device copy)
   long long blk_cap = 0;
   double* blkv = nullptr;
@@ -255,13 +255,13 @@ int vg_solver_add_batch(vg_solver* s, vg_batch* b, const double* poses_host, int
                           cudaMemcpyHostToDevice, ctx->stream));
   VG_CUDA(cudaMemcpyAsync(s->offs, offsets, sizeof(long long) * V, cudaMemcpyHostToDevice,
                           ctx->stream));
-  if (s->pairs_of != b || s->pairs_sig != P) {
+  if (s->pairs_of != b || s->pairs_gen != b->asm_gen) {
     VG_CHECK(grow(ctx, &s->pairs, &s->pairs_cap, std::max<long long>(2 * P, 1)));
     if (P)
       VG_CUDA(cudaMemcpyAsync(s->pairs, b->asm_pairs.data(), sizeof(int) * 2 * P,
                               cudaMemcpyHostToDevice, ctx->stream));
     s->pairs_of = b;
-    s->pairs_sig = P;
+    s->pairs_gen = b->asm_gen;
   }
   VG_CHECK(vg_batch_assemble_poses_device(b, s->poses, V_poses, s->ne));
   k_scatter_ne<<<grid_for(36 * V + 6 * V + 36 * P), 256, 0, ctx->stream>>>(
