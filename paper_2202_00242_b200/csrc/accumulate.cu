@@ -41,6 +41,9 @@ namespace vg {
 #ifndef VG_K4B_MINB
 #define VG_K4B_MINB 15
 #endif
+#ifndef VG_K4B_STAGES
+#define VG_K4B_STAGES 2  // shared-memory ring depth of the fast-path linearize K4b
+#endif
 #ifndef VG_K4B_MINB_GEN
 #define VG_K4B_MINB_GEN 15
 #endif
@@ -1146,7 +1149,8 @@ static int launch_acc_range(vg_ctx* ctx, vg_batch* b, int kmode, int off, int cn
   // PT = 1: every point fp32-exact, one 16 B point unit per lane (more L1 left)
   if (b->all_f32)
     return b->all_plane
-               ? launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB, 1, 1>, s1, d, b->items + off, cnt, b->hits, p, st)
+               ? launch_acc_kernel(ctx, k_accumulate<0, VG_K4B_STAGES, VG_K4B_MINB, 1, 1>,
+                                   sizeof(AccSmem<VG_K4B_STAGES, 1>) * kAccWarps, d, b->items + off, cnt, b->hits, p, st)
                : launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB_GEN, 1, 0>, s1, d, b->items + off, cnt, b->hits, p, st);
   return b->all_plane
              ? launch_acc_kernel(ctx, k_accumulate<0, 2, VG_K4B_MINB_GEN, 2, 1>, s2, d, b->items + off, cnt, b->hits, p, st)
