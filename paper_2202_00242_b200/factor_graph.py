@@ -60,10 +60,6 @@ def submap_key(index: int) -> Key:
     return Key("submap-pose", index)
 
 
-def _pose_of(kind: str, value):
-    return value if kind == "submap-pose" else value.pose
-
-
 class FactorLinearization:
     """Gradient/Hessian blocks of one factor (factor_graph.py:102-111)."""
 
@@ -90,6 +86,41 @@ class Factor:
 # ---- the batching shim ---------------------------------------------------------------------
 
 
+class _PoseTable:
+    """The (V + fixed, 8) pose table of a batch's variables at given values (the C-ABI layout,
+    geometry.pose_row).  When `values` holds the same key objects in the same order as the
+    last call — the LM's candidate dicts are built from the graph's own keys
+    (factor_graph.py:539-544) — the per-key dict lookups are skipped."""
+
+    def __init__(self, var_keys, fixed):
+        self.var_keys = var_keys
+        self.fixed = fixed
+        self.submap = [k.kind == "submap-pose" for k in var_keys]
+        self._order = None  # (the key objects of values, index of each variable among them)
+
+    def build(self, values) -> np.ndarray:
+        keys = self.var_keys
+        order = self._order
+        if (order is not None and len(values) == len(order[0])
+                and all(a is b for a, b in zip(values, order[0]))):
+            listed = list(values.values())
+            vals = [listed[i] for i in order[1]]
+        else:
+            vals = [values[k] for k in keys]
+            pos = {id(k): i for i, k in enumerate(values)}
+            idx = [pos.get(id(k)) for k in keys]
+            self._order = None if None in idx else (tuple(values), idx)
+        poses = [v if sub else v.pose for v, sub in zip(vals, self.submap)]
+        n = len(keys)
+        table = np.empty((n + self.fixed.shape[0], 8))
+        if n:
+            table[:n, :4] = [p.rotation.quat for p in poses]
+            table[:n, 4:7] = [p.translation for p in poses]
+            table[:n, 7] = 0.0
+        table[n:] = self.fixed
+        return table
+
+
 class _Batcher:
     """Registry of live GPU matching factors and the cache of flattened device batches."""
 
@@ -104,8 +135,14 @@ class _Batcher:
         f._serial = next(self._serial)
         self._live[f._serial] = f
 
-    def _batch_for(self, group):
-        sig = tuple(f._serial for f in group)
+    def _remember(self, sig, entry):
+        self._batches[sig] = entry
+        while len(self._batches) > 8:
+            self._batches.popitem(last=False)
+
+    def _batch_for(self, group, sig=None):
+        """(device batch, pose table builder, gate thresholds) of exactly `group`."""
+        sig = tuple(f._serial for f in group) if sig is None else sig
         hit = self._batches.get(sig)
         if hit is not None:
             self._batches.move_to_end(sig)
@@ -124,15 +161,13 @@ class _Batcher:
                 fixed_rows.append(pose_row(f.fixed_target_pose))
             else:
                 vt.append(var_index[f.keys[1]])
+        mins = [f.min_inliers for f in group]
         batch = _lib.DeviceBatch([device_cloud(f.source) for f in group],
                                  [_as_device_map(f.target_map) for f in group],
-                                 [f.unary for f in group], [f.min_inliers for f in group],
-                                 vs, vt)
-        fixed = np.array(fixed_rows).reshape(-1, 8)
-        entry = (batch, var_keys, fixed, [weakref.ref(f) for f in group])
-        self._batches[sig] = entry
-        while len(self._batches) > 8:
-            self._batches.popitem(last=False)
+                                 [f.unary for f in group], mins, vs, vt)
+        table = _PoseTable(var_keys, np.array(fixed_rows).reshape(-1, 8))
+        entry = (batch, table, np.asarray(mins, dtype=np.float64), [weakref.ref(f) for f in group])
+        self._remember(sig, entry)
         return entry
 
     def evaluate(self, values, mode: int, requester: "MatchingCostFactor") -> None:
@@ -154,33 +189,21 @@ class _Batcher:
         # factors sharing a target map adjacent: the batch's item order is then target-major
         # (map reuse in L2) and its pipelined host copy moves contiguous record ranges
         group.sort(key=lambda f: id(f.target_map))
-        batch, var_keys, fixed, _ = self._batch_for(group)
-        poses = np.empty((len(var_keys) + fixed.shape[0], 8))
-        for i, k in enumerate(var_keys):
-            poses[i] = pose_row(_pose_of(k.kind, values[k]))
-        if fixed.shape[0]:
-            poses[len(var_keys):] = fixed
+        batch, table, _, _ = self._batch_for(group)
         # fp64 records into pinned memory (the staged copies overlap the compute); the compact
         # fp32 record (linearize_poses_f32) halves the PCIe bytes for callers that take fp32
         # blocks, but here the per-factor Python unpacking dominates either way
-        out = batch.linearize_poses(poses, mode)
+        out = batch.linearize_poses(table.build(values), mode)
         self.evaluations += 1
         for f, rec in zip(group, out):
             f._store(values, mode, rec)
 
-
-    def gated_costs(self, group, values) -> np.ndarray:
+    def gated_costs(self, group, values, sig=None) -> np.ndarray:
         """Per-factor gated cost of `group` at `values` (MatchingCostFactor.cost, factor order)
         from ONE cost-mode launch over exactly these factors."""
-        batch, var_keys, fixed, _ = self._batch_for(group)
-        poses = np.empty((len(var_keys) + fixed.shape[0], 8))
-        for i, k in enumerate(var_keys):
-            poses[i] = pose_row(_pose_of(k.kind, values[k]))
-        if fixed.shape[0]:
-            poses[len(var_keys):] = fixed
-        rec = batch.linearize_poses(poses, _lib.MODE_COST)
+        batch, table, mins, _ = self._batch_for(group, sig)
+        rec = batch.linearize_poses(table.build(values), _lib.MODE_COST)
         self.evaluations += 1
-        mins = np.fromiter((f.min_inliers for f in group), np.float64, len(group))
         return np.where(rec[:, 1] >= mins, rec[:, 0], 0.0)
 
     def assemble(self, group, values, var_keys) -> "_lib.NormalEquations":
@@ -189,10 +212,10 @@ class _Batcher:
         batch, poses = self.assembly_batch(group, values, var_keys)
         return batch.assemble_poses(poses)
 
-    def assembly_batch(self, group, values, var_keys):
+    def assembly_batch(self, group, values, var_keys, sig=None):
         """(device batch set up to assemble `group` over `var_keys`, its pose table at
         `values`) — one evaluation of the normal equations follows."""
-        sig = ("asm", tuple(f._serial for f in group), tuple(var_keys))
+        sig = ("asm", tuple(f._serial for f in group) if sig is None else sig, tuple(var_keys))
         hit = self._batches.get(sig)
         if hit is None:
             index = {k: i for i, k in enumerate(var_keys)}
@@ -209,19 +232,13 @@ class _Batcher:
                                      [f.unary for f in group], [f.min_inliers for f in group],
                                      vs, vt)
             batch.assemble_setup(len(var_keys))
-            hit = (batch, np.array(fixed_rows).reshape(-1, 8), [weakref.ref(f) for f in group])
-            self._batches[sig] = hit
-            while len(self._batches) > 8:
-                self._batches.popitem(last=False)
+            hit = (batch, _PoseTable(list(var_keys), np.array(fixed_rows).reshape(-1, 8)),
+                   [weakref.ref(f) for f in group])
+            self._remember(sig, hit)
         self._batches.move_to_end(sig)
-        batch, fixed, _ = hit
-        poses = np.empty((len(var_keys) + fixed.shape[0], 8))
-        for i, k in enumerate(var_keys):
-            poses[i] = pose_row(_pose_of(k.kind, values[k]))
-        if fixed.shape[0]:
-            poses[len(var_keys):] = fixed
+        batch, table, _ = hit
         self.evaluations += 1
-        return batch, poses
+        return batch, table.build(values)
 
 
 _BATCHER = _Batcher()
@@ -320,24 +337,42 @@ class MatchingCostFactor(Factor):
 
 # ---- FactorGraph methods replaced by integrate.patch (factor_graph.py:472-474, 522-536) ------
 
-def _split_factors(graph, positions: bool = False):
-    """(GPU matching factors, the rest) of a graph — and with `positions` their indices in
-    graph.factors — cached while its factor list is unchanged."""
-    facs = graph.factors
-    sig = (id(facs), len(facs), id(facs[-1]) if facs else 0)
-    cached = graph.__dict__.get("_vgicp_split")
-    if cached is None or cached[0] != sig:
-        gpu, rest, gpos, rpos = [], [], [], []
+class _Split:
+    """A graph's GPU matching factors and the rest, their positions in graph.factors, and the
+    GPU group's batch signature (built once, not per evaluation)."""
+
+    __slots__ = ("key", "gpu", "rest", "gpos", "rpos", "serials")
+
+    def __init__(self, key, facs):
+        self.key = key
+        self.gpu, self.rest, gpos, self.rpos = [], [], [], []
         for i, f in enumerate(facs):
             if isinstance(f, MatchingCostFactor) and not f._empty:
-                gpu.append(f)
+                self.gpu.append(f)
                 gpos.append(i)
             else:
-                rest.append(f)
-                rpos.append(i)
-        cached = (sig, gpu, rest, np.array(gpos, dtype=np.int64), rpos)
-        graph.__dict__["_vgicp_split"] = cached
-    return cached[1:] if positions else cached[1:3]
+                self.rest.append(f)
+                self.rpos.append(i)
+        self.gpos = np.array(gpos, dtype=np.int64)
+        self.serials = tuple(f._serial for f in self.gpu)
+
+
+def _split(graph) -> _Split:
+    """The graph's _Split, cached while its factor list is unchanged (the reference only
+    appends to it or replaces it: factor_graph.py:465, 701)."""
+    facs = graph.factors
+    key = (id(facs), len(facs), id(facs[-1]) if facs else 0)
+    sp = graph.__dict__.get("_vgicp_split")
+    if sp is None or sp.key != key:
+        sp = _Split(key, facs)
+        graph.__dict__["_vgicp_split"] = sp
+    return sp
+
+
+def _split_factors(graph):
+    """(GPU matching factors, the rest) of a graph."""
+    sp = _split(graph)
+    return sp.gpu, sp.rest
 
 
 #: (patched reference class, method name) -> the reference's own function (integrate.patch)
@@ -366,12 +401,12 @@ def graph_total_cost(self, values=None) -> float:
     reference sums them — Python's sum() over the factor-ordered list (same terms, same
     order, same summation, so the same float)."""
     values = self.values if values is None else values
-    gpu, rest, gpos, rpos = _split_factors(self, positions=True)
-    if not gpu:
+    sp = _split(self)
+    if not sp.gpu:
         return float(sum(f.cost(values) for f in self.factors))
     costs = np.empty(len(self.factors))
-    costs[gpos] = _BATCHER.gated_costs(gpu, values)
-    for i, f in zip(rpos, rest):
+    costs[sp.gpos] = _BATCHER.gated_costs(sp.gpu, values, sp.serials)
+    for i, f in zip(sp.rpos, sp.rest):
         costs[i] = f.cost(values)
     return float(sum(costs.tolist()))
 
@@ -449,11 +484,12 @@ class DeviceNormalEquations:
         """H, g := the normal equations at `values`; returns the total cost (:522-536)."""
         s = self.solver
         s.reset()
-        gpu, rest = _split_factors(self.graph)
+        sp = _split(self.graph)
+        gpu, rest = sp.gpu, sp.rest
         cost = 0.0
         if gpu:
             keys = list(self.graph.values)
-            batch, poses = _BATCHER.assembly_batch(gpu, values, keys)
+            batch, poses = _BATCHER.assembly_batch(gpu, values, keys, sp.serials)
             cost += s.add_batch(batch, poses, [self.slices[k].start for k in keys])
         if rest:
             blocks: dict = {}

@@ -219,3 +219,39 @@ def test_f32_record_decoding():
     c, n = _lib.record_cost_inliers_f32(rec)
     assert np.array_equal(c, costs) and np.array_equal(n, inl.astype(np.int64))
     assert c.dtype == np.float64 and n.dtype == np.int64
+
+
+def test_pose_table_builder_matches_pose_row():
+    """factor_graph._PoseTable (the batch pose table at given values, with the key-order fast
+    path) equals the row-by-row geometry.pose_row table for submap poses and frame states,
+    whether or not `values` keeps the last call's key objects and order."""
+    from types import SimpleNamespace
+
+    from paper_2202_00242_b200.factor_graph import _PoseTable, frame_key, submap_key
+
+    rng = np.random.default_rng(3)
+
+    def pose():
+        return G.Se3Pose(G.so3_exp(rng.normal(size=3)), rng.normal(size=3))
+
+    keys = [submap_key(i) for i in range(5)] + [frame_key(i) for i in range(3)]
+    fixed = np.array([G.pose_row(pose())])
+    vals = {k: (pose() if k.kind == "submap-pose" else SimpleNamespace(pose=pose()))
+            for k in keys}
+    var_keys = [keys[i] for i in (3, 0, 6, 1, 5)]
+    table = _PoseTable(var_keys, fixed)
+
+    def want(values):
+        rows = [G.pose_row(values[k] if k.kind == "submap-pose" else values[k].pose)
+                for k in var_keys]
+        return np.vstack([np.array(rows), fixed])
+
+    assert np.array_equal(table.build(vals), want(vals))          # slow path, learns order
+    moved = {k: (pose() if k.kind == "submap-pose" else SimpleNamespace(pose=pose()))
+             for k in vals}                                       # same key objects/order
+    assert np.array_equal(table.build(moved), want(moved))        # fast path
+    shuffled = dict(reversed(list(moved.items())))                # other order
+    assert np.array_equal(table.build(shuffled), want(shuffled))
+    fresh = {submap_key(k.index) if k.kind == "submap-pose" else frame_key(k.index): v
+             for k, v in moved.items()}                           # equal, not identical keys
+    assert np.array_equal(table.build(fresh), want(fresh))
