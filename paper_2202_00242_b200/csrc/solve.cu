@@ -338,6 +338,8 @@ int vg_solver_factor(vg_solver* s, double lam, double jitter, int32_t method, in
     return VG_OK;
   };
   s->factored = 0;
+  // the context's stream may have been rerouted (vg_ctx_set_stream) since the handle was made
+  VG_SOLVER(cusolverDnSetStream(s->handle, ctx->stream));
   VG_CHECK(damped());
   VG_SOLVER(cusolverDnXpotrf(s->handle, s->params, CUBLAS_FILL_MODE_LOWER, n, CUDA_R_64F, s->A,
                              n, CUDA_R_64F, s->work, s->work_bytes, s->hwork.data(),
@@ -374,6 +376,7 @@ int vg_solver_solve(vg_solver* s, const double* rhs_host, int64_t nrhs, double* 
   vg_ctx* ctx = s->ctx;
   const long long n = s->dim;
   VG_CHECK(solver_grow_rhs(s, nrhs));
+  VG_SOLVER(cusolverDnSetStream(s->handle, ctx->stream));
   if (rhs_host) {
     VG_CUDA(cudaMemcpyAsync(s->x, rhs_host, sizeof(double) * n * nrhs, cudaMemcpyHostToDevice,
                             ctx->stream));
