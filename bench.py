@@ -481,6 +481,7 @@ def run_ours(args):
     poses_host = torch.from_numpy(wl.pose_table.copy()).pin_memory()
     e2e_ms, e2e64_ms = [], []
     e2e64_line = cost_line = None
+    hits_per_step = None
     if world == 1:
         out_host = torch.empty((F_r, REC), dtype=torch.float64).pin_memory()
         out32_host = torch.empty((F_r, _lib.REC_LINEARIZE_F32), dtype=torch.float32).pin_memory()
@@ -519,7 +520,9 @@ def run_ours(args):
             ce[k].record()
         torch.cuda.synchronize()
         cms = sum(a.elapsed_time(b) for a, b in zip(cs, ce)) / args.steps
+        hits_per_step = int(cost_dev.view(-1, 2)[:, 1].sum().item())
         cost_line = {"value": total_points / (cms / 1e3), "unit": UNIT, "ms_per_step": cms,
+                     "kernel": "K4c k_cost_fused (lookup + cost fused) after K-compose, then K5",
                      "api": "vg_batch_linearize_poses_device(VG_MODE_COST)"}
     else:
         ne_host = torch.empty(ex.size, dtype=torch.float64).pin_memory()
@@ -658,6 +661,13 @@ def run_ours(args):
                          "kernel": "K4 = k_lookup_fast (K4a) + k_accumulate<0> (K4b)",
                          "kernel_ms": statistics.mean(k4_ms),
                          "bytes_per_corr": BYTES_PER_CORR, "peak_kind": peak_kind,
+                         "hits_per_step": hits_per_step,
+                         # the bytes a miss does not need (its source covariance and voxel
+                         # record, 60 of the 84 B) left out: SURVEY §8d's 84 B charges them
+                         "hits_only": (None if hits_per_step is None else {
+                             "bytes": 24 * my_points + 60 * hits_per_step,
+                             "frac": (24 * my_points + 60 * hits_per_step) / k4_avg_s / 1e9
+                                     / peak}),
                          "ncu": ncu_metrics()},
             "clocks": clocks,
             "cpu_baseline": cpu,
