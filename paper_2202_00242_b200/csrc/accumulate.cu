@@ -872,7 +872,9 @@ __global__ void __launch_bounds__(32, kMinBlocks)
 struct CostSmem {
   float4 rec[2][32][kRecStride];
 };
-template <int kMinBlocks, int OWN_REG>
+// MODE 0 (linearize, the 28 accumulators and K4b's transpose reduction): the fused variant
+// kept for measurement only (VGICP_LIN_FUSED=1).
+template <int kMinBlocks, int OWN_REG, int MODE = 1>
 __global__ void __launch_bounds__(32, kMinBlocks)
     k_cost_fused(const ItemHdr* __restrict__ hdrs, int n_items, double* __restrict__ partials) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -965,7 +967,8 @@ __global__ void __launch_bounds__(32, kMinBlocks)
     return slot;
   };
   double acc[28];
-  acc[27] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 28; ++k) acc[k] = 0.0;
   int cnt = 0;
   bool prev_hit = false;
   float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);  // OWN_REG: previous round's point, covariance
@@ -1015,10 +1018,10 @@ __global__ void __launch_bounds__(32, kMinBlocks)
       __syncwarp();
       if (prev_hit) {
         if (OWN_REG)
-          hit_core<1, 1>(pp.x, pp.y, pp.z, s0p, s1p, s2p, smr.rec[(r - 1) & 1][lane], R, t, 1.0,
-                         acc);
+          hit_core<MODE, 1>(pp.x, pp.y, pp.z, s0p, s1p, s2p, smr.rec[(r - 1) & 1][lane], R, t,
+                            1.0, acc);
         else
-          hit_math<1, 1, 1>(sm.stage[(r - 1) & 1], lane, false, R, t, 1.0, acc);
+          hit_math<MODE, 1, 1>(sm.stage[(r - 1) & 1], lane, false, R, t, 1.0, acc);
       }
       __syncwarp();  // stage (r - 1) & 1 is refilled by round r + 1
     }
@@ -1039,17 +1042,29 @@ __global__ void __launch_bounds__(32, kMinBlocks)
   __syncwarp();
   if (r > 0 && prev_hit) {
     if (OWN_REG)
-      hit_core<1, 1>(pp.x, pp.y, pp.z, s0p, s1p, s2p, smr.rec[(r - 1) & 1][lane], R, t, 1.0, acc);
+      hit_core<MODE, 1>(pp.x, pp.y, pp.z, s0p, s1p, s2p, smr.rec[(r - 1) & 1][lane], R, t, 1.0,
+                        acc);
     else
-      hit_math<1, 1, 1>(sm.stage[(r - 1) & 1], lane, false, R, t, 1.0, acc);
+      hit_math<MODE, 1, 1>(sm.stage[(r - 1) & 1], lane, false, R, t, 1.0, acc);
   }
-  double c = acc[27];
+  if (MODE == 1) {
+    double c = acc[27];
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
-  if (lane == 0) {
-    partials[2 * (size_t)w] = c;
-    partials[2 * (size_t)w + 1] = (double)cnt;
+    for (int s = 16; s >= 1; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+    if (lane == 0) {
+      partials[2 * (size_t)w] = c;
+      partials[2 * (size_t)w + 1] = (double)cnt;
+    }
+    return;
   }
+  double v[32];
+#pragma unroll
+  for (int k = 0; k < 28; ++k) v[k] = acc[k];
+  v[28] = lane == 0 ? (double)cnt : 0.0;
+  v[29] = 0.0;
+  v[30] = 0.0;
+  v[31] = 0.0;
+  partials[(size_t)w * kPartialStride + lane] = warp_transpose_reduce32(v, lane);
 }
 
 }  // namespace vg
@@ -1184,9 +1199,33 @@ static int launch_cost_fused(vg_ctx* ctx, vg_batch* b, int off, int cnt, cudaStr
   return 0;
 }
 
+#ifndef VG_LIN_FUSED_MINB
+#define VG_LIN_FUSED_MINB 14
+#endif
+// linearize mode through the fused kernel (measurement only: DESIGN.md §9)
+static bool lin_fused(const vg_batch* b, int kmode) {
+  static const int env = [] {
+    const char* e = getenv("VGICP_LIN_FUSED");
+    return e ? atoi(e) : 0;
+  }();
+  return env && kmode == 0 && b->key_mode == 1 && b->all_pow2 && b->all_f32 && b->all_plane;
+}
+
+static int launch_lin_fused(vg_ctx* ctx, vg_batch* b, int off, int cnt, cudaStream_t st) {
+  const size_t smem = sizeof(CostSmem);
+  auto kern = k_cost_fused<VG_LIN_FUSED_MINB, 1, 0>;
+  VG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  VG_CUDA(launch_pdl(kern, dim3(cnt), dim3(32), smem, st, (const ItemHdr*)(b->hdrs + off), cnt,
+                     b->partials + (size_t)off * kPartialStride));
+  ctx->launches++;
+  VG_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi) {
   if (hi <= lo) return 0;
   if (cost_fused(b, kmode)) return launch_cost_fused(ctx, b, lo, hi - lo, ctx->stream);
+  if (lin_fused(b, kmode)) return launch_lin_fused(ctx, b, lo, hi - lo, ctx->stream);
   VG_CHECK(launch_lookup_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
   if (kmode != 2) VG_CHECK(launch_acc_range(ctx, b, kmode, lo, hi - lo, ctx->stream));
   return 0;
