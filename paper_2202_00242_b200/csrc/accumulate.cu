@@ -1202,13 +1202,16 @@ static int launch_cost_fused(vg_ctx* ctx, vg_batch* b, int off, int cnt, cudaStr
 #ifndef VG_LIN_FUSED_MINB
 #define VG_LIN_FUSED_MINB 14
 #endif
-// linearize mode through the fused kernel (measurement only: DESIGN.md §9)
+// linearize mode through the fused kernel (VGICP_LIN_FUSED=1; measurement only): large batches
+// run 16% slower fused, config 1's single factor 5% faster (0.037 vs 0.039 ms) — not enabled
+// by size, so a factor's record does not change with the path its batch takes
 static bool lin_fused(const vg_batch* b, int kmode) {
   static const int env = [] {
     const char* e = getenv("VGICP_LIN_FUSED");
     return e ? atoi(e) : 0;
   }();
-  return env && kmode == 0 && b->key_mode == 1 && b->all_pow2 && b->all_f32 && b->all_plane;
+  return env == 1 && kmode == 0 && b->key_mode == 1 && b->all_pow2 && b->all_f32 &&
+         b->all_plane;
 }
 
 static int launch_lin_fused(vg_ctx* ctx, vg_batch* b, int off, int cnt, cudaStream_t st) {
