@@ -108,6 +108,10 @@ int vg_ctx_destroy(vg_ctx* ctx) {
     cudaStreamDestroy(ctx->side_stream);
     for (auto& e : ctx->events) cudaEventDestroy(e);
   }
+  if (ctx->comp3) {
+    cudaStreamSynchronize(ctx->comp3);
+    cudaStreamDestroy(ctx->comp3);
+  }
   if (ctx->comp2) {
     cudaStreamSynchronize(ctx->comp2);
     cudaStreamDestroy(ctx->comp2);
@@ -824,22 +828,28 @@ static int run_to_host(vg_batch* b, int mode, void* out_host, int fmt = 0) {
     const char* e = getenv("VGICP_STAGE_STREAMS");
     return e ? atoi(e) : 0;
   }();
-  const int nstreams = nstreams_env > 0 ? nstreams_env : (b->stages >= 6 ? 2 : 1);
+  const int nstreams =
+      std::min(3, nstreams_env > 0 ? nstreams_env : (b->stages >= 6 ? 2 : 1));
   cudaStream_t home = ctx->stream;
   struct Restore {
     vg_ctx* c;
     cudaStream_t s;
     ~Restore() { c->stream = s; }
   } restore{ctx, home};
-  if (nstreams == 2) {
+  cudaStream_t comp[3] = {home, nullptr, nullptr};
+  if (nstreams >= 2) {
     if (!ctx->comp2) VG_CUDA(cudaStreamCreateWithFlags(&ctx->comp2, cudaStreamNonBlocking));
+    if (nstreams == 3 && !ctx->comp3)
+      VG_CUDA(cudaStreamCreateWithFlags(&ctx->comp3, cudaStreamNonBlocking));
+    comp[1] = ctx->comp2;
+    comp[2] = ctx->comp3;
     VG_CUDA(cudaEventRecord(ctx->events[40], home));
-    VG_CUDA(cudaStreamWaitEvent(ctx->comp2, ctx->events[40], 0));
+    for (int k = 1; k < nstreams; ++k) VG_CUDA(cudaStreamWaitEvent(comp[k], ctx->events[40], 0));
   }
   for (int s = 0; s < b->stages; ++s) {
     const int f0 = b->stage_factors[s], f1 = b->stage_factors[s + 1];
-    if (nstreams == 2) {
-      ctx->stream = (s & 1) ? ctx->comp2 : home;
+    if (nstreams >= 2) {
+      ctx->stream = comp[s % nstreams];
       if (s > 0) VG_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->events[20 + s - 1], 0));
       VG_CHECK(launch_accumulate_range_ev(ctx, b, kmode, b->stage_items[s],
                                           b->stage_items[s + 1], ctx->events[20 + s]));
@@ -867,10 +877,12 @@ static int run_to_host(vg_batch* b, int mode, void* out_host, int fmt = 0) {
     fprintf(stderr, "\n");
     for (auto& e : tr) cudaEventDestroy(e);
   }
-  if (nstreams == 2 && ctx->comp2) {
+  if (nstreams >= 2) {
     ctx->stream = home;
-    VG_CUDA(cudaEventRecord(ctx->events[41], ctx->comp2));
-    VG_CUDA(cudaStreamWaitEvent(home, ctx->events[41], 0));
+    for (int k = 1; k < nstreams; ++k) {
+      VG_CUDA(cudaEventRecord(ctx->events[40 + k], comp[k]));
+      VG_CUDA(cudaStreamWaitEvent(home, ctx->events[40 + k], 0));
+    }
   }
   // the compute stream must not run ahead of the copies that still read the device records
   VG_CUDA(cudaEventRecord(ctx->events[b->stages], ctx->side_stream));

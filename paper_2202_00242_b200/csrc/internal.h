@@ -17,6 +17,7 @@ struct vg_ctx {
   cudaStream_t stream = nullptr;  // where all work is enqueued
   cudaStream_t side_stream = nullptr;  // host-output copies of the staged pipeline
   cudaStream_t comp2 = nullptr;        // second compute stream (odd stages, overlapped)
+  cudaStream_t comp3 = nullptr;        // third compute stream (VGICP_STAGE_STREAMS=3)
   cudaEvent_t events[65] = {};
   long long launches = 0;         // kernels launched (bench evidence)
   // scratch (grown on demand, stream-ordered reuse)
