@@ -284,6 +284,26 @@ def lm_iteration(wl):
     return out
 
 
+def odometry_pipeline():
+    """The reference's own OdometryEstimator on a 30-frame synthetic LiDAR-IMU sequence
+    (tools/odometry_replay.py), through the drop-in and unmodified, each in its own process:
+    wall-clock seconds per frame (the drop-in's first frames include its one-time setup)."""
+    if not (ROOT / "baseline" / "_ref" / "limapper").is_dir():
+        return {"unavailable": "reference not installed in baseline/_ref"}
+    out = {"frames": 30, "sequence": "reference synthetic.square_loop_scene: 20 m loop, "
+                                      "128 x 16 rays at 10 Hz, 200 Hz IMU",
+           "api": "limapper OdometryEstimator.process_frame (odometry.py:222-293), "
+                  "drop-in = integrate.patch"}
+    for mode in ("dropin", "reference"):
+        try:
+            r = subprocess.run([sys.executable, str(ROOT / "tools" / "odometry_replay.py"),
+                                "--mode", mode], capture_output=True, text=True, timeout=300)
+            out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as exc:
+            out[mode] = {"error": repr(exc)[:200]}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -597,12 +617,13 @@ def run_ours(args):
             except Exception as exc:
                 configs["4"]["lm_iteration"] = {"error": repr(exc)[:300]}
         ctx.set_stream(stream.cuda_stream)
-    lm_line = None
+    lm_line = odo_line = None
     if world == 1 and not args.no_lm:
         try:
             lm_line = lm_iteration(wl)
         except Exception as exc:  # report, never sink the bench line
             lm_line = {"error": repr(exc)[:300]}
+        odo_line = odometry_pipeline()
     if rank == 0:
         clocks = clk.summary()
         cpu = None
@@ -653,6 +674,7 @@ def run_ours(args):
             "e2e_normal_equations": ne_line,
             "cost_mode": cost_line,
             "lm_iteration": lm_line,
+            "odometry_pipeline": odo_line,
             "configs": configs,
             "multi_gpu": multi,
             "gpu_launches": int(launches),
