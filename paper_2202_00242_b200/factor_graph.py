@@ -452,6 +452,11 @@ def graph_assemble_dense(self, values, slices, dim):
 # small dense branch (dim <= dense_threshold) stays the reference's own code.
 
 
+#: the dense device system (H and its damped copy, 16 * dim^2 bytes: 14.4 GB at 30,000) is used
+#: up to this tangent dimension; larger graphs keep the reference's sparse host solve
+DEVICE_SOLVE_MAX_DIM = 30000
+
+
 def _ref_module(graph):
     """The module defining the reference FactorGraph (LmSettings, OptimizeResult, errors)."""
     for cls in type(graph).__mro__:
@@ -564,7 +569,7 @@ def graph_optimize_lm(self, settings=None):
     ref = _ref_module(self)
     settings = settings or ref.LmSettings()
     slices, dim = self._slices()
-    if dim <= settings.dense_threshold:
+    if dim <= settings.dense_threshold or dim > DEVICE_SOLVE_MAX_DIM:
         return _original(self, "optimize_lm")(self, settings)
     self.check_structure()
     values = dict(self.values)
@@ -619,7 +624,7 @@ def graph_marginal_covariance(self, key):
     device above the dense threshold (same jitter retry); the reference's method below it."""
     ref = _ref_module(self)
     slices, dim = self._slices()
-    if dim <= ref.LmSettings().dense_threshold:
+    if dim <= ref.LmSettings().dense_threshold or dim > DEVICE_SOLVE_MAX_DIM:
         return _original(self, "marginal_covariance")(self, key)
     ne = DeviceNormalEquations.of(self, slices, dim)
     ne.assemble(self.values)
