@@ -1236,8 +1236,10 @@ int launch_accumulate_range(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi)
 
 int launch_accumulate_range_ev(vg_ctx* ctx, vg_batch* b, int kmode, int lo, int hi,
                                cudaEvent_t after_lookup) {
-  if (cost_fused(b, kmode)) {  // one kernel: the event marks its end
-    if (hi > lo) VG_CHECK(launch_cost_fused(ctx, b, lo, hi - lo, ctx->stream));
+  if (cost_fused(b, kmode) || lin_fused(b, kmode)) {  // one kernel: the event marks its end
+    if (hi > lo)
+      VG_CHECK(cost_fused(b, kmode) ? launch_cost_fused(ctx, b, lo, hi - lo, ctx->stream)
+                                    : launch_lin_fused(ctx, b, lo, hi - lo, ctx->stream));
     VG_CUDA(cudaEventRecord(after_lookup, ctx->stream));
     return 0;
   }
