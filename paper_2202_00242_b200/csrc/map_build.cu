@@ -38,6 +38,80 @@ __global__ void k_pack_keys(const double* __restrict__ xyz, long long n, double 
   }
 }
 
+// Bounds of the packed keys (K2's first pass, with k_pack_keys' output): per block a
+// shared-memory min / max of the key and of its three fields as the reference's round trip
+// decodes them (hi = key >> 42 arithmetic, mid = bits 21..41, lo = bits 0..20; the signed int64
+// order of keys is the lexicographic order of (hi, mid, lo)), then 64-bit atomics.
+// b[0..7] = min hi, max hi, min mid, max mid, min lo, max lo, min key, max key.
+__global__ void k_key_bounds(const long long* __restrict__ keys, long long n,
+                             long long* __restrict__ b) {
+  long long v[8] = {LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN,
+                    LLONG_MAX, LLONG_MIN, LLONG_MAX, LLONG_MIN};
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long k = keys[i];
+    const long long f[4] = {k >> 42, (k >> 21) & ((1LL << 21) - 1), k & ((1LL << 21) - 1), k};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      v[2 * a] = min(v[2 * a], f[a]);
+      v[2 * a + 1] = max(v[2 * a + 1], f[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+      const long long o = __shfl_xor_sync(0xffffffffu, v[a], s);
+      v[a] = (a & 1) ? max(v[a], o) : min(v[a], o);
+    }
+  // one atomic per value and block (a grid of a few hundred blocks): per-warp atomics on the
+  // eight shared addresses serialise into milliseconds
+  __shared__ long long sw[32][8];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int a = 0; a < 8; ++a) sw[w][a] = v[a];
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const int a = threadIdx.x;
+    long long r = sw[0][a];
+    for (int q = 1; q < nw; ++q) r = (a & 1) ? max(r, sw[q][a]) : min(r, sw[q][a]);
+    if (a & 1) atomicMax(b + a, r);
+    else atomicMin(b + a, r);
+  }
+}
+
+__global__ void k_bounds_init(long long* __restrict__ b) {
+  if (threadIdx.x < 8) b[threadIdx.x] = (threadIdx.x & 1) ? LLONG_MIN : LLONG_MAX;
+}
+
+// order-preserving 32-bit local key: fields relative to the bounds, (hi, mid, lo) packed
+// most-significant first in sh / sm / 0 bit positions
+__global__ void k_local_keys(const long long* __restrict__ keys, long long n,
+                             const long long* __restrict__ b, int sh, int sm,
+                             unsigned* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long k = keys[i];
+    out[i] = (sh < 32 ? (unsigned)((k >> 42) - b[0]) << sh : 0u) |
+             ((unsigned)(((k >> 21) & ((1LL << 21) - 1)) - b[2]) << sm) |
+             (unsigned)((k & ((1LL << 21) - 1)) - b[4]);
+  }
+}
+
+// the packed key of each unique local key (k_local_keys inverted)
+__global__ void k_unlocal_keys(const unsigned* __restrict__ local, const int* __restrict__ m,
+                               const long long* __restrict__ b, int sh, int sm,
+                               long long* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < *m; i += gridDim.x * blockDim.x) {
+    const unsigned u = local[i];
+    const long long hi = (long long)(sh < 32 ? u >> sh : 0u) + b[0];
+    const long long mid = (long long)((u >> sm) & ((1u << (sh - sm)) - 1u)) + b[2];
+    const long long lo = (long long)(sm ? u & ((1u << sm) - 1u) : 0u) + b[4];
+    out[i] = (long long)((unsigned long long)hi << 42) | (mid << 21) | lo;
+  }
+}
+
 // fp64 AoS (n x 3 points, n x 9 covariances) -> fp32 xyz + fp64 covariance SoA
 __global__ void k_cloud_pack(const double* __restrict__ xyz, const double* __restrict__ cov,
                              long long n, float4* __restrict__ a, double2* __restrict__ c0,
@@ -524,10 +598,29 @@ static void make_record_tmap(vg_map* map, unsigned long long rows) {
   map->tmap = d;
 }
 
-int launch_map_finish(vg_ctx* ctx, vg_map* map) {
+// bounds (k_key_bounds layout) of the map's keys when the build computed them on the device:
+// the local frame and the empty marker then come without copying the keys to the host
+int launch_map_finish(vg_ctx* ctx, vg_map* map, const long long* bounds) {
   long long empty = (long long)0x8000000000000000ull;
   map->kmode = 0;
-  if (map->m) {
+  if (map->m && bounds && bounds[6] != LLONG_MIN) {
+    const long long lo[3] = {bounds[0] - kKeyOffset, bounds[2] - kKeyOffset, bounds[4] - kKeyOffset};
+    const long long hi[3] = {bounds[1] - kKeyOffset, bounds[3] - kKeyOffset, bounds[5] - kKeyOffset};
+    const bool fits = hi[0] - lo[0] < 2048 && hi[1] - lo[1] < 2048 && hi[2] - lo[2] < 1023 &&
+                      lo[0] > INT_MIN && lo[1] > INT_MIN && lo[2] > INT_MIN &&
+                      hi[0] < INT_MAX && hi[1] < INT_MAX && hi[2] < INT_MAX &&
+                      map->m < (1LL << 31);
+    if (fits) {
+      map->kmode = 1;
+      map->bx = (int)lo[0];
+      map->by = (int)lo[1];
+      map->bz = (int)lo[2];
+      map->ex = (int)(hi[0] - lo[0] + 1);
+      map->ey = (int)(hi[1] - lo[1] + 1);
+      map->ez = (int)(hi[2] - lo[2] + 1);
+    }
+    // the smallest key is above INT64_MIN, so INT64_MIN itself is absent (kmode 0 marker)
+  } else if (map->m) {
     // local key frame from the decoded keys (all keys scanned on the host)
     std::vector<long long> hk((size_t)map->m);
     VG_CUDA(cudaMemcpyAsync(hk.data(), map->keys, sizeof(long long) * map->m,
@@ -672,18 +765,55 @@ int launch_map_build(vg_ctx* ctx, const vg_cloud* cl, double res, vg_map* map) {
   VG_CUDA(temps.alloc(&counts, (size_t)n));
   VG_CUDA(temps.alloc(&offsets, (size_t)n));
   VG_CUDA(temps.alloc(&num_runs, 1));
+  long long* bnd = nullptr;
+  VG_CUDA(temps.alloc(&bnd, 8));
   k_pack_keys<<<grid1(n, 256), 256, 0, st>>>(cl->xyz64, n, res, keys, idx);
-  ctx->launches++;
+  k_bounds_init<<<1, 32, 0, st>>>(bnd);
+  k_key_bounds<<<(unsigned)std::min<long long>((n + 255) / 256, 2 * 148), 256, 0, st>>>(keys, n, bnd);
+  ctx->launches += 3;
   VG_CUDA(cudaGetLastError());
-  cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st);
-  cub::DeviceRunLengthEncode::Encode(nullptr, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st);
-  cub::DeviceScan::ExclusiveSum(nullptr, t3, counts, offsets, (int)n, st);
-  tmp_bytes = t1 > t2 ? t1 : t2;
-  tmp_bytes = tmp_bytes > t3 ? tmp_bytes : t3;
-  VG_CUDA(temps.alloc((unsigned char**)&tmp, tmp_bytes));
-  VG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st));
-  VG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st));
+  long long hb[8];
+  VG_CUDA(cudaMemcpyAsync(hb, bnd, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  VG_CUDA(cudaStreamSynchronize(st));
+  // the (hi, mid, lo) fields' spans: when they fit 32 bits together, sort order-preserving 32-bit
+  // local keys over just those bits (3-4 radix passes of 4-byte keys instead of 8 passes of
+  // 8-byte keys; same stable permutation, so the same cells in the same member order)
+  auto bits = [](long long span) {
+    int b = 0;
+    while (b < 40 && (1LL << b) < span + 1) ++b;
+    return b;
+  };
+  const int bh = bits(hb[1] - hb[0]), bm = bits(hb[3] - hb[2]), bl = bits(hb[5] - hb[4]);
+  const bool local32 = bh + bm + bl <= 32 && getenv("VGICP_MAP_SORT64") == nullptr;
   int m = 0;
+  if (local32) {
+    unsigned *lk = nullptr, *lk_sorted = nullptr, *ulk = nullptr;
+    VG_CUDA(temps.alloc(&lk, (size_t)n));
+    VG_CUDA(temps.alloc(&lk_sorted, (size_t)n));
+    VG_CUDA(temps.alloc(&ulk, (size_t)n));
+    const int sm = bl, sh = bl + bm, nbits = std::max(1, bh + bm + bl);
+    k_local_keys<<<grid1(n, 256), 256, 0, st>>>(keys, n, bnd, sh, sm, lk);
+    ctx->launches++;
+    VG_CUDA(cudaGetLastError());
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, lk, lk_sorted, idx, perm, (int)n, 0, nbits, st);
+    cub::DeviceRunLengthEncode::Encode(nullptr, t2, lk_sorted, ulk, counts, num_runs, (int)n, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, t3, counts, offsets, (int)n, st);
+    tmp_bytes = std::max(std::max(t1, t2), t3);
+    VG_CUDA(temps.alloc((unsigned char**)&tmp, tmp_bytes));
+    VG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t1, lk, lk_sorted, idx, perm, (int)n, 0, nbits, st));
+    VG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, t2, lk_sorted, ulk, counts, num_runs, (int)n, st));
+    k_unlocal_keys<<<grid1(n, 256), 256, 0, st>>>(ulk, num_runs, bnd, sh, sm, ukeys);
+    ctx->launches++;
+    VG_CUDA(cudaGetLastError());
+  } else {
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st);
+    cub::DeviceRunLengthEncode::Encode(nullptr, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, t3, counts, offsets, (int)n, st);
+    tmp_bytes = std::max(std::max(t1, t2), t3);
+    VG_CUDA(temps.alloc((unsigned char**)&tmp, tmp_bytes));
+    VG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, t1, keys, keys_sorted, idx, perm, (int)n, 0, 64, st));
+    VG_CUDA(cub::DeviceRunLengthEncode::Encode(tmp, t2, keys_sorted, ukeys, counts, num_runs, (int)n, st));
+  }
   VG_CUDA(cudaMemcpyAsync(&m, num_runs, sizeof(int), cudaMemcpyDeviceToHost, st));
   VG_CUDA(cudaStreamSynchronize(st));
   VG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, t3, counts, offsets, m, st));
@@ -700,5 +830,5 @@ int launch_map_build(vg_ctx* ctx, const vg_cloud* cl, double res, vg_map* map) {
       offsets, counts, perm, cl->xyz64, cl->cov64, m, map->means, map->covs, map->counts);
   ctx->launches += 2;
   VG_CUDA(cudaGetLastError());
-  return launch_map_finish(ctx, map);
+  return launch_map_finish(ctx, map, hb);
 }
