@@ -196,7 +196,7 @@ def knn_search(frame, k: int) -> np.ndarray:
     if n < k:
         raise FrameTooSparse(f"frame has {n} points, need at least {k}")
     cloud = device_cloud(frame, with_covs=False)
-    out = np.empty((n, k), dtype=np.int64)
+    out = _lib.PINNED.empty((n, k), np.int64)  # page-locked: the copy runs at PCIe speed
     ctx = cloud.ctx
     _lib.check(ctx.lib.vg_knn(ctx.handle, cloud.handle, int(k), _lib.iptr(out)), "knn_search")
     return out
@@ -212,8 +212,8 @@ def estimate_covariances(frame, plane_eps: float = 1e-3):
     nbrs = np.ascontiguousarray(frame.neighbors, dtype=np.int64)
     k = nbrs.shape[1]
     cloud = device_cloud(frame, with_covs=False)
-    covs = np.empty((n, 3, 3))
-    degen = np.empty(n, dtype=np.uint8)
+    covs = _lib.PINNED.empty((n, 3, 3))
+    degen = _lib.PINNED.empty((n,), np.uint8)
     ctx = cloud.ctx
     _lib.check(ctx.lib.vg_covariances(ctx.handle, cloud.handle, _lib.iptr(nbrs), int(k),
                                       float(plane_eps), _lib.dptr(covs),
