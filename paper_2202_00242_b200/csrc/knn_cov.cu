@@ -384,6 +384,8 @@ static int launch_knn_grid(vg_ctx* ctx, const vg_cloud* cl, int k, long long* nb
   const int blocks = (n + 127) / 128;
   if (k <= 8)
     k_knn_grid<8><<<blocks, 128, 0, st>>>(sorted, n, k, g, start, nbrs_dev);
+  else if (k == 10)  // the reference's default (config.py:22): no padding slots to sort through
+    k_knn_grid<10><<<blocks, 128, 0, st>>>(sorted, n, k, g, start, nbrs_dev);
   else if (k <= 16)
     k_knn_grid<16><<<blocks, 128, 0, st>>>(sorted, n, k, g, start, nbrs_dev);
   else
@@ -407,6 +409,8 @@ int launch_knn(vg_ctx* ctx, const vg_cloud* cl, int k, long long* nbrs_dev) {
   const int blocks = (n + kKnnTile - 1) / kKnnTile;
   if (k <= 8)
     k_knn<8><<<blocks, kKnnTile, 0, ctx->stream>>>(cl->xyz64, n, k, nbrs_dev);
+  else if (k == 10)  // the reference's default: an exact-size register top-k
+    k_knn<10><<<blocks, kKnnTile, 0, ctx->stream>>>(cl->xyz64, n, k, nbrs_dev);
   else if (k <= 16)
     k_knn<16><<<blocks, kKnnTile, 0, ctx->stream>>>(cl->xyz64, n, k, nbrs_dev);
   else if (k <= 32)
