@@ -205,6 +205,17 @@ __global__ void __launch_bounds__(128)
   const int cy = knn_cell_axis(qy, g.oy, g.inv_h, g.dy);
   const int cz = knn_cell_axis(qz, g.oz, g.inv_h, g.dz);
   const int rmax = max(max(g.dx, g.dy), g.dz);
+  // distance from the query to the nearest face of its own cell that has cells beyond it:
+  // after ring R every unscanned point is at least R h + f0 away (R h alone assumes the query
+  // sits on a face), so a query deep inside a dense cell stops after its own cell
+  auto face = [&](double v, double o, int c, int d) {
+    const double lo = o + c * g.h;
+    const double a = c > 0 ? v - lo : DBL_MAX, b = c < d - 1 ? lo + g.h - v : DBL_MAX;
+    return fmin(a, b);
+  };
+  const double f0 = fmax(fmin(fmin(face(qx, g.ox, cx, g.dx), face(qy, g.oy, cy, g.dy)),
+                              face(qz, g.oz, cz, g.dz)),
+                         0.0);
   for (int R = 0;; ++R) {
     // the shell of cells at Chebyshev distance R
     for (int ix = max(cx - R, 0); ix <= min(cx + R, g.dx - 1); ++ix) {
@@ -223,10 +234,10 @@ __global__ void __launch_bounds__(128)
         }
       }
     }
-    // every unscanned point is farther than R * h (up to the rounding of the cell
+    // every unscanned point is farther than R h + f0 (up to the rounding of the cell
     // assignment, hence the margin); ties at the bound are scanned too
-    const double bound = (R - 1e-6) * g.h;
-    if (R >= rmax || (R > 0 && d[KM - 1] < bound * bound)) break;
+    const double bound = fmin(R * g.h + f0, 0.5 * DBL_MAX) - 2e-6 * g.h;
+    if (R >= rmax || (bound > 0.0 && d[KM - 1] < bound * bound)) break;
   }
 #pragma unroll
   for (int j = 0; j < KM; ++j)
