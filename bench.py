@@ -221,6 +221,21 @@ def cpu_reference(wl, args, steps, warmup, one_process=False):
             f"0..{args.cpu_targets - 1}), {sample['points']} correspondences per pass, "
             f"oracle linearization, {procs}-process fork pool, {steps} passes")
     extra = {"cpu_model": cpu_baseline.cpu_model(), "cpu_count": os.cpu_count()}
+    # the same sample through the reference package itself (baseline/_ref), beside the oracle
+    # port the arm reports: the port restates it, this shows the two run at the same speed
+    ref = ROOT / "baseline" / "_ref"
+    if (ref / "limapper").is_dir() and str(ref) not in sys.path:
+        sys.path.append(str(ref))
+    try:
+        rr = cpu_baseline.time_sample_reference(sample, steps, warmup)
+    except Exception as exc:
+        rr = None
+        extra["reference_package"] = {"error": repr(exc)[:200]}
+    if rr is not None:
+        extra["reference_package"] = {
+            "value": rr[0], "unit": UNIT, "seconds_per_pass": rr[1], "processes": rr[2],
+            "sample": "the same factors through limapper.registration.linearize_matching_cost "
+                      "(the unmodified reference from baseline/_ref), same fork pool"}
     if one_process:
         r1, s1, _ = cpu_baseline.time_sample(sample, 1, 0, processes=1)
         extra["one_process"] = {"value": r1, "unit": UNIT, "seconds_per_pass": s1,

@@ -74,7 +74,8 @@ def build_sample(wl, n_targets: int = 16, knn: int = 10, processes: int | None =
     _WL = None
     R, t = O.relative_transforms(wl.pose_table, wl.pairs[fids, 0], wl.pairs[fids, 1])
     return {"fids": fids, "pairs": wl.pairs[fids], "maps": maps, "sources": sources, "R": R,
-            "t": t, "points": int(sum(len(sources[int(i)][0]) for i in wl.pairs[fids, 0]))}
+            "t": t, "poses": wl.pose_table.copy(),
+            "points": int(sum(len(sources[int(i)][0]) for i in wl.pairs[fids, 0]))}
 
 
 def cpu_model() -> str:
@@ -104,12 +105,50 @@ def _work(chunk):
     return n
 
 
+_REF = None  # limapper objects of the sample (reference-package timing)
+
+
+def _work_ref(chunk):
+    """The same factors through the reference package's own public API
+    (limapper.registration.linearize_matching_cost, registration.py:251-269)."""
+    s, (reg, frames, maps, poses) = _SAMPLE, _REF
+    n = 0
+    for f in chunk:
+        i, j = (int(v) for v in s["pairs"][f])
+        try:
+            reg.linearize_matching_cost(frames[i], maps[j], poses[i], poses[j])
+        except Exception:  # DegenerateConstraint: still evaluated
+            pass
+        n += len(frames[i])
+    return n
+
+
+def reference_objects(sample):
+    """limapper Frames / GaussianVoxelMaps / Se3Poses of the sample (None when the reference
+    package is not importable, e.g. from baseline/_ref)."""
+    try:
+        import limapper.geometry as G
+        import limapper.preprocess as P
+        import limapper.registration as reg
+    except Exception:
+        return None
+    frames = {i: P.Frame(points=pts, stamps=np.zeros(len(pts)), stamp=0.0, covs=covs,
+                         deskewed=True) for i, (pts, covs) in sample["sources"].items()}
+    maps = {j: reg.GaussianVoxelMap(m[0], m[1], m[2], m[3], m[4])
+            for j, m in sample["maps"].items()}
+    need = set(int(v) for v in sample["pairs"].ravel())
+    poses = {v: G.Se3Pose(G.Rotation(sample["poses"][v, :4]), sample["poses"][v, 4:7].copy())
+             for v in need}
+    return reg, frames, maps, poses
+
+
 class Runner:
     """Keeps a fork()ed pool alive across timed steps."""
 
-    def __init__(self, sample, processes: int | None = None):
+    def __init__(self, sample, processes: int | None = None, work=None):
         global _SAMPLE
         _SAMPLE = sample
+        self.work = work or _work
         self.sample = sample
         self.processes = processes or os.cpu_count() or 1
         F = len(sample["pairs"])
@@ -120,8 +159,8 @@ class Runner:
 
     def step(self) -> int:
         if self.pool is None:
-            return sum(_work(c) for c in self.chunks)
-        return sum(self.pool.map(_work, self.chunks))
+            return sum(self.work(c) for c in self.chunks)
+        return sum(self.pool.map(self.work, self.chunks))
 
     def close(self):
         if self.pool is not None:
@@ -129,9 +168,21 @@ class Runner:
             self.pool.join()
 
 
-def time_sample(sample, steps: int, warmup: int = 1, processes: int | None = None):
+def time_sample_reference(sample, steps: int, warmup: int = 1, processes: int | None = None):
+    """time_sample through the reference package itself (limapper importable); None if not."""
+    global _REF
+    _REF = reference_objects(sample)
+    if _REF is None:
+        return None
+    try:
+        return time_sample(sample, steps, warmup, processes, work=_work_ref)
+    finally:
+        _REF = None
+
+
+def time_sample(sample, steps: int, warmup: int = 1, processes: int | None = None, work=None):
     """Returns (corr_per_s, seconds_per_step, processes)."""
-    r = Runner(sample, processes)
+    r = Runner(sample, processes, work)
     try:
         for _ in range(warmup):
             r.step()
