@@ -193,6 +193,18 @@ def run_preprocess(args):
                "sample": f"the same scan once: kNN + covariances {1e3 * (b - a):.0f} ms, 3 map "
                          f"builds {1e3 * (c - b):.0f} ms (single-threaded NumPy/SciPy, as the "
                          f"reference)"}
+    # device-resident figure beside it: kNN + covariances of a resident cloud with the results
+    # left on the device (wall clock around the call and a context synchronize: no transfers)
+    cloud = _lib.DeviceCloud(pts, None)
+    dev_ms = []
+    for i in range(max(3, args.steps // 10) + 2):
+        cloud.ctx.synchronize()
+        a = time.perf_counter()
+        _lib.check(cloud.ctx.lib.vg_cloud_estimate_covariances(cloud.ctx.handle, cloud.handle,
+                                                               10, 1e-3, None, None, None))
+        cloud.ctx.synchronize()
+        if i >= 2:
+            dev_ms.append((time.perf_counter() - a) * 1e3)
     k = statistics.median(knn_ms)
     m = statistics.median(map_ms)
     return {"metric": "points preprocessed/sec (kNN k=10 + covariances)", "value": n / (k / 1e3),
@@ -202,6 +214,10 @@ def run_preprocess(args):
                        "knn": 10, "resolutions_m": [0.5, 1.0, 2.0],
                        "timing": "wall clock around the host API calls (upload included)"},
             "map_build": {"value": 3 * n / (m / 1e3), "unit": "points/s", "ms_per_step": m},
+            "device_resident": {"value": n / (statistics.median(dev_ms) / 1e3),
+                                "unit": "points/s", "ms_per_step": statistics.median(dev_ms),
+                                "what": "kNN + covariances of a device cloud, results kept on "
+                                        "the device (wall clock, no host transfers)"},
             "cpu_baseline": cpu}
 
 
