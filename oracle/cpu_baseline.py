@@ -117,7 +117,7 @@ def _work_ref(chunk):
         i, j = (int(v) for v in s["pairs"][f])
         try:
             reg.linearize_matching_cost(frames[i], maps[j], poses[i], poses[j])
-        except Exception:  # DegenerateConstraint: still evaluated
+        except reg.DegenerateConstraint:  # still evaluated (anything else propagates)
             pass
         n += len(frames[i])
     return n
@@ -131,6 +131,10 @@ def reference_objects(sample):
         import limapper.preprocess as P
         import limapper.registration as reg
     except Exception:
+        return None
+    # only the unmodified reference: a process that applied integrate.patch runs the drop-in
+    # under these names
+    if getattr(reg.linearize_matching_cost, "__module__", "") != "limapper.registration":
         return None
     frames = {i: P.Frame(points=pts, stamps=np.zeros(len(pts)), stamp=0.0, covs=covs,
                          deskewed=True) for i, (pts, covs) in sample["sources"].items()}
