@@ -107,9 +107,10 @@ class _PoseTable:
             vals = [listed[i] for i in order[1]]
         else:
             vals = [values[k] for k in keys]
-            pos = {id(k): i for i, k in enumerate(values)}
-            idx = [pos.get(id(k)) for k in keys]
-            self._order = None if None in idx else (tuple(values), idx)
+            # positions by key equality (factors often hold equal but distinct Key objects),
+            # remembered for dicts holding these same key objects in this order
+            pos = {k: i for i, k in enumerate(values)}
+            self._order = (tuple(values), [pos[k] for k in keys])
         poses = [v if sub else v.pose for v, sub in zip(vals, self.submap)]
         n = len(keys)
         table = np.empty((n + self.fixed.shape[0], 8))
