@@ -135,3 +135,18 @@ def test_check_structure_matches_reference(lm, seed):
     g.__dict__.pop("_vgicp_checked", None)
     b = _run(lambda: original(g))
     assert a[0] == b[0] and (a[0] == "ok" or str(a[1]) == str(b[1]))
+
+
+def test_graphs_beyond_the_device_bound_keep_the_reference_solve(lm, monkeypatch):
+    """Above DEVICE_SOLVE_MAX_DIM the dense device system is not built: optimize_lm is the
+    reference's own (its sparse host solve)."""
+    lw, fg, original = lm
+    from paper_2202_00242_b200 import factor_graph as vfg
+
+    monkeypatch.setattr(vfg, "DEVICE_SOLVE_MAX_DIM", 100)
+    monkeypatch.setattr(vfg.DeviceNormalEquations, "of",
+                        classmethod(lambda cls, g, s, d: pytest.fail("device path taken")))
+    settings = fg.LmSettings(max_iterations=3)
+    g1, _, _ = lw.local_mapping_lm(frames=41, matching=False)
+    g2, _, _ = lw.local_mapping_lm(frames=41, matching=False)
+    _same(_run(lambda: g1.optimize_lm(settings)), _run(lambda: original(g2, settings)))
